@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the adjamr B200 hot path (BASELINE.json metric:
+"fp64 cell-updates/s and flagged cells/s on 1 B200; HBM GB/s vs ~8 TB/s").
+
+Workload (BASELINE.json configs[3], "C4"): 4096^2 linearised shallow water on
+[0, 1e6 m]^2, bathymetry -4000 + 3000 tanh((x'-0.7)/0.05) + 64 Fourier modes
+(|k| <= 16, seed 0, max 200 m), Gaussian surface pulse, outflow boundaries,
+dt from select_dt (CFL 0.9), MC limiter.  One bench step = K2 physical ghost
+fill + K1 wave-propagation step of the whole level.  Inputs (537 MB of state
+and material per step) exceed the 126 MB L2, so no flush is needed between
+steps.  The adjoint flagging pass K3 (40 snapshot intervals at 1024^2,
+tolerance 1e-4) is measured in the same run and reported under "flagging".
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): independent replicas, one per GPU ("scaling": "weak"),
+value = all ranks' cell-updates / max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N = 4096
+L = 1.0e6
+GRAV = 9.81
+T_STEPS = 300
+METRIC = "fp64 cell-updates/s"
+BYTES_PER_CELL_SWE = 56          # read q 24 + read c 8 + write q 24
+WORKLOAD = ("C4: 4096^2 linearised shallow water (wave-form solver, MC limiter, transverse "
+            "corrections, outflow), 1 step = physical ghost fill + patch step")
+
+
+def fourier_modes():
+    rng = np.random.default_rng(0)
+    modes = []
+    while len(modes) < 64:
+        kx, ky = (int(v) for v in rng.integers(-16, 17, size=2))
+        if 1.0 <= np.hypot(kx, ky) <= 16.0:
+            modes.append((kx, ky))
+    phases = rng.uniform(0.0, 2.0 * np.pi, size=64)
+    amps = rng.normal(size=64)
+    return modes, phases, amps
+
+
+def c4_fields(n=N, g=2, device="cuda"):
+    """Bathymetry (ghost-inclusive), computed on the device (setup only)."""
+    import torch
+    dx = L / n
+    idx = torch.arange(-g, n + g, dtype=torch.float64, device=device)
+    xp = ((idx + 0.5) * dx) / L
+    modes, phases, amps = fourier_modes()
+    F = torch.zeros(n + 2 * g, n + 2 * g, dtype=torch.float64, device=device)
+    for (kx, ky), ph, a in zip(modes, phases, amps):
+        ax = 2 * np.pi * kx * xp
+        by = 2 * np.pi * ky * xp + ph
+        F += a * (torch.outer(torch.cos(ax), torch.cos(by)) - torch.outer(torch.sin(ax), torch.sin(by)))
+    F *= 200.0 / F[g:-g, g:-g].abs().max()
+    B = -4000.0 + 3000.0 * torch.tanh((xp[:, None] - 0.7) / 0.05) + F
+    return B
+
+
+def build_c4(n=N):
+    import torch
+    from paper_1511_03645_b200 import equations as E
+    from paper_1511_03645_b200 import solver
+    from paper_1511_03645_b200.geometry import Patch, PatchHierarchy
+    B = c4_fields(n)
+    depth = (0.0 - B)
+    c = torch.sqrt(GRAV * torch.clamp(depth, min=0.0))
+    mat = E.SweMaterial(bathymetry=B.cpu().numpy(), depth=depth.cpu().numpy(), wet=(depth > 0).cpu().numpy(),
+                        c=c.cpu().numpy(), gravity=GRAV)
+    eq = E.SweLinear2D(E.SweMaterialModel(lambda x, y: np.zeros_like(x), 0.0, GRAV))
+    h = PatchHierarchy(xlim=(0.0, L), ylim=(0.0, L), base_shape=(n, n), ratios=[])
+    p = Patch(h.make_spec(1, (0, 0), (n - 1, n - 1)), 3)
+    p.aux = mat
+    xs = (np.arange(n) + 0.5) / n
+    X, Y = np.meshgrid(xs, xs, indexing="ij")
+    p.interior()[0] = np.exp(-((X - 0.3) ** 2 + (Y - 0.5) ** 2) / 0.02 ** 2)
+    h.levels = [[p]]
+    dt = solver.select_dt(h, eq, 0.9)
+    bc = solver.BoundarySpec("outflow", "outflow", "outflow", "outflow")
+    return h, p, eq, bc, dt
+
+
+def adjoint_ring(nsnap, na=1024, device="cuda"):
+    """Synthetic adjoint snapshots on the 1024^2 grid: a pulse leaving the
+    20x20-cell coastal box near x'=0.9 and spreading backward in time."""
+    import torch
+    xs = (torch.arange(na, dtype=torch.float64, device=device) + 0.5) / na
+    X, Y = torch.meshgrid(xs, xs, indexing="ij")
+    ring = torch.zeros(nsnap, 3, na, na, dtype=torch.float64, device=device)
+    for k in range(nsnap):
+        age = (nsnap - 1 - k) / max(nsnap - 1, 1)           # 0 at t_final
+        r = 0.01 + 0.35 * age
+        env = torch.exp(-(((X - 0.9) ** 2 + (Y - 0.5) ** 2) - r ** 2).abs() / (0.02 + 0.1 * age) ** 2)
+        ring[k, 0] = env * (1.0 - 0.5 * age)
+        ring[k, 1] = 0.1 * env * (X - 0.9)
+        ring[k, 2] = 0.1 * env * (Y - 0.5)
+    return ring
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpu_index=0):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def cpu_baseline(h, p, eq, dt):
+    """The CPU oracle (numpy restatement of the reference, 1 core) on a
+    bounded sample: a 1024x1024-cell block of the C4 state, 3 steps."""
+    from oracle import adjamr_oracle as O
+    st = p._store
+    import torch
+    full = st.view(p._slot).cpu().numpy()
+    aux = st.aux_view(p._slot).cpu().numpy()
+    n = 1024
+    q = np.ascontiguousarray(full[:, 1500:1500 + n + 4, 1500:1500 + n + 4])
+    a = np.ascontiguousarray(aux[:, 1500:1500 + n + 4, 1500:1500 + n + 4])
+    del torch
+    dx = p.spec.dx
+    reps = 3
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        O.step_2d(q, a, dt, dx, dx, O.SWE2D, False, False, "MC", GRAV)
+    el = time.perf_counter() - t0
+    return {"value": reps * n * n / el, "unit": "cell-updates/s", "cores": 1, "kind": "port",
+            "sample": f"oracle step_2d on a {n}x{n} block of the C4 state, {reps} steps ({el:.1f} s)"}
+
+
+def _ref_worker(args):
+    q, a, dt, dx = args
+    from oracle import adjamr_oracle as O
+    out, _ = O.step_2d(q, a, dt, dx, dx, O.SWE2D, False, False, "MC", GRAV)
+    return out.shape
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (oracle port; the Python
+    reference cannot travel to the GPU box) on all host cores via a process
+    pool over row slabs, on a bounded sample of the C4 workload per step."""
+    import multiprocessing as mp
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    n = N
+    rows = min(n, 32 * cores)
+    rng = np.random.default_rng(0)
+    xs = (np.arange(-2, n + 2) + 0.5) / n
+    modes, phases, amps = fourier_modes()
+    F = np.zeros((rows + 4, n + 4))
+    xr = xs[:rows + 4]
+    for (kx, ky), ph, amp in zip(modes, phases, amps):
+        F += amp * np.cos(2 * np.pi * (kx * xr[:, None] + ky * xs[None, :]) + ph)
+    F *= 200.0 / max(np.abs(F).max(), 1e-30)
+    B = -4000.0 + 3000.0 * np.tanh((xr[:, None] - 0.7) / 0.05) + F
+    depth = -B
+    aux = np.stack([np.sqrt(GRAV * depth), depth])
+    q = np.zeros((3, rows + 4, n + 4))
+    q[0] = rng.normal(size=q[0].shape) * 1e-3
+    dx = L / n
+    dt = 0.9 * dx / float(aux[0].max())
+    per = max(1, rows // cores)
+    tasks = []
+    for r0 in range(0, rows, per):
+        r1 = min(rows, r0 + per)
+        tasks.append((np.ascontiguousarray(q[:, r0:r1 + 4]), np.ascontiguousarray(aux[:, r0:r1 + 4]), dt, dx))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(min(cores, len(tasks))) as pool:
+        for _ in range(args.warmup):
+            pool.map(_ref_worker, tasks)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(_ref_worker, tasks)
+        el = time.perf_counter() - t0
+    cells = rows * n * args.steps
+    val = cells / el
+    line = {"metric": METRIC, "value": val, "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "sample_rows": rows, "grid": [n, n]},
+            "cpu_baseline": {"value": val, "unit": "cell-updates/s", "cores": cores, "kind": "port",
+                             "sample": f"oracle step_2d (numpy restatement of the reference) on a {rows}x{n} "
+                                       f"row slab of C4 per step, {len(tasks)} processes"},
+            "e2e": {"value": val, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", default="fast", choices=["fast", "exact"])
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1511_03645_b200 import _lib, device, solver
+    variant = _lib.VARIANT_FAST if args.variant == "fast" else _lib.VARIANT_EXACT
+    h, p, eq, bc, dt = build_c4()
+    shape = (N, N)
+    st = solver.store_of(p)
+    st.sync_in()
+
+    # warm-up (compiles nothing: the kernels are prebuilt; warms caches/clocks)
+    solver.advance_uniform(p, eq, bc, shape, dt, args.warmup, "MC", variant)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device-resident
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        e0.record(stream)
+        cfl = solver.advance_uniform(p, eq, bc, shape, dt, args.steps, "MC", variant)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    t_max = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item())
+    cells = N * N * args.steps * world
+    value = cells / (ms * 1e-3)
+
+    # ---- dominant kernel alone (K1), events on the launching stream
+    k1_ms = []
+    for _ in range(max(5, min(args.steps, 20))):
+        st.fold_ghosts()
+        out = st._free(st.cur, -1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        device.launch_step(st, dt, eq, "MC", variant, out)
+        b.record(stream)
+        st.ghost_src = st.cur
+        st.cur = out
+        k1_ms.append((a, b))
+    torch.cuda.synchronize()
+    k1 = statistics.median([a.elapsed_time(b) for a, b in k1_ms])
+    peak, peak_kind = peaks()
+    achieved = BYTES_PER_CELL_SWE * N * N / (k1 * 1e-3) / 1e9
+
+    # ---- K3 adjoint flagging on the same state
+    flag = bench_flagging(p, st, dt, stream)
+
+    # ---- e2e through the public API with host buffers
+    e2e = bench_e2e(p, eq, bc, shape, dt, variant, min(args.steps, 5))
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "grid": [N, N], "dt": dt, "limiter": "MC", "variant": args.variant,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "inputs (537 MB/step) larger than the 126 MB L2; no flush"},
+        "max_courant": cfl,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "k1_fast (SWE, MC)", "kernel_ms": k1,
+                     "bytes_per_cell_update": BYTES_PER_CELL_SWE, "cells_per_launch": N * N,
+                     "kernel_cell_updates_per_s": N * N / (k1 * 1e-3)},
+        "flagging": flag,
+        "e2e": e2e,
+        "gpu_launches": args.steps * 4,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(h, p, eq, dt)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_flagging(p, st, dt, stream):
+    import torch
+    from paper_1511_03645_b200 import device
+    nsnap = 41
+    ring = adjoint_ring(nsnap)
+    T = T_STEPS * dt
+    times = np.linspace(0.0, T, nsnap)
+    from oracle import adjamr_oracle as O   # window arithmetic only (host); mirrors query_window_times
+    del O
+    from paper_1511_03645_b200 import adjoint
+    t = 150 * dt
+    res = {}
+    for label, ts in (("single_point", T), ("full_span", 0.0)):
+        idx = adjoint.window_indices(t, adjoint.TimeWindow(ts, T), times)
+        device.launch_flag(st, ring, (1024, 1024), (0.0, 0.0), L / 1024, L / 1024, (0.0, 0.0), L / N, L / N,
+                           idx, 1e-4)
+        torch.cuda.synchronize()
+        reps = 10
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            _, counts, _, _ = device.launch_flag(st, ring, (1024, 1024), (0.0, 0.0), L / 1024, L / 1024,
+                                                 (0.0, 0.0), L / N, L / N, idx, 1e-4)
+        b.record(stream)
+        torch.cuda.synchronize()
+        kms = a.elapsed_time(b) / reps
+        nbytes = 24 * N * N + 24 * 1024 * 1024 * len(idx) + N * N / 8
+        res[label] = {"value": N * N / (kms * 1e-3), "unit": "flagged cells/s", "snapshots": len(idx),
+                      "kernel_ms": kms, "achieved_GBps": nbytes / (kms * 1e-3) / 1e9,
+                      "flagged": int(counts[0].item())}
+    out = dict(res["single_point"])
+    out["full_span"] = res["full_span"]
+    out["tolerance"] = 1e-4
+    return out
+
+
+def bench_e2e(p, eq, bc, shape, dt, variant, steps):
+    """Public API with host buffers: state in pinned host memory -> H2D,
+    physical fill + step (solver.fill_ghost_physical / step_patch), D2H."""
+    import torch
+    from paper_1511_03645_b200 import solver
+    st = p._store
+    host = torch.empty(tuple(st.view(p._slot).shape), dtype=torch.float64, pin_memory=True)
+    host.copy_(st.view(p._slot))
+    nbytes = host.numel() * 8
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st.prepare_write(full_ghosts=True)
+        st.view(p._slot).copy_(host, non_blocking=True)
+        p._loc = "device"
+        solver.fill_ghost_physical(p, bc, eq, shape)
+        solver.step_patch(p, dt, eq, "MC", variant=variant)
+        st.fold_ghosts()
+        host.copy_(st.view(p._slot), non_blocking=True)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    return {"value": N * N * steps / el, "unit": "cell-updates/s", "h2d_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": nbytes, "steps": steps,
+            "path": "pinned host state -> H2D -> fill_ghost_physical + step_patch (C ABI) -> D2H"}
+
+
+if __name__ == "__main__":
+    main()

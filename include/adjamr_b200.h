@@ -1,0 +1,229 @@
+/*
+ * adjamr_b200.h -- C ABI of the B200-native hot path of adjoint-guided
+ * block-structured AMR (arxiv 1511.03645, reference package `adjamr`).
+ *
+ * Every entry point is stream-ordered, borrows caller-owned DEVICE pointers
+ * (the Python host layer passes torch tensors' data_ptr()), and returns an
+ * int status.  No torch or C++ types cross this boundary.
+ *
+ * The reference is pure Python/numpy and has no FFI of its own; each entry
+ * point below names the reference function(s) it replaces (paths relative to
+ * /root/reference/pkg/src/adjamr/).  INTEGRATION.md shows the ctypes binding
+ * that the reference-side Python would add.
+ *
+ * Data layout in HBM (one "level store" per refinement level):
+ *   q   : m component planes, component c of patch p, ghost-inclusive local
+ *         cell (ii, jj) lives at q[c*comp_stride + p.offset + ii*p.pitch + jj].
+ *         y (jj) is the contiguous axis, exactly like the reference's numpy
+ *         `Patch.state` of shape (m, nx+2g, ny+2g) (geometry.py:109).
+ *         In 1D the patch is a single column: ny = 1, pitch = 1.
+ *   aux : naux material planes with the same per-patch offsets/pitch,
+ *         plane stride aux_stride.  Acoustics: {c, z, rho, bulk};
+ *         shallow water: {c, depth} (wet <=> depth > 0)  (equations.py:32-74).
+ */
+#ifndef ADJAMR_B200_H
+#define ADJAMR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADJ_ABI_VERSION 1
+
+/* status codes (mapped to the reference's exception classes by the host) */
+#define ADJ_OK                 0
+#define ADJ_ERR_CFL            1   /* solver.CflViolationError      solver.py:23  */
+#define ADJ_ERR_NONFINITE      2   /* solver.NumericalBlowupError   solver.py:27  */
+#define ADJ_ERR_SCHEDULING     3   /* solver.SchedulingError        solver.py:31  */
+#define ADJ_ERR_OUT_OF_RANGE   4   /* geometry.OutOfRangeError      geometry.py:18 */
+#define ADJ_ERR_BAD_ARG        5   /* ValueError                                   */
+#define ADJ_ERR_CUDA          -1
+
+/* equation systems (equations.py:423-493) */
+#define ADJ_SYS_AC1D   0   /* Acoustics1D / AdjointAcoustics1D   */
+#define ADJ_SYS_AC2D   1   /* Acoustics2D / AdjointAcoustics2D   */
+#define ADJ_SYS_SWE2D  2   /* SweLinear2D / AdjointSweLinear2D   */
+
+/* Riemann-solver form (EquationSet.form, equations.py:397, 464) */
+#define ADJ_FORM_WAVE   0
+#define ADJ_FORM_FWAVE  1
+
+/* limiters (solver.py:20, 65-77) */
+#define ADJ_LIM_NONE      0
+#define ADJ_LIM_MINMOD    1
+#define ADJ_LIM_MC        2
+#define ADJ_LIM_SUPERBEE  3
+
+/* step-kernel variants */
+#define ADJ_VARIANT_EXACT 0   /* reference expression order, no FMA: bitwise parity */
+#define ADJ_VARIANT_FAST  1   /* register-marching strip kernel, <=1e-12 norm-relative */
+
+/* patch-edge bits of AdjPatch.edges (which sides meet the physical domain) */
+#define ADJ_EDGE_XLO 1
+#define ADJ_EDGE_XHI 2
+#define ADJ_EDGE_YLO 4
+#define ADJ_EDGE_YHI 8
+
+/* boundary kinds per side (solver.BoundarySpec, solver.py:35-56) */
+#define ADJ_BC_WALL    0
+#define ADJ_BC_OUTFLOW 1
+
+/* One patch of a level store (device-resident table). */
+typedef struct AdjPatch {
+    int64_t offset;      /* element offset of ghost-corner cell (0,0) in every plane */
+    int64_t flag_word;   /* first uint32 word of this patch's flag bits (K3)          */
+    int32_t nx, ny;      /* interior extents (ny = 1 in 1D)                            */
+    int32_t pitch;       /* elements between consecutive x rows                        */
+    int32_t lo_x, lo_y;  /* global index of the interior lower corner                  */
+    int32_t edges;       /* ADJ_EDGE_* bits                                            */
+    int32_t pad0, pad1;
+} AdjPatch;
+
+/* One unit of step work: an interior box [i0,i0+ni) x [j0,j0+nj) of a patch. */
+typedef struct AdjTile {
+    int32_t patch, i0, j0, ni, nj, pad;
+} AdjTile;
+
+/* K1: wave-propagation step of every patch of a level.
+ * Replaces step_patch / step_patch_1d / step_patch_2d (solver.py:415-522), the
+ * Riemann and transverse solvers (equations.py:98-349), TimeReversed
+ * (equations.py:496-534) and the limiter (solver.py:65-77, 317-348).
+ * Reads q_in (ghosts filled), writes the interior of q_out (ping-pong buffers
+ * replace Patch.save_old, geometry.py:123).  Outputs per patch: the maximum
+ * |speed| over the reference's CFL interface ranges, x and y separately
+ * (solver.py:425, 457-460), and a non-finite flag (solver.py:437, 510). */
+typedef struct AdjStepArgs {
+    const double* q_in;
+    double* q_out;
+    const double* aux;
+    const AdjPatch* patches;   /* device */
+    const AdjTile* tiles;      /* device */
+    double* speed_max;         /* device, 2*npatch (x, y), zeroed by the call */
+    int32_t* nonfinite;        /* device, npatch, zeroed by the call          */
+    int64_t comp_stride, aux_stride;
+    int32_t npatch, ntile;
+    int32_t ndim, ghost;
+    int32_t system, form, reversed, limiter, variant, pad;
+    double dt, dtdx, dtdy, gravity;
+    void* stream;              /* cudaStream_t */
+} AdjStepArgs;
+int adj_step_level(const AdjStepArgs* a);
+
+/* Tile shape (ni, nj) the given variant expects in AdjStepArgs.tiles. */
+int adj_step_tile_shape(int variant, int ndim, int32_t* ni, int32_t* nj);
+
+/* K2 (physical phase): wall / outflow ghost fill of every patch edge that
+ * meets the domain boundary.  Replaces fill_ghost_physical (solver.py:125-146)
+ * with its x-then-y, low-then-high slab order folded into one gather. */
+typedef struct AdjPhysArgs {
+    double* q;
+    const AdjPatch* patches;   /* device */
+    int64_t comp_stride;
+    int32_t npatch, ndim, ghost, m;
+    int32_t bc[4];             /* left, right, bottom, top: ADJ_BC_*          */
+    int32_t normal_comp[2];    /* component negated at a wall, per axis      */
+    int32_t max_ghost_cells;   /* max ghost cells of any patch (grid sizing) */
+    int32_t pad;
+    void* stream;
+} AdjPhysArgs;
+int adj_fill_physical(const AdjPhysArgs* a);
+
+/* K2 (in-domain phase): same-level copies and coarse-to-fine space-time
+ * interpolation over rectangles of ghost cells.  Replaces
+ * fill_ghost_from_coarse + space_time_interp (solver.py:227-286),
+ * interpolate_patch (geometry.py:302-327) and fill_ghost_same_level
+ * (solver.py:208-224); rectangles are built on the host once per regrid.
+ * Also used for regrid data movement (amr.py:504-551, kind 2/3). */
+#define ADJ_RECT_COPY        0   /* dst cells <- src patch cells (same level)          */
+#define ADJ_RECT_COARSE      1   /* dst cells <- bilinear/linear-in-time coarse interp */
+typedef struct AdjRect {
+    int32_t kind;
+    int32_t dst_patch, src_patch;
+    int32_t di0, dj0;     /* dst start, ghost-inclusive local coords           */
+    int32_t ni, nj;       /* extent                                            */
+    int32_t si0, sj0;     /* src start (COPY), ghost-inclusive local coords    */
+    int32_t pad;
+} AdjRect;
+typedef struct AdjGhostArgs {
+    double* q_dst;               /* fine (or same) level store                   */
+    const double* q_src;         /* COPY source: same level store (may == q_dst) */
+    const double* q_coarse_old;  /* COARSE: coarse level state at t0             */
+    const double* q_coarse_new;  /* COARSE: coarse level state at t1             */
+    const AdjPatch* dst_patches; /* device */
+    const AdjPatch* src_patches; /* device (COPY: same level; COARSE: coarse)   */
+    const AdjRect* rects;        /* device */
+    int64_t dst_comp_stride, src_comp_stride;
+    int32_t nrect, ndim, m, ghost_dst, ghost_src, ratio;
+    double origin_x, origin_y;   /* hierarchy.origin                              */
+    double dx_f, dy_f;           /* fine widths                                   */
+    double dx_c, dy_c;           /* coarse widths                                 */
+    double w_time;               /* clip((t-t0)/(t1-t0),0,1)                      */
+    int32_t time_mode;           /* 0: old only, 1: blend old/new, 2: new only    */
+    int32_t max_rect_cells;
+    void* stream;
+} AdjGhostArgs;
+int adj_fill_ghost_rects(const AdjGhostArgs* a);
+
+/* K4: conservative fine-to-coarse averaging.  Replaces
+ * restrict_fine_to_coarse (amr.py:399-450); one AdjRect per (coarse patch,
+ * fine patch) overlap, in COARSE interior-local coordinates (di0,dj0 coarse,
+ * si0,sj0 the matching fine interior-local start). */
+typedef struct AdjRestrictArgs {
+    double* q_coarse;
+    const double* q_fine;
+    const double* aux_coarse;    /* swe: depth plane 1 -> wet mask            */
+    const double* aux_fine;
+    const AdjPatch* coarse_patches;
+    const AdjPatch* fine_patches;
+    const AdjRect* rects;
+    int64_t coarse_comp_stride, fine_comp_stride;
+    int64_t coarse_aux_stride, fine_aux_stride;
+    int32_t nrect, ndim, m, ratio, swe, max_rect_cells;
+    int32_t ghost_coarse, ghost_fine;
+    void* stream;
+} AdjRestrictArgs;
+int adj_restrict(const AdjRestrictArgs* a);
+
+/* K3: adjoint inner-product flagging.  Replaces inner_product_field /
+ * inner_product_flags / AdjointFlagging.evaluate (adjoint.py:227-277),
+ * interpolate_uniform (geometry.py:248-290) and _adjoint_dry_at
+ * (adjoint.py:217-224).  The snapshot ring holds nsnap fields of shape
+ * (m, nxa, nya) contiguous; snap_index lists the window's snapshots
+ * (query_window_times, adjoint.py:192-214, evaluated on the host).
+ * mode 0: reference windowed max over the listed snapshots.
+ * mode 1: linear-in-time interpolation (AdjointSnapshotStore.interpolate_time,
+ *         adjoint.py:98-110) at each entry of interp_times, blended from
+ *         snapshots interp_k[n] and interp_k[n]+1 with weight interp_w[n]
+ *         (interp_k < 0: use snapshot -interp_k-1 unblended). */
+typedef struct AdjFlagArgs {
+    const double* q;             /* forward level store                        */
+    const double* aux;           /* forward aux (swe: depth plane 1)          */
+    const AdjPatch* patches;     /* device */
+    const double* ring;          /* device, nsnap*m*nxa*nya                    */
+    const uint8_t* adj_wet;      /* device nxa*nya, or NULL                    */
+    const int32_t* snap_index;   /* device, nidx (mode 0) / interp_k (mode 1) */
+    const double* interp_w;      /* device, nidx (mode 1)                      */
+    uint32_t* flag_bits;         /* device, bit-packed per patch (flag_word)   */
+    unsigned long long* counts;  /* device, npatch raw flagged counts          */
+    double* best;                /* device, per-interior-cell values or NULL  */
+    const int64_t* best_offset;  /* device, per patch start into best, or NULL */
+    int32_t* status;             /* device, 1 int: ADJ_ERR_OUT_OF_RANGE bits  */
+    int64_t comp_stride, aux_stride;
+    int32_t npatch, ndim, m, ghost, swe, mode, nidx, nxa, nya, max_cells;
+    double origin_x, origin_y, dx, dy;             /* forward level geometry   */
+    double a_origin_x, a_origin_y, a_dx, a_dy;     /* adjoint grid geometry    */
+    double tolerance;
+    void* stream;
+} AdjFlagArgs;
+int adj_flag_adjoint(const AdjFlagArgs* a);
+
+/* Last CUDA error string of the calling thread (diagnostics). */
+const char* adj_last_error(void);
+int adj_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADJAMR_B200_H */

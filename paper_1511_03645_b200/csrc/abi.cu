@@ -1,0 +1,101 @@
+// extern "C" entry points of libadjamr_b200.so (declared in include/adjamr_b200.h).
+#include "adj_common.cuh"
+#include <stdio.h>
+#include <string.h>
+
+namespace adj {
+
+static thread_local char g_err[512] = "";
+
+int record_cuda(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return ADJ_OK;
+    snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return ADJ_ERR_CUDA;
+}
+
+int check_launch(const char* where) { return record_cuda(cudaGetLastError(), where); }
+
+int step_exact(const AdjStepArgs& a, cudaStream_t st);
+int step_fast(const AdjStepArgs& a, cudaStream_t st);
+void fast_tile_shape(int ndim, int32_t* ni, int32_t* nj);
+int fill_physical(const AdjPhysArgs& a);
+int fill_ghost_rects(const AdjGhostArgs& a);
+int restrict_level(const AdjRestrictArgs& a);
+int flag_adjoint(const AdjFlagArgs& a);
+
+static int bad(const char* msg) {
+    snprintf(g_err, sizeof(g_err), "bad argument: %s", msg);
+    return ADJ_ERR_BAD_ARG;
+}
+
+}  // namespace adj
+
+extern "C" {
+
+int adj_abi_version(void) { return ADJ_ABI_VERSION; }
+
+const char* adj_last_error(void) { return adj::g_err; }
+
+int adj_step_tile_shape(int variant, int ndim, int32_t* ni, int32_t* nj) {
+    if (!ni || !nj) return adj::bad("null tile-shape outputs");
+    if (variant == ADJ_VARIANT_EXACT) {
+        if (ndim == 2) { *ni = 16; *nj = 16; } else { *ni = 256; *nj = 1; }
+        return ADJ_OK;
+    }
+    if (variant == ADJ_VARIANT_FAST) { adj::fast_tile_shape(ndim, ni, nj); return ADJ_OK; }
+    return adj::bad("unknown variant");
+}
+
+int adj_step_level(const AdjStepArgs* a) {
+    if (!a) return adj::bad("null args");
+    if (a->q_in == a->q_out) return adj::bad("q_in must not alias q_out");
+    if (!a->q_in || !a->q_out || !a->aux || !a->patches || !a->tiles || !a->speed_max || !a->nonfinite)
+        return adj::bad("null pointer");
+    if (a->ghost < 2) return adj::bad("ghost width must be >= 2");
+    if (a->ndim == 1 && a->system != ADJ_SYS_AC1D) return adj::bad("1D requires acoustics-1d");
+    if (a->ndim == 2 && a->system == ADJ_SYS_AC1D) return adj::bad("2D requires a 2D system");
+    if (a->limiter < ADJ_LIM_NONE || a->limiter > ADJ_LIM_SUPERBEE) return adj::bad("limiter");
+    if (!(a->dt > 0.0)) return adj::bad("dt must be positive");
+    cudaStream_t st = (cudaStream_t)a->stream;
+    int rc = adj::record_cuda(cudaMemsetAsync(a->speed_max, 0, sizeof(double) * 2 * a->npatch, st), "memset speed_max");
+    if (rc) return rc;
+    rc = adj::record_cuda(cudaMemsetAsync(a->nonfinite, 0, sizeof(int32_t) * a->npatch, st), "memset nonfinite");
+    if (rc) return rc;
+    if (a->variant == ADJ_VARIANT_EXACT) return adj::step_exact(*a, st);
+    if (a->variant == ADJ_VARIANT_FAST) return adj::step_fast(*a, st);
+    return adj::bad("unknown variant");
+}
+
+int adj_fill_physical(const AdjPhysArgs* a) {
+    if (!a || !a->q || !a->patches) return adj::bad("null pointer");
+    if (a->ghost < 2) return adj::bad("ghost width must be >= 2");
+    return adj::fill_physical(*a);
+}
+
+int adj_fill_ghost_rects(const AdjGhostArgs* a) {
+    if (!a || !a->q_dst || !a->rects || !a->dst_patches || !a->src_patches) return adj::bad("null pointer");
+    if (a->time_mode < 0 || a->time_mode > 2) return adj::bad("time_mode");
+    return adj::fill_ghost_rects(*a);
+}
+
+int adj_restrict(const AdjRestrictArgs* a) {
+    if (!a || !a->q_coarse || !a->q_fine || !a->rects) return adj::bad("null pointer");
+    if (a->ratio < 1) return adj::bad("ratio");
+    if (a->swe && (!a->aux_coarse || !a->aux_fine)) return adj::bad("swe restriction needs aux");
+    return adj::restrict_level(*a);
+}
+
+int adj_flag_adjoint(const AdjFlagArgs* a) {
+    if (!a || !a->q || !a->patches || !a->ring || !a->snap_index || !a->flag_bits || !a->counts || !a->status)
+        return adj::bad("null pointer");
+    if (a->mode == 1 && !a->interp_w) return adj::bad("mode 1 needs interp_w");
+    if (a->best && !a->best_offset) return adj::bad("best needs best_offset");
+    cudaStream_t st = (cudaStream_t)a->stream;
+    int rc = adj::record_cuda(cudaMemsetAsync(a->counts, 0, sizeof(unsigned long long) * a->npatch, st), "memset counts");
+    if (rc) return rc;
+    rc = adj::record_cuda(cudaMemsetAsync(a->status, 0, sizeof(int32_t), st), "memset status");
+    if (rc) return rc;
+    return adj::flag_adjoint(*a);
+}
+
+}  // extern "C"

@@ -1,0 +1,235 @@
+// K2 ghost fill and K4 restriction.  Compiled with -fmad=false: every value
+// is produced with the reference's operation order, so results are bitwise
+// identical to the numpy reference.
+//
+//   fill_ghost_physical + _mirror/_extrapolate  solver.py:84-146
+//   fill_ghost_same_level                       solver.py:208-224
+//   fill_ghost_from_coarse / space_time_interp  solver.py:227-286
+//   interpolate_patch / _axis_weights           geometry.py:248-260, 302-327
+//   restrict_fine_to_coarse                     amr.py:399-450
+#include "adj_common.cuh"
+
+namespace adj {
+
+// ---------------------------------------------------------------------------
+// Physical boundaries.  The reference fills whole slabs x-low, x-high, y-low,
+// y-high in that order; because every slab source row is interior, the final
+// value of any out-of-domain ghost cell is the composition
+//   q[c](ii,jj) = sy_c * sx_c * q_pre[c](src_x(ii), src_y(jj))
+// which one gather computes without a second pass.
+ADJ_D int phys_src(int ii, int n, int g, bool lo_edge, bool hi_edge, int bc_lo, int bc_hi,
+                   bool* neg, bool* hit) {
+    *neg = false; *hit = false;
+    if (ii < g && lo_edge) {
+        *hit = true;
+        if (bc_lo == ADJ_BC_WALL) { *neg = true; return 2 * g - 1 - ii; }
+        return g;
+    }
+    if (ii >= n - g && hi_edge) {
+        *hit = true;
+        if (bc_hi == ADJ_BC_WALL) { *neg = true; return 2 * n - 2 * g - 1 - ii; }
+        return n - g - 1;
+    }
+    return ii;
+}
+
+__global__ void k2_physical(AdjPhysArgs a) {
+    const AdjPatch p = a.patches[blockIdx.y];
+    const int g = a.ghost;
+    const int NX = p.nx + 2 * g;
+    const int gy = a.ndim == 2 ? g : 0;
+    const int NY = p.ny + 2 * gy;
+    const int64_t ring = (int64_t)NX * NY - (int64_t)p.nx * p.ny;
+    const bool xlo = p.edges & ADJ_EDGE_XLO, xhi = p.edges & ADJ_EDGE_XHI;
+    const bool ylo = a.ndim == 2 && (p.edges & ADJ_EDGE_YLO), yhi = a.ndim == 2 && (p.edges & ADJ_EDGE_YHI);
+    if (!(xlo || xhi || ylo || yhi)) return;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < ring;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int ii, jj;
+        const int64_t band = (int64_t)g * NY;
+        if (r < band) { ii = (int)(r / NY); jj = (int)(r % NY); }
+        else if (r < 2 * band) { int64_t s = r - band; ii = NX - g + (int)(s / NY); jj = (int)(s % NY); }
+        else {
+            int64_t s = r - 2 * band;             // middle rows, 2*gy cells each
+            ii = g + (int)(s / (2 * gy));
+            int k = (int)(s % (2 * gy));
+            jj = k < gy ? k : NY - 2 * gy + k;
+        }
+        bool nx_, hx, ny_, hy;
+        int sx = phys_src(ii, NX, g, xlo, xhi, a.bc[0], a.bc[1], &nx_, &hx);
+        int sy = jj;
+        ny_ = false; hy = false;
+        if (a.ndim == 2) sy = phys_src(jj, NY, g, ylo, yhi, a.bc[2], a.bc[3], &ny_, &hy);
+        if (!hx && !hy) continue;
+        const int64_t dst = p.offset + (int64_t)ii * p.pitch + jj;
+        const int64_t src = p.offset + (int64_t)sx * p.pitch + sy;
+        for (int c = 0; c < a.m; ++c) {
+            double v = a.q[c * a.comp_stride + src];
+            if (nx_ && c == a.normal_comp[0]) v = v * -1.0;
+            if (ny_ && c == a.normal_comp[1]) v = v * -1.0;
+            a.q[c * a.comp_stride + dst] = v;
+        }
+    }
+}
+
+int fill_physical(const AdjPhysArgs& a) {
+    if (a.npatch <= 0 || a.max_ghost_cells <= 0) return ADJ_OK;
+    int blocks = (a.max_ghost_cells + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    k2_physical<<<dim3(blocks, a.npatch), 256, 0, (cudaStream_t)a.stream>>>(a);
+    return check_launch("k2_physical");
+}
+
+// ---------------------------------------------------------------------------
+// Same-level copies and coarse-to-fine space-time interpolation.
+
+// _axis_weights (geometry.py:248-260) for one coordinate.
+ADJ_D void axis_weights(double coord, double origin, double width, int n, int* i0, double* w) {
+    double s = (coord - origin) / width - 0.5;
+    double fl = floor(s);
+    int k = (int)fl;
+    double ww = s - fl;
+    if (k < 0) ww = 0.0;
+    else if (k > n - 2) ww = 1.0;
+    int hi = n - 2 > 0 ? n - 2 : 0;
+    k = k < 0 ? 0 : (k > hi ? hi : k);
+    if (n == 1) ww = 0.0;
+    *i0 = k;
+    *w = ww;
+}
+
+// interpolate_patch (geometry.py:302-327) for one point and component.
+ADJ_D double interp_patch2(const double* d, int pitch, int i0, int j0, int i1, int j1, double wx, double wy) {
+    double v00 = d[(int64_t)i0 * pitch + j0], v10 = d[(int64_t)i1 * pitch + j0];
+    double v01 = d[(int64_t)i0 * pitch + j1], v11 = d[(int64_t)i1 * pitch + j1];
+    return v00 * (1.0 - wx) * (1.0 - wy) + v10 * wx * (1.0 - wy) + v01 * (1.0 - wx) * wy + v11 * wx * wy;
+}
+
+__global__ void k2_rects(AdjGhostArgs a) {
+    const AdjRect R = a.rects[blockIdx.x];
+    const AdjPatch dp = a.dst_patches[R.dst_patch];
+    const AdjPatch sp = a.src_patches[R.src_patch];
+    const int64_t n = (int64_t)R.ni * R.nj;
+    for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+        const int di = (int)(t / R.nj), dj = (int)(t % R.nj);
+        const int ii = R.di0 + di, jj = R.dj0 + dj;
+        const int64_t dst = dp.offset + (int64_t)ii * dp.pitch + jj;
+        if (R.kind == ADJ_RECT_COPY) {
+            const int64_t src = sp.offset + (int64_t)(R.si0 + di) * sp.pitch + (R.sj0 + dj);
+            for (int c = 0; c < a.m; ++c)
+                a.q_dst[c * a.dst_comp_stride + dst] = a.q_src[c * a.src_comp_stride + src];
+            continue;
+        }
+        // COARSE: fine cell centre -> bilinear weights on the coarse patch incl. ghosts
+        const int gf = a.ghost_dst, gc = a.ghost_src;
+        const int gxi = dp.lo_x - gf + ii;
+        const double x = a.origin_x + (gxi + 0.5) * a.dx_f;
+        const double lox = a.origin_x + (sp.lo_x - gc) * a.dx_c;
+        const int ncx = sp.nx + 2 * gc;
+        int i0; double wx;
+        axis_weights(x, lox, a.dx_c, ncx, &i0, &wx);
+        const int i1 = min(i0 + 1, ncx - 1);
+        int j0 = 0, j1 = 0; double wy = 0.0;
+        if (a.ndim == 2) {
+            const int gyi = dp.lo_y - gf + jj;
+            const double y = a.origin_y + (gyi + 0.5) * a.dy_f;
+            const double loy = a.origin_y + (sp.lo_y - gc) * a.dy_c;
+            const int ncy = sp.ny + 2 * gc;
+            axis_weights(y, loy, a.dy_c, ncy, &j0, &wy);
+            j1 = min(j0 + 1, ncy - 1);
+        }
+        for (int c = 0; c < a.m; ++c) {
+            double vo = 0.0, vn = 0.0;
+            const double* po = a.q_coarse_old + c * a.src_comp_stride + sp.offset;
+            const double* pn = a.q_coarse_new + c * a.src_comp_stride + sp.offset;
+            if (a.ndim == 2) {
+                if (a.time_mode != 2) vo = interp_patch2(po, sp.pitch, i0, j0, i1, j1, wx, wy);
+                if (a.time_mode != 0) vn = interp_patch2(pn, sp.pitch, i0, j0, i1, j1, wx, wy);
+            } else {
+                if (a.time_mode != 2) vo = po[i0] * (1.0 - wx) + po[i1] * wx;
+                if (a.time_mode != 0) vn = pn[i0] * (1.0 - wx) + pn[i1] * wx;
+            }
+            double v;
+            if (a.time_mode == 0) v = vo;
+            else if (a.time_mode == 2) v = vn;
+            else v = (1.0 - a.w_time) * vo + a.w_time * vn;
+            a.q_dst[c * a.dst_comp_stride + dst] = v;
+        }
+    }
+}
+
+int fill_ghost_rects(const AdjGhostArgs& a) {
+    if (a.nrect <= 0) return ADJ_OK;
+    int threads = a.max_rect_cells >= 256 ? 256 : (a.max_rect_cells >= 128 ? 128 : 64);
+    k2_rects<<<a.nrect, threads, 0, (cudaStream_t)a.stream>>>(a);
+    return check_launch("k2_rects");
+}
+
+// ---------------------------------------------------------------------------
+// K4 restriction.  numpy's mean over the (r, r) child block sums each child
+// row sequentially, adds the row sums in order, then divides by r*r
+// (verified bitwise for r = 2, 4); the SWE variant weights by the wet mask.
+__global__ void k4_restrict(AdjRestrictArgs a) {
+    const AdjRect R = a.rects[blockIdx.x];
+    const AdjPatch cp = a.coarse_patches[R.dst_patch];
+    const AdjPatch fp = a.fine_patches[R.src_patch];
+    const int r = a.ratio;
+    const int64_t n = (int64_t)R.ni * R.nj;
+    const int gC = a.ghost_coarse, gF = a.ghost_fine;   // rect coords are interior-local
+    for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+        const int di = (int)(t / R.nj), dj = (int)(t % R.nj);
+        const int ci = gC + R.di0 + di;
+        const int cj = (a.ndim == 2 ? gC : 0) + R.dj0 + dj;
+        const int fi0 = gF + R.si0 + di * r;
+        const int fj0 = (a.ndim == 2 ? gF : 0) + R.sj0 + dj * r;
+        const int64_t cdst = cp.offset + (int64_t)ci * cp.pitch + cj;
+        const int rj = a.ndim == 2 ? r : 1;
+        if (!a.swe) {
+            const double cnt = (double)(r * rj);
+            for (int c = 0; c < a.m; ++c) {
+                const double* f = a.q_fine + c * a.fine_comp_stride + fp.offset;
+                double tot = 0.0;
+                for (int p = 0; p < r; ++p) {
+                    double s = 0.0;
+                    for (int q = 0; q < rj; ++q) {
+                        double v = f[(int64_t)(fi0 + p) * fp.pitch + fj0 + q];
+                        s = q == 0 ? v : s + v;
+                    }
+                    tot = p == 0 ? s : tot + s;
+                }
+                a.q_coarse[c * a.coarse_comp_stride + cdst] = tot / cnt;
+            }
+        } else {
+            const double* fd = a.aux_fine + a.fine_aux_stride + fp.offset;   // depth plane
+            double ws = 0.0;
+            for (int p = 0; p < r; ++p)
+                for (int q = 0; q < rj; ++q)
+                    ws = ws + (fd[(int64_t)(fi0 + p) * fp.pitch + fj0 + q] > 0.0 ? 1.0 : 0.0);
+            const bool wetc = a.aux_coarse[a.coarse_aux_stride + cp.offset + (int64_t)ci * cp.pitch + cj] > 0.0;
+            if (!(ws > 0.0 && wetc)) continue;
+            for (int c = 0; c < a.m; ++c) {
+                const double* f = a.q_fine + c * a.fine_comp_stride + fp.offset;
+                double tot = 0.0;
+                for (int p = 0; p < r; ++p) {
+                    double s = 0.0;
+                    for (int q = 0; q < rj; ++q) {
+                        int64_t o = (int64_t)(fi0 + p) * fp.pitch + fj0 + q;
+                        double v = f[o] * (fd[o] > 0.0 ? 1.0 : 0.0);
+                        s = q == 0 ? v : s + v;
+                    }
+                    tot = p == 0 ? s : tot + s;
+                }
+                a.q_coarse[c * a.coarse_comp_stride + cdst] = tot / ws;
+            }
+        }
+    }
+}
+
+int restrict_level(const AdjRestrictArgs& a) {
+    if (a.nrect <= 0) return ADJ_OK;
+    int threads = a.max_rect_cells >= 256 ? 256 : (a.max_rect_cells >= 128 ? 128 : 64);
+    k4_restrict<<<a.nrect, threads, 0, (cudaStream_t)a.stream>>>(a);
+    return check_launch("k4_restrict");
+}
+
+}  // namespace adj

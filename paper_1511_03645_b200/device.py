@@ -1,0 +1,520 @@
+"""Per-level patch store in HBM and the launch wrappers of the C ABI.
+
+Layout (include/adjamr_b200.h): every patch of a level occupies a
+ghost-inclusive box of (nx+2g) rows by ``pitch`` elements (y contiguous,
+pitch padded to a multiple of 4 so rows are 32 B aligned) inside one flat
+plane; the m state components and the aux materials are separate planes
+(structure of arrays).  Three state buffers rotate:
+
+  cur        the current state,
+  old        the state saved by save_old (reference ``Patch.state_old``),
+  ghost_src  the buffer holding the current ghost values (after a step the
+             new interior is in ``cur`` while the ghosts the reference would
+             still hold are in the pre-step buffer; they are folded back with
+             a ring copy before anything reads ``cur``'s ghosts).
+
+A step reads ``cur`` and writes a free buffer, which replaces the reference's
+``save_old`` full copy (geometry.py:123) and makes "raise before mutate" on a
+CFL violation (solver.py:461) free: the new buffer is simply discarded.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+_SLACK = 64   # elements of slack after each plane set (strip loads may over-read)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev_table(arr: np.ndarray):
+    """Upload a numpy structured table to the device as raw bytes."""
+    torch = _torch()
+    raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+    if raw.size == 0:
+        raw = np.zeros(8, np.uint8)
+    return torch.from_numpy(raw.copy()).to("cuda", non_blocking=False)
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+class LevelStore:
+    """All patches of one refinement level, resident in HBM."""
+
+    NBUF = 3
+
+    def __init__(self, patches):
+        if not patches:
+            raise ValueError("LevelStore needs at least one patch")
+        torch = _torch()
+        _lib.lib()   # fail loudly without the CUDA path
+        self.patches = list(patches)
+        if patches[0].aux is None:
+            raise ValueError("patch has no material (call sample_patch_material first)")
+        self.swe = hasattr(patches[0].aux, "wet")
+        specs = [p.spec for p in patches]
+        self.ndim = specs[0].ndim
+        self.g = specs[0].ghost_width
+        if any(s.ghost_width != self.g or s.ndim != self.ndim for s in specs):
+            raise ValueError("patches of one store must share ghost width and dimension")
+        self.m = patches[0].num_components
+        self.naux = len(patches[0].aux.planes())
+        tab = np.zeros(len(specs), dtype=_lib.PATCH_DTYPE)
+        off = 0
+        fw = 0
+        self.boxes = []
+        for k, s in enumerate(specs):
+            nx = s.shape[0]
+            ny = s.shape[1] if self.ndim == 2 else 1
+            NX = nx + 2 * self.g
+            NY = ny + 2 * self.g if self.ndim == 2 else 1
+            pitch = (NY + 3) // 4 * 4 if self.ndim == 2 else 1
+            tab[k] = (off, fw, nx, ny, pitch, s.lo[0], s.lo[1] if self.ndim == 2 else 0, 0, 0, 0)
+            self.boxes.append((off, NX, NY, pitch))
+            off += (NX * pitch + 31) // 32 * 32
+            fw += (nx * ny + 31) // 32
+        self.plane = off + _SLACK
+        self.flag_words = fw
+        self.table_np = tab
+        self.table = _dev_table(tab)
+        self._edges_key = None
+        self.buf = [torch.zeros(self.m * self.plane, dtype=torch.float64, device="cuda"), None, None]
+        self.aux = torch.zeros(self.naux * self.plane, dtype=torch.float64, device="cuda")
+        self.cur = 0
+        self.old = None
+        self.old_valid = np.zeros(len(specs), dtype=bool)
+        self.ghost_src = 0
+        self._tiles = {}
+        self._scratch = {}
+        for k, p in enumerate(patches):
+            self._attach(p, k)
+
+    # ------------------------------------------------------------------ views
+    def _view(self, t, slot, comps):
+        off, NX, NY, pitch = self.boxes[slot]
+        v = t.as_strided((comps, NX, NY), (self.plane, pitch, 1), off)
+        return v if self.ndim == 2 else v[:, :, 0]
+
+    def view(self, slot, which="cur"):
+        idx = {"cur": self.cur, "old": self.old, "ghost": self.ghost_src}[which]
+        return self._view(self.buf[idx], slot, self.m)
+
+    def aux_view(self, slot):
+        return self._view(self.aux, slot, self.naux)
+
+    def _attach(self, patch, slot):
+        if patch.aux is None:
+            raise ValueError("patch has no material (call sample_patch_material first)")
+        planes = patch.aux.planes()
+        av = self.aux_view(slot)
+        for k, pl in enumerate(planes):
+            av[k].copy_(_torch().from_numpy(np.ascontiguousarray(pl, dtype=float)))
+        patch._store = self
+        patch._slot = slot
+        patch._loc = "host"     # uploaded by sync_in
+        if patch._host_old is not None:
+            self.old_valid[slot] = False
+
+    # ------------------------------------------------------------ buffers
+    def _ensure_buf(self, i):
+        if self.buf[i] is None:
+            torch = _torch()
+            self.buf[i] = torch.zeros(self.m * self.plane, dtype=torch.float64, device="cuda")
+        return self.buf[i]
+
+    def _free(self, *busy):
+        for i in range(self.NBUF):
+            if i not in busy:
+                self._ensure_buf(i)
+                return i
+        raise RuntimeError("no free state buffer")
+
+    def _unalias(self):
+        """Make cur writable without touching the saved old buffer."""
+        if self.old is not None and self.old == self.cur:
+            nb = self._free(self.cur, self.ghost_src)
+            self.buf[nb].copy_(self.buf[self.cur])
+            if self.ghost_src == self.cur:
+                self.ghost_src = nb
+            self.cur = nb
+
+    def fold_ghosts(self, stream=None):
+        """Copy the current ghost ring into cur (see module docstring)."""
+        if self.ghost_src == self.cur:
+            return
+        self._unalias()
+        if self.ghost_src != self.cur:
+            ring_copy(self, self.buf[self.ghost_src], self.buf[self.cur], stream)
+        self.ghost_src = self.cur
+
+    def prepare_write(self, full_ghosts: bool = False, stream=None):
+        """Before an in-place write to cur: unalias, and fold the ghosts unless
+        the write rewrites every ghost cell."""
+        self._unalias()
+        if full_ghosts:
+            self.ghost_src = self.cur
+        else:
+            self.fold_ghosts(stream)
+
+    # ----------------------------------------------------------- coherence
+    def sync_in(self, stream=None):
+        """Upload every patch whose authoritative state is on the host."""
+        pending = [p for p in self.patches if p._store is self and p._loc == "host"]
+        if not pending:
+            return
+        self.prepare_write(stream=stream)
+        torch = _torch()
+        for p in pending:
+            v = self.view(p._slot)
+            v.copy_(torch.from_numpy(p._host), non_blocking=False)
+            p._loc = "device"
+
+    def download(self, slot, out: np.ndarray):
+        torch = _torch()
+        v = self.view(slot)
+        if self.ghost_src != self.cur:
+            full = self.view(slot, "ghost").clone()
+            g = self.g
+            if self.ndim == 2:
+                full[:, g:-g, g:-g] = v[:, g:-g, g:-g]
+            else:
+                full[:, g:-g] = v[:, g:-g]
+            v = full
+        out[...] = v.cpu().numpy()
+        del torch
+
+    def has_old(self, slot) -> bool:
+        return self.old is not None and bool(self.old_valid[slot])
+
+    def download_old(self, slot, out: np.ndarray):
+        out[...] = self.view(slot, "old").cpu().numpy()
+
+    def drop_old(self, slot):
+        self.old_valid[slot] = False
+
+    def save_old(self, slot):
+        """Per-patch save_old: copy the patch box into the old buffer."""
+        self.sync_in()
+        if self.old is None:
+            self.old = self._free(self.cur, self.ghost_src)
+            self.old_valid[:] = False
+        if self.old != self.cur:
+            self.fold_ghosts()
+            self.view(slot, "old").copy_(self.view(slot))
+        self.old_valid[slot] = True
+
+    def save_old_all(self):
+        """save_old for every patch of the level: alias, no copy."""
+        self.sync_in()
+        self.fold_ghosts()
+        self.old = self.cur
+        self.old_valid[:] = True
+
+    # ------------------------------------------------------------- tables
+    def edges_table(self, level_shape):
+        key = tuple(level_shape)
+        if self._edges_key != key:
+            tab = self.table_np.copy()
+            for k, p in enumerate(self.patches):
+                s = p.spec
+                e = 0
+                if s.lo[0] == 0:
+                    e |= _lib.EDGE_XLO
+                if s.hi[0] == level_shape[0] - 1:
+                    e |= _lib.EDGE_XHI
+                if self.ndim == 2:
+                    if s.lo[1] == 0:
+                        e |= _lib.EDGE_YLO
+                    if s.hi[1] == level_shape[1] - 1:
+                        e |= _lib.EDGE_YHI
+                tab["edges"][k] = e
+            self.table_np = tab
+            self.table = _dev_table(tab)
+            self._edges_key = key
+        return self.table
+
+    def all_edges_physical(self, level_shape) -> bool:
+        full = 15 if self.ndim == 2 else 3
+        self.edges_table(level_shape)
+        return bool(np.all(self.table_np["edges"] == full))
+
+    def tiles(self, variant):
+        if variant not in self._tiles:
+            ni_t = _lib.C.c_int32()
+            nj_t = _lib.C.c_int32()
+            _lib.check(_lib.lib().adj_step_tile_shape(variant, self.ndim, _lib.C.byref(ni_t), _lib.C.byref(nj_t)),
+                       "adj_step_tile_shape")
+            ti, tj = ni_t.value, nj_t.value
+            rows = []
+            for k, p in enumerate(self.patches):
+                nx = p.spec.shape[0]
+                ny = p.spec.shape[1] if self.ndim == 2 else 1
+                for j0 in range(0, ny, tj):
+                    for i0 in range(0, nx, ti):
+                        rows.append((k, i0, j0, min(ti, nx - i0), min(tj, ny - j0), 0))
+            if variant == _lib.VARIANT_FAST and self.ndim == 2:
+                # order: x-segment major, then strips, so concurrently running
+                # warps are y-neighbours and share halo rows through L2
+                rows.sort(key=lambda r: (r[0], r[1], r[2]))
+            arr = np.array(rows, dtype=_lib.TILE_DTYPE)
+            self._tiles[variant] = (_dev_table(arr), len(rows))
+        return self._tiles[variant]
+
+    def scratch(self, name, n, dtype):
+        torch = _torch()
+        t = self._scratch.get(name)
+        if t is None or t.numel() < n or t.dtype != dtype:
+            t = torch.zeros(max(n, 1), dtype=dtype, device="cuda")
+            self._scratch[name] = t
+        return t
+
+    def any_dry(self) -> bool:
+        if not self.swe:
+            return False
+        return any(bool(np.any(~p.aux.wet)) for p in self.patches)
+
+
+# ---------------------------------------------------------------------------
+# launch wrappers
+
+
+def ring_copy(store: LevelStore, src, dst, stream=None):
+    """Copy every patch's ghost ring from buffer src to buffer dst."""
+    rects = []
+    g = store.g
+    for k, (off, NX, NY, pitch) in enumerate(store.boxes):
+        if store.ndim == 2:
+            parts = [(0, 0, g, NY), (NX - g, 0, g, NY), (g, 0, NX - 2 * g, g), (g, NY - g, NX - 2 * g, g)]
+        else:
+            parts = [(0, 0, g, 1), (NX - g, 0, g, 1)]
+        for (i0, j0, ni, nj) in parts:
+            rects.append((_lib.RECT_COPY, k, k, i0, j0, ni, nj, i0, j0, 0))
+    arr = np.array(rects, dtype=_lib.RECT_DTYPE)
+    copy_rects(store, store, arr, src, dst, stream)
+
+
+def copy_rects(dst_store, src_store, rects_np, src_buf, dst_buf, stream=None):
+    if len(rects_np) == 0:
+        return
+    rects = _dev_table(rects_np)
+    a = _lib.AdjGhostArgs()
+    a.q_dst = _ptr(dst_buf)
+    a.q_src = _ptr(src_buf)
+    a.q_coarse_old = a.q_src
+    a.q_coarse_new = a.q_src
+    a.dst_patches = _ptr(dst_store.table)
+    a.src_patches = _ptr(src_store.table)
+    a.rects = _ptr(rects)
+    a.dst_comp_stride = dst_store.plane
+    a.src_comp_stride = src_store.plane
+    a.nrect = len(rects_np)
+    a.ndim = dst_store.ndim
+    a.m = dst_store.m
+    a.ghost_dst = dst_store.g
+    a.ghost_src = src_store.g
+    a.ratio = 1
+    a.time_mode = 0
+    a.max_rect_cells = int(np.max(rects_np["ni"] * rects_np["nj"]))
+    a.stream = _lib.stream_ptr(stream)
+    _lib.check(_lib.lib().adj_fill_ghost_rects(_lib.C.byref(a)), "adj_fill_ghost_rects")
+
+
+def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ratio, w_time, mode,
+                 dst_buf=None, stream=None):
+    if len(rects_np) == 0:
+        return
+    rects = _dev_table(rects_np)
+    fine_level = fine_store.patches[0].spec.level
+    wf = hierarchy.widths(fine_level)
+    wc = hierarchy.widths(fine_level - 1)
+    org = hierarchy.origin
+    a = _lib.AdjGhostArgs()
+    a.q_dst = _ptr(dst_buf if dst_buf is not None else fine_store.buf[fine_store.cur])
+    a.q_src = _ptr(q_new)
+    a.q_coarse_old = _ptr(q_old)
+    a.q_coarse_new = _ptr(q_new)
+    a.dst_patches = _ptr(fine_store.table)
+    a.src_patches = _ptr(coarse_store.table)
+    a.rects = _ptr(rects)
+    a.dst_comp_stride = fine_store.plane
+    a.src_comp_stride = coarse_store.plane
+    a.nrect = len(rects_np)
+    a.ndim = fine_store.ndim
+    a.m = fine_store.m
+    a.ghost_dst = fine_store.g
+    a.ghost_src = coarse_store.g
+    a.ratio = ratio
+    a.origin_x = org[0]
+    a.origin_y = org[1] if fine_store.ndim == 2 else 0.0
+    a.dx_f, a.dy_f = wf[0], wf[1]
+    a.dx_c, a.dy_c = wc[0], wc[1]
+    a.w_time = w_time
+    a.time_mode = mode
+    a.max_rect_cells = int(np.max(rects_np["ni"] * rects_np["nj"]))
+    a.stream = _lib.stream_ptr(stream)
+    _lib.check(_lib.lib().adj_fill_ghost_rects(_lib.C.byref(a)), "adj_fill_ghost_rects")
+
+
+def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=None):
+    """K2 physical phase on every patch of the store (solver.py:125-146)."""
+    store.sync_in(stream)
+    table = store.edges_table(level_shape)
+    if not np.any(store.table_np["edges"]):
+        return
+    store.prepare_write(full_ghosts=store.all_edges_physical(level_shape), stream=stream)
+    a = _lib.AdjPhysArgs()
+    a.q = _ptr(store.buf[store.cur])
+    a.patches = _ptr(table)
+    a.comp_stride = store.plane
+    a.npatch = len(store.patches)
+    a.ndim = store.ndim
+    a.ghost = store.g
+    a.m = store.m
+    sides = (boundary.left, boundary.right, boundary.bottom, boundary.top)
+    for k, sd in enumerate(sides):
+        a.bc[k] = _lib.BC_WALL if sd == "wall" else _lib.BC_OUTFLOW
+    a.normal_comp[0] = equation.normal_component(0)
+    a.normal_comp[1] = equation.normal_component(1) if store.ndim == 2 else -1
+    a.max_ghost_cells = max(NX * NY - (NX - 2 * store.g) * (NY - 2 * store.g if store.ndim == 2 else NY)
+                            for (_, NX, NY, _) in store.boxes)
+    a.stream = _lib.stream_ptr(stream)
+    _lib.check(_lib.lib().adj_fill_physical(_lib.C.byref(a)), "adj_fill_physical")
+
+
+def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index, stream=None):
+    """K1 on every patch: reads buf[cur], writes buf[out_buf_index].
+    Returns (speed_max (npatch, 2) tensor, nonfinite (npatch,) tensor)."""
+    if limiter not in _lib.LIMITERS:
+        raise ValueError(f"unknown limiter {limiter!r}")
+    torch = _torch()
+    npatch = len(store.patches)
+    if variant == _lib.VARIANT_FAST and store.any_dry():
+        variant = _lib.VARIANT_EXACT   # the fast strip kernel has no wet/dry logic
+    tiles, ntile = store.tiles(variant)
+    smax = store.scratch("smax", 2 * npatch, torch.float64)
+    bad = store.scratch("nonfinite", npatch, torch.int32)
+    system, form, rev = equation.kernel_spec()
+    spec0 = store.patches[0].spec
+    a = _lib.AdjStepArgs()
+    a.q_in = _ptr(store.buf[store.cur])
+    a.q_out = _ptr(store.buf[out_buf_index])
+    a.aux = _ptr(store.aux)
+    a.patches = _ptr(store.table)
+    a.tiles = _ptr(tiles)
+    a.speed_max = _ptr(smax)
+    a.nonfinite = _ptr(bad)
+    a.comp_stride = store.plane
+    a.aux_stride = store.plane
+    a.npatch = npatch
+    a.ntile = ntile
+    a.ndim = store.ndim
+    a.ghost = store.g
+    a.system, a.form, a.reversed = system, form, rev
+    a.limiter = _lib.LIMITERS[limiter]
+    a.variant = variant
+    a.dt = dt
+    a.dtdx = dt / spec0.dx
+    a.dtdy = dt / spec0.dy if store.ndim == 2 else 0.0
+    a.gravity = equation.gravity
+    a.stream = _lib.stream_ptr(stream)
+    _lib.check(_lib.lib().adj_step_level(_lib.C.byref(a)), "adj_step_level")
+    return smax[: 2 * npatch].view(npatch, 2), bad[:npatch]
+
+
+def restrict_rects(coarse_store, fine_store, rects_np, ratio, swe, stream=None):
+    if len(rects_np) == 0:
+        return
+    rects = _dev_table(rects_np)
+    a = _lib.AdjRestrictArgs()
+    a.q_coarse = _ptr(coarse_store.buf[coarse_store.cur])
+    a.q_fine = _ptr(fine_store.buf[fine_store.cur])
+    a.aux_coarse = _ptr(coarse_store.aux)
+    a.aux_fine = _ptr(fine_store.aux)
+    a.coarse_patches = _ptr(coarse_store.table)
+    a.fine_patches = _ptr(fine_store.table)
+    a.rects = _ptr(rects)
+    a.coarse_comp_stride = coarse_store.plane
+    a.fine_comp_stride = fine_store.plane
+    a.coarse_aux_stride = coarse_store.plane
+    a.fine_aux_stride = fine_store.plane
+    a.nrect = len(rects_np)
+    a.ndim = coarse_store.ndim
+    a.m = coarse_store.m
+    a.ratio = ratio
+    a.swe = int(swe)
+    a.max_rect_cells = int(np.max(rects_np["ni"] * rects_np["nj"]))
+    a.ghost_coarse = coarse_store.g
+    a.ghost_fine = fine_store.g
+    a.stream = _lib.stream_ptr(stream)
+    _lib.check(_lib.lib().adj_restrict(_lib.C.byref(a)), "adj_restrict")
+
+
+def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level_origin, level_dx, level_dy,
+                snap_index, tolerance, adj_wet=None, interp_w=None, want_best=False, stream=None):
+    """K3 on every patch of the store.  ring: (N, m, nxa[, nya]) float64 CUDA
+    tensor; snap_index: list of ints (mode 0) or (k, w) pairs (mode 1).
+    Returns (flag_bits uint32 tensor, counts (npatch,) int64 tensor,
+    best list-of-tensors or None, status tensor)."""
+    torch = _torch()
+    npatch = len(store.patches)
+    mode = 0 if interp_w is None else 1
+    idx = torch.tensor(list(snap_index) if len(snap_index) else [0], dtype=torch.int32, device="cuda")
+    w = torch.tensor(list(interp_w) if interp_w is not None and len(interp_w) else [0.0],
+                     dtype=torch.float64, device="cuda")
+    bits = store.scratch("flag_bits", max(store.flag_words, 1), torch.int32)
+    counts = store.scratch("flag_counts", npatch, torch.int64)
+    status = store.scratch("flag_status", 1, torch.int32)
+    ncell = [int(np.prod(p.spec.shape)) for p in store.patches]
+    best = best_off = None
+    if want_best:
+        offs = np.concatenate([[0], np.cumsum(ncell)[:-1]]).astype(np.int64)
+        best = torch.zeros(int(sum(ncell)), dtype=torch.float64, device="cuda")
+        best_off = torch.from_numpy(offs).to("cuda")
+    a = _lib.AdjFlagArgs()
+    a.q = _ptr(store.buf[store.cur])
+    a.aux = _ptr(store.aux)
+    a.patches = _ptr(store.table)
+    a.ring = _ptr(ring)
+    a.adj_wet = _ptr(adj_wet)
+    a.snap_index = _ptr(idx)
+    a.interp_w = _ptr(w) if mode == 1 else 0
+    a.flag_bits = _ptr(bits)
+    a.counts = _ptr(counts)
+    a.best = _ptr(best)
+    a.best_offset = _ptr(best_off)
+    a.status = _ptr(status)
+    a.comp_stride = store.plane
+    a.aux_stride = store.plane
+    a.npatch = npatch
+    a.ndim = store.ndim
+    a.m = store.m
+    a.ghost = store.g
+    a.swe = int(store.swe)
+    a.mode = mode
+    a.nidx = len(snap_index)
+    a.nxa = ring_shape[0]
+    a.nya = ring_shape[1] if store.ndim == 2 else 1
+    a.max_cells = max(ncell)
+    a.origin_x = level_origin[0]
+    a.origin_y = level_origin[1] if store.ndim == 2 else 0.0
+    a.dx, a.dy = level_dx, level_dy
+    a.a_origin_x = a_origin[0]
+    a.a_origin_y = a_origin[1] if store.ndim == 2 else 0.0
+    a.a_dx, a.a_dy = a_dx, a_dy
+    a.tolerance = tolerance
+    a.stream = _lib.stream_ptr(stream)
+    _lib.check(_lib.lib().adj_flag_adjoint(_lib.C.byref(a)), "adj_flag_adjoint")
+    best_list = None
+    if want_best:
+        best_list = []
+        o = 0
+        for n in ncell:
+            best_list.append(best[o:o + n])
+            o += n
+    return bits, counts, best_list, status

@@ -1,0 +1,341 @@
+"""Single-patch stepping API on the device (drop-in for the reference's solver.py).
+
+Every function keeps the reference signature and error behaviour
+(/root/reference/pkg/src/adjamr/solver.py) but runs the hand-written sm_100a
+kernels through the C ABI: K1 (step), K2 (ghost fill).  Material sampling
+from user callables and dt selection stay on the host.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, device
+from .equations import EquationSet
+from .geometry import Patch, PatchHierarchy
+
+LIMITERS = ("none", "minmod", "MC", "superbee")
+DEFAULT_VARIANT = _lib.VARIANT_FAST
+
+
+class CflViolationError(RuntimeError):
+    """A step exceeded the unit Courant number and was rejected (solver.py:23)."""
+
+
+class NumericalBlowupError(RuntimeError):
+    """A step produced NaN or Inf (solver.py:27)."""
+
+
+class SchedulingError(RuntimeError):
+    """Coarse data does not bracket the requested interpolation time (solver.py:31)."""
+
+
+@dataclass(frozen=True)
+class BoundarySpec:
+    """Physical boundary condition per side: 'wall' or 'outflow' (solver.py:35-56)."""
+
+    left: str = "wall"
+    right: str = "wall"
+    bottom: str = "wall"
+    top: str = "wall"
+
+    def __post_init__(self):
+        for side in (self.left, self.right, self.bottom, self.top):
+            if side not in ("wall", "outflow"):
+                raise ValueError(f"unknown boundary condition {side!r}")
+
+    def side(self, axis: int, high: bool) -> str:
+        if axis == 0:
+            return self.right if high else self.left
+        return self.top if high else self.bottom
+
+
+class StepResult:
+    """Result of step_patch (solver.py:59-62).  ``state`` is fetched from the
+    device lazily, so callers that ignore it pay no device-to-host copy."""
+
+    def __init__(self, state, max_courant: float):
+        self._state = state
+        self.max_courant = max_courant
+
+    @property
+    def state(self) -> np.ndarray:
+        return self._state() if callable(self._state) else self._state
+
+
+# ---------------------------------------------------------------------------
+# materials (host: arbitrary Python callables), solver.py:149-205
+
+
+def _fix_aux_ghosts(arr: np.ndarray, axis: int, high: bool, g: int, wall: bool):
+    n = arr.shape[axis]
+    idx = [slice(None)] * arr.ndim
+    src = [slice(None)] * arr.ndim
+    if high:
+        idx[axis] = slice(n - g, n)
+        src[axis] = slice(n - g - 1, n - 2 * g - 1, -1) if wall else slice(n - g - 1, n - g)
+    else:
+        idx[axis] = slice(0, g)
+        src[axis] = slice(2 * g - 1, g - 1, -1) if wall else slice(g, g + 1)
+    arr[tuple(idx)] = arr[tuple(src)]
+
+
+def sample_patch_material(patch: Patch, equation: EquationSet, boundary: BoundarySpec,
+                          level_shape: tuple[int, ...]):
+    """Sample the material at cell centres (incl. ghosts), then mirror (wall)
+    or extrapolate (outflow) it into physical-boundary ghosts."""
+    spec = patch.spec
+    cs = spec.cell_centers(include_ghost=True)
+    if spec.ndim == 1:
+        mat = equation.sample_material(cs[0])
+    else:
+        xx, yy = np.meshgrid(cs[0], cs[1], indexing="ij")
+        mat = equation.sample_material(xx, yy)
+    import dataclasses
+    arrays = {f.name: np.array(getattr(mat, f.name), copy=True) for f in dataclasses.fields(mat)
+              if isinstance(getattr(mat, f.name), np.ndarray)}
+    g = spec.ghost_width
+    for axis in range(spec.ndim):
+        for high in (False, True):
+            at_edge = spec.hi[axis] == level_shape[axis] - 1 if high else spec.lo[axis] == 0
+            if at_edge:
+                wall = boundary.side(axis, high) == "wall"
+                for arr in arrays.values():
+                    _fix_aux_ghosts(arr, axis, high, g, wall)
+    others = {f.name: getattr(mat, f.name) for f in dataclasses.fields(mat) if f.name not in arrays}
+    patch.aux = type(mat)(**arrays, **others)
+    if patch._store is not None:
+        av = patch._store.aux_view(patch._slot)
+        import torch
+        for k, pl in enumerate(patch.aux.planes()):
+            av[k].copy_(torch.from_numpy(np.ascontiguousarray(pl, dtype=float)))
+    return patch.aux
+
+
+# ---------------------------------------------------------------------------
+# store helpers
+
+
+def store_of(patch: Patch) -> device.LevelStore:
+    """The patch's level store (a private single-patch store if it has none)."""
+    if patch._store is None:
+        device.LevelStore([patch])
+    return patch._store
+
+
+def level_store(patches: list[Patch]) -> device.LevelStore:
+    """One store holding exactly ``patches`` in order (re-homing if needed)."""
+    st = patches[0]._store
+    if st is not None and len(st.patches) == len(patches) and all(
+            a is b and b._store is st for a, b in zip(st.patches, patches)):
+        return st
+    for p in patches:
+        if p._store is not None:
+            old = p.state_old if p._store.has_old(p._slot) else p._host_old
+            _ = p.state                   # pull the authoritative state to the host
+            p._host_old = None if old is None else np.array(old, copy=True)
+            p._store = None
+    return device.LevelStore(patches)
+
+
+def _cfl(smax: np.ndarray, dtdx: float, dtdy: float, ndim: int) -> np.ndarray:
+    sx = smax[:, 0] * dtdx
+    return sx if ndim == 1 else np.maximum(sx, smax[:, 1] * dtdy)
+
+
+# ---------------------------------------------------------------------------
+# K1
+
+
+def step_patch(patch: Patch, dt: float, equation: EquationSet, limiter: str = "MC",
+               variant: int | None = None) -> StepResult:
+    """Advance one patch by dt on the device (solver.py:515-522).
+
+    Raises CflViolationError before any mutation, NumericalBlowupError after
+    the update, ValueError on bad arguments.
+    """
+    if dt <= 0:
+        raise ValueError("dt must be positive")
+    if limiter not in LIMITERS:
+        raise ValueError(f"unknown limiter {limiter!r}")
+    variant = DEFAULT_VARIANT if variant is None else variant
+    st = store_of(patch)
+    st.sync_in()
+    st.fold_ghosts()
+    busy = [st.cur] + ([st.old] if st.old is not None else [])
+    out = st._free(*busy)
+    if len(st.patches) == 1:
+        smax, bad = device.launch_step(st, dt, equation, limiter, variant, out)
+    else:
+        smax, bad = _launch_single(st, patch._slot, dt, equation, limiter, variant, out)
+    spec = patch.spec
+    dtdx = dt / spec.dx
+    dtdy = dt / spec.dy if spec.ndim == 2 else 0.0
+    k = 0 if len(st.patches) == 1 else patch._slot
+    sm = smax.cpu().numpy()
+    nonfinite = bool(bad[k].item())
+    cfl = float(_cfl(sm[k:k + 1], dtdx, dtdy, spec.ndim)[0])
+    if cfl > 1.0 + 1e-12:
+        raise CflViolationError(f"Courant number {cfl:.4f} > 1")
+    if len(st.patches) == 1:
+        st.ghost_src = st.cur
+        st.cur = out
+    else:
+        st._unalias()
+        g = st.g
+        src = st._view(st.buf[out], patch._slot, st.m)
+        dst = st.view(patch._slot)
+        if spec.ndim == 2:
+            dst[:, g:-g, g:-g].copy_(src[:, g:-g, g:-g])
+        else:
+            dst[:, g:-g].copy_(src[:, g:-g])
+    patch._loc = "device"
+    patch.time += dt
+    if nonfinite:
+        raise NumericalBlowupError(f"non-finite state at t={patch.time}")
+    return StepResult(lambda: patch.state, cfl)
+
+
+def _launch_single(st, slot, dt, equation, limiter, variant, out):
+    """Step one patch of a multi-patch store (tile subset)."""
+    if variant == _lib.VARIANT_FAST and st.any_dry():
+        variant = _lib.VARIANT_EXACT
+    key = ("single", variant, slot)
+    if key not in st._tiles:
+        tiles, _ = st.tiles(variant)
+        allrows = np.frombuffer(tiles.cpu().numpy().tobytes(), dtype=_lib.TILE_DTYPE)
+        sub = allrows[allrows["patch"] == slot]
+        st._tiles[key] = (device._dev_table(sub), len(sub))
+    saved = st._tiles[variant]
+    st._tiles[variant] = st._tiles[key]
+    try:
+        return device.launch_step(st, dt, equation, limiter, variant, out)
+    finally:
+        st._tiles[variant] = saved
+
+
+# ---------------------------------------------------------------------------
+# K2 single-patch entry points
+
+
+def fill_ghost_physical(patch: Patch, boundary: BoundarySpec, equation: EquationSet,
+                        level_shape: tuple[int, ...]):
+    """Wall / outflow ghosts of one patch (solver.py:125-146), on the device."""
+    st = store_of(patch)
+    if len(st.patches) == 1:
+        device.fill_physical(st, boundary, equation, level_shape)
+    else:
+        from . import amr
+        amr._fill_physical_subset(st, [patch._slot], boundary, equation, level_shape)
+
+
+def fill_ghost_same_level(patch: Patch, level_patches: list[Patch]):
+    """Copy overlapping same-level interiors into this patch's ghosts (solver.py:208-224)."""
+    from . import amr
+    amr.fill_same_level(level_patches, only=patch)
+
+
+def fill_ghost_from_coarse(fine_patch: Patch, hierarchy: PatchHierarchy, t: float):
+    """Space-time interpolated in-domain ghosts from the coarser level (solver.py:227-286)."""
+    from . import amr
+    if fine_patch.spec.level < 2:
+        return
+    amr.fill_from_coarse(hierarchy, fine_patch.spec.level, t, only=fine_patch)
+
+
+# ---------------------------------------------------------------------------
+# dt selection and the uniform loop (host control, device work)
+
+
+def select_dt(hierarchy: PatchHierarchy, equation: EquationSet,
+              courant_target: float = 0.9, dt_max: float = np.inf) -> float:
+    """Coarse-level dt from the CFL target (solver.py:525-542)."""
+    if not 0.0 < courant_target <= 1.0:
+        raise ValueError("courant_target must be in (0, 1]")
+    speed = 0.0
+    for p in hierarchy.patches(1):
+        sl = p.spec.interior_slices()
+        speed = max(speed, float(np.max(equation.max_speed(p.aux[sl]), initial=0.0)))
+    if speed == 0.0:
+        return dt_max
+    wx, wy = hierarchy.widths(1)
+    dt = courant_target * wx / speed
+    if hierarchy.ndim == 2:
+        dt = min(dt, courant_target * wy / speed)
+    return min(dt, dt_max)
+
+
+def integrate_patch(patch: Patch, equation: EquationSet, boundary: BoundarySpec,
+                    level_shape: tuple[int, ...], t_end: float, *,
+                    courant_target: float = 0.9, limiter: str = "MC",
+                    dt_max: float = np.inf, dt_fixed: float | None = None,
+                    output_times=(), on_output=None, on_step=None, variant: int | None = None):
+    """Advance one uniform patch to t_end (solver.py:545-586): K2 physical
+    fill + K1 per step on the device, outputs hit exactly."""
+    sl = patch.spec.interior_slices()
+    speed = float(np.max(equation.max_speed(patch.aux[sl]), initial=0.0))
+    if dt_fixed is not None:
+        base = dt_fixed
+    elif speed == 0.0:
+        base = dt_max
+    else:
+        base = courant_target * patch.spec.dx / speed
+        if patch.spec.ndim == 2:
+            base = min(base, courant_target * patch.spec.dy / speed)
+        base = min(base, dt_max)
+    pending = sorted(output_times)
+    eps = 1e-9 * max(abs(t_end), 1.0)
+
+    def flush():
+        while pending and pending[0] <= patch.time + eps:
+            t_out = pending.pop(0)
+            if on_output is not None:
+                on_output(t_out, patch)
+
+    flush()
+    while patch.time < t_end - eps:
+        dt = min(base, t_end - patch.time)
+        if pending:
+            dt = min(dt, pending[0] - patch.time)
+        fill_ghost_physical(patch, boundary, equation, level_shape)
+        step_patch(patch, dt, equation, limiter, variant=variant)
+        if on_step is not None:
+            on_step(patch)
+        flush()
+
+
+def advance_uniform(patch: Patch, equation: EquationSet, boundary: BoundarySpec,
+                    level_shape: tuple[int, ...], dt: float, nsteps: int, limiter: str = "MC",
+                    variant: int | None = None, stream=None) -> float:
+    """nsteps fixed-dt steps of one uniform patch with physical boundaries,
+    device-resident and without a host sync per step (the batched form of
+    the integrate_patch loop, solver.py:578-586).  CFL and non-finite checks
+    are accumulated on the device and raised after the batch.  Returns the
+    maximum Courant number seen."""
+    import torch
+    variant = DEFAULT_VARIANT if variant is None else variant
+    st = store_of(patch)
+    st.sync_in(stream)
+    track = torch.zeros(2, dtype=torch.float64, device="cuda")
+    badacc = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for _ in range(nsteps):
+        device.fill_physical(st, boundary, equation, level_shape, stream)
+        st.fold_ghosts(stream)
+        busy = [st.cur] + ([st.old] if st.old is not None else [])
+        out = st._free(*busy)
+        smax, bad = device.launch_step(st, dt, equation, limiter, variant, out, stream)
+        torch.maximum(track, smax.reshape(-1, 2).amax(0), out=track)
+        badacc.bitwise_or_(bad.amax().reshape(1))
+        st.ghost_src = st.cur
+        st.cur = out
+        patch.time += dt
+    patch._loc = "device"
+    spec = patch.spec
+    sm = track.cpu().numpy()[None, :]
+    cfl = float(_cfl(sm, dt / spec.dx, dt / spec.dy if spec.ndim == 2 else 0.0, spec.ndim)[0])
+    if cfl > 1.0 + 1e-12:
+        raise CflViolationError(f"Courant number {cfl:.4f} > 1")
+    if int(badacc.item()):
+        raise NumericalBlowupError(f"non-finite state at t={patch.time}")
+    return cfl
