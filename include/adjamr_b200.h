@@ -102,6 +102,10 @@ typedef struct AdjStepArgs {
     const AdjTile* tiles;      /* device */
     double* speed_max;         /* device, 2*npatch (x, y), zeroed by the call */
     int32_t* nonfinite;        /* device, npatch, zeroed by the call          */
+    int32_t* work_counter;     /* device, 1 int tile queue head, zeroed by the call */
+    const double* static_speed;/* optional device (x, y) per patch: material speed bound over the
+                                  CFL ranges; when given, the FAST variant (no dry cells) copies it
+                                  to speed_max instead of reducing per face (same values) */
     int64_t comp_stride, aux_stride;
     int32_t npatch, ntile;
     int32_t ndim, ghost;

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libadjamr_b200.so")
+LIB_PATH = os.environ.get("ADJAMR_LIB") or os.path.join(HERE, "libadjamr_b200.so")
 
 # constants mirrored from the header
 ADJ_OK, ADJ_ERR_CFL, ADJ_ERR_NONFINITE, ADJ_ERR_SCHEDULING = 0, 1, 2, 3
@@ -49,7 +49,7 @@ P, D, I32, I64 = C.c_void_p, C.c_double, C.c_int32, C.c_int64
 
 class AdjStepArgs(C.Structure):
     _fields_ = [("q_in", P), ("q_out", P), ("aux", P), ("patches", P), ("tiles", P),
-                ("speed_max", P), ("nonfinite", P), ("comp_stride", I64), ("aux_stride", I64),
+                ("speed_max", P), ("nonfinite", P), ("work_counter", P), ("static_speed", P), ("comp_stride", I64), ("aux_stride", I64),
                 ("npatch", I32), ("ntile", I32), ("ndim", I32), ("ghost", I32),
                 ("system", I32), ("form", I32), ("reversed", I32), ("limiter", I32),
                 ("variant", I32), ("pad", I32),

@@ -1,0 +1,815 @@
+"""Multilevel driver: device level sweep + host clustering and bookkeeping.
+
+Drop-in for the reference's amr.py (/root/reference/pkg/src/adjamr/amr.py).
+The level sweep is device work: ghost fill (K2: coarse space-time
+interpolation, same-level copies, physical boundaries -- amr.py:479-491),
+the batched patch step (K1), fine-to-coarse averaging (K4, amr.py:399-450),
+adjoint flagging of a whole level in one K3 launch, and the regrid data
+movement (new interiors from the parent and old patches, amr.py:504-551).
+Flag buffering, signature-bisection clustering, nesting clip and patch
+bookkeeping stay on the host, as north_star prescribes.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib, device
+from .geometry import Patch, PatchHierarchy, allowed_region_mask
+from .solver import (BoundarySpec, CflViolationError, NumericalBlowupError, SchedulingError,
+                     level_store, sample_patch_material)
+
+
+@dataclass
+class FlagField:
+    flags: np.ndarray
+    lo: tuple[int, ...]
+    level: int
+    strategy_name: str
+    time: float
+
+
+@dataclass(frozen=True)
+class ClusterBox:
+    lo: tuple[int, ...]
+    hi: tuple[int, ...]
+    efficiency: float
+
+    @property
+    def shape(self):
+        return tuple(h - l + 1 for l, h in zip(self.lo, self.hi))
+
+
+@dataclass(frozen=True)
+class RefinementRegion:
+    min_level: int
+    max_level: int
+    t1: float
+    t2: float
+    rect: tuple[float, ...]
+
+    def __post_init__(self):
+        if self.min_level > self.max_level:
+            raise ValueError("min_level must be <= max_level")
+
+    def contains_time(self, t: float) -> bool:
+        return self.t1 <= t <= self.t2
+
+    def cell_mask(self, spec) -> np.ndarray:
+        cs = spec.cell_centers()
+        inx = (cs[0] >= self.rect[0]) & (cs[0] <= self.rect[1])
+        if spec.ndim == 1:
+            return inx
+        iny = (cs[1] >= self.rect[2]) & (cs[1] <= self.rect[3])
+        return np.logical_and.outer(inx, iny)
+
+
+# ---------------------------------------------------------------------------
+# flagging strategies (amr.py:75-134); the adjoint one lives in adjoint.py
+
+
+class FlaggingStrategy:
+    name = "base"
+
+    def evaluate(self, patch: Patch) -> np.ndarray:
+        raise NotImplementedError
+
+
+class DifferenceFlagging(FlaggingStrategy):
+    name = "difference"
+
+    def __init__(self, tolerance: float):
+        if tolerance <= 0:
+            raise ValueError("tolerance must be positive")
+        self.tolerance = tolerance
+
+    def evaluate(self, patch):
+        g = patch.spec.ghost_width
+        q = patch.state
+        shape = patch.spec.shape
+        big = np.zeros(shape)
+        for axis in range(patch.spec.ndim):
+            d = np.abs(np.diff(q, axis=1 + axis))
+            for start in (g - 1, g):
+                sl = [slice(g, g + n) for n in shape]
+                sl[axis] = slice(start, start + shape[axis])
+                big = np.maximum(big, np.max(d[(slice(None), *sl)], axis=0))
+        return big > self.tolerance
+
+
+class SurfaceFlagging(FlaggingStrategy):
+    name = "surface"
+
+    def __init__(self, tolerance: float):
+        if tolerance <= 0:
+            raise ValueError("tolerance must be positive")
+        self.tolerance = tolerance
+
+    def evaluate(self, patch):
+        sl = patch.spec.interior_slices()
+        flags = np.abs(patch.state[(0, *sl)]) > self.tolerance
+        if hasattr(patch.aux, "wet"):
+            flags &= patch.aux.wet[sl]
+        return flags
+
+
+class EverywhereFlagging(FlaggingStrategy):
+    name = "everywhere"
+
+    def evaluate(self, patch):
+        return np.ones(patch.spec.shape, dtype=bool)
+
+
+def _apply_regions(flags, spec, t, regions):
+    new_level = spec.level + 1
+    for r in regions:
+        if r.contains_time(t) and new_level <= r.min_level:
+            flags |= r.cell_mask(spec)
+    for r in regions:
+        if r.contains_time(t) and new_level > r.max_level:
+            flags &= ~r.cell_mask(spec)
+    return flags
+
+
+def flag_cells(patch: Patch, strategy: FlaggingStrategy, regions=()) -> FlagField:
+    """Strategy flags then region overrides (amr.py:137-154)."""
+    flags = np.array(strategy.evaluate(patch), dtype=bool)
+    flags = _apply_regions(flags, patch.spec, patch.time, regions)
+    return FlagField(flags=flags, lo=patch.spec.lo, level=patch.spec.level,
+                     strategy_name=strategy.name, time=patch.time)
+
+
+def buffer_flags(flags: FlagField, buffer_cells: int) -> FlagField:
+    """Box dilation of radius buffer_cells, clipped to the patch (amr.py:157-179)."""
+    if buffer_cells < 0:
+        raise ValueError("buffer_cells must be >= 0")
+    out = flags.flags.copy()
+    for axis in range(out.ndim):
+        grown = out.copy()
+        n = out.shape[axis]
+        for s in range(1, min(buffer_cells, n - 1) + 1):
+            a = [slice(None)] * out.ndim
+            b = [slice(None)] * out.ndim
+            a[axis], b[axis] = slice(0, n - s), slice(s, n)
+            grown[tuple(a)] |= out[tuple(b)]
+            grown[tuple(b)] |= out[tuple(a)]
+        out = grown
+    return FlagField(flags=out, lo=flags.lo, level=flags.level, strategy_name=flags.strategy_name,
+                     time=flags.time)
+
+
+# ---------------------------------------------------------------------------
+# signature-bisection clustering (amr.py:186-337)
+
+
+def _sig(mask, axis):
+    other = tuple(a for a in range(mask.ndim) if a != axis)
+    return mask.sum(axis=other) if other else mask.astype(int)
+
+
+def _bbox(mask):
+    nz = np.nonzero(mask)
+    if nz[0].size == 0:
+        return None
+    return tuple(int(a.min()) for a in nz), tuple(int(a.max()) for a in nz)
+
+
+def _choose_cut(sub):
+    """Hole nearest the centre (best over axes), else the strongest Laplacian
+    sign change of the signature, else the midpoint of the longest axis."""
+    best = None
+    for axis in range(sub.ndim):
+        sig = _sig(sub, axis)
+        holes = np.flatnonzero(sig == 0)
+        if holes.size:
+            mid = (sig.size - 1) / 2.0
+            k = int(holes[np.argmin(np.abs(holes - mid))])
+            score = abs(k - mid) / max(sig.size, 1)
+            if best is None or score < best[0]:
+                best = (score, axis, k)
+    if best is not None:
+        return "hole", best[1], best[2]
+    best = None
+    for axis in range(sub.ndim):
+        sig = _sig(sub, axis)
+        n = sig.size
+        if n < 4:
+            continue
+        lap = sig[2:] - 2 * sig[1:-1] + sig[:-2]
+        mid = (n - 1) / 2.0
+        for k in range(lap.size - 1):
+            if lap[k] * lap[k + 1] < 0:
+                key = (abs(lap[k + 1] - lap[k]), -abs((k + 1.5) - mid))
+                if best is None or key > best[0]:
+                    best = (key, axis, k + 1)
+    if best is not None:
+        return "edge", best[1], best[2]
+    axis = int(np.argmax(sub.shape))
+    if sub.shape[axis] < 2:
+        return None
+    return "edge", axis, sub.shape[axis] // 2 - 1
+
+
+def _children(lo, hi, cut):
+    kind, axis, k = cut
+    a_hi, b_lo = list(hi), list(lo)
+    if kind == "hole":
+        a_hi[axis] = lo[axis] + k - 1
+        b_lo[axis] = lo[axis] + k + 1
+    else:
+        a_hi[axis] = lo[axis] + k
+        b_lo[axis] = lo[axis] + k + 1
+    kids = []
+    if a_hi[axis] >= lo[axis]:
+        kids.append((tuple(lo), tuple(a_hi)))
+    if hi[axis] >= b_lo[axis]:
+        kids.append((tuple(b_lo), tuple(hi)))
+    return kids
+
+
+def _box_slice(lo, hi):
+    return tuple(slice(l, h + 1) for l, h in zip(lo, hi))
+
+
+def _tight_efficiency(mask, box):
+    sub = mask[_box_slice(*box)]
+    bb = _bbox(sub)
+    if bb is None:
+        return 1.0
+    core = sub[_box_slice(*bb)]
+    return float(core.sum()) / core.size
+
+
+def cluster(flags, efficiency_threshold: float, max_edge: int | None = None) -> list[ClusterBox]:
+    """Cover all flagged cells with efficient rectangles (amr.py:244-309)."""
+    if not 0.0 < efficiency_threshold <= 1.0:
+        raise ValueError("efficiency_threshold must be in (0, 1]")
+    if isinstance(flags, FlagField):
+        mask, offset = flags.flags, flags.lo
+    else:
+        mask = np.asarray(flags, dtype=bool)
+        offset = (0,) * mask.ndim
+    boxes: list[ClusterBox] = []
+    top = _bbox(mask)
+    if top is None:
+        return boxes
+    todo = [top]
+
+    def emit(lo, hi, eff):
+        boxes.append(ClusterBox(lo=tuple(l + o for l, o in zip(lo, offset)),
+                                hi=tuple(h + o for h, o in zip(hi, offset)), efficiency=eff))
+
+    while todo:
+        lo, hi = todo.pop()
+        bb = _bbox(mask[_box_slice(lo, hi)])
+        if bb is None:
+            continue
+        lo, hi = tuple(l + b for l, b in zip(lo, bb[0])), tuple(l + b for l, b in zip(lo, bb[1]))
+        sub = mask[_box_slice(lo, hi)]
+        eff = int(sub.sum()) / sub.size
+        oversize = max_edge is not None and max(sub.shape) > max_edge
+        if eff >= efficiency_threshold and not oversize:
+            if eff < 1.0:
+                cut = _choose_cut(sub)
+                if cut is not None:
+                    kids = _children(lo, hi, cut)
+                    effs = [_tight_efficiency(mask, kb) for kb in kids]
+                    if effs and min(effs) > eff + 1e-12:
+                        todo.extend(kids)
+                        continue
+            emit(lo, hi, eff)
+            continue
+        if oversize and eff >= efficiency_threshold:
+            axis = int(np.argmax(sub.shape))
+            cut = ("edge", axis, sub.shape[axis] // 2 - 1)
+        else:
+            cut = _choose_cut(sub)
+        if cut is None:
+            emit(lo, hi, eff)
+            continue
+        todo.extend(_children(lo, hi, cut))
+    return boxes
+
+
+def _runs(row):
+    """Maximal runs of True as (start, end) inclusive."""
+    v = np.concatenate([[False], np.asarray(row, dtype=bool), [False]])
+    d = np.diff(v.astype(np.int8))
+    starts = np.flatnonzero(d == 1)
+    ends = np.flatnonzero(d == -1) - 1
+    return [(int(a), int(b)) for a, b in zip(starts, ends)]
+
+
+def _allowed_rectangles(box: ClusterBox, allowed, mask):
+    """Trim a box to the nesting-allowed region (amr.py:344-382)."""
+    sub = allowed[_box_slice(box.lo, box.hi)]
+    if sub.all():
+        return [box]
+    rects = []
+    if sub.ndim == 1:
+        rects = [((box.lo[0] + a,), (box.lo[0] + b,)) for a, b in _runs(sub)]
+    else:
+        i = 0
+        while i < sub.shape[0]:
+            runs = _runs(sub[i])
+            j = i
+            while j + 1 < sub.shape[0] and _runs(sub[j + 1]) == runs:
+                j += 1
+            rects += [((box.lo[0] + i, box.lo[1] + a), (box.lo[0] + j, box.lo[1] + b)) for a, b in runs]
+            i = j + 1
+    out = []
+    for lo, hi in rects:
+        f = mask[_box_slice(lo, hi)]
+        if f.any():
+            out.append(ClusterBox(lo=lo, hi=hi, efficiency=int(f.sum()) / f.size))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# context
+
+
+@dataclass
+class AmrContext:
+    equation: object
+    boundary: BoundarySpec
+    strategy: FlaggingStrategy
+    limiter: str = "MC"
+    regions: tuple = ()
+    regrid_interval: int = 1
+    buffer_cells: int = 3
+    efficiency: float = 0.7
+    max_patch_edge: int = 60
+    step_counts: dict = field(default_factory=dict)
+    cell_steps: dict = field(default_factory=dict)
+    flagged_per_regrid: list = field(default_factory=list)
+    on_level_advanced: object = None
+    variant: int = _lib.VARIANT_FAST
+
+    def count_step(self, level: int, cells: int):
+        self.cell_steps[level] = self.cell_steps.get(level, 0) + cells
+
+
+# ---------------------------------------------------------------------------
+# device ghost fill (K2) with host-built rectangle lists
+
+
+def _ghost_strips(spec):
+    """Ghost ring of a patch as global-index boxes (lo, hi) inclusive."""
+    g = spec.ghost_width
+    if spec.ndim == 1:
+        return [((spec.lo[0] - g,), (spec.lo[0] - 1,)), ((spec.hi[0] + 1,), (spec.hi[0] + g,))]
+    (x0, y0), (x1, y1) = spec.lo, spec.hi
+    return [((x0 - g, y0 - g), (x0 - 1, y1 + g)), ((x1 + 1, y0 - g), (x1 + g, y1 + g)),
+            ((x0, y0 - g), (x1, y0 - 1)), ((x0, y1 + 1), (x1, y1 + g))]
+
+
+def _intersect(alo, ahi, blo, bhi):
+    lo = tuple(max(a, b) for a, b in zip(alo, blo))
+    hi = tuple(min(a, b) for a, b in zip(ahi, bhi))
+    return None if any(l > h for l, h in zip(lo, hi)) else (lo, hi)
+
+
+def _boxes(patches):
+    lo = np.array([p.spec.lo for p in patches], dtype=np.int64)
+    hi = np.array([p.spec.hi for p in patches], dtype=np.int64)
+    return lo, hi
+
+
+def _candidates(lo_arr, hi_arr, qlo, qhi):
+    ok = np.ones(len(lo_arr), dtype=bool)
+    for a in range(lo_arr.shape[1]):
+        ok &= (lo_arr[:, a] <= qhi[a]) & (hi_arr[:, a] >= qlo[a])
+    return np.flatnonzero(ok)
+
+
+def _rect(kind, dst, src, dlo, dspec, extent, slo=None, sspec=None):
+    g = dspec.ghost_width
+    di = [dlo[a] - (dspec.lo[a] - g) for a in range(dspec.ndim)]
+    si = [0, 0]
+    if slo is not None:
+        gs = sspec.ghost_width
+        si = [slo[a] - (sspec.lo[a] - gs) for a in range(sspec.ndim)]
+    if dspec.ndim == 1:
+        return (kind, dst, src, di[0], 0, extent[0], 1, si[0], 0, 0)
+    return (kind, dst, src, di[0], di[1], extent[0], extent[1], si[0], si[1], 0)
+
+
+def build_ghost_rects(hierarchy: PatchHierarchy, level: int, only=None):
+    """Rectangles for the in-domain ghost phases of one level:
+    coarse rects grouped by coarse patch, then same-level copy rects.
+    Returns (coarse {coarse slot: [rect]}, copy [rect], covered cells per patch)."""
+    patches = hierarchy.patches(level)
+    shape = hierarchy.level_shape(level)
+    dom_lo, dom_hi = (0,) * hierarchy.ndim, tuple(n - 1 for n in shape)
+    same_lo, same_hi = _boxes(patches)
+    coarse = hierarchy.patches(level - 1) if level >= 2 else []
+    r = hierarchy.ratio_to_finer(level - 1) if level >= 2 else 1
+    if coarse:
+        c_lo, c_hi = _boxes(coarse)
+        cf_lo, cf_hi = c_lo * r, (c_hi + 1) * r - 1
+    coarse_rects: dict[int, list] = {}
+    copy_rects = []
+    covered = np.zeros(len(patches), dtype=np.int64)
+    for k, p in enumerate(patches):
+        if only is not None and p is not only:
+            continue
+        for slo, shi in _ghost_strips(p.spec):
+            box = _intersect(slo, shi, dom_lo, dom_hi)
+            if box is None:
+                continue
+            # physical cells of this strip are out of domain; in-domain part only
+            if coarse:
+                for c in _candidates(cf_lo, cf_hi, *box):
+                    ib = _intersect(*box, tuple(cf_lo[c]), tuple(cf_hi[c]))
+                    if ib is not None:
+                        ext = [h - l + 1 for l, h in zip(*ib)]
+                        coarse_rects.setdefault(int(c), []).append(
+                            _rect(_lib.RECT_COARSE, k, int(c), ib[0], p.spec, ext))
+                        covered[k] += int(np.prod(ext))
+            for o in _candidates(same_lo, same_hi, *box):
+                if o == k:
+                    continue
+                ib = _intersect(*box, tuple(same_lo[o]), tuple(same_hi[o]))
+                if ib is not None:
+                    ext = [h - l + 1 for l, h in zip(*ib)]
+                    copy_rects.append(_rect(_lib.RECT_COPY, k, int(o), ib[0], p.spec, ext, ib[0],
+                                            patches[o].spec))
+                    if not coarse:
+                        covered[k] += int(np.prod(ext))
+    return coarse_rects, copy_rects, covered
+
+
+def _ring_and_physical(spec, level_shape):
+    """(ghost ring size, out-of-domain ghost cells) of a patch."""
+    g = spec.ghost_width
+    tot = np.prod([n + 2 * g for n in spec.shape]) - np.prod(spec.shape)
+    ind = 1
+    for a in range(spec.ndim):
+        lo = max(spec.lo[a] - g, 0)
+        hi = min(spec.hi[a] + g, level_shape[a] - 1)
+        ind *= hi - lo + 1
+    return int(tot), int(np.prod([n + 2 * g for n in spec.shape]) - ind)
+
+
+def _coarse_time_mode(cp: Patch, t: float):
+    """space_time_interp scheduling (solver.py:266-286) -> (mode, w)."""
+    eps = 1e-9 * max(abs(cp.time), 1.0)
+    has_old = cp.time_old is not None and (
+        (cp._store is not None and cp._store.has_old(cp._slot)) or cp._host_old is not None)
+    if not has_old:
+        if abs(t - cp.time) > eps:
+            raise SchedulingError(f"coarse patch has no saved state bracketing t={t} (at {cp.time})")
+        return 2, 1.0
+    t0, t1 = cp.time_old, cp.time
+    if not t0 - eps <= t <= t1 + eps:
+        raise SchedulingError(f"t={t} outside coarse bracket [{t0}, {t1}]")
+    if t1 == t0:
+        return 0, 0.0
+    w = float(np.clip((t - t0) / (t1 - t0), 0.0, 1.0))
+    if w == 0.0:
+        return 0, 0.0
+    return 1, w
+
+
+def _coarse_old_buffer(cst):
+    """Device buffer holding every coarse patch's state_old (uploading host
+    copies for patches whose saved state only exists on the host)."""
+    import torch
+    need = [p for p in cst.patches if not cst.has_old(p._slot) and p._host_old is not None]
+    if need:
+        if cst.old is None or cst.old == cst.cur:
+            if cst.old == cst.cur:
+                cst._unalias()
+            cst.old = cst._free(cst.cur, cst.ghost_src)
+        for p in need:
+            cst.view(p._slot, "old").copy_(torch.from_numpy(p._host_old))
+            cst.old_valid[p._slot] = True
+            p._host_old = None
+    return cst.buf[cst.old] if cst.old is not None else cst.buf[cst.cur]
+
+
+def fill_from_coarse(hierarchy: PatchHierarchy, level: int, t: float, only=None, _rects=None):
+    patches = hierarchy.patches(level)
+    coarse = hierarchy.patches(level - 1)
+    if level < 2 or not patches or not coarse:
+        return
+    st = level_store(patches)
+    cst = level_store(coarse)
+    st.sync_in()
+    cst.sync_in()
+    cst.fold_ghosts()
+    crects, _, _ = _rects if _rects is not None else build_ghost_rects(hierarchy, level, only)
+    if not crects:
+        return
+    st.prepare_write(full_ghosts=False)
+    old_buf = _coarse_old_buffer(cst)
+    groups: dict = {}
+    for c, rl in crects.items():
+        groups.setdefault(_coarse_time_mode(coarse[c], t), []).extend(rl)
+    r = hierarchy.ratio_to_finer(level - 1)
+    for (mode, w), rl in groups.items():
+        device.coarse_rects(st, cst, np.array(rl, dtype=_lib.RECT_DTYPE), old_buf, cst.buf[cst.cur],
+                            hierarchy, r, w, mode)
+
+
+def fill_same_level(level_patches, only=None, _rects=None):
+    if not level_patches:
+        return
+    st = level_store(level_patches)
+    st.sync_in()
+    if _rects is None:
+        h = _pseudo_hierarchy(level_patches)
+        _, rects, _ = build_ghost_rects(h, 1, only)
+    else:
+        rects = _rects
+    if not rects:
+        return
+    st.prepare_write(full_ghosts=False)
+    device.copy_rects(st, st, np.array(rects, dtype=_lib.RECT_DTYPE), st.buf[st.cur], st.buf[st.cur])
+
+
+def _pseudo_hierarchy(patches):
+    """A one-level hierarchy wide enough to hold the patches (same-level rects only)."""
+    hi = np.max([p.spec.hi for p in patches], axis=0) + 1 + patches[0].spec.ghost_width
+    nd = patches[0].spec.ndim
+    h = PatchHierarchy(xlim=(0.0, 1.0), ylim=None if nd == 1 else (0.0, 1.0),
+                       base_shape=tuple(int(v) for v in hi), ratios=[])
+    h.levels = [list(patches)]
+    return h
+
+
+def _fill_physical_subset(st, slots, boundary, equation, level_shape):
+    device.fill_physical(st, boundary, equation, level_shape, slots=slots)
+
+
+class _LevelRects:
+    """Cached ghost/restriction rectangles of one level (rebuilt on regrid)."""
+
+    def __init__(self, hierarchy, level):
+        self.key = (id(hierarchy), level, tuple(id(p) for p in hierarchy.patches(level)),
+                    tuple(id(p) for p in hierarchy.patches(level - 1)) if level >= 2 else ())
+        self.ghost = build_ghost_rects(hierarchy, level)
+        shape = hierarchy.level_shape(level)
+        self.full = True
+        for k, p in enumerate(hierarchy.patches(level)):
+            ring, phys = _ring_and_physical(p.spec, shape)
+            if self.ghost[2][k] + phys < ring:
+                self.full = False
+                break
+
+
+_RECT_CACHE: dict = {}
+
+
+def _level_rects(hierarchy, level):
+    lr = _RECT_CACHE.get((id(hierarchy), level))
+    key = (id(hierarchy), level, tuple(id(p) for p in hierarchy.patches(level)),
+           tuple(id(p) for p in hierarchy.patches(level - 1)) if level >= 2 else ())
+    if lr is None or lr.key != key:
+        lr = _LevelRects(hierarchy, level)
+        _RECT_CACHE[(id(hierarchy), level)] = lr
+    return lr
+
+
+def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrContext):
+    """Coarse interpolation, then same-level copies, then physical boundaries
+    (amr.py:479-491), each a batched device launch over the whole level."""
+    patches = hierarchy.patches(level)
+    if not patches:
+        return
+    st = level_store(patches)
+    st.sync_in()
+    lr = _level_rects(hierarchy, level)
+    crects, copies, _ = lr.ghost
+    st.prepare_write(full_ghosts=lr.full)
+    if level >= 2 and crects:
+        fill_from_coarse(hierarchy, level, t, _rects=lr.ghost)
+    if copies:
+        device.copy_rects(st, st, np.array(copies, dtype=_lib.RECT_DTYPE), st.buf[st.cur], st.buf[st.cur])
+    device.fill_physical(st, ctx.boundary, ctx.equation, hierarchy.level_shape(level))
+    st.ghost_src = st.cur
+
+
+def make_patch(hierarchy: PatchHierarchy, level: int, lo, hi, ctx: AmrContext, time: float) -> Patch:
+    spec = hierarchy.make_spec(level, lo, hi)
+    p = Patch(spec, ctx.equation.m, time=time)
+    sample_patch_material(p, ctx.equation, ctx.boundary, hierarchy.level_shape(level))
+    return p
+
+
+# ---------------------------------------------------------------------------
+# restriction (K4)
+
+
+def _restrict_rects(coarse, fine, r):
+    c_lo, c_hi = _boxes(coarse)
+    rects = []
+    for fk, fp in enumerate(fine):
+        flo = tuple(l // r for l in fp.spec.lo)
+        fhi = tuple(h // r for h in fp.spec.hi)
+        for c in _candidates(c_lo, c_hi, flo, fhi):
+            ib = _intersect(flo, fhi, tuple(c_lo[c]), tuple(c_hi[c]))
+            if ib is None:
+                continue
+            lo, hi = ib
+            ext = [h - l + 1 for l, h in zip(lo, hi)]
+            di = [lo[a] - c_lo[c][a] for a in range(len(lo))]
+            si = [lo[a] * r - fp.spec.lo[a] for a in range(len(lo))]
+            if len(lo) == 1:
+                rects.append((0, int(c), fk, di[0], 0, ext[0], 1, si[0], 0, 0))
+            else:
+                rects.append((0, int(c), fk, di[0], di[1], ext[0], ext[1], si[0], si[1], 0))
+    return np.array(rects, dtype=_lib.RECT_DTYPE)
+
+
+def restrict_fine_to_coarse(hierarchy: PatchHierarchy, level: int):
+    """Coarse cells covered by level+1 <- mean of their fine children (amr.py:399-450)."""
+    fine = hierarchy.patches(level + 1)
+    coarse = hierarchy.patches(level)
+    if not fine or not coarse:
+        return
+    r = hierarchy.ratio_to_finer(level)
+    cst = level_store(coarse)
+    fst = level_store(fine)
+    cst.sync_in()
+    fst.sync_in()
+    key = ("restrict", id(cst), id(fst))
+    rects = cst._tiles.get(key)
+    if rects is None:
+        rects = _restrict_rects(coarse, fine, r)
+        cst._tiles[key] = rects
+    cst._unalias()
+    device.restrict_rects(cst, fst, rects, r, cst.swe)
+
+
+# ---------------------------------------------------------------------------
+# regrid (flags on device, clustering on host, data movement on device)
+
+
+def _flag_level(parents, ctx: AmrContext):
+    from .adjoint import AdjointFlagging
+    if isinstance(ctx.strategy, AdjointFlagging):
+        flags, counts = ctx.strategy.evaluate_level(parents)
+    else:
+        flags = [np.array(ctx.strategy.evaluate(p), dtype=bool) for p in parents]
+        counts = None
+    out = []
+    for p, f in zip(parents, flags):
+        f = _apply_regions(np.array(f, dtype=bool), p.spec, p.time, ctx.regions)
+        out.append(FlagField(flags=f, lo=p.spec.lo, level=p.spec.level, strategy_name=ctx.strategy.name,
+                             time=p.time))
+    return out
+
+
+def regrid(hierarchy: PatchHierarchy, level: int, ctx: AmrContext, deepest: int | None = None):
+    """Rebuild levels level..deepest from parent flags (amr.py:554-599)."""
+    if level < 2:
+        raise ValueError("cannot regrid the base level")
+    deepest = deepest if deepest is not None else hierarchy.max_levels
+    for lev in range(level, deepest + 1):
+        parent = lev - 1
+        parents = hierarchy.patches(parent)
+        while len(hierarchy.levels) < lev:
+            hierarchy.levels.append([])
+        if not parents:
+            hierarchy.levels[lev - 1] = []
+            continue
+        t = parents[0].time
+        fill_level_ghosts(hierarchy, parent, t, ctx)
+        mask = np.zeros(hierarchy.level_shape(parent), dtype=bool)
+        raw = 0
+        for ff in _flag_level(parents, ctx):
+            raw += int(ff.flags.sum())
+            bf = buffer_flags(ff, ctx.buffer_cells)
+            sl = _box_slice(ff.lo, tuple(l + n - 1 for l, n in zip(ff.lo, bf.flags.shape)))
+            mask[sl] |= bf.flags
+        ctx.flagged_per_regrid.append(raw)
+        allowed = allowed_region_mask(hierarchy, parent)
+        clipped = mask & allowed
+        ratio = hierarchy.ratio_to_finer(parent)
+        boxes = cluster(clipped, ctx.efficiency, max_edge=max(1, ctx.max_patch_edge // ratio))
+        rects = [rb for b in boxes for rb in _allowed_rectangles(b, allowed, clipped)]
+        old = hierarchy.patches(lev)
+        new = [make_patch(hierarchy, lev, tuple(l * ratio for l in rb.lo),
+                          tuple((h + 1) * ratio - 1 for h in rb.hi), ctx, t) for rb in rects]
+        if new:
+            _fill_new_level(hierarchy, lev, new, old, parents, t)
+        hierarchy.levels[lev - 1] = new
+
+
+def _fill_new_level(hierarchy, lev, new, old, parents, t):
+    """New interiors: space(-time) interpolation from the parents, then the
+    old patches' overlapping interiors (amr.py:504-551), on the device."""
+    st = device.LevelStore(new)
+    for p in new:
+        p._loc = "device"          # contents are produced here, nothing to upload
+    cst = level_store(parents)
+    cst.sync_in()
+    cst.fold_ghosts()
+    r = hierarchy.ratio_to_finer(lev - 1)
+    c_lo, c_hi = _boxes(parents)
+    cf_lo, cf_hi = c_lo * r, (c_hi + 1) * r - 1
+    groups: dict = {}
+    for k, p in enumerate(new):
+        for c in _candidates(cf_lo, cf_hi, p.spec.lo, p.spec.hi):
+            ib = _intersect(p.spec.lo, p.spec.hi, tuple(cf_lo[c]), tuple(cf_hi[c]))
+            if ib is not None:
+                ext = [h - l + 1 for l, h in zip(*ib)]
+                groups.setdefault(_coarse_time_mode(parents[c], t), []).append(
+                    _rect(_lib.RECT_COARSE, k, int(c), ib[0], p.spec, ext))
+    old_buf = _coarse_old_buffer(cst)
+    for (mode, w), rl in groups.items():
+        device.coarse_rects(st, cst, np.array(rl, dtype=_lib.RECT_DTYPE), old_buf, cst.buf[cst.cur],
+                            hierarchy, r, w, mode)
+    if old:
+        ost = level_store(old)
+        ost.sync_in()
+        o_lo, o_hi = _boxes(old)
+        copies = []
+        for k, p in enumerate(new):
+            for o in _candidates(o_lo, o_hi, p.spec.lo, p.spec.hi):
+                ib = _intersect(p.spec.lo, p.spec.hi, tuple(o_lo[o]), tuple(o_hi[o]))
+                if ib is not None:
+                    ext = [h - l + 1 for l, h in zip(*ib)]
+                    copies.append(_rect(_lib.RECT_COPY, k, int(o), ib[0], p.spec, ext, ib[0], old[o].spec))
+        if copies:
+            device.copy_rects(st, ost, np.array(copies, dtype=_lib.RECT_DTYPE), ost.buf[ost.cur], st.buf[st.cur])
+
+
+# ---------------------------------------------------------------------------
+# the subcycled advance (amr.py:602-644)
+
+
+def _retry_half_steps(st, slot, patch, dt, ctx):
+    """Reference CFL retry: two dt/2 steps from the saved state with the
+    ghosts filled at t, no refill in between (amr.py:627-631)."""
+    import torch
+    from . import solver
+    tmp = Patch(patch.spec, patch.num_components, time=patch.time_old)
+    tmp.aux = patch.aux
+    tmp.state = st.view(slot, "old").cpu().numpy()
+    solver.step_patch(tmp, dt / 2.0, ctx.equation, ctx.limiter, variant=ctx.variant)
+    solver.step_patch(tmp, dt / 2.0, ctx.equation, ctx.limiter, variant=ctx.variant)
+    ts = tmp._store
+    g = st.g
+    inner = (slice(None),) + (slice(g, -g),) * st.ndim
+    st.view(slot)[inner].copy_(ts.view(tmp._slot)[inner])
+    del torch
+
+
+def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext):
+    """save_old + step of every patch of the level in one K1 launch, with the
+    reference's per-patch CFL retry and cell-step accounting (amr.py:620-631)."""
+    patches = hierarchy.patches(level)
+    st = level_store(patches)
+    st.save_old_all()
+    for p in patches:
+        p.time_old = p.time
+    out = st._free(st.cur)
+    smax, bad = device.launch_step(st, dt, ctx.equation, ctx.limiter, ctx.variant, out)
+    spec = patches[0].spec
+    dtdx = dt / spec.dx
+    dtdy = dt / spec.dy if spec.ndim == 2 else 0.0
+    sm = smax.cpu().numpy()
+    cfl = sm[:, 0] * dtdx if spec.ndim == 1 else np.maximum(sm[:, 0] * dtdx, sm[:, 1] * dtdy)
+    nonfinite = bad.cpu().numpy()
+    st.ghost_src = st.cur
+    st.cur = out
+    for k, p in enumerate(patches):
+        cells = int(np.prod(p.spec.shape))
+        if cfl[k] > 1.0 + 1e-12:
+            _retry_half_steps(st, k, p, dt, ctx)
+            ctx.count_step(level, 2 * cells)
+        else:
+            ctx.count_step(level, cells)
+            if nonfinite[k]:
+                p.time += dt
+                raise NumericalBlowupError(f"non-finite state at t={p.time}")
+        p._loc = "device"
+
+
+def advance_hierarchy(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext):
+    """Advance one level by dt, recursively subcycling finer levels (amr.py:602-644)."""
+    count = ctx.step_counts.get(level, 0)
+    if level < hierarchy.max_levels and count > 0 and count % ctx.regrid_interval == 0:
+        regrid(hierarchy, level + 1, ctx)
+    patches = hierarchy.patches(level)
+    if not patches:
+        return
+    t = patches[0].time
+    fill_level_ghosts(hierarchy, level, t, ctx)
+    step_level(hierarchy, level, dt, ctx)
+    t_new = t + dt
+    for p in patches:
+        p.time = t_new
+    if ctx.on_level_advanced is not None:
+        ctx.on_level_advanced(hierarchy, level, t_new)
+    ctx.step_counts[level] = count + 1
+    if level < hierarchy.max_levels and hierarchy.patches(level + 1):
+        fill_level_ghosts(hierarchy, level, t_new, ctx)
+        ratio = hierarchy.ratio_to_finer(level)
+        for _ in range(ratio):
+            advance_hierarchy(hierarchy, level + 1, dt / ratio, ctx)
+        restrict_fine_to_coarse(hierarchy, level)

@@ -40,7 +40,11 @@ def _stale(out: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, ptxas_info: bool = False) -> str:
+def build(verbose: bool = False, ptxas_info: bool = False, lib: str = LIB, build_dir: str = BUILD,
+          extra: list[str] | None = None) -> str:
+    """Compile every unit (only stale ones) and link ``lib``."""
+    BUILD = build_dir
+    LIB = lib
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, "adj_common.cuh"),
                os.path.join(HERE, "..", "include", "adjamr_b200.h")]
@@ -51,7 +55,7 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
         o = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(o)
         if _stale(o, [s, *headers, __file__]):
-            cmd = [nvcc(), *ARCH, *COMMON, *flags, "-c", s, "-o", o]
+            cmd = [nvcc(), *ARCH, *COMMON, *flags, *(extra or []), "-c", s, "-o", o]
             if ptxas_info:
                 cmd += ["-Xptxas", "-v"]
             if verbose:

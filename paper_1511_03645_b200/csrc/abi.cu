@@ -49,7 +49,8 @@ int adj_step_tile_shape(int variant, int ndim, int32_t* ni, int32_t* nj) {
 int adj_step_level(const AdjStepArgs* a) {
     if (!a) return adj::bad("null args");
     if (a->q_in == a->q_out) return adj::bad("q_in must not alias q_out");
-    if (!a->q_in || !a->q_out || !a->aux || !a->patches || !a->tiles || !a->speed_max || !a->nonfinite)
+    if (!a->q_in || !a->q_out || !a->aux || !a->patches || !a->tiles || !a->speed_max || !a->nonfinite ||
+        !a->work_counter)
         return adj::bad("null pointer");
     if (a->ghost < 2) return adj::bad("ghost width must be >= 2");
     if (a->ndim == 1 && a->system != ADJ_SYS_AC1D) return adj::bad("1D requires acoustics-1d");
@@ -57,9 +58,16 @@ int adj_step_level(const AdjStepArgs* a) {
     if (a->limiter < ADJ_LIM_NONE || a->limiter > ADJ_LIM_SUPERBEE) return adj::bad("limiter");
     if (!(a->dt > 0.0)) return adj::bad("dt must be positive");
     cudaStream_t st = (cudaStream_t)a->stream;
-    int rc = adj::record_cuda(cudaMemsetAsync(a->speed_max, 0, sizeof(double) * 2 * a->npatch, st), "memset speed_max");
+    int rc;
+    if (a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed)
+        rc = adj::record_cuda(cudaMemcpyAsync(a->speed_max, a->static_speed, sizeof(double) * 2 * a->npatch,
+                                              cudaMemcpyDeviceToDevice, st), "copy static_speed");
+    else
+        rc = adj::record_cuda(cudaMemsetAsync(a->speed_max, 0, sizeof(double) * 2 * a->npatch, st), "memset speed_max");
     if (rc) return rc;
     rc = adj::record_cuda(cudaMemsetAsync(a->nonfinite, 0, sizeof(int32_t) * a->npatch, st), "memset nonfinite");
+    if (rc) return rc;
+    rc = adj::record_cuda(cudaMemsetAsync(a->work_counter, 0, sizeof(int32_t), st), "memset work_counter");
     if (rc) return rc;
     if (a->variant == ADJ_VARIANT_EXACT) return adj::step_exact(*a, st);
     if (a->variant == ADJ_VARIANT_FAST) return adj::step_fast(*a, st);

@@ -25,6 +25,10 @@
 // variant (host dispatch), so no wet/dry logic is needed here.
 #include "adj_common.cuh"
 
+#ifndef K1_MIN_BLOCKS
+#define K1_MIN_BLOCKS 3   // CTAs of 128 threads per SM the register budget targets
+#endif
+
 namespace adj {
 
 void fast_tile_shape(int ndim, int32_t* ni, int32_t* nj) {
@@ -35,27 +39,37 @@ namespace fast {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-ADJ_D double rcp(double x) {  // x > 0, normal
+ADJ_D double rcp(double x) {  // x > 0, normal: MUFU seed + one cubic Newton step
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
+    const double e = fma(-x, r, 1.0);
+    return fma(r, fma(e, e, e), r);   // r (1 + e + e^2): relative error ~e^3
 }
+
+ADJ_D double dmin(double a, double b) { return a < b ? a : b; }
+ADJ_D double dmax(double a, double b) { return a > b ? a : b; }
 
 ADJ_D double sh_dn(double v) { return __shfl_down_sync(FULL, v, 1); }  // from lane+1 (row j+1)
 ADJ_D double sh_up(double v) { return __shfl_up_sync(FULL, v, 1); }    // from lane-1 (row j-1)
 
-// division-free limited strength lim(A,B) = phi(B/A) * A (solver.py:65-77)
+// Division-free limited strength, doubled: 2 phi(B/A) A (solver.py:65-77).
+// With theta = B/A, phi(theta) A is 0 when A, B have opposite signs and
+// otherwise sign(A) times  MC: min(|A+B|/2, 2|A|, 2|B|);  minmod: min(|A|,|B|);
+// superbee: max(min(|A|, 2|B|), min(2|A|, |B|)).  The factor 1/2 is folded
+// into the per-cell 1/(2(1+m^2)) the result is multiplied by.
 template <int LIM>
-ADJ_D double limab(double A, double B) {
-    const double a = fabs(A);
-    const double b = A < 0.0 ? -B : B;
+ADJ_D double limab2(double A, double B) {
+    const double a = fabs(A), b = fabs(B);
     double r;
-    if (LIM == ADJ_LIM_MINMOD) r = fmax(0.0, fmin(a, b));
-    else if (LIM == ADJ_LIM_MC) r = fmax(0.0, fmin(fmin(0.5 * (a + b), a + a), b + b));
-    else r = fmax(0.0, fmax(fmin(a, b + b), fmin(a + a, b)));  // superbee
+    if (LIM == ADJ_LIM_MINMOD) {
+        const double m = dmin(a, b);
+        r = m + m;
+    } else if (LIM == ADJ_LIM_MC) {
+        r = dmin(fabs(A + B), 4.0 * dmin(a, b));
+    } else {
+        r = dmax(dmin(a + a, 4.0 * b), dmin(4.0 * a, b + b));
+    }
+    r = (__double2hiint(A) ^ __double2hiint(B)) < 0 ? 0.0 : r;
     return copysign(r, A);
 }
 
@@ -65,7 +79,7 @@ ADJ_D double limab(double A, double B) {
 // (acoustics K = c z, shallow water c^2); fx: f-wave flux factor (acoustics
 // 1/rho, shallow water g h = c^2).
 struct Mat {
-    double c, m, k1i, kx, ky, tr, fx;
+    double c, m, k1, k1i, kx, ky, tr, fx;   // k1 = 1+m^2, k1i = 1/(2 k1)
 };
 
 template <int SYS, int FORM>
@@ -74,7 +88,8 @@ ADJ_D Mat make_mat(double c, double z, double dtdx, double dtdy) {
     Mat t;
     t.c = c;
     t.m = SWE ? c : z;
-    t.k1i = rcp(fma(t.m, t.m, 1.0));
+    t.k1 = fma(t.m, t.m, 1.0);
+    t.k1i = rcp(t.k1 + t.k1);
     const double hx = 0.5 * fma(-dtdx, c, 1.0), hy = 0.5 * fma(-dtdy, c, 1.0);
     t.kx = FW ? hx : c * hx;
     t.ky = FW ? hy : c * hy;
@@ -147,12 +162,12 @@ ADJ_D void correction(const Face& f, double s0_nb, double P0_nb, double s1_nb, d
     if (LIM == ADJ_LIM_NONE) {
         p0 = f.s0; p1 = f.s1;
     } else {
-        const double A0 = f.s0 * fma(L.m, L.m, 1.0);
-        const double A1 = f.s1 * fma(R.m, R.m, 1.0);
+        const double A0 = f.s0 * L.k1;
+        const double A1 = f.s1 * R.k1;
         const double B0 = s0_nb * (REV ? P0_nb : f.P);
         const double B1 = s1_nb * (REV ? P1_nb : f.P);
-        p0 = limab<LIM>(A0, B0) * L.k1i;
-        p1 = limab<LIM>(A1, B1) * R.k1i;
+        p0 = limab2<LIM>(A0, B0) * L.k1i;
+        p1 = limab2<LIM>(A1, B1) * R.k1i;
     }
     // coefficients: wave 0.5|s|(1-dtd|s|) for both; f-wave sign(s) 0.5(1-dtd|s|)
     const double u0 = (FW ? -kL : kL) * p0;
@@ -184,165 +199,252 @@ ADJ_D void transverse(double f0, double h, const Mat& b, const Mat& a,
 
 struct Raw { double q0, q1, q2, c, z; };
 
-template <int SYS, int FORM, bool REV, int LIM>
-__global__ void __launch_bounds__(128) k1_fast(AdjStepArgs a) {
-    constexpr bool SWE = SYS == ADJ_SYS_SWE2D;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tid = blockIdx.x * 4 + warp;
-    if (tid >= a.ntile) return;
-    const AdjTile T = a.tiles[tid];
-    const AdjPatch p = a.patches[T.patch];
-    const int g = a.ghost;
-    const int NY = p.ny + 2 * g;
-    const int jj = g + T.j0 - 2 + lane;                       // ghost-inclusive row of this lane
-    const int jl = jj < 0 ? 0 : (jj > NY - 1 ? NY - 1 : jj);  // clamped load row
-    const bool out_lane = lane >= 2 && lane < 2 + T.nj;
-    const bool yface_cfl = lane >= 1 && lane < 2 + T.nj;      // own top face in CFL range
-    const int64_t cs = a.comp_stride, as = a.aux_stride;
-    const double* __restrict__ qin = a.q_in + p.offset + jl;
-    const double* __restrict__ aux = a.aux + p.offset + jl;
-    double* __restrict__ qout = a.q_out + p.offset + jl;
-    const int pitch = p.pitch;
-    const double dtdx = a.dtdx, dtdy = a.dtdy;
-    const double hx = 0.5 * dtdx, hy = 0.5 * dtdy;
+constexpr int RING = 6;   // columns in flight per warp (cp.async prefetch distance)
 
-    auto load = [&](int s) {
-        const int64_t o = (int64_t)(g + s) * pitch;
-        Raw r;
-        r.q0 = __ldg(qin + o); r.q1 = __ldg(qin + cs + o); r.q2 = __ldg(qin + 2 * cs + o);
-        r.c = __ldg(aux + o);
-        r.z = SWE ? 0.0 : __ldg(aux + as + o);
-        return r;
-    };
+// One warp's march along x over an output strip.  Every carried quantity
+// lives in a 3-slot ring indexed by (column mod 3); column<K> is the body of
+// the march for a column in slot K, so the 3-way unrolled loop rotates roles
+// by renaming instead of moving registers.
+template <int SYS, int FORM, bool REV, int LIM, bool CFL>
+struct Strip {
+    static constexpr bool SWE = SYS == ADJ_SYS_SWE2D;
+    const double* __restrict__ qin;
+    const double* __restrict__ aux;
+    double* __restrict__ qout;
+    int64_t cs, as;
+    int pitch, g, i0, ni, s_last;
+    bool out_lane, yface_cfl;
+    double dtdx, dtdy, hx, hy;
 
-    const int s_first = T.i0 - 2, s_last = T.i0 + T.ni + 1;
-    Raw pf0 = load(s_first), pf1 = load(s_first + 1);
+    double* ring;                  // this warp's cp.async ring: [RING][NARR][32]
+    int lane;
+    Mat m[3];
+    double q0[3], q1[3], q2[3];
+    Face xf[3];                    // xf[k]: x-face left of column k
+    double sy0[3], sy2[3];         // Sy(column)
+    double gt0[3], gt2[3];         // gtil, own top face, of column
+    double cy0[3], cy2[3];         // limited y correction of column
+    double bpy0[3], bpy1[3];       // bp of transverse(Sy(column))
+    double ft0[3], ft1[3];         // ftil at the x-face left of column
+    double sx0[3], sx1[3];         // Sx(column)
+    double cup[3], mup[3];         // row j+1 materials of column
+    double smx, smy;
+    bool bad;
 
-    // pipeline state (see header comment for the schedule)
-    Mat mprv{}, mpp{};                 // materials of columns s-1, s-2
-    double qprv0 = 0, qprv1 = 0, qprv2 = 0, qpp0 = 0, qpp1 = 0, qpp2 = 0;
-    double cup_prv = 0, mup_prv = 0;   // row j+1 material of column s-1
-    Face xp{}, xpp{};                  // x-faces s-3/2, s-5/2 (s-1/2 is computed per step)
-    double corry_prv0 = 0, corry_prv2 = 0;   // corr_y of column s-1
-    double bpY_prv0 = 0, bpY_prv1 = 0;       // bp of transverse(Sy(s-2))
-    double ftil_old0 = 0, ftil_old1 = 0;     // ftil at face s-5/2
-    double gt_pp0 = 0, gt_pp2 = 0;           // gtil of column s-2 (own top face)
-    double sx_pp0 = 0, sx_pp1 = 0;           // Sx(s-2)
-    double sy_prv0 = 0, sy_prv2 = 0, sy_pp0 = 0, sy_pp2 = 0;
-    double smx = 0.0, smy = 0.0;
-    bool bad = false;
+    static constexpr int NARR = SWE ? 4 : 5;
 
-    for (int s = s_first; s <= s_last; ++s) {
-        const Raw cr = pf0;
-        pf0 = pf1;
-        if (s + 2 <= s_last) pf1 = load(s + 2);
-        const Mat mc = make_mat<SYS, FORM>(cr.c, cr.z, dtdx, dtdy);
+    // issue the cp.async copies of column s into ring slot (s - s_first) % RING;
+    // one commit group per column, empty groups past the strip end
+    ADJ_D void prefetch(int s, int slot) const {
+        if (s <= s_last) {
+            const int64_t o = (int64_t)(g + s) * pitch;
+            const double* src[5] = {qin + o, qin + cs + o, qin + 2 * cs + o, aux + o, aux + as + o};
+#pragma unroll
+            for (int k = 0; k < NARR; ++k) {
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + (slot * NARR + k) * 32 + lane);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src[k]) : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
 
-        // ---- B: x-face s-1/2 between columns s-1 and s
-        const Face xf = solve_face<SYS, FORM, REV>(qprv0, qprv1, cr.q0, cr.q1, mprv, mc);
-        if (s >= T.i0 && s <= T.i0 + T.ni && out_lane) smx = fmax(smx, fmax(mprv.c, mc.c));
+    ADJ_D Raw fetch(int slot) const {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(RING - 1) : "memory");
+        const double* r = ring + slot * NARR * 32 + lane;
+        Raw v;
+        v.q0 = r[0]; v.q1 = r[32]; v.q2 = r[64]; v.c = r[96];
+        v.z = SWE ? 0.0 : r[128];
+        return v;
+    }
 
-        // ---- C: y-face between rows j and j+1 at column s
+    template <int K>
+    ADJ_D void column(int s, int slot) {
+        constexpr int C = K, P = (K + 2) % 3, PP = (K + 1) % 3;
+        const Raw cr = fetch(slot);
+        prefetch(s + RING, slot);
+        m[C] = make_mat<SYS, FORM>(cr.c, cr.z, dtdx, dtdy);
+        // CFL: max |speed| of the faces is the max material speed of the cells
+        // they touch (fast path = no dry cells): x-faces of this strip touch
+        // columns [i0-1, i0+ni] of the output rows, y-faces rows j0-1..j0+nj
+        // of the output columns (solver.py:457-460)
+        if (CFL) {
+            if (s >= i0 - 1 && s <= i0 + ni && out_lane) smx = cr.c > smx ? cr.c : smx;
+            if (s >= i0 && s < i0 + ni && yface_cfl) smy = cr.c > smy ? cr.c : smy;
+        }
+        q0[C] = cr.q0; q1[C] = cr.q1; q2[C] = cr.q2;
+
+        // ---- x-face s-1/2 between columns s-1 and s
+        xf[C] = solve_face<SYS, FORM, REV>(q0[P], q1[P], cr.q0, cr.q1, m[P], m[C]);
+
+        // ---- y-face between rows j and j+1 at column s
         const double uq0 = sh_dn(cr.q0), uq2 = sh_dn(cr.q2);
-        Mat mu;
-        mu.c = sh_dn(mc.c);
-        mu.m = SWE ? mu.c : sh_dn(mc.m);
-        mu.k1i = sh_dn(mc.k1i);
-        mu.ky = sh_dn(mc.ky);
+        Mat mu{};
+        mu.c = sh_dn(m[C].c);
+        mu.m = SWE ? mu.c : sh_dn(m[C].m);
+        mu.k1i = sh_dn(m[C].k1i);
+        mu.k1 = fma(mu.m, mu.m, 1.0);
+        mu.ky = sh_dn(m[C].ky);
         mu.kx = 0.0;
         mu.tr = SWE ? mu.c * mu.c : mu.c * mu.m;
-        mu.fx = FORM == ADJ_FORM_FWAVE ? sh_dn(mc.fx) : 0.0;
-        const Face yf = solve_face<SYS, FORM, REV>(cr.q0, cr.q2, uq0, uq2, mc, mu);
-        if (s >= T.i0 && s < T.i0 + T.ni && yface_cfl) smy = fmax(smy, fmax(mc.c, mu.c));
-        double gc0, gc2;
+        mu.fx = FORM == ADJ_FORM_FWAVE ? sh_dn(m[C].fx) : 0.0;
+        const Face yf = solve_face<SYS, FORM, REV>(cr.q0, cr.q2, uq0, uq2, m[C], mu);
         {
-            // neighbours: next face = lane+1, previous face = lane-1
             const double s0n = REV ? sh_up(yf.s0) : sh_dn(yf.s0);
             const double s1n = REV ? sh_dn(yf.s1) : sh_up(yf.s1);
             const double P0n = REV ? sh_up(yf.P) : 0.0;
             const double P1n = REV ? sh_dn(yf.P) : 0.0;
-            correction<SYS, FORM, REV, LIM>(yf, s0n, P0n, s1n, P1n, mc, mu, mc.ky, mu.ky, gc0, gc2);
+            correction<SYS, FORM, REV, LIM>(yf, s0n, P0n, s1n, P1n, m[C], mu, m[C].ky, mu.ky, cy0[C], cy2[C]);
         }
-        const double apb0 = sh_up(yf.ap0), apb2 = sh_up(yf.ap1);
-        const double sy0 = yf.am0 + apb0, sy2 = yf.am1 + apb2;   // Sy(s)
+        sy0[C] = yf.am0 + sh_up(yf.ap0);
+        sy2[C] = yf.am1 + sh_up(yf.ap1);
+        cup[C] = mu.c;
+        mup[C] = mu.m;
 
-        // ---- D: Sx(s-1) and its transverse split with rows j-1, j+1 of column s-1
-        const double sx0 = xp.ap0 + xf.am0, sx1 = xp.ap1 + xf.am1;
-        double gt0, gt2;   // gtil of column s-1, own top face
+        // ---- Sx(s-1) and its transverse split with rows j-1, j+1 of column s-1
+        sx0[P] = xf[P].ap0 + xf[C].am0;
+        sx1[P] = xf[P].ap1 + xf[C].am1;
         {
-            Mat mb;  // row j-1 at column s-1
-            mb.c = sh_up(mprv.c);
-            mb.m = SWE ? mb.c : sh_up(mprv.m);
+            Mat mb{};
+            mb.c = sh_up(m[P].c);
+            mb.m = SWE ? mb.c : sh_up(m[P].m);
             mb.tr = SWE ? mb.c * mb.c : mb.c * mb.m;
-            Mat ma;  // row j+1 at column s-1
-            ma.c = cup_prv; ma.m = mup_prv;
+            Mat ma{};
+            ma.c = cup[P]; ma.m = mup[P];
             ma.tr = SWE ? ma.c * ma.c : ma.c * ma.m;
             double bm0, bmv, bp0, bpv;
-            transverse<SYS, FORM, REV>(sx0, hx, mb, ma, bm0, bmv, bp0, bpv);
-            const double bmu0 = sh_dn(bm0), bmu2 = sh_dn(bmv);   // bm of row j+1 -> own top face
-            gt0 = corry_prv0 - (bp0 + bmu0);
-            gt2 = corry_prv2 - (bpv + bmu2);
+            transverse<SYS, FORM, REV>(sx0[P], hx, mb, ma, bm0, bmv, bp0, bpv);
+            gt0[P] = cy0[P] - (bp0 + sh_dn(bm0));
+            gt2[P] = cy2[P] - (bpv + sh_dn(bmv));
         }
 
-        // ---- E: transverse of Sy(s-1) with columns s-2, s; x-limiter of face s-3/2
-        double ft0, ft1;   // ftil at face s-3/2
+        // ---- transverse of Sy(s-1) with columns s-2, s; x-limiter of face s-3/2
         {
             double bm0, bmv, bp0, bpv;
-            transverse<SYS, FORM, REV>(sy_prv0, hy, mpp, mc, bm0, bmv, bp0, bpv);
+            transverse<SYS, FORM, REV>(sy0[P], hy, m[PP], m[C], bm0, bmv, bp0, bpv);
             double fc0, fc1;
-            correction<SYS, FORM, REV, LIM>(xp, REV ? xpp.s0 : xf.s0, xpp.P, REV ? xf.s1 : xpp.s1, xf.P,
-                                            mpp, mprv, mpp.kx, mprv.kx, fc0, fc1);
-            ft0 = fc0 - (bpY_prv0 + bm0);
-            ft1 = fc1 - (bpY_prv1 + bmv);
-            bpY_prv0 = bp0; bpY_prv1 = bpv;
+            correction<SYS, FORM, REV, LIM>(xf[P], REV ? xf[PP].s0 : xf[C].s0, xf[PP].P,
+                                            REV ? xf[C].s1 : xf[PP].s1, xf[C].P,
+                                            m[PP], m[P], m[PP].kx, m[P].kx, fc0, fc1);
+            ft0[P] = fc0 - (bpy0[PP] + bm0);
+            ft1[P] = fc1 - (bpy1[PP] + bmv);
+            bpy0[P] = bp0; bpy1[P] = bpv;
         }
 
-        // ---- F: update cell s-2
-        {
-            const double gb0 = sh_up(gt_pp0), gb2 = sh_up(gt_pp2);
-            if (s >= T.i0 + 2 && out_lane) {
-                const double d0 = -dtdx * ((sx_pp0 + ft0) - ftil_old0) - dtdy * ((sy_pp0 + gt_pp0) - gb0);
-                const double d1 = -dtdx * ((sx_pp1 + ft1) - ftil_old1);
-                const double d2 = -dtdy * ((sy_pp2 + gt_pp2) - gb2);
-                const double n0 = qpp0 + d0, n1 = qpp1 + d1, n2 = qpp2 + d2;
-                const int64_t o = (int64_t)(g + s - 2) * pitch;
-                qout[o] = n0; qout[cs + o] = n1; qout[2 * cs + o] = n2;
-                bad |= !(isfinite(n0) && isfinite(n1) && isfinite(n2));
-            }
+        // ---- update cell s-2
+        const double gb0 = sh_up(gt0[PP]), gb2 = sh_up(gt2[PP]);
+        if (s >= i0 + 2 && s <= s_last && out_lane) {
+            const double d0 = -dtdx * ((sx0[PP] + ft0[P]) - ft0[PP]) - dtdy * ((sy0[PP] + gt0[PP]) - gb0);
+            const double d1 = -dtdx * ((sx1[PP] + ft1[P]) - ft1[PP]);
+            const double d2 = -dtdy * ((sy2[PP] + gt2[PP]) - gb2);
+            const double n0 = q0[PP] + d0, n1 = q1[PP] + d1, n2 = q2[PP] + d2;
+            const int64_t o = (int64_t)(g + s - 2) * pitch;
+            qout[o] = n0; qout[cs + o] = n1; qout[2 * cs + o] = n2;
+            bad |= !(isfinite(n0) && isfinite(n1) && isfinite(n2));
         }
-
-        // ---- shift the pipeline
-        ftil_old0 = ft0; ftil_old1 = ft1;
-        gt_pp0 = gt0; gt_pp2 = gt2;
-        sx_pp0 = sx0; sx_pp1 = sx1;
-        sy_pp0 = sy_prv0; sy_pp2 = sy_prv2;
-        sy_prv0 = sy0; sy_prv2 = sy2;
-        corry_prv0 = gc0; corry_prv2 = gc2;
-        xpp = xp; xp = xf;
-        mpp = mprv; mprv = mc;
-        qpp0 = qprv0; qpp1 = qprv1; qpp2 = qprv2;
-        qprv0 = cr.q0; qprv1 = cr.q1; qprv2 = cr.q2;
-        cup_prv = mu.c; mup_prv = mu.m;
     }
 
-    smx = warp_max(smx);
-    smy = warp_max(smy);
-    const unsigned anybad = __ballot_sync(FULL, bad);
-    if (lane == 0) {
-        if (smx > 0.0) atomic_max_nonneg(&a.speed_max[2 * T.patch], smx);
-        if (smy > 0.0) atomic_max_nonneg(&a.speed_max[2 * T.patch + 1], smy);
-        if (anybad) a.nonfinite[T.patch] = 1;
+    ADJ_D void run(const AdjTile& T, const AdjPatch& p, const AdjStepArgs& a, int lane_, double* ring_) {
+        lane = lane_;
+        ring = ring_;
+        g = a.ghost;
+        const int NY = p.ny + 2 * g;
+        const int jj = g + T.j0 - 2 + lane;
+        const int jl = jj < 0 ? 0 : (jj > NY - 1 ? NY - 1 : jj);
+        out_lane = lane >= 2 && lane < 2 + T.nj;
+        yface_cfl = lane >= 1 && lane < 3 + T.nj;
+        cs = a.comp_stride; as = a.aux_stride;
+        qin = a.q_in + p.offset + jl;
+        aux = a.aux + p.offset + jl;
+        qout = a.q_out + p.offset + jl;
+        pitch = p.pitch;
+        dtdx = a.dtdx; dtdy = a.dtdy;
+        hx = 0.5 * dtdx; hy = 0.5 * dtdy;
+        i0 = T.i0; ni = T.ni;
+        const int s_first = T.i0 - 2;
+        s_last = T.i0 + T.ni + 1;
+#pragma unroll
+        for (int k = 0; k < RING; ++k) prefetch(s_first + k, k);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            m[k] = Mat{}; xf[k] = Face{};
+            q0[k] = q1[k] = q2[k] = 0.0;
+            sy0[k] = sy2[k] = gt0[k] = gt2[k] = cy0[k] = cy2[k] = 0.0;
+            bpy0[k] = bpy1[k] = ft0[k] = ft1[k] = sx0[k] = sx1[k] = cup[k] = mup[k] = 0.0;
+        }
+        // columns beyond s_last (at most two, rounding the march to whole
+        // rotations) compute on stale registers and write nothing
+        int slot = 0;
+#pragma unroll 1
+        for (int s = s_first; s <= s_last; s += 3) {
+            column<0>(s, slot);
+            slot = slot + 1 == RING ? 0 : slot + 1;
+            column<1>(s + 1, slot);
+            slot = slot + 1 == RING ? 0 : slot + 1;
+            column<2>(s + 2, slot);
+            slot = slot + 1 == RING ? 0 : slot + 1;
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
     }
+};
+
+template <int SYS, int FORM, bool REV, int LIM, bool CFL>
+__global__ void __launch_bounds__(128, K1_MIN_BLOCKS) k1_fast(AdjStepArgs a) {
+    const int lane = threadIdx.x & 31;
+    __shared__ int s_tile[4];
+    constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL>::NARR;
+    __shared__ __align__(16) double s_ring[4][RING * NARR * 32];
+    const int warp = threadIdx.x >> 5;
+    // persistent warps: pull strip tiles from a global queue until empty
+    for (;;) {
+        if (lane == 0) s_tile[warp] = atomicAdd(a.work_counter, 1);
+        __syncwarp();
+        const int tid = s_tile[warp];
+        __syncwarp();
+        if (tid >= a.ntile) break;
+        const AdjTile T = a.tiles[tid];
+        const AdjPatch p = a.patches[T.patch];
+        Strip<SYS, FORM, REV, LIM, CFL> S;
+        S.smx = 0.0; S.smy = 0.0; S.bad = false;
+        S.run(T, p, a, lane, s_ring[warp]);
+        const double smx = warp_max(S.smx), smy = warp_max(S.smy);
+        const unsigned anybad = __ballot_sync(FULL, S.bad);
+        if (lane == 0) {
+            if (CFL && smx > 0.0) atomic_max_nonneg(&a.speed_max[2 * T.patch], smx);
+            if (CFL && smy > 0.0) atomic_max_nonneg(&a.speed_max[2 * T.patch + 1], smy);
+            if (anybad) a.nonfinite[T.patch] = 1;
+        }
+    }
+}
+
+template <int SYS, int FORM, bool REV, int LIM, bool CFL>
+static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
+    static int blocks_per_sm = 0, sms = 0;
+    if (blocks_per_sm == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL>, 128, 0);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    int blocks = blocks_per_sm * sms;
+    const int need = (a.ntile + 3) / 4;
+    if (blocks > need) blocks = need;
+    k1_fast<SYS, FORM, REV, LIM, CFL><<<blocks, 128, 0, st>>>(a);
+}
+
+template <int SYS, int FORM, bool REV, int LIM>
+static void launch_kernel(const AdjStepArgs& a, cudaStream_t st) {
+    if (a.static_speed) launch_cfl<SYS, FORM, REV, LIM, false>(a, st);
+    else launch_cfl<SYS, FORM, REV, LIM, true>(a, st);
 }
 
 template <int SYS, int FORM, bool REV>
 static void launch_lim(const AdjStepArgs& a, cudaStream_t st) {
-    const int blocks = (a.ntile + 3) / 4;
     switch (a.limiter) {
-        case ADJ_LIM_NONE: k1_fast<SYS, FORM, REV, ADJ_LIM_NONE><<<blocks, 128, 0, st>>>(a); break;
-        case ADJ_LIM_MINMOD: k1_fast<SYS, FORM, REV, ADJ_LIM_MINMOD><<<blocks, 128, 0, st>>>(a); break;
-        case ADJ_LIM_MC: k1_fast<SYS, FORM, REV, ADJ_LIM_MC><<<blocks, 128, 0, st>>>(a); break;
-        default: k1_fast<SYS, FORM, REV, ADJ_LIM_SUPERBEE><<<blocks, 128, 0, st>>>(a); break;
+        case ADJ_LIM_NONE: launch_kernel<SYS, FORM, REV, ADJ_LIM_NONE>(a, st); break;
+        case ADJ_LIM_MINMOD: launch_kernel<SYS, FORM, REV, ADJ_LIM_MINMOD>(a, st); break;
+        case ADJ_LIM_MC: launch_kernel<SYS, FORM, REV, ADJ_LIM_MC>(a, st); break;
+        default: launch_kernel<SYS, FORM, REV, ADJ_LIM_SUPERBEE>(a, st); break;
     }
 }
 

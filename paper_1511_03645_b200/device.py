@@ -92,6 +92,8 @@ class LevelStore:
         self.ghost_src = 0
         self._tiles = {}
         self._scratch = {}
+        self._dry = None
+        self._static_speed = None
         for k, p in enumerate(patches):
             self._attach(p, k)
 
@@ -274,10 +276,31 @@ class LevelStore:
             self._scratch[name] = t
         return t
 
+    def static_speed(self):
+        """Per patch (x, y): the largest material speed of the cells the CFL
+        face ranges touch (solver.py:457-460).  Equal to the per-face |speed|
+        maximum whenever no cell is dry; cached on the device."""
+        if getattr(self, "_static_speed", None) is None:
+            g = self.g
+            sp = np.zeros((len(self.patches), 2))
+            for k, p in enumerate(self.patches):
+                c = np.asarray(p.aux.c, dtype=float)
+                if self.ndim == 2:
+                    sp[k, 0] = np.max(c[g - 1:c.shape[0] - g + 1, g:c.shape[1] - g])
+                    sp[k, 1] = np.max(c[g:c.shape[0] - g, g - 1:c.shape[1] - g + 1])
+                else:
+                    sp[k, 0] = np.max(c[g - 1:c.shape[0] - g + 1])
+            self._static_speed = _torch().from_numpy(sp.reshape(-1).copy()).to("cuda")
+        return self._static_speed
+
     def any_dry(self) -> bool:
+        """Whether any cell of the level is dry (cached; materials are static
+        and re-sampled only through sample_patch_material, which resets it)."""
         if not self.swe:
             return False
-        return any(bool(np.any(~p.aux.wet)) for p in self.patches)
+        if self._dry is None:
+            self._dry = any(bool(np.any(~p.aux.wet)) for p in self.patches)
+        return self._dry
 
 
 # ---------------------------------------------------------------------------
@@ -361,13 +384,22 @@ def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ra
     _lib.check(_lib.lib().adj_fill_ghost_rects(_lib.C.byref(a)), "adj_fill_ghost_rects")
 
 
-def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=None):
-    """K2 physical phase on every patch of the store (solver.py:125-146)."""
+def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=None, slots=None):
+    """K2 physical phase on every patch of the store (solver.py:125-146);
+    ``slots`` restricts it to a subset of patches."""
     store.sync_in(stream)
     table = store.edges_table(level_shape)
     if not np.any(store.table_np["edges"]):
         return
-    store.prepare_write(full_ghosts=store.all_edges_physical(level_shape), stream=stream)
+    full = store.all_edges_physical(level_shape)
+    if slots is not None:
+        sub = store.table_np.copy()
+        keep = np.zeros(len(sub), dtype=bool)
+        keep[list(slots)] = True
+        sub["edges"][~keep] = 0
+        table = _dev_table(sub)
+        full = full and bool(np.all(keep))
+    store.prepare_write(full_ghosts=full, stream=stream)
     a = _lib.AdjPhysArgs()
     a.q = _ptr(store.buf[store.cur])
     a.patches = _ptr(table)
@@ -399,6 +431,7 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     tiles, ntile = store.tiles(variant)
     smax = store.scratch("smax", 2 * npatch, torch.float64)
     bad = store.scratch("nonfinite", npatch, torch.int32)
+    counter = store.scratch("work_counter", 1, torch.int32)
     system, form, rev = equation.kernel_spec()
     spec0 = store.patches[0].spec
     a = _lib.AdjStepArgs()
@@ -409,6 +442,8 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     a.tiles = _ptr(tiles)
     a.speed_max = _ptr(smax)
     a.nonfinite = _ptr(bad)
+    a.work_counter = _ptr(counter)
+    a.static_speed = _ptr(store.static_speed()) if variant == _lib.VARIANT_FAST and store.ndim == 2 else 0
     a.comp_stride = store.plane
     a.aux_stride = store.plane
     a.npatch = npatch

@@ -106,6 +106,8 @@ def sample_patch_material(patch: Patch, equation: EquationSet, boundary: Boundar
     others = {f.name: getattr(mat, f.name) for f in dataclasses.fields(mat) if f.name not in arrays}
     patch.aux = type(mat)(**arrays, **others)
     if patch._store is not None:
+        patch._store._dry = None
+        patch._store._static_speed = None
         av = patch._store.aux_view(patch._slot)
         import torch
         for k, pl in enumerate(patch.aux.planes()):
