@@ -322,6 +322,7 @@ def solve_adjoint(equation, boundary, functional: FunctionalSpec, window: TimeWi
 
     def on_output(t_rev, p):
         k = len(labels)
+        st.sync_in()
         st.fold_ghosts()
         ring[len(ring) - 1 - k].copy_(st.view(p._slot)[inner])
         labels.append(t_rev)

@@ -166,14 +166,50 @@ int fill_ghost_rects(const AdjGhostArgs& a) {
 }
 
 // ---------------------------------------------------------------------------
-// K4 restriction.  numpy's mean over the (r, r) child block sums each child
-// row sequentially, adds the row sums in order, then divides by r*r
-// (verified bitwise for r = 2, 4); the SWE variant weights by the wet mask.
+// K4 restriction.  numpy's mean over the (r, r) child block (amr.py:440-450)
+// sums each child row sequentially and adds the row sums in order, then
+// divides by r*r -- except when the coarse box is one cell wide in y: numpy
+// then reduces the r*r block as one flat row-major run with its pairwise
+// summation (8 partial sums once n >= 8).  Both orders are reproduced so the
+// result is bitwise equal; the SWE variant weights by the wet mask.
+ADJ_D double block_sum(const double* f, const double* wet, int64_t pitch, int fi0, int fj0, int r, int rj,
+                       bool flat) {
+    auto val = [&](int p, int q) {
+        const int64_t o = (int64_t)(fi0 + p) * pitch + fj0 + q;
+        return wet ? f[o] * (wet[o] > 0.0 ? 1.0 : 0.0) : f[o];
+    };
+    if (flat) {
+        const int n = r * rj;
+        if (n < 8) {
+            double s = val(0, 0);
+            for (int e = 1; e < n; ++e) s = s + val(e / rj, e % rj);
+            return s;
+        }
+        double acc[8];
+        for (int e = 0; e < 8; ++e) acc[e] = val(e / rj, e % rj);
+        int e = 8;
+        for (; e + 8 <= n; e += 8)
+            for (int j = 0; j < 8; ++j) acc[j] = acc[j] + val((e + j) / rj, (e + j) % rj);
+        double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        for (; e < n; ++e) s = s + val(e / rj, e % rj);
+        return s;
+    }
+    double tot = 0.0;
+    for (int p = 0; p < r; ++p) {
+        double s = val(p, 0);
+        for (int q = 1; q < rj; ++q) s = s + val(p, q);
+        tot = p == 0 ? s : tot + s;
+    }
+    return tot;
+}
+
 __global__ void k4_restrict(AdjRestrictArgs a) {
     const AdjRect R = a.rects[blockIdx.x];
     const AdjPatch cp = a.coarse_patches[R.dst_patch];
     const AdjPatch fp = a.fine_patches[R.src_patch];
     const int r = a.ratio;
+    const int rj = a.ndim == 2 ? r : 1;
+    const bool flat = a.ndim == 2 && R.nj == 1;
     const int64_t n = (int64_t)R.ni * R.nj;
     const int gC = a.ghost_coarse, gF = a.ghost_fine;   // rect coords are interior-local
     for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
@@ -181,23 +217,13 @@ __global__ void k4_restrict(AdjRestrictArgs a) {
         const int ci = gC + R.di0 + di;
         const int cj = (a.ndim == 2 ? gC : 0) + R.dj0 + dj;
         const int fi0 = gF + R.si0 + di * r;
-        const int fj0 = (a.ndim == 2 ? gF : 0) + R.sj0 + dj * r;
+        const int fj0 = (a.ndim == 2 ? gF : 0) + R.sj0 + dj * rj;
         const int64_t cdst = cp.offset + (int64_t)ci * cp.pitch + cj;
-        const int rj = a.ndim == 2 ? r : 1;
         if (!a.swe) {
             const double cnt = (double)(r * rj);
             for (int c = 0; c < a.m; ++c) {
                 const double* f = a.q_fine + c * a.fine_comp_stride + fp.offset;
-                double tot = 0.0;
-                for (int p = 0; p < r; ++p) {
-                    double s = 0.0;
-                    for (int q = 0; q < rj; ++q) {
-                        double v = f[(int64_t)(fi0 + p) * fp.pitch + fj0 + q];
-                        s = q == 0 ? v : s + v;
-                    }
-                    tot = p == 0 ? s : tot + s;
-                }
-                a.q_coarse[c * a.coarse_comp_stride + cdst] = tot / cnt;
+                a.q_coarse[c * a.coarse_comp_stride + cdst] = block_sum(f, nullptr, fp.pitch, fi0, fj0, r, rj, flat) / cnt;
             }
         } else {
             const double* fd = a.aux_fine + a.fine_aux_stride + fp.offset;   // depth plane
@@ -209,17 +235,7 @@ __global__ void k4_restrict(AdjRestrictArgs a) {
             if (!(ws > 0.0 && wetc)) continue;
             for (int c = 0; c < a.m; ++c) {
                 const double* f = a.q_fine + c * a.fine_comp_stride + fp.offset;
-                double tot = 0.0;
-                for (int p = 0; p < r; ++p) {
-                    double s = 0.0;
-                    for (int q = 0; q < rj; ++q) {
-                        int64_t o = (int64_t)(fi0 + p) * fp.pitch + fj0 + q;
-                        double v = f[o] * (fd[o] > 0.0 ? 1.0 : 0.0);
-                        s = q == 0 ? v : s + v;
-                    }
-                    tot = p == 0 ? s : tot + s;
-                }
-                a.q_coarse[c * a.coarse_comp_stride + cdst] = tot / ws;
+                a.q_coarse[c * a.coarse_comp_stride + cdst] = block_sum(f, fd, fp.pitch, fi0, fj0, r, rj, flat) / ws;
             }
         }
     }

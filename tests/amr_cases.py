@@ -37,9 +37,9 @@ CASES = {
         system="ac", ndim=2, xlim=(-4.0, 4.0), ylim=(-4.0, 4.0), base=(24, 24), ratios=(2, 2),
         material=(lambda x, y: np.full_like(np.asarray(x, float), 4.0),
                   lambda x, y: np.ones_like(np.asarray(x, float))),
-        bc=("wall", "wall", "wall", "wall"), ic=_gauss2(-1.0, 1.0, 8.0),
-        strategy="adjoint", functional=("box", (2.0, 3.0, -3.0, -2.0), (1.0, 0.0, 0.0)),
-        window=(1.5, 1.5), adjoint_shape=(32, 32), snapshot_dt=0.1, tol=2e-3,
+        bc=("wall", "wall", "wall", "wall"), ic=_gauss2(0.0, 0.0, 8.0),
+        strategy="adjoint", functional=("box", (1.5, 2.5, -2.5, -1.5), (1.0, 0.0, 0.0)),
+        window=(2.0, 2.0), adjoint_shape=(32, 32), snapshot_dt=0.1, tol=1e-3,
         regrid_interval=2, buffer=2, efficiency=0.7, max_patch_edge=24, steps=6),
     # heterogeneous 2D acoustics, mixed boundaries, ratios 2 then 4
     "ac2d_hetero": dict(

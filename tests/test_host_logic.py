@@ -1,0 +1,58 @@
+"""Host-side AMR bookkeeping vs the reference's golden outputs (CPU only)."""
+import numpy as np
+import pytest
+
+from paper_1511_03645_b200 import amr
+from paper_1511_03645_b200.geometry import Patch, PatchHierarchy, allowed_region_mask
+from tests.golden_io import load
+
+H = load("host.npz")
+CL = sorted(k for k in H if k.startswith("c"))
+
+
+@pytest.mark.parametrize("case", CL)
+def test_cluster_buffer_rectangles(case):
+    d = H[case]
+    mask = d["mask"].astype(bool)
+    nd = mask.ndim
+    me = None if d["max_edge"] < 0 else int(d["max_edge"])
+    boxes = amr.cluster(mask, float(d["eff"]), max_edge=me)
+    got = np.array([[*b.lo, *b.hi, b.efficiency] for b in boxes], dtype=float).reshape(-1, 2 * nd + 1)
+    assert np.array_equal(got, d["boxes"])
+    ff = amr.FlagField(flags=mask, lo=(0,) * nd, level=1, strategy_name="x", time=0.0)
+    assert np.array_equal(amr.buffer_flags(ff, int(d["buf"])).flags, d["buffered"])
+    allowed = d["allowed"].astype(bool)
+    rects = []
+    for b in boxes:
+        rects += amr._allowed_rectangles(b, allowed, mask & allowed)
+    got = np.array([[*b.lo, *b.hi, b.efficiency] for b in rects], dtype=float).reshape(-1, 2 * nd + 1)
+    assert np.array_equal(got, d["rects"])
+
+
+@pytest.mark.parametrize("case", sorted(k for k in H if k.startswith("n")))
+def test_allowed_region(case):
+    d = H[case]
+    h = PatchHierarchy(xlim=(0, 1), ylim=(0, 1), base_shape=(16, 12), ratios=[2])
+    h.levels = [[Patch(h.make_spec(1, tuple(b[:2]), tuple(b[2:])), 3) for b in d["boxes"].reshape(-1, 4)]]
+    assert np.array_equal(allowed_region_mask(h, 1), d["allowed"])
+
+
+def test_ghost_rect_cover_is_exact():
+    """Ghost rectangles of a level cover each in-domain ghost cell exactly once
+    per source kind (same-level sources are disjoint interiors)."""
+    h = PatchHierarchy(xlim=(0, 1), ylim=(0, 1), base_shape=(8, 8), ratios=[2])
+    coarse = [Patch(h.make_spec(1, (0, 0), (7, 7)), 3)]
+    fine = [Patch(h.make_spec(2, lo, hi), 3) for lo, hi in [((2, 2), (7, 9)), ((8, 2), (13, 5)), ((8, 6), (11, 11))]]
+    h.levels = [coarse, fine]
+    crects, copies, covered = amr.build_ghost_rects(h, 2)
+    for k, p in enumerate(fine):
+        ring, phys = amr._ring_and_physical(p.spec, h.level_shape(2))
+        assert covered[k] + phys == ring
+    seen = {}
+    for r in copies:
+        key = r[1]
+        for i in range(r[5]):
+            for j in range(r[6]):
+                cell = (key, r[3] + i, r[4] + j)
+                assert cell not in seen
+                seen[cell] = 1
