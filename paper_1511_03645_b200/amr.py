@@ -477,6 +477,8 @@ def _coarse_old_buffer(cst):
     """Device buffer holding every coarse patch's state_old (uploading host
     copies for patches whose saved state only exists on the host)."""
     import torch
+    if cst.old is not None and bool(np.all(cst.old_valid)):
+        return cst.buf[cst.old]
     need = [p for p in cst.patches if not cst.has_old(p._slot) and p._host_old is not None]
     if need:
         if cst.old is None or cst.old == cst.cur:
@@ -491,6 +493,8 @@ def _coarse_old_buffer(cst):
 
 
 def fill_from_coarse(hierarchy: PatchHierarchy, level: int, t: float, only=None, _rects=None):
+    """In-domain ghosts of one level (or of the patch ``only``) by coarse
+    space-time interpolation (solver.py:227-286)."""
     patches = hierarchy.patches(level)
     coarse = hierarchy.patches(level - 1)
     if level < 2 or not patches or not coarse:
@@ -544,33 +548,60 @@ def _fill_physical_subset(st, slots, boundary, equation, level_shape):
     device.fill_physical(st, boundary, equation, level_shape, slots=slots)
 
 
-class _LevelRects:
-    """Cached ghost/restriction rectangles of one level (rebuilt on regrid)."""
+class LevelPlan:
+    """Launch plan of one level for the batched sweep: its store, the coarse
+    store, device-resident ghost / restriction rectangle tables and the
+    coverage flag.  Rebuilt only when the level's patch list changes (regrid)."""
 
-    def __init__(self, hierarchy, level):
-        self.key = (id(hierarchy), level, tuple(id(p) for p in hierarchy.patches(level)),
-                    tuple(id(p) for p in hierarchy.patches(level - 1)) if level >= 2 else ())
-        self.ghost = build_ghost_rects(hierarchy, level)
+    def __init__(self, hierarchy: PatchHierarchy, level: int):
+        patches = hierarchy.patches(level)
+        self.plist = hierarchy.levels[level - 1]
+        self.n = len(patches)
+        self.ends = (patches[0], patches[-1])
+        self.st = level_store(patches)
+        self.clist = hierarchy.levels[level - 2] if level >= 2 else None
+        coarse = hierarchy.patches(level - 1) if level >= 2 else []
+        self.cst = level_store(coarse) if coarse else None
+        crects, copies, covered = build_ghost_rects(hierarchy, level)
+        self.crects_by_patch = crects
+        allc = [r for rl in crects.values() for r in rl]
+        self.coarse_all = device.RectTable(allc)
+        self.copies = device.RectTable(copies)
         shape = hierarchy.level_shape(level)
-        self.full = True
-        for k, p in enumerate(hierarchy.patches(level)):
-            ring, phys = _ring_and_physical(p.spec, shape)
-            if self.ghost[2][k] + phys < ring:
-                self.full = False
-                break
+        self.full = all(covered[k] + _ring_and_physical(p.spec, shape)[1] >= _ring_and_physical(p.spec, shape)[0]
+                        for k, p in enumerate(patches))
+        self.restrict_to = None      # (coarse store, RectTable) for restriction into level-1
+
+    def valid(self, hierarchy, level) -> bool:
+        ps = hierarchy.levels[level - 1] if level - 1 < len(hierarchy.levels) else None
+        if ps is not self.plist or len(ps) != self.n or not ps or (ps[0], ps[-1]) != self.ends:
+            return False
+        if ps[0]._store is not self.st:
+            return False
+        if level >= 2:
+            cl = hierarchy.levels[level - 2]
+            if cl is not self.clist or (cl and cl[0]._store is not self.cst):
+                return False
+        return True
 
 
-_RECT_CACHE: dict = {}
+def _plan(hierarchy: PatchHierarchy, level: int) -> LevelPlan:
+    plans = hierarchy.__dict__.setdefault("_plans", {})
+    pl = plans.get(level)
+    if pl is None or not pl.valid(hierarchy, level):
+        pl = LevelPlan(hierarchy, level)
+        plans[level] = pl
+    return pl
 
 
-def _level_rects(hierarchy, level):
-    lr = _RECT_CACHE.get((id(hierarchy), level))
-    key = (id(hierarchy), level, tuple(id(p) for p in hierarchy.patches(level)),
-           tuple(id(p) for p in hierarchy.patches(level - 1)) if level >= 2 else ())
-    if lr is None or lr.key != key:
-        lr = _LevelRects(hierarchy, level)
-        _RECT_CACHE[(id(hierarchy), level)] = lr
-    return lr
+def _store_time_mode(cst, t):
+    """(mode, w) shared by every coarse patch, or None when they differ."""
+    if cst.time_synced:
+        has_old = cst.old is not None and bool(np.all(cst.old_valid))
+        probe = cst.patches[0]
+        mode = _coarse_time_mode(probe, t) if has_old or probe._host_old is None else None
+        return mode
+    return None
 
 
 def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrContext):
@@ -579,15 +610,29 @@ def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrC
     patches = hierarchy.patches(level)
     if not patches:
         return
-    st = level_store(patches)
+    pl = _plan(hierarchy, level)
+    st = pl.st
     st.sync_in()
-    lr = _level_rects(hierarchy, level)
-    crects, copies, _ = lr.ghost
-    st.prepare_write(full_ghosts=lr.full)
-    if level >= 2 and crects:
-        fill_from_coarse(hierarchy, level, t, _rects=lr.ghost)
-    if copies:
-        device.copy_rects(st, st, np.array(copies, dtype=_lib.RECT_DTYPE), st.buf[st.cur], st.buf[st.cur])
+    st.prepare_write(full_ghosts=pl.full)
+    if level >= 2 and pl.coarse_all.n:
+        cst = pl.cst
+        cst.sync_in()
+        cst.fold_ghosts()
+        old_buf = _coarse_old_buffer(cst)
+        mw = _store_time_mode(cst, t)
+        r = hierarchy.ratio_to_finer(level - 1)
+        if mw is not None:
+            device.coarse_rects(st, cst, pl.coarse_all, old_buf, cst.buf[cst.cur], hierarchy, r, mw[1], mw[0])
+        else:
+            groups: dict = {}
+            coarse = hierarchy.patches(level - 1)
+            for c, rl in pl.crects_by_patch.items():
+                groups.setdefault(_coarse_time_mode(coarse[c], t), []).extend(rl)
+            for (mode, w), rl in groups.items():
+                device.coarse_rects(st, cst, np.array(rl, dtype=_lib.RECT_DTYPE), old_buf, cst.buf[cst.cur],
+                                    hierarchy, r, w, mode)
+    if pl.copies.n:
+        device.copy_rects(st, st, pl.copies, st.buf[st.cur], st.buf[st.cur])
     device.fill_physical(st, ctx.boundary, ctx.equation, hierarchy.level_shape(level))
     st.ghost_src = st.cur
 
@@ -631,17 +676,14 @@ def restrict_fine_to_coarse(hierarchy: PatchHierarchy, level: int):
     if not fine or not coarse:
         return
     r = hierarchy.ratio_to_finer(level)
-    cst = level_store(coarse)
-    fst = level_store(fine)
+    fpl = _plan(hierarchy, level + 1)
+    cst, fst = fpl.cst, fpl.st
     cst.sync_in()
     fst.sync_in()
-    key = ("restrict", id(cst), id(fst))
-    rects = cst._tiles.get(key)
-    if rects is None:
-        rects = _restrict_rects(coarse, fine, r)
-        cst._tiles[key] = rects
+    if fpl.restrict_to is None or fpl.restrict_to[0] is not cst:
+        fpl.restrict_to = (cst, device.RectTable(_restrict_rects(coarse, fine, r)))
     cst._unalias()
-    device.restrict_rects(cst, fst, rects, r, cst.swe)
+    device.restrict_rects(cst, fst, fpl.restrict_to[1], r, cst.swe)
 
 
 # ---------------------------------------------------------------------------
@@ -703,8 +745,8 @@ def _fill_new_level(hierarchy, lev, new, old, parents, t):
     """New interiors: space(-time) interpolation from the parents, then the
     old patches' overlapping interiors (amr.py:504-551), on the device."""
     st = device.LevelStore(new)
-    for p in new:
-        p._loc = "device"          # contents are produced here, nothing to upload
+    st.set_all_device()            # contents are produced here, nothing to upload
+    st.set_level_times(t, None)
     cst = level_store(parents)
     cst.sync_in()
     cst.fold_ghosts()
@@ -761,37 +803,65 @@ def _retry_half_steps(st, slot, patch, dt, ctx):
 
 def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext):
     """save_old + step of every patch of the level in one K1 launch, with the
-    reference's per-patch CFL retry and cell-step accounting (amr.py:620-631)."""
+    reference's per-patch CFL retry and cell-step accounting (amr.py:620-631).
+
+    On the fast path (no dry cells) the CFL bound is the static per-patch
+    material speed, so no device->host sync is needed; non-finite results are
+    accumulated on the device and raised at the end of the top-level advance."""
     patches = hierarchy.patches(level)
-    st = level_store(patches)
+    pl = _plan(hierarchy, level)
+    st = pl.st
+    t = patches[0].time
     st.save_old_all()
-    for p in patches:
-        p.time_old = p.time
+    st.set_level_times(t, t)
     out = st._free(st.cur)
     smax, bad = device.launch_step(st, dt, ctx.equation, ctx.limiter, ctx.variant, out)
     spec = patches[0].spec
     dtdx = dt / spec.dx
     dtdy = dt / spec.dy if spec.ndim == 2 else 0.0
-    sm = smax.cpu().numpy()
+    static = ctx.variant == _lib.VARIANT_FAST and st.ndim == 2 and not st.any_dry()
+    sm = st.static_speed_np() if static else smax.cpu().numpy()
     cfl = sm[:, 0] * dtdx if spec.ndim == 1 else np.maximum(sm[:, 0] * dtdx, sm[:, 1] * dtdy)
-    nonfinite = bad.cpu().numpy()
     st.ghost_src = st.cur
     st.cur = out
-    for k, p in enumerate(patches):
-        cells = int(np.prod(p.spec.shape))
-        if cfl[k] > 1.0 + 1e-12:
-            _retry_half_steps(st, k, p, dt, ctx)
-            ctx.count_step(level, 2 * cells)
-        else:
-            ctx.count_step(level, cells)
-            if nonfinite[k]:
-                p.time += dt
-                raise NumericalBlowupError(f"non-finite state at t={p.time}")
-        p._loc = "device"
+    st.set_all_device()
+    retry = np.flatnonzero(cfl > 1.0 + 1e-12)
+    extra = int(sum(int(np.prod(patches[k].spec.shape)) for k in retry))
+    ctx.count_step(level, st.total_cells + extra)
+    for k in retry:
+        _retry_half_steps(st, int(k), patches[int(k)], dt, ctx)
+    if static:
+        ctx.__dict__.setdefault("_pending_bad", []).append((bad.amax(), t + dt))
+    else:
+        nf = bad.cpu().numpy()
+        if np.any(nf):
+            raise NumericalBlowupError(f"non-finite state at t={t + dt}")
+
+
+def _raise_pending(ctx):
+    pend = ctx.__dict__.pop("_pending_bad", [])
+    if not pend:
+        return
+    import torch
+    flags = torch.stack([b for b, _ in pend]).cpu().numpy()
+    hit = np.flatnonzero(flags)
+    if hit.size:
+        raise NumericalBlowupError(f"non-finite state at t={pend[int(hit[0])][1]}")
 
 
 def advance_hierarchy(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext):
     """Advance one level by dt, recursively subcycling finer levels (amr.py:602-644)."""
+    depth = ctx.__dict__.get("_depth", 0)
+    ctx._depth = depth + 1
+    try:
+        _advance(hierarchy, level, dt, ctx)
+    finally:
+        ctx._depth = depth
+    if depth == 0:
+        _raise_pending(ctx)
+
+
+def _advance(hierarchy, level, dt, ctx):
     count = ctx.step_counts.get(level, 0)
     if level < hierarchy.max_levels and count > 0 and count % ctx.regrid_interval == 0:
         regrid(hierarchy, level + 1, ctx)
@@ -802,8 +872,8 @@ def advance_hierarchy(hierarchy: PatchHierarchy, level: int, dt: float, ctx: Amr
     fill_level_ghosts(hierarchy, level, t, ctx)
     step_level(hierarchy, level, dt, ctx)
     t_new = t + dt
-    for p in patches:
-        p.time = t_new
+    st = patches[0]._store
+    st.set_level_times(t_new, t)
     if ctx.on_level_advanced is not None:
         ctx.on_level_advanced(hierarchy, level, t_new)
     ctx.step_counts[level] = count + 1
@@ -811,5 +881,5 @@ def advance_hierarchy(hierarchy: PatchHierarchy, level: int, dt: float, ctx: Amr
         fill_level_ghosts(hierarchy, level, t_new, ctx)
         ratio = hierarchy.ratio_to_finer(level)
         for _ in range(ratio):
-            advance_hierarchy(hierarchy, level + 1, dt / ratio, ctx)
+            _advance(hierarchy, level + 1, dt / ratio, ctx)
         restrict_fine_to_coarse(hierarchy, level)

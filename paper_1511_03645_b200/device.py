@@ -94,6 +94,13 @@ class LevelStore:
         self._scratch = {}
         self._dry = None
         self._static_speed = None
+        self._static_speed_np = None
+        self.all_device = False
+        self.time_synced = False
+        self.level_time = 0.0
+        self.level_time_old = None
+        self.total_cells = int(sum(int(np.prod(p.spec.shape)) for p in patches))
+        self.nonfinite_acc = None
         for k, p in enumerate(patches):
             self._attach(p, k)
 
@@ -117,11 +124,39 @@ class LevelStore:
         av = self.aux_view(slot)
         for k, pl in enumerate(planes):
             av[k].copy_(_torch().from_numpy(np.ascontiguousarray(pl, dtype=float)))
+        patch._time = patch.time          # detach level-synchronised fields of a previous store
+        patch._time_old = patch.time_old
+        patch._loc_own = "host"           # uploaded by sync_in
         patch._store = self
         patch._slot = slot
-        patch._loc = "host"     # uploaded by sync_in
         if patch._host_old is not None:
             self.old_valid[slot] = False
+
+    # ------------------------------------------- level-synchronised fields
+    def set_all_device(self):
+        """Every patch's authoritative state is in cur (O(1))."""
+        self.all_device = True
+
+    def break_all_device(self):
+        for p in self.patches:
+            if p._store is self:
+                p._loc_own = "device"
+        self.all_device = False
+
+    def set_level_times(self, t, t_old):
+        """All patches share (time, time_old) (O(1))."""
+        self.time_synced = True
+        self.level_time = float(t)
+        self.level_time_old = None if t_old is None else float(t_old)
+
+    def break_time_sync(self):
+        if not self.time_synced:
+            return
+        self.time_synced = False
+        for p in self.patches:
+            if p._store is self:
+                p._time = self.level_time
+                p._time_old = self.level_time_old
 
     # ------------------------------------------------------------ buffers
     def _ensure_buf(self, i):
@@ -167,6 +202,8 @@ class LevelStore:
     # ----------------------------------------------------------- coherence
     def sync_in(self, stream=None):
         """Upload every patch whose authoritative state is on the host."""
+        if self.all_device:
+            return
         pending = [p for p in self.patches if p._store is self and p._loc == "host"]
         if not pending:
             return
@@ -290,8 +327,13 @@ class LevelStore:
                     sp[k, 1] = np.max(c[g:c.shape[0] - g, g - 1:c.shape[1] - g + 1])
                 else:
                     sp[k, 0] = np.max(c[g - 1:c.shape[0] - g + 1])
+            self._static_speed_np = sp
             self._static_speed = _torch().from_numpy(sp.reshape(-1).copy()).to("cuda")
         return self._static_speed
+
+    def static_speed_np(self):
+        self.static_speed()
+        return self._static_speed_np
 
     def any_dry(self) -> bool:
         """Whether any cell of the level is dry (cached; materials are static
@@ -322,10 +364,26 @@ def ring_copy(store: LevelStore, src, dst, stream=None):
     copy_rects(store, store, arr, src, dst, stream)
 
 
+class RectTable:
+    """A rectangle list resident on the device (built once per regrid)."""
+
+    def __init__(self, rects_np):
+        rects_np = np.asarray(rects_np, dtype=_lib.RECT_DTYPE)
+        self.n = len(rects_np)
+        self.max_cells = int(np.max(rects_np["ni"] * rects_np["nj"])) if self.n else 0
+        self.dev = _dev_table(rects_np) if self.n else None
+        self.np = rects_np
+
+
+def _as_table(rects):
+    return rects if isinstance(rects, RectTable) else RectTable(rects)
+
+
 def copy_rects(dst_store, src_store, rects_np, src_buf, dst_buf, stream=None):
-    if len(rects_np) == 0:
+    tab = _as_table(rects_np)
+    if tab.n == 0:
         return
-    rects = _dev_table(rects_np)
+    rects = tab.dev
     a = _lib.AdjGhostArgs()
     a.q_dst = _ptr(dst_buf)
     a.q_src = _ptr(src_buf)
@@ -336,23 +394,24 @@ def copy_rects(dst_store, src_store, rects_np, src_buf, dst_buf, stream=None):
     a.rects = _ptr(rects)
     a.dst_comp_stride = dst_store.plane
     a.src_comp_stride = src_store.plane
-    a.nrect = len(rects_np)
+    a.nrect = tab.n
     a.ndim = dst_store.ndim
     a.m = dst_store.m
     a.ghost_dst = dst_store.g
     a.ghost_src = src_store.g
     a.ratio = 1
     a.time_mode = 0
-    a.max_rect_cells = int(np.max(rects_np["ni"] * rects_np["nj"]))
+    a.max_rect_cells = tab.max_cells
     a.stream = _lib.stream_ptr(stream)
     _lib.check(_lib.lib().adj_fill_ghost_rects(_lib.C.byref(a)), "adj_fill_ghost_rects")
 
 
 def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ratio, w_time, mode,
                  dst_buf=None, stream=None):
-    if len(rects_np) == 0:
+    tab = _as_table(rects_np)
+    if tab.n == 0:
         return
-    rects = _dev_table(rects_np)
+    rects = tab.dev
     fine_level = fine_store.patches[0].spec.level
     wf = hierarchy.widths(fine_level)
     wc = hierarchy.widths(fine_level - 1)
@@ -367,7 +426,7 @@ def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ra
     a.rects = _ptr(rects)
     a.dst_comp_stride = fine_store.plane
     a.src_comp_stride = coarse_store.plane
-    a.nrect = len(rects_np)
+    a.nrect = tab.n
     a.ndim = fine_store.ndim
     a.m = fine_store.m
     a.ghost_dst = fine_store.g
@@ -379,7 +438,7 @@ def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ra
     a.dx_c, a.dy_c = wc[0], wc[1]
     a.w_time = w_time
     a.time_mode = mode
-    a.max_rect_cells = int(np.max(rects_np["ni"] * rects_np["nj"]))
+    a.max_rect_cells = tab.max_cells
     a.stream = _lib.stream_ptr(stream)
     _lib.check(_lib.lib().adj_fill_ghost_rects(_lib.C.byref(a)), "adj_fill_ghost_rects")
 
@@ -463,9 +522,10 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
 
 
 def restrict_rects(coarse_store, fine_store, rects_np, ratio, swe, stream=None):
-    if len(rects_np) == 0:
+    tab = _as_table(rects_np)
+    if tab.n == 0:
         return
-    rects = _dev_table(rects_np)
+    rects = tab.dev
     a = _lib.AdjRestrictArgs()
     a.q_coarse = _ptr(coarse_store.buf[coarse_store.cur])
     a.q_fine = _ptr(fine_store.buf[fine_store.cur])
@@ -478,12 +538,12 @@ def restrict_rects(coarse_store, fine_store, rects_np, ratio, swe, stream=None):
     a.fine_comp_stride = fine_store.plane
     a.coarse_aux_stride = coarse_store.plane
     a.fine_aux_stride = fine_store.plane
-    a.nrect = len(rects_np)
+    a.nrect = tab.n
     a.ndim = coarse_store.ndim
     a.m = coarse_store.m
     a.ratio = ratio
     a.swe = int(swe)
-    a.max_rect_cells = int(np.max(rects_np["ni"] * rects_np["nj"]))
+    a.max_rect_cells = tab.max_cells
     a.ghost_coarse = coarse_store.g
     a.ghost_fine = fine_store.g
     a.stream = _lib.stream_ptr(stream)

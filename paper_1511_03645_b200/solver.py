@@ -137,6 +137,8 @@ def level_store(patches: list[Patch]) -> device.LevelStore:
             old = p.state_old if p._store.has_old(p._slot) else p._host_old
             _ = p.state                   # pull the authoritative state to the host
             p._host_old = None if old is None else np.array(old, copy=True)
+            p._time, p._time_old = p.time, p.time_old
+            p._loc_own = "host"
             p._store = None
     return device.LevelStore(patches)
 
