@@ -94,6 +94,104 @@ def build_c4(n=N):
     return h, p, eq, bc, dt
 
 
+C5_STEPS_NOTE = ("C5: 3-level acoustics hierarchy (K=4, rho=1), base 1024^2 in 1024 patches of 32^2, "
+                 "ratios 2, 4; 32^2 fine patches from seed 3 covering ~40% / nested; 1 step = one coarse "
+                 "step of advance_hierarchy (ghost fill + step + restriction on 11 level-steps)")
+
+
+def c5_layout(seed=3, cover=0.40):
+    """Patch boxes of the C5 hierarchy (global index boxes per level)."""
+    rng = np.random.default_rng(seed)
+    n1 = 1024
+    lvl1 = [((i * 32, j * 32), (i * 32 + 31, j * 32 + 31)) for i in range(n1 // 32) for j in range(n1 // 32)]
+    # level 2: 64x64 slots of 32^2 fine cells; grow flagged clusters (discs) until ~40% of slots
+    slots2 = np.zeros((64, 64), bool)
+    yy, xx = np.meshgrid(np.arange(64), np.arange(64), indexing="ij")
+    while slots2.mean() < cover:
+        cx, cy = rng.uniform(4, 60, size=2)
+        r = rng.uniform(3, 9)
+        slots2 |= (xx - cx) ** 2 + (yy - cy) ** 2 <= r * r
+    lvl2 = [((i * 32, j * 32), (i * 32 + 31, j * 32 + 31)) for i, j in zip(*np.nonzero(slots2))]
+    # level 3: 256x256 slots (each 8x8 level-2 cells); allowed where the level-2
+    # union eroded by one level-2 cell contains the footprint (proper nesting)
+    m2 = np.kron(slots2, np.ones((32, 32), bool))          # 2048^2 level-2 mask
+    pad = np.pad(m2, 1, mode="edge")
+    er = np.ones_like(m2)
+    for di in range(3):
+        for dj in range(3):
+            er &= pad[di:di + 2048, dj:dj + 2048]
+    foot = er.reshape(256, 8, 256, 8).all(axis=(1, 3))
+    cand = np.argwhere(foot)
+    target = int(round(0.35 * len(lvl1 + lvl2) + 0.0))
+    want = min(len(cand), 4096 - len(lvl1) - len(lvl2))
+    pick = rng.permutation(len(cand))[:want] if want < len(cand) else np.arange(len(cand))
+    del target
+    lvl3 = [((int(i) * 32, int(j) * 32), (int(i) * 32 + 31, int(j) * 32 + 31)) for i, j in sorted(map(tuple, cand[pick]))]
+    return lvl1, lvl2, lvl3
+
+
+def build_c5(variant):
+    from paper_1511_03645_b200 import adjoint, amr, solver
+    from paper_1511_03645_b200 import equations as E
+    from paper_1511_03645_b200.geometry import PatchHierarchy
+    eq = E.Acoustics2D(E.AcousticsMaterialModel(lambda x, y: np.full_like(np.asarray(x, float), 4.0),
+                                                lambda x, y: np.ones_like(np.asarray(x, float))))
+    bc = solver.BoundarySpec()
+    ctx = amr.AmrContext(equation=eq, boundary=bc, strategy=amr.EverywhereFlagging(), limiter="MC",
+                         regrid_interval=10 ** 9, variant=variant)
+    h = PatchHierarchy(xlim=(0.0, 1.0), ylim=(0.0, 1.0), base_shape=(1024, 1024), ratios=[2, 4])
+    h.levels = []
+    for lev, boxes in enumerate(c5_layout(), start=1):
+        ps = []
+        for lo, hi in boxes:
+            p = amr.make_patch(h, lev, lo, hi, ctx, time=0.0)
+            cs = p.spec.cell_centers()
+            X, Y = np.meshgrid(cs[0], cs[1], indexing="ij")
+            p.interior()[0] = np.exp(-200.0 * ((X - 0.45) ** 2 + (Y - 0.55) ** 2))
+            ps.append(p)
+        h.levels.append(ps)
+    dt = solver.select_dt(h, eq, 0.9)
+    del adjoint
+    return h, eq, ctx, dt
+
+
+def bench_c5(steps, warmup, variant):
+    """Level sweep of the C5 hierarchy; cell-updates counted as amr.py:623-631 does."""
+    import torch
+    from paper_1511_03645_b200 import amr
+    t0 = time.perf_counter()
+    h, eq, ctx, dt = build_c5(variant)
+    setup = time.perf_counter() - t0
+    for _ in range(warmup):
+        amr.advance_hierarchy(h, 1, dt, ctx)
+    graph = amr.SweepGraph(h, dt, ctx)          # capture two coarse steps, replay
+    graph.advance(2)
+    torch.cuda.synchronize()
+    steps += steps % 2
+    c0 = sum(ctx.cell_steps.values())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record()
+    graph.advance(steps)
+    e1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    ms = e0.elapsed_time(e1)
+    cells = sum(ctx.cell_steps.values()) - c0
+    npatch = [len(h.patches(l)) for l in (1, 2, 3)]
+    # eager (one host-orchestrated launch sequence per coarse step), for reference
+    e0.record()
+    for _ in range(2):
+        amr.advance_hierarchy(h, 1, dt, ctx)
+    e1.record()
+    torch.cuda.synchronize()
+    eager_ms = e0.elapsed_time(e1) / 2
+    return {"value": cells / (ms * 1e-3), "unit": "cell-updates/s", "ms_per_coarse_step": ms / steps,
+            "eager_ms_per_coarse_step": eager_ms, "cuda_graph": True,
+            "host_wall_ms_per_coarse_step": 1e3 * wall / steps, "cell_updates_per_coarse_step": cells // steps,
+            "patches_per_level": npatch, "setup_s": setup, "workload": C5_STEPS_NOTE}
+
+
 def adjoint_ring(nsnap, na=1024, device="cuda"):
     """Synthetic adjoint snapshots on the 1024^2 grid: a pulse leaving the
     20x20-cell coastal box near x'=0.9 and spreading backward in time."""
@@ -258,6 +356,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--no-c5", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -328,6 +427,7 @@ def main():
 
     # ---- e2e through the public API with host buffers
     e2e = bench_e2e(p, eq, bc, shape, dt, variant, min(args.steps, 5))
+    c5 = None if args.no_c5 else bench_c5(min(args.steps, 10), 3, variant)
 
     line = {
         "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
@@ -343,6 +443,7 @@ def main():
                      "bytes_per_cell_update": BYTES_PER_CELL_SWE, "cells_per_launch": N * N,
                      "kernel_cell_updates_per_s": N * N / (k1 * 1e-3)},
         "flagging": flag,
+        "c5_batched_patches": c5,
         "e2e": e2e,
         "gpu_launches": args.steps * 4,
         "clocks": clk.summary(),

@@ -164,6 +164,7 @@ typedef struct AdjGhostArgs {
     double dx_f, dy_f;           /* fine widths                                   */
     double dx_c, dy_c;           /* coarse widths                                 */
     double w_time;               /* clip((t-t0)/(t1-t0),0,1)                      */
+    const double* w_time_dev;    /* optional: read w from device memory (graph replay) */
     int32_t time_mode;           /* 0: old only, 1: blend old/new, 2: new only    */
     int32_t max_rect_cells;
     void* stream;

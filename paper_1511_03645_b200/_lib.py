@@ -68,7 +68,7 @@ class AdjGhostArgs(C.Structure):
                 ("dst_comp_stride", I64), ("src_comp_stride", I64),
                 ("nrect", I32), ("ndim", I32), ("m", I32), ("ghost_dst", I32), ("ghost_src", I32),
                 ("ratio", I32), ("origin_x", D), ("origin_y", D), ("dx_f", D), ("dy_f", D),
-                ("dx_c", D), ("dy_c", D), ("w_time", D), ("time_mode", I32),
+                ("dx_c", D), ("dy_c", D), ("w_time", D), ("w_time_dev", P), ("time_mode", I32),
                 ("max_rect_cells", I32), ("stream", P)]
 
 
@@ -125,10 +125,16 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     return lib
 
 
+_cuda_ok = None
+
+
 def lib() -> C.CDLL:
     """The loaded library; raises when the CUDA path is unavailable."""
-    import torch
-    if not torch.cuda.is_available():
+    global _cuda_ok
+    if _cuda_ok is None:
+        import torch
+        _cuda_ok = bool(torch.cuda.is_available())
+    if not _cuda_ok:
         raise NativeUnavailableError("no CUDA device: the adjamr B200 path has no CPU fallback")
     return load_library()
 

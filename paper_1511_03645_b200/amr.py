@@ -831,7 +831,13 @@ def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext
     for k in retry:
         _retry_half_steps(st, int(k), patches[int(k)], dt, ctx)
     if static:
-        ctx.__dict__.setdefault("_pending_bad", []).append((bad.amax(), t + dt))
+        if not device.SHADOW:
+            import torch
+            acc = ctx.__dict__.get("_bad_acc")
+            if acc is None:
+                acc = ctx._bad_acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+            torch.maximum(acc, bad.amax().reshape(1), out=acc)
+            ctx._bad_pending = True
     else:
         nf = bad.cpu().numpy()
         if np.any(nf):
@@ -839,14 +845,15 @@ def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext
 
 
 def _raise_pending(ctx):
-    pend = ctx.__dict__.pop("_pending_bad", [])
-    if not pend:
+    """Device-accumulated non-finite flag of the fast path (one sync per
+    top-level advance; skipped while a sweep is being captured or shadowed)."""
+    if not ctx.__dict__.get("_bad_pending") or ctx.__dict__.get("_defer_checks"):
         return
-    import torch
-    flags = torch.stack([b for b, _ in pend]).cpu().numpy()
-    hit = np.flatnonzero(flags)
-    if hit.size:
-        raise NumericalBlowupError(f"non-finite state at t={pend[int(hit[0])][1]}")
+    ctx._bad_pending = False
+    acc = ctx._bad_acc
+    if int(acc.item()):
+        acc.zero_()
+        raise NumericalBlowupError("non-finite state during the advance")
 
 
 def advance_hierarchy(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext):
@@ -883,3 +890,87 @@ def _advance(hierarchy, level, dt, ctx):
         for _ in range(ratio):
             _advance(hierarchy, level + 1, dt / ratio, ctx)
         restrict_fine_to_coarse(hierarchy, level)
+
+
+class SweepGraph:
+    """CUDA-graph replay of the level sweep (advance_hierarchy without regrid).
+
+    The launch sequence of two coarse steps is fixed once plans exist, and the
+    buffer rotation of every level store has period two, so two coarse steps
+    are captured once and replayed.  The host bookkeeping (times, step and
+    cell counters, buffer roles) is kept exact by re-running the orchestration
+    in shadow mode (device.SHADOW: nothing is launched) before every replay.
+    Only valid on the static-CFL fast path (fast variant, 2D, no dry cells)
+    and while no regrid is due; ``advance`` checks both."""
+
+    def __init__(self, hierarchy: PatchHierarchy, dt: float, ctx: AmrContext):
+        import torch
+        self.h, self.dt, self.ctx = hierarchy, dt, ctx
+        if ctx.variant != _lib.VARIANT_FAST or hierarchy.ndim != 2:
+            raise ValueError("SweepGraph needs the fast 2D path")
+        for _ in range(2):                      # warm-up: plans, stores, buffers, caches
+            advance_hierarchy(hierarchy, 1, dt, ctx)
+        for lev in range(1, hierarchy.num_levels() + 1):
+            st = _plan(hierarchy, lev).st
+            if st.any_dry():
+                raise ValueError("SweepGraph needs a level without dry cells")
+            for i in range(st.NBUF):
+                st._ensure_buf(i)
+        torch.cuda.synchronize()
+        before = self._roles()
+        self.params = device.ParamSlots()
+        self.graph = torch.cuda.CUDAGraph()
+        ctx._defer_checks = True
+        device.PARAMS = self.params
+        try:
+            with torch.cuda.graph(self.graph):
+                for _ in range(2):
+                    advance_hierarchy(hierarchy, 1, dt, ctx)
+        finally:
+            ctx._defer_checks = False
+            device.PARAMS = None
+        self.params.upload()
+        if self._roles() != before:
+            raise RuntimeError("level sweep is not 2-periodic; cannot replay")
+        self.graph.replay()                     # the device catches up with the captured steps
+
+    def _roles(self):
+        out = []
+        for lev in range(1, self.h.num_levels() + 1):
+            st = _plan(self.h, lev).st
+            out.append((id(st), st.cur, st.old, st.ghost_src))
+        return out
+
+    def _regrid_due(self, steps: int) -> bool:
+        c = self.ctx.step_counts
+        for lev in range(1, self.h.max_levels):
+            n = c.get(lev, 0)
+            per = 1
+            for l2 in range(1, lev):
+                per *= self.h.ratio_to_finer(l2)
+            if any((n + k) > 0 and (n + k) % self.ctx.regrid_interval == 0 for k in range(steps * per)):
+                return True
+        return False
+
+    def advance(self, coarse_steps: int):
+        """Advance by an even number of coarse steps (graph replays)."""
+        if coarse_steps % 2:
+            raise ValueError("SweepGraph advances in pairs of coarse steps")
+        if self._regrid_due(coarse_steps):
+            raise ValueError("a regrid falls inside the replayed steps")
+        for _ in range(coarse_steps // 2):
+            device.SHADOW = True
+            device.PARAMS = self.params
+            self.params.rewind()
+            self.ctx._defer_checks = True
+            try:
+                for _ in range(2):
+                    advance_hierarchy(self.h, 1, self.dt, self.ctx)
+            finally:
+                device.SHADOW = False
+                device.PARAMS = None
+                self.ctx._defer_checks = False
+            self.params.upload()
+            self.graph.replay()
+        self.ctx._bad_pending = True
+        _raise_pending(self.ctx)

@@ -138,21 +138,29 @@ __global__ void k2_rects(AdjGhostArgs a) {
             axis_weights(y, loy, a.dy_c, ncy, &j0, &wy);
             j1 = min(j0 + 1, ncy - 1);
         }
+        // graph replays read the weight from device memory; a negative value
+        // there means "old state only" (w == 0 or t1 == t0, solver.py:280-284)
+        double wt = a.w_time;
+        int tmode = a.time_mode;
+        if (a.w_time_dev) {
+            wt = *a.w_time_dev;
+            tmode = wt < 0.0 ? 0 : 1;
+        }
         for (int c = 0; c < a.m; ++c) {
             double vo = 0.0, vn = 0.0;
             const double* po = a.q_coarse_old + c * a.src_comp_stride + sp.offset;
             const double* pn = a.q_coarse_new + c * a.src_comp_stride + sp.offset;
             if (a.ndim == 2) {
-                if (a.time_mode != 2) vo = interp_patch2(po, sp.pitch, i0, j0, i1, j1, wx, wy);
-                if (a.time_mode != 0) vn = interp_patch2(pn, sp.pitch, i0, j0, i1, j1, wx, wy);
+                if (tmode != 2) vo = interp_patch2(po, sp.pitch, i0, j0, i1, j1, wx, wy);
+                if (tmode != 0) vn = interp_patch2(pn, sp.pitch, i0, j0, i1, j1, wx, wy);
             } else {
-                if (a.time_mode != 2) vo = po[i0] * (1.0 - wx) + po[i1] * wx;
-                if (a.time_mode != 0) vn = pn[i0] * (1.0 - wx) + pn[i1] * wx;
+                if (tmode != 2) vo = po[i0] * (1.0 - wx) + po[i1] * wx;
+                if (tmode != 0) vn = pn[i0] * (1.0 - wx) + pn[i1] * wx;
             }
             double v;
-            if (a.time_mode == 0) v = vo;
-            else if (a.time_mode == 2) v = vn;
-            else v = (1.0 - a.w_time) * vo + a.w_time * vn;
+            if (tmode == 0) v = vo;
+            else if (tmode == 2) v = vn;
+            else v = (1.0 - wt) * vo + wt * vn;
             a.q_dst[c * a.dst_comp_stride + dst] = v;
         }
     }

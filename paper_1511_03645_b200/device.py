@@ -25,6 +25,46 @@ from . import _lib
 
 _SLACK = 64   # elements of slack after each plane set (strip loads may over-read)
 
+# Shadow mode: the host bookkeeping of a level sweep runs (buffer rotation,
+# times, counters) but no work is launched -- used to keep the host state in
+# step with CUDA-graph replays of the same sweep (amr.SweepGraph).
+SHADOW = False
+
+
+class ParamSlots:
+    """Per-launch scalar parameters of a captured sweep that change between
+    replays (the coarse-to-fine time weight).  During capture every
+    coarse-rect launch takes the next slot and reads its weight from device
+    memory; shadow runs rewrite the host copy in the same order; ``upload``
+    refreshes the device copy before a replay."""
+
+    def __init__(self, cap=1024):
+        import torch
+        self.cap = cap
+        self.vals: list[float] = []
+        self.dev = torch.zeros(cap, dtype=torch.float64, device="cuda")
+
+    def take(self, w: float) -> int:
+        k = len(self.vals)
+        if k >= self.cap:
+            raise RuntimeError("too many time-weight slots in one captured sweep")
+        self.vals.append(float(w))
+        return int(self.dev.data_ptr()) + 8 * k
+
+    def upload(self):
+        """Stream-ordered copy of the slot values (a fresh pinned staging
+        buffer per upload; torch keeps it alive until the copy ran)."""
+        import torch
+        if self.vals:
+            h = torch.tensor(self.vals, dtype=torch.float64).pin_memory()
+            self.dev[: len(self.vals)].copy_(h, non_blocking=True)
+
+    def rewind(self):
+        self.vals = []
+
+
+PARAMS: ParamSlots | None = None
+
 
 def _torch():
     import torch
@@ -100,6 +140,9 @@ class LevelStore:
         self.level_time = 0.0
         self.level_time_old = None
         self.total_cells = int(sum(int(np.prod(p.spec.shape)) for p in patches))
+        self.max_ghost_cells = max(NX_ * NY_ - (NX_ - 2 * self.g) * (NY_ - 2 * self.g if self.ndim == 2 else NY_)
+                                   for (_, NX_, NY_, _) in self.boxes)
+        self._phys_args = {}
         self.nonfinite_acc = None
         for k, p in enumerate(patches):
             self._attach(p, k)
@@ -176,7 +219,8 @@ class LevelStore:
         """Make cur writable without touching the saved old buffer."""
         if self.old is not None and self.old == self.cur:
             nb = self._free(self.cur, self.ghost_src)
-            self.buf[nb].copy_(self.buf[self.cur])
+            if not SHADOW:
+                self.buf[nb].copy_(self.buf[self.cur])
             if self.ghost_src == self.cur:
                 self.ghost_src = nb
             self.cur = nb
@@ -257,6 +301,8 @@ class LevelStore:
 
     # ------------------------------------------------------------- tables
     def edges_table(self, level_shape):
+        """Patch table with edge bits for this level shape (all patches), and
+        the compacted table of the patches that touch the domain boundary."""
         key = tuple(level_shape)
         if self._edges_key != key:
             tab = self.table_np.copy()
@@ -276,6 +322,8 @@ class LevelStore:
             self.table_np = tab
             self.table = _dev_table(tab)
             self._edges_key = key
+            sel = tab[tab["edges"] != 0]
+            self._edge_tab = (_dev_table(sel), len(sel))
         return self.table
 
     def all_edges_physical(self, level_shape) -> bool:
@@ -351,6 +399,8 @@ class LevelStore:
 
 def ring_copy(store: LevelStore, src, dst, stream=None):
     """Copy every patch's ghost ring from buffer src to buffer dst."""
+    if SHADOW:
+        return
     rects = []
     g = store.g
     for k, (off, NX, NY, pitch) in enumerate(store.boxes):
@@ -381,7 +431,7 @@ def _as_table(rects):
 
 def copy_rects(dst_store, src_store, rects_np, src_buf, dst_buf, stream=None):
     tab = _as_table(rects_np)
-    if tab.n == 0:
+    if tab.n == 0 or SHADOW:
         return
     rects = tab.dev
     a = _lib.AdjGhostArgs()
@@ -411,6 +461,13 @@ def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ra
     tab = _as_table(rects_np)
     if tab.n == 0:
         return
+    wptr = 0
+    if PARAMS is not None:          # captured sweep: the weight (mode) is read from device memory
+        if mode == 2:
+            raise RuntimeError("coarse patches without saved state cannot be graph-replayed")
+        wptr = PARAMS.take(w_time if mode == 1 else -1.0)
+    if SHADOW:
+        return
     rects = tab.dev
     fine_level = fine_store.patches[0].spec.level
     wf = hierarchy.widths(fine_level)
@@ -437,6 +494,7 @@ def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ra
     a.dx_f, a.dy_f = wf[0], wf[1]
     a.dx_c, a.dy_c = wc[0], wc[1]
     a.w_time = w_time
+    a.w_time_dev = wptr
     a.time_mode = mode
     a.max_rect_cells = tab.max_cells
     a.stream = _lib.stream_ptr(stream)
@@ -447,8 +505,9 @@ def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=Non
     """K2 physical phase on every patch of the store (solver.py:125-146);
     ``slots`` restricts it to a subset of patches."""
     store.sync_in(stream)
-    table = store.edges_table(level_shape)
-    if not np.any(store.table_np["edges"]):
+    store.edges_table(level_shape)
+    table, nedge = store._edge_tab
+    if nedge == 0:
         return
     full = store.all_edges_physical(level_shape)
     if slots is not None:
@@ -456,14 +515,19 @@ def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=Non
         keep = np.zeros(len(sub), dtype=bool)
         keep[list(slots)] = True
         sub["edges"][~keep] = 0
-        table = _dev_table(sub)
+        sub = sub[sub["edges"] != 0]
+        table, nedge = _dev_table(sub), len(sub)
         full = full and bool(np.all(keep))
+        if nedge == 0:
+            return
     store.prepare_write(full_ghosts=full, stream=stream)
+    if SHADOW:
+        return
     a = _lib.AdjPhysArgs()
     a.q = _ptr(store.buf[store.cur])
     a.patches = _ptr(table)
     a.comp_stride = store.plane
-    a.npatch = len(store.patches)
+    a.npatch = nedge
     a.ndim = store.ndim
     a.ghost = store.g
     a.m = store.m
@@ -472,8 +536,7 @@ def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=Non
         a.bc[k] = _lib.BC_WALL if sd == "wall" else _lib.BC_OUTFLOW
     a.normal_comp[0] = equation.normal_component(0)
     a.normal_comp[1] = equation.normal_component(1) if store.ndim == 2 else -1
-    a.max_ghost_cells = max(NX * NY - (NX - 2 * store.g) * (NY - 2 * store.g if store.ndim == 2 else NY)
-                            for (_, NX, NY, _) in store.boxes)
+    a.max_ghost_cells = store.max_ghost_cells
     a.stream = _lib.stream_ptr(stream)
     _lib.check(_lib.lib().adj_fill_physical(_lib.C.byref(a)), "adj_fill_physical")
 
@@ -491,6 +554,8 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     smax = store.scratch("smax", 2 * npatch, torch.float64)
     bad = store.scratch("nonfinite", npatch, torch.int32)
     counter = store.scratch("work_counter", 1, torch.int32)
+    if SHADOW:
+        return smax[: 2 * npatch].view(npatch, 2), bad[:npatch]
     system, form, rev = equation.kernel_spec()
     spec0 = store.patches[0].spec
     a = _lib.AdjStepArgs()
@@ -523,7 +588,7 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
 
 def restrict_rects(coarse_store, fine_store, rects_np, ratio, swe, stream=None):
     tab = _as_table(rects_np)
-    if tab.n == 0:
+    if tab.n == 0 or SHADOW:
         return
     rects = tab.dev
     a = _lib.AdjRestrictArgs()
