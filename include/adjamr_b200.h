@@ -106,13 +106,20 @@ typedef struct AdjStepArgs {
     const double* static_speed;/* optional device (x, y) per patch: material speed bound over the
                                   CFL ranges; when given, the FAST variant (no dry cells) copies it
                                   to speed_max instead of reducing per face (same values) */
+    const int32_t* job_offsets;/* optional (FAST + static_speed): warp job j = tiles[job_offsets[j],
+                                  job_offsets[j+1]); each tile of a job is a row strip placed at
+                                  lanes [pad, pad + nj + 4) of the warp, all with the same ni */
+    int32_t njob, pad2;
     int64_t comp_stride, aux_stride;
     int32_t npatch, ntile;
     int32_t ndim, ghost;
-    int32_t system, form, reversed, limiter, variant, pad;
+    int32_t system, form, reversed, limiter, variant, flags;   /* ADJ_STEP_* bits */
     double dt, dtdx, dtdy, gravity;
     void* stream;              /* cudaStream_t */
 } AdjStepArgs;
+/* AdjStepArgs.flags */
+#define ADJ_STEP_KEEP_NONFINITE 1   /* do not zero nonfinite: accumulate over launches */
+#define ADJ_STEP_NO_SPEED_OUT   2   /* do not write speed_max (caller uses static_speed) */
 int adj_step_level(const AdjStepArgs* a);
 
 /* Tile shape (ni, nj) the given variant expects in AdjStepArgs.tiles. */
@@ -151,20 +158,24 @@ typedef struct AdjRect {
     int32_t pad;
 } AdjRect;
 typedef struct AdjGhostArgs {
-    double* q_dst;               /* fine (or same) level store                   */
-    const double* q_src;         /* COPY source: same level store (may == q_dst) */
-    const double* q_coarse_old;  /* COARSE: coarse level state at t0             */
-    const double* q_coarse_new;  /* COARSE: coarse level state at t1             */
+    double* q_dst;               /* destination level store                        */
+    const double* q_src;         /* COPY source level store (may == q_dst)          */
+    const double* q_coarse_old;  /* COARSE: coarse level state at t0                */
+    const double* q_coarse_new;  /* COARSE: coarse level state at t1                */
     const AdjPatch* dst_patches; /* device */
-    const AdjPatch* src_patches; /* device (COPY: same level; COARSE: coarse)   */
-    const AdjRect* rects;        /* device */
-    int64_t dst_comp_stride, src_comp_stride;
+    const AdjPatch* src_patches; /* device, COPY sources                            */
+    const AdjPatch* coarse_patches; /* device, COARSE sources                       */
+    const AdjRect* rects;        /* device; COPY and COARSE rects may be mixed when disjoint */
+    int64_t dst_comp_stride, src_comp_stride, coarse_comp_stride;
     int32_t nrect, ndim, m, ghost_dst, ghost_src, ratio;
     double origin_x, origin_y;   /* hierarchy.origin                              */
     double dx_f, dy_f;           /* fine widths                                   */
     double dx_c, dy_c;           /* coarse widths                                 */
     double w_time;               /* clip((t-t0)/(t1-t0),0,1)                      */
     const double* w_time_dev;    /* optional: read w from device memory (graph replay) */
+    const double* axis_w;        /* optional per-rect axis weights: COARSE rect r has its ni x-weights at
+                                    axis_w[rect.pad], then its nj y-weights (geometry.py:248-260) */
+    const int32_t* axis_i;       /* matching lower stencil indices (same layout)               */
     int32_t time_mode;           /* 0: old only, 1: blend old/new, 2: new only    */
     int32_t max_rect_cells;
     void* stream;
@@ -215,6 +226,12 @@ typedef struct AdjFlagArgs {
     double* best;                /* device, per-interior-cell values or NULL  */
     const int64_t* best_offset;  /* device, per patch start into best, or NULL */
     int32_t* status;             /* device, 1 int: ADJ_ERR_OUT_OF_RANGE bits  */
+    const double* axis_w;        /* optional per-patch row (x) then column (y) weights into the
+                                    adjoint grid (interpolate_uniform arithmetic, host-precomputed);
+                                    patch k's rows start at axis_off[2k], columns at axis_off[2k+1] */
+    const int32_t* axis_i;       /* matching lower stencil indices                               */
+    const int32_t* axis_dry;     /* matching _adjoint_dry_at cell indices (SWE), or NULL         */
+    const int64_t* axis_off;     /* 2 per patch                                                  */
     int64_t comp_stride, aux_stride;
     int32_t npatch, ndim, m, ghost, swe, mode, nidx, nxa, nya, max_cells;
     double origin_x, origin_y, dx, dy;             /* forward level geometry   */

@@ -23,6 +23,7 @@ VARIANT_EXACT, VARIANT_FAST = 0, 1
 EDGE_XLO, EDGE_XHI, EDGE_YLO, EDGE_YHI = 1, 2, 4, 8
 BC_WALL, BC_OUTFLOW = 0, 1
 RECT_COPY, RECT_COARSE = 0, 1
+STEP_KEEP_NONFINITE, STEP_NO_SPEED_OUT = 1, 2
 
 
 class NativeUnavailableError(RuntimeError):
@@ -49,10 +50,11 @@ P, D, I32, I64 = C.c_void_p, C.c_double, C.c_int32, C.c_int64
 
 class AdjStepArgs(C.Structure):
     _fields_ = [("q_in", P), ("q_out", P), ("aux", P), ("patches", P), ("tiles", P),
-                ("speed_max", P), ("nonfinite", P), ("work_counter", P), ("static_speed", P), ("comp_stride", I64), ("aux_stride", I64),
+                ("speed_max", P), ("nonfinite", P), ("work_counter", P), ("static_speed", P), ("job_offsets", P),
+                ("njob", I32), ("pad2", I32), ("comp_stride", I64), ("aux_stride", I64),
                 ("npatch", I32), ("ntile", I32), ("ndim", I32), ("ghost", I32),
                 ("system", I32), ("form", I32), ("reversed", I32), ("limiter", I32),
-                ("variant", I32), ("pad", I32),
+                ("variant", I32), ("flags", I32),
                 ("dt", D), ("dtdx", D), ("dtdy", D), ("gravity", D), ("stream", P)]
 
 
@@ -64,11 +66,11 @@ class AdjPhysArgs(C.Structure):
 
 class AdjGhostArgs(C.Structure):
     _fields_ = [("q_dst", P), ("q_src", P), ("q_coarse_old", P), ("q_coarse_new", P),
-                ("dst_patches", P), ("src_patches", P), ("rects", P),
-                ("dst_comp_stride", I64), ("src_comp_stride", I64),
+                ("dst_patches", P), ("src_patches", P), ("coarse_patches", P), ("rects", P),
+                ("dst_comp_stride", I64), ("src_comp_stride", I64), ("coarse_comp_stride", I64),
                 ("nrect", I32), ("ndim", I32), ("m", I32), ("ghost_dst", I32), ("ghost_src", I32),
                 ("ratio", I32), ("origin_x", D), ("origin_y", D), ("dx_f", D), ("dy_f", D),
-                ("dx_c", D), ("dy_c", D), ("w_time", D), ("w_time_dev", P), ("time_mode", I32),
+                ("dx_c", D), ("dy_c", D), ("w_time", D), ("w_time_dev", P), ("axis_w", P), ("axis_i", P), ("time_mode", I32),
                 ("max_rect_cells", I32), ("stream", P)]
 
 
@@ -84,7 +86,8 @@ class AdjRestrictArgs(C.Structure):
 class AdjFlagArgs(C.Structure):
     _fields_ = [("q", P), ("aux", P), ("patches", P), ("ring", P), ("adj_wet", P),
                 ("snap_index", P), ("interp_w", P), ("flag_bits", P), ("counts", P), ("best", P),
-                ("best_offset", P), ("status", P), ("comp_stride", I64), ("aux_stride", I64),
+                ("best_offset", P), ("status", P), ("axis_w", P), ("axis_i", P), ("axis_dry", P),
+                ("axis_off", P), ("comp_stride", I64), ("aux_stride", I64),
                 ("npatch", I32), ("ndim", I32), ("m", I32), ("ghost", I32), ("swe", I32),
                 ("mode", I32), ("nidx", I32), ("nxa", I32), ("nya", I32), ("max_cells", I32),
                 ("origin_x", D), ("origin_y", D), ("dx", D), ("dy", D),

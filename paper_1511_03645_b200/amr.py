@@ -396,9 +396,39 @@ def _rect(kind, dst, src, dlo, dspec, extent, slo=None, sspec=None):
     return (kind, dst, src, di[0], di[1], extent[0], extent[1], si[0], si[1], 0)
 
 
-def build_ghost_rects(hierarchy: PatchHierarchy, level: int, only=None):
+def _subtract(box, holes):
+    """Cells of ``box`` (lo, hi) not in any of ``holes``, as rectangles
+    (row runs along the box's longer axis; ghost strips are 2 cells thick)."""
+    (lo, hi) = box
+    shape = tuple(h - l + 1 for l, h in zip(lo, hi))
+    m = np.ones(shape, dtype=bool)
+    for hl, hh in holes:
+        ib = _intersect(lo, hi, hl, hh)
+        if ib is not None:
+            m[tuple(slice(a - l, b - l + 1) for a, b, l in zip(ib[0], ib[1], lo))] = False
+    if m.all():
+        return [box]
+    out = []
+    if m.ndim == 1:
+        for a, b in _runs(m):
+            out.append(((lo[0] + a,), (lo[0] + b,)))
+        return out
+    if shape[0] <= shape[1]:
+        for i in range(shape[0]):
+            for a, b in _runs(m[i]):
+                out.append(((lo[0] + i, lo[1] + a), (lo[0] + i, lo[1] + b)))
+    else:
+        for j in range(shape[1]):
+            for a, b in _runs(m[:, j]):
+                out.append(((lo[0] + a, lo[1] + j), (lo[0] + b, lo[1] + j)))
+    return out
+
+
+def build_ghost_rects(hierarchy: PatchHierarchy, level: int, only=None, disjoint: bool = False):
     """Rectangles for the in-domain ghost phases of one level:
     coarse rects grouped by coarse patch, then same-level copy rects.
+    ``disjoint``: coarse rects exclude the cells a same-level copy overwrites
+    (same final values, one launch, less interpolation).
     Returns (coarse {coarse slot: [rect]}, copy [rect], covered cells per patch)."""
     patches = hierarchy.patches(level)
     shape = hierarchy.level_shape(level)
@@ -420,14 +450,7 @@ def build_ghost_rects(hierarchy: PatchHierarchy, level: int, only=None):
             if box is None:
                 continue
             # physical cells of this strip are out of domain; in-domain part only
-            if coarse:
-                for c in _candidates(cf_lo, cf_hi, *box):
-                    ib = _intersect(*box, tuple(cf_lo[c]), tuple(cf_hi[c]))
-                    if ib is not None:
-                        ext = [h - l + 1 for l, h in zip(*ib)]
-                        coarse_rects.setdefault(int(c), []).append(
-                            _rect(_lib.RECT_COARSE, k, int(c), ib[0], p.spec, ext))
-                        covered[k] += int(np.prod(ext))
+            holes = []
             for o in _candidates(same_lo, same_hi, *box):
                 if o == k:
                     continue
@@ -436,8 +459,26 @@ def build_ghost_rects(hierarchy: PatchHierarchy, level: int, only=None):
                     ext = [h - l + 1 for l, h in zip(*ib)]
                     copy_rects.append(_rect(_lib.RECT_COPY, k, int(o), ib[0], p.spec, ext, ib[0],
                                             patches[o].spec))
-                    if not coarse:
-                        covered[k] += int(np.prod(ext))
+                    holes.append(ib)
+                    covered[k] += int(np.prod(ext))
+            if coarse:
+                pieces = _subtract(box, holes) if disjoint else [box]
+                for piece in pieces:
+                    for c in _candidates(cf_lo, cf_hi, *piece):
+                        ib = _intersect(*piece, tuple(cf_lo[c]), tuple(cf_hi[c]))
+                        if ib is not None:
+                            ext = [h - l + 1 for l, h in zip(*ib)]
+                            coarse_rects.setdefault(int(c), []).append(
+                                _rect(_lib.RECT_COARSE, k, int(c), ib[0], p.spec, ext))
+                            if disjoint:
+                                covered[k] += int(np.prod(ext))
+                if not disjoint:
+                    # coverage of the strip by coarse interpolation alone
+                    for c in _candidates(cf_lo, cf_hi, *box):
+                        ib = _intersect(*box, tuple(cf_lo[c]), tuple(cf_hi[c]))
+                        if ib is not None:
+                            covered[k] += int(np.prod([h - l + 1 for l, h in zip(*ib)]))
+                    covered[k] -= sum(int(np.prod([h - l + 1 for l, h in zip(*hb)])) for hb in holes)
     return coarse_rects, copy_rects, covered
 
 
@@ -563,10 +604,14 @@ class LevelPlan:
         coarse = hierarchy.patches(level - 1) if level >= 2 else []
         self.cst = level_store(coarse) if coarse else None
         crects, copies, covered = build_ghost_rects(hierarchy, level)
-        self.crects_by_patch = crects
-        allc = [r for rl in crects.values() for r in rl]
-        self.coarse_all = device.RectTable(allc)
+        self.crects_by_patch = crects            # full strips (unsynchronised fallback)
         self.copies = device.RectTable(copies)
+        dcr, _, _ = build_ghost_rects(hierarchy, level, disjoint=True)
+        allc = [r for rl in dcr.values() for r in rl]
+        geom = (self.st, self.cst, hierarchy) if self.cst is not None else None
+        self.coarse_all = device.RectTable(allc, geom if allc else None)
+        # coarse (disjoint from the copies) + copies: one launch when times are synchronised
+        self.combined = device.RectTable(allc + list(copies), geom if allc else None)
         shape = hierarchy.level_shape(level)
         self.full = all(covered[k] + _ring_and_physical(p.spec, shape)[1] >= _ring_and_physical(p.spec, shape)[0]
                         for k, p in enumerate(patches))
@@ -614,6 +659,7 @@ def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrC
     st = pl.st
     st.sync_in()
     st.prepare_write(full_ghosts=pl.full)
+    copies_done = False
     if level >= 2 and pl.coarse_all.n:
         cst = pl.cst
         cst.sync_in()
@@ -622,7 +668,10 @@ def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrC
         mw = _store_time_mode(cst, t)
         r = hierarchy.ratio_to_finer(level - 1)
         if mw is not None:
-            device.coarse_rects(st, cst, pl.coarse_all, old_buf, cst.buf[cst.cur], hierarchy, r, mw[1], mw[0])
+            # disjoint coarse + copy rectangles in one launch
+            device.coarse_rects(st, cst, pl.combined, old_buf, cst.buf[cst.cur], hierarchy, r, mw[1], mw[0],
+                                copy_src=st.buf[st.cur], copy_patches=st.table)
+            copies_done = True
         else:
             groups: dict = {}
             coarse = hierarchy.patches(level - 1)
@@ -631,7 +680,7 @@ def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrC
             for (mode, w), rl in groups.items():
                 device.coarse_rects(st, cst, np.array(rl, dtype=_lib.RECT_DTYPE), old_buf, cst.buf[cst.cur],
                                     hierarchy, r, w, mode)
-    if pl.copies.n:
+    if pl.copies.n and not copies_done:
         device.copy_rects(st, st, pl.copies, st.buf[st.cur], st.buf[st.cur])
     device.fill_physical(st, ctx.boundary, ctx.equation, hierarchy.level_shape(level))
     st.ghost_src = st.cur
@@ -763,7 +812,7 @@ def _fill_new_level(hierarchy, lev, new, old, parents, t):
                     _rect(_lib.RECT_COARSE, k, int(c), ib[0], p.spec, ext))
     old_buf = _coarse_old_buffer(cst)
     for (mode, w), rl in groups.items():
-        device.coarse_rects(st, cst, np.array(rl, dtype=_lib.RECT_DTYPE), old_buf, cst.buf[cst.cur],
+        device.coarse_rects(st, cst, device.RectTable(rl, (st, cst, hierarchy)), old_buf, cst.buf[cst.cur],
                             hierarchy, r, w, mode)
     if old:
         ost = level_store(old)
@@ -815,11 +864,11 @@ def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext
     st.save_old_all()
     st.set_level_times(t, t)
     out = st._free(st.cur)
-    smax, bad = device.launch_step(st, dt, ctx.equation, ctx.limiter, ctx.variant, out)
+    static = ctx.variant == _lib.VARIANT_FAST and st.ndim == 2 and not st.any_dry()
+    smax, bad = device.launch_step(st, dt, ctx.equation, ctx.limiter, ctx.variant, out, accumulate=static)
     spec = patches[0].spec
     dtdx = dt / spec.dx
     dtdy = dt / spec.dy if spec.ndim == 2 else 0.0
-    static = ctx.variant == _lib.VARIANT_FAST and st.ndim == 2 and not st.any_dry()
     sm = st.static_speed_np() if static else smax.cpu().numpy()
     cfl = sm[:, 0] * dtdx if spec.ndim == 1 else np.maximum(sm[:, 0] * dtdx, sm[:, 1] * dtdy)
     st.ghost_src = st.cur
@@ -831,13 +880,9 @@ def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext
     for k in retry:
         _retry_half_steps(st, int(k), patches[int(k)], dt, ctx)
     if static:
-        if not device.SHADOW:
-            import torch
-            acc = ctx.__dict__.get("_bad_acc")
-            if acc is None:
-                acc = ctx._bad_acc = torch.zeros(1, dtype=torch.int32, device="cuda")
-            torch.maximum(acc, bad.amax().reshape(1), out=acc)
-            ctx._bad_pending = True
+        # non-finite flags accumulate in the store (no per-step reduction)
+        ctx.__dict__.setdefault("_bad_stores", {})[id(st)] = st
+        ctx._bad_pending = True
     else:
         nf = bad.cpu().numpy()
         if np.any(nf):
@@ -850,9 +895,14 @@ def _raise_pending(ctx):
     if not ctx.__dict__.get("_bad_pending") or ctx.__dict__.get("_defer_checks"):
         return
     ctx._bad_pending = False
-    acc = ctx._bad_acc
-    if int(acc.item()):
-        acc.zero_()
+    stores = list(ctx.__dict__.get("_bad_stores", {}).values())
+    ctx._bad_stores = {}
+    hit = False
+    for st in stores:
+        if st.nonfinite_acc is not None and bool(st.nonfinite_acc.any().item()):
+            st.nonfinite_acc.zero_()
+            hit = True
+    if hit:
         raise NumericalBlowupError("non-finite state during the advance")
 
 

@@ -58,15 +58,20 @@ int adj_step_level(const AdjStepArgs* a) {
     if (a->limiter < ADJ_LIM_NONE || a->limiter > ADJ_LIM_SUPERBEE) return adj::bad("limiter");
     if (!(a->dt > 0.0)) return adj::bad("dt must be positive");
     cudaStream_t st = (cudaStream_t)a->stream;
-    int rc;
-    if (a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed)
-        rc = adj::record_cuda(cudaMemcpyAsync(a->speed_max, a->static_speed, sizeof(double) * 2 * a->npatch,
-                                              cudaMemcpyDeviceToDevice, st), "copy static_speed");
-    else
+    int rc = ADJ_OK;
+    const bool static_cfl = a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed;
+    if (static_cfl) {
+        if (!(a->flags & ADJ_STEP_NO_SPEED_OUT))
+            rc = adj::record_cuda(cudaMemcpyAsync(a->speed_max, a->static_speed, sizeof(double) * 2 * a->npatch,
+                                                  cudaMemcpyDeviceToDevice, st), "copy static_speed");
+    } else {
         rc = adj::record_cuda(cudaMemsetAsync(a->speed_max, 0, sizeof(double) * 2 * a->npatch, st), "memset speed_max");
+    }
     if (rc) return rc;
-    rc = adj::record_cuda(cudaMemsetAsync(a->nonfinite, 0, sizeof(int32_t) * a->npatch, st), "memset nonfinite");
-    if (rc) return rc;
+    if (!(a->flags & ADJ_STEP_KEEP_NONFINITE)) {
+        rc = adj::record_cuda(cudaMemsetAsync(a->nonfinite, 0, sizeof(int32_t) * a->npatch, st), "memset nonfinite");
+        if (rc) return rc;
+    }
     rc = adj::record_cuda(cudaMemsetAsync(a->work_counter, 0, sizeof(int32_t), st), "memset work_counter");
     if (rc) return rc;
     if (a->variant == ADJ_VARIANT_EXACT) return adj::step_exact(*a, st);
@@ -81,7 +86,8 @@ int adj_fill_physical(const AdjPhysArgs* a) {
 }
 
 int adj_fill_ghost_rects(const AdjGhostArgs* a) {
-    if (!a || !a->q_dst || !a->rects || !a->dst_patches || !a->src_patches) return adj::bad("null pointer");
+    if (!a || !a->q_dst || !a->rects || !a->dst_patches || !(a->src_patches || a->coarse_patches))
+        return adj::bad("null pointer");
     if (a->time_mode < 0 || a->time_mode > 2) return adj::bad("time_mode");
     return adj::fill_ghost_rects(*a);
 }

@@ -199,7 +199,8 @@ ADJ_D void transverse(double f0, double h, const Mat& b, const Mat& a,
 
 struct Raw { double q0, q1, q2, c, z; };
 
-constexpr int RING = 6;   // columns in flight per warp (cp.async prefetch distance)
+constexpr int GROUPS = 2;          // cp.async groups (of 3 columns) in flight per warp
+constexpr int RING = 3 * GROUPS;   // column slots of the per-warp ring
 
 // One warp's march along x over an output strip.  Every carried quantity
 // lives in a 3-slot ring indexed by (column mod 3); column<K> is the body of
@@ -212,7 +213,7 @@ struct Strip {
     const double* __restrict__ aux;
     double* __restrict__ qout;
     int64_t cs, as;
-    int pitch, g, i0, ni, s_last;
+    int pitch, g, i0, ni, s_last, colbase;   // s: column relative to the strip (i0 = 0)
     bool out_lane, yface_cfl;
     double dtdx, dtdy, hx, hy;
 
@@ -233,11 +234,10 @@ struct Strip {
 
     static constexpr int NARR = SWE ? 4 : 5;
 
-    // issue the cp.async copies of column s into ring slot (s - s_first) % RING;
-    // one commit group per column, empty groups past the strip end
+    // issue the cp.async copies of column s into ring slot `slot`
     ADJ_D void prefetch(int s, int slot) const {
         if (s <= s_last) {
-            const int64_t o = (int64_t)(g + s) * pitch;
+            const int64_t o = (int64_t)(colbase + s) * pitch;
             const double* src[5] = {qin + o, qin + cs + o, qin + 2 * cs + o, aux + o, aux + as + o};
 #pragma unroll
             for (int k = 0; k < NARR; ++k) {
@@ -245,11 +245,11 @@ struct Strip {
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src[k]) : "memory");
             }
         }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
 
-    ADJ_D Raw fetch(int slot) const {
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(RING - 1) : "memory");
+    ADJ_D static void commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+    ADJ_D Raw read(int slot) const {
         const double* r = ring + slot * NARR * 32 + lane;
         Raw v;
         v.q0 = r[0]; v.q1 = r[32]; v.q2 = r[64]; v.c = r[96];
@@ -258,10 +258,8 @@ struct Strip {
     }
 
     template <int K>
-    ADJ_D void column(int s, int slot) {
+    ADJ_D void column(int s, const Raw& cr) {
         constexpr int C = K, P = (K + 2) % 3, PP = (K + 1) % 3;
-        const Raw cr = fetch(slot);
-        prefetch(s + RING, slot);
         m[C] = make_mat<SYS, FORM>(cr.c, cr.z, dtdx, dtdy);
         // CFL: max |speed| of the faces is the max material speed of the cells
         // they touch (fast path = no dry cells): x-faces of this strip touch
@@ -337,21 +335,24 @@ struct Strip {
             const double d1 = -dtdx * ((sx1[PP] + ft1[P]) - ft1[PP]);
             const double d2 = -dtdy * ((sy2[PP] + gt2[PP]) - gb2);
             const double n0 = q0[PP] + d0, n1 = q1[PP] + d1, n2 = q2[PP] + d2;
-            const int64_t o = (int64_t)(g + s - 2) * pitch;
+            const int64_t o = (int64_t)(colbase + s - 2) * pitch;
             qout[o] = n0; qout[cs + o] = n1; qout[2 * cs + o] = n2;
             bad |= !(isfinite(n0) && isfinite(n1) && isfinite(n2));
         }
     }
 
-    ADJ_D void run(const AdjTile& T, const AdjPatch& p, const AdjStepArgs& a, int lane_, double* ring_) {
+    // Lane setup for a strip T placed at lanes [lane0, lane0 + nj + 4).
+    ADJ_D void setup(const AdjTile& T, const AdjPatch& p, const AdjStepArgs& a, int lane_, int lane0,
+                     double* ring_) {
         lane = lane_;
         ring = ring_;
         g = a.ghost;
+        const int l = lane - lane0;
         const int NY = p.ny + 2 * g;
-        const int jj = g + T.j0 - 2 + lane;
+        const int jj = g + T.j0 - 2 + l;
         const int jl = jj < 0 ? 0 : (jj > NY - 1 ? NY - 1 : jj);
-        out_lane = lane >= 2 && lane < 2 + T.nj;
-        yface_cfl = lane >= 1 && lane < 3 + T.nj;
+        out_lane = l >= 2 && l < 2 + T.nj;
+        yface_cfl = l >= 1 && l < 3 + T.nj;
         cs = a.comp_stride; as = a.aux_stride;
         qin = a.q_in + p.offset + jl;
         aux = a.aux + p.offset + jl;
@@ -359,11 +360,18 @@ struct Strip {
         pitch = p.pitch;
         dtdx = a.dtdx; dtdy = a.dtdy;
         hx = 0.5 * dtdx; hy = 0.5 * dtdy;
-        i0 = T.i0; ni = T.ni;
-        const int s_first = T.i0 - 2;
-        s_last = T.i0 + T.ni + 1;
+        colbase = g + T.i0;
+        i0 = 0; ni = T.ni;
+    }
+
+    ADJ_D void run() {
+        const int s_first = -2;
+        s_last = ni + 1;
 #pragma unroll
-        for (int k = 0; k < RING; ++k) prefetch(s_first + k, k);
+        for (int gI = 0; gI < GROUPS; ++gI) {
+            for (int k = 0; k < 3; ++k) prefetch(s_first + 3 * gI + k, 3 * gI + k);
+            commit();
+        }
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             m[k] = Mat{}; xf[k] = Face{};
@@ -373,15 +381,21 @@ struct Strip {
         }
         // columns beyond s_last (at most two, rounding the march to whole
         // rotations) compute on stale registers and write nothing
-        int slot = 0;
+        int base = 0;
 #pragma unroll 1
         for (int s = s_first; s <= s_last; s += 3) {
-            column<0>(s, slot);
-            slot = slot + 1 == RING ? 0 : slot + 1;
-            column<1>(s + 1, slot);
-            slot = slot + 1 == RING ? 0 : slot + 1;
-            column<2>(s + 2, slot);
-            slot = slot + 1 == RING ? 0 : slot + 1;
+            // one wait per group of three columns, then the group's slots are
+            // refilled with the columns RING ahead
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(GROUPS - 1) : "memory");
+            const Raw r0 = read(base), r1 = read(base + 1), r2 = read(base + 2);
+            prefetch(s + RING, base);
+            prefetch(s + RING + 1, base + 1);
+            prefetch(s + RING + 2, base + 2);
+            commit();
+            column<0>(s, r0);
+            column<1>(s + 1, r1);
+            column<2>(s + 2, r2);
+            base = base + 3 == RING ? 0 : base + 3;
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
     }
@@ -395,24 +409,39 @@ __global__ void __launch_bounds__(128, K1_MIN_BLOCKS) k1_fast(AdjStepArgs a) {
     __shared__ __align__(16) double s_ring[4][RING * NARR * 32];
     const int warp = threadIdx.x >> 5;
     // persistent warps: pull strip tiles from a global queue until empty
+    const int njob = a.job_offsets ? a.njob : a.ntile;
     for (;;) {
         if (lane == 0) s_tile[warp] = atomicAdd(a.work_counter, 1);
         __syncwarp();
-        const int tid = s_tile[warp];
+        const int job = s_tile[warp];
         __syncwarp();
-        if (tid >= a.ntile) break;
-        const AdjTile T = a.tiles[tid];
+        if (job >= njob) break;
+        // this lane's strip: single-strip jobs use all lanes; packed jobs
+        // stack up to four short strips (same ni) along the lanes
+        int tix = job, lane0 = 0;
+        if (a.job_offsets) {
+            const int t0 = a.job_offsets[job], t1 = a.job_offsets[job + 1];
+            tix = t1 - 1;
+            lane0 = a.tiles[tix].pad;
+            for (int t = t0; t < t1 - 1; ++t) {
+                const int next0 = a.tiles[t + 1].pad;
+                if (lane < next0) { tix = t; lane0 = a.tiles[t].pad; break; }
+            }
+        }
+        const AdjTile T = a.tiles[tix];
         const AdjPatch p = a.patches[T.patch];
         Strip<SYS, FORM, REV, LIM, CFL> S;
         S.smx = 0.0; S.smy = 0.0; S.bad = false;
-        S.run(T, p, a, lane, s_ring[warp]);
-        const double smx = warp_max(S.smx), smy = warp_max(S.smy);
-        const unsigned anybad = __ballot_sync(FULL, S.bad);
-        if (lane == 0) {
-            if (CFL && smx > 0.0) atomic_max_nonneg(&a.speed_max[2 * T.patch], smx);
-            if (CFL && smy > 0.0) atomic_max_nonneg(&a.speed_max[2 * T.patch + 1], smy);
-            if (anybad) a.nonfinite[T.patch] = 1;
+        S.setup(T, p, a, lane, lane0, s_ring[warp]);
+        S.run();
+        if (CFL) {   // single-strip jobs only (packed jobs require static_speed)
+            const double smx = warp_max(S.smx), smy = warp_max(S.smy);
+            if (lane == 0) {
+                if (smx > 0.0) atomic_max_nonneg(&a.speed_max[2 * T.patch], smx);
+                if (smy > 0.0) atomic_max_nonneg(&a.speed_max[2 * T.patch + 1], smy);
+            }
         }
+        if (S.bad) a.nonfinite[T.patch] = 1;
     }
 }
 
@@ -427,7 +456,7 @@ static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     int blocks = blocks_per_sm * sms;
-    const int need = (a.ntile + 3) / 4;
+    const int need = ((a.job_offsets ? a.njob : a.ntile) + 3) / 4;
     if (blocks > need) blocks = need;
     k1_fast<SYS, FORM, REV, LIM, CFL><<<blocks, 128, 0, st>>>(a);
 }
@@ -435,7 +464,7 @@ static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
 template <int SYS, int FORM, bool REV, int LIM>
 static void launch_kernel(const AdjStepArgs& a, cudaStream_t st) {
     if (a.static_speed) launch_cfl<SYS, FORM, REV, LIM, false>(a, st);
-    else launch_cfl<SYS, FORM, REV, LIM, true>(a, st);
+    else if (!a.job_offsets) launch_cfl<SYS, FORM, REV, LIM, true>(a, st);
 }
 
 template <int SYS, int FORM, bool REV>

@@ -105,12 +105,19 @@ ADJ_D double interp_patch2(const double* d, int pitch, int i0, int j0, int i1, i
     return v00 * (1.0 - wx) * (1.0 - wy) + v10 * wx * (1.0 - wy) + v01 * (1.0 - wx) * wy + v11 * wx * wy;
 }
 
-__global__ void k2_rects(AdjGhostArgs a) {
-    const AdjRect R = a.rects[blockIdx.x];
+// One warp per rectangle, RECTS_PER_CTA warps per CTA (ghost rectangles are
+// small: 2 x 32 cells for a 32^2 patch side).
+constexpr int RECTS_PER_CTA = 8;
+
+__global__ void __launch_bounds__(32 * RECTS_PER_CTA) k2_rects(AdjGhostArgs a) {
+    const int rid = blockIdx.x * RECTS_PER_CTA + (threadIdx.x >> 5);
+    if (rid >= a.nrect) return;
+    const int lane = threadIdx.x & 31;
+    const AdjRect R = a.rects[rid];
     const AdjPatch dp = a.dst_patches[R.dst_patch];
-    const AdjPatch sp = a.src_patches[R.src_patch];
+    const AdjPatch sp = R.kind == ADJ_RECT_COPY ? a.src_patches[R.src_patch] : a.coarse_patches[R.src_patch];
     const int64_t n = (int64_t)R.ni * R.nj;
-    for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+    for (int64_t t = lane; t < n; t += 32) {
         const int di = (int)(t / R.nj), dj = (int)(t % R.nj);
         const int ii = R.di0 + di, jj = R.dj0 + dj;
         const int64_t dst = dp.offset + (int64_t)ii * dp.pitch + jj;
@@ -121,23 +128,32 @@ __global__ void k2_rects(AdjGhostArgs a) {
             continue;
         }
         // COARSE: fine cell centre -> bilinear weights on the coarse patch incl. ghosts
-        const int gf = a.ghost_dst, gc = a.ghost_src;
-        const int gxi = dp.lo_x - gf + ii;
-        const double x = a.origin_x + (gxi + 0.5) * a.dx_f;
-        const double lox = a.origin_x + (sp.lo_x - gc) * a.dx_c;
+        const int gc = a.ghost_src;
         const int ncx = sp.nx + 2 * gc;
-        int i0; double wx;
-        axis_weights(x, lox, a.dx_c, ncx, &i0, &wx);
-        const int i1 = min(i0 + 1, ncx - 1);
-        int j0 = 0, j1 = 0; double wy = 0.0;
-        if (a.ndim == 2) {
-            const int gyi = dp.lo_y - gf + jj;
-            const double y = a.origin_y + (gyi + 0.5) * a.dy_f;
-            const double loy = a.origin_y + (sp.lo_y - gc) * a.dy_c;
-            const int ncy = sp.ny + 2 * gc;
-            axis_weights(y, loy, a.dy_c, ncy, &j0, &wy);
-            j1 = min(j0 + 1, ncy - 1);
+        int i0, j0 = 0, j1 = 0;
+        double wx, wy = 0.0;
+        if (a.axis_w) {            // host-precomputed (same arithmetic, per rect row / column)
+            i0 = a.axis_i[R.pad + di];
+            wx = a.axis_w[R.pad + di];
+            if (a.ndim == 2) {
+                j0 = a.axis_i[R.pad + R.ni + dj];
+                wy = a.axis_w[R.pad + R.ni + dj];
+            }
+        } else {
+            const int gf = a.ghost_dst;
+            const int gxi = dp.lo_x - gf + ii;
+            const double x = a.origin_x + (gxi + 0.5) * a.dx_f;
+            const double lox = a.origin_x + (sp.lo_x - gc) * a.dx_c;
+            axis_weights(x, lox, a.dx_c, ncx, &i0, &wx);
+            if (a.ndim == 2) {
+                const int gyi = dp.lo_y - gf + jj;
+                const double y = a.origin_y + (gyi + 0.5) * a.dy_f;
+                const double loy = a.origin_y + (sp.lo_y - gc) * a.dy_c;
+                axis_weights(y, loy, a.dy_c, sp.ny + 2 * gc, &j0, &wy);
+            }
         }
+        const int i1 = min(i0 + 1, ncx - 1);
+        if (a.ndim == 2) j1 = min(j0 + 1, sp.ny + 2 * gc - 1);
         // graph replays read the weight from device memory; a negative value
         // there means "old state only" (w == 0 or t1 == t0, solver.py:280-284)
         double wt = a.w_time;
@@ -148,8 +164,8 @@ __global__ void k2_rects(AdjGhostArgs a) {
         }
         for (int c = 0; c < a.m; ++c) {
             double vo = 0.0, vn = 0.0;
-            const double* po = a.q_coarse_old + c * a.src_comp_stride + sp.offset;
-            const double* pn = a.q_coarse_new + c * a.src_comp_stride + sp.offset;
+            const double* po = a.q_coarse_old + c * a.coarse_comp_stride + sp.offset;
+            const double* pn = a.q_coarse_new + c * a.coarse_comp_stride + sp.offset;
             if (a.ndim == 2) {
                 if (tmode != 2) vo = interp_patch2(po, sp.pitch, i0, j0, i1, j1, wx, wy);
                 if (tmode != 0) vn = interp_patch2(pn, sp.pitch, i0, j0, i1, j1, wx, wy);
@@ -168,8 +184,8 @@ __global__ void k2_rects(AdjGhostArgs a) {
 
 int fill_ghost_rects(const AdjGhostArgs& a) {
     if (a.nrect <= 0) return ADJ_OK;
-    int threads = a.max_rect_cells >= 256 ? 256 : (a.max_rect_cells >= 128 ? 128 : 64);
-    k2_rects<<<a.nrect, threads, 0, (cudaStream_t)a.stream>>>(a);
+    const int blocks = (a.nrect + RECTS_PER_CTA - 1) / RECTS_PER_CTA;
+    k2_rects<<<blocks, 32 * RECTS_PER_CTA, 0, (cudaStream_t)a.stream>>>(a);
     return check_launch("k2_rects");
 }
 

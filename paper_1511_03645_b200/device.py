@@ -332,25 +332,51 @@ class LevelStore:
         return bool(np.all(self.table_np["edges"] == full))
 
     def tiles(self, variant):
+        """Work tables of a step variant: (tiles, ntile, job_offsets, njob).
+        FAST 2D: strips of <= 28 rows x <= 128 columns; full strips are one warp
+        job each, the short remainder strips of several patches are packed
+        into shared warp jobs (lanes [pad, pad + nj + 4)), so 32-row patches
+        keep 80% of the lanes busy instead of 50%."""
         if variant not in self._tiles:
             ni_t = _lib.C.c_int32()
             nj_t = _lib.C.c_int32()
             _lib.check(_lib.lib().adj_step_tile_shape(variant, self.ndim, _lib.C.byref(ni_t), _lib.C.byref(nj_t)),
                        "adj_step_tile_shape")
             ti, tj = ni_t.value, nj_t.value
-            rows = []
+            full, short = [], {}
             for k, p in enumerate(self.patches):
                 nx = p.spec.shape[0]
                 ny = p.spec.shape[1] if self.ndim == 2 else 1
-                for j0 in range(0, ny, tj):
-                    for i0 in range(0, nx, ti):
-                        rows.append((k, i0, j0, min(ti, nx - i0), min(tj, ny - j0), 0))
+                for i0 in range(0, nx, ti):
+                    ni = min(ti, nx - i0)
+                    for j0 in range(0, ny, tj):
+                        nj = min(tj, ny - j0)
+                        if variant == _lib.VARIANT_FAST and self.ndim == 2 and nj < tj and nj + 4 <= 16:
+                            short.setdefault(ni, []).append((k, i0, j0, ni, nj, 0))
+                        else:
+                            full.append((k, i0, j0, ni, nj, 0))
             if variant == _lib.VARIANT_FAST and self.ndim == 2:
-                # order: x-segment major, then strips, so concurrently running
-                # warps are y-neighbours and share halo rows through L2
-                rows.sort(key=lambda r: (r[0], r[1], r[2]))
-            arr = np.array(rows, dtype=_lib.TILE_DTYPE)
-            self._tiles[variant] = (_dev_table(arr), len(rows))
+                # x-segment major, then strips: concurrently running warps are
+                # y-neighbours and share halo rows through L2
+                full.sort(key=lambda r: (r[0], r[1], r[2]))
+                rows, offs = list(full), list(range(len(full) + 1))
+                for ni, lst in sorted(short.items()):
+                    lane = 32
+                    for (k, i0, j0, ni_, nj, _) in lst:
+                        if lane + nj + 4 > 32:
+                            lane = 0
+                            offs.append(len(rows))
+                        rows.append((k, i0, j0, ni_, nj, lane))
+                        lane += nj + 4
+                offs = sorted(set(offs + [len(rows)]))
+                arr = np.array(rows, dtype=_lib.TILE_DTYPE)
+                jobs = np.array(offs, dtype=np.int32)
+                self._tiles[variant] = (_dev_table(arr), len(rows), _torch().from_numpy(jobs).to("cuda"),
+                                        len(jobs) - 1)
+            else:
+                rows = full + [r for lst in short.values() for r in lst]
+                arr = np.array(rows, dtype=_lib.TILE_DTYPE)
+                self._tiles[variant] = (_dev_table(arr), len(rows), None, len(rows))
         return self._tiles[variant]
 
     def scratch(self, name, n, dtype):
@@ -415,14 +441,67 @@ def ring_copy(store: LevelStore, src, dst, stream=None):
 
 
 class RectTable:
-    """A rectangle list resident on the device (built once per regrid)."""
+    """A rectangle list resident on the device (built once per regrid).
+    With ``coarse_geom`` = (fine_store, coarse_store, hierarchy) the
+    interpolation weights of every COARSE rect are precomputed per row and
+    column (``axis_weights``) and stored alongside."""
 
-    def __init__(self, rects_np):
-        rects_np = np.asarray(rects_np, dtype=_lib.RECT_DTYPE)
+    def __init__(self, rects_np, coarse_geom=None):
+        rects_np = np.array(rects_np, dtype=_lib.RECT_DTYPE)
         self.n = len(rects_np)
         self.max_cells = int(np.max(rects_np["ni"] * rects_np["nj"])) if self.n else 0
+        self.axis_w = self.axis_i = None
+        if coarse_geom is not None and self.n:
+            w, i = axis_weight_tables(rects_np, *coarse_geom)
+            torch = _torch()
+            self.axis_w = torch.from_numpy(w).to("cuda")
+            self.axis_i = torch.from_numpy(i).to("cuda")
         self.dev = _dev_table(rects_np) if self.n else None
         self.np = rects_np
+
+
+def _axis_weights_np(coord, origin, width, n):
+    """_axis_weights (geometry.py:248-260), vectorised, same IEEE operations."""
+    s = (coord - origin) / width - 0.5
+    i0 = np.floor(s).astype(np.int64)
+    w = s - i0
+    w = np.where(i0 < 0, 0.0, np.where(i0 > n - 2, 1.0, w))
+    i0 = np.clip(i0, 0, max(n - 2, 0))
+    if n == 1:
+        w = np.zeros_like(w)
+    return i0, w
+
+
+def axis_weight_tables(rects, fine_store, coarse_store, hierarchy):
+    """Per COARSE rect: x weights of its rows then y weights of its columns;
+    sets rects["pad"] to the rect's offset into the tables."""
+    level = fine_store.patches[0].spec.level
+    wf = hierarchy.widths(level)
+    wc = hierarchy.widths(level - 1)
+    org = hierarchy.origin
+    gf, gc = fine_store.g, coarse_store.g
+    ws, js = [], []
+    off = 0
+    for r in rects:
+        if r["kind"] != _lib.RECT_COARSE:
+            continue
+        dp = fine_store.patches[int(r["dst_patch"])].spec
+        sp = coarse_store.patches[int(r["src_patch"])].spec
+        axes = [(0, int(r["di0"]), int(r["ni"]))]
+        if fine_store.ndim == 2:
+            axes.append((1, int(r["dj0"]), int(r["nj"])))
+        r["pad"] = off
+        for ax, d0, n in axes:
+            gidx = dp.lo[ax] - gf + d0 + np.arange(n)
+            coord = org[ax] + (gidx + 0.5) * wf[ax]
+            lo_phys = org[ax] + (sp.lo[ax] - gc) * wc[ax]
+            i0, w = _axis_weights_np(coord, lo_phys, wc[ax], sp.shape[ax] + 2 * gc)
+            ws.append(w)
+            js.append(i0.astype(np.int32))
+            off += n
+    if not ws:
+        return np.zeros(1), np.zeros(1, np.int32)
+    return np.concatenate(ws).astype(np.float64), np.concatenate(js).astype(np.int32)
 
 
 def _as_table(rects):
@@ -437,8 +516,6 @@ def copy_rects(dst_store, src_store, rects_np, src_buf, dst_buf, stream=None):
     a = _lib.AdjGhostArgs()
     a.q_dst = _ptr(dst_buf)
     a.q_src = _ptr(src_buf)
-    a.q_coarse_old = a.q_src
-    a.q_coarse_new = a.q_src
     a.dst_patches = _ptr(dst_store.table)
     a.src_patches = _ptr(src_store.table)
     a.rects = _ptr(rects)
@@ -457,7 +534,9 @@ def copy_rects(dst_store, src_store, rects_np, src_buf, dst_buf, stream=None):
 
 
 def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ratio, w_time, mode,
-                 dst_buf=None, stream=None):
+                 dst_buf=None, stream=None, copy_src=None, copy_patches=None):
+    """COARSE rects (and, when given, disjoint same-level COPY rects in the
+    same launch, sourced from ``copy_src`` with the fine store's layout)."""
     tab = _as_table(rects_np)
     if tab.n == 0:
         return
@@ -475,14 +554,16 @@ def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ra
     org = hierarchy.origin
     a = _lib.AdjGhostArgs()
     a.q_dst = _ptr(dst_buf if dst_buf is not None else fine_store.buf[fine_store.cur])
-    a.q_src = _ptr(q_new)
+    a.q_src = _ptr(copy_src)
     a.q_coarse_old = _ptr(q_old)
     a.q_coarse_new = _ptr(q_new)
     a.dst_patches = _ptr(fine_store.table)
-    a.src_patches = _ptr(coarse_store.table)
+    a.src_patches = _ptr(copy_patches)
+    a.coarse_patches = _ptr(coarse_store.table)
     a.rects = _ptr(rects)
     a.dst_comp_stride = fine_store.plane
-    a.src_comp_stride = coarse_store.plane
+    a.src_comp_stride = fine_store.plane
+    a.coarse_comp_stride = coarse_store.plane
     a.nrect = tab.n
     a.ndim = fine_store.ndim
     a.m = fine_store.m
@@ -495,6 +576,8 @@ def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ra
     a.dx_c, a.dy_c = wc[0], wc[1]
     a.w_time = w_time
     a.w_time_dev = wptr
+    a.axis_w = _ptr(tab.axis_w)
+    a.axis_i = _ptr(tab.axis_i)
     a.time_mode = mode
     a.max_rect_cells = tab.max_cells
     a.stream = _lib.stream_ptr(stream)
@@ -541,18 +624,28 @@ def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=Non
     _lib.check(_lib.lib().adj_fill_physical(_lib.C.byref(a)), "adj_fill_physical")
 
 
-def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index, stream=None):
+def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index, stream=None,
+                accumulate=False):
     """K1 on every patch: reads buf[cur], writes buf[out_buf_index].
-    Returns (speed_max (npatch, 2) tensor, nonfinite (npatch,) tensor)."""
+    Returns (speed_max (npatch, 2) tensor, nonfinite (npatch,) tensor).
+    ``accumulate`` (static-CFL fast path only): no per-launch memsets; the
+    non-finite flags accumulate in ``store.nonfinite_acc`` and speed_max is
+    not written (the caller uses the static bound)."""
     if limiter not in _lib.LIMITERS:
         raise ValueError(f"unknown limiter {limiter!r}")
     torch = _torch()
     npatch = len(store.patches)
     if variant == _lib.VARIANT_FAST and store.any_dry():
         variant = _lib.VARIANT_EXACT   # the fast strip kernel has no wet/dry logic
-    tiles, ntile = store.tiles(variant)
+    tiles, ntile, jobs, njob = store.tiles(variant)
     smax = store.scratch("smax", 2 * npatch, torch.float64)
-    bad = store.scratch("nonfinite", npatch, torch.int32)
+    accumulate = accumulate and variant == _lib.VARIANT_FAST and store.ndim == 2
+    if accumulate:
+        if store.nonfinite_acc is None:
+            store.nonfinite_acc = torch.zeros(npatch, dtype=torch.int32, device="cuda")
+        bad = store.nonfinite_acc
+    else:
+        bad = store.scratch("nonfinite", npatch, torch.int32)
     counter = store.scratch("work_counter", 1, torch.int32)
     if SHADOW:
         return smax[: 2 * npatch].view(npatch, 2), bad[:npatch]
@@ -568,6 +661,8 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     a.nonfinite = _ptr(bad)
     a.work_counter = _ptr(counter)
     a.static_speed = _ptr(store.static_speed()) if variant == _lib.VARIANT_FAST and store.ndim == 2 else 0
+    a.job_offsets = _ptr(jobs)
+    a.njob = njob
     a.comp_stride = store.plane
     a.aux_stride = store.plane
     a.npatch = npatch
@@ -577,6 +672,7 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     a.system, a.form, a.reversed = system, form, rev
     a.limiter = _lib.LIMITERS[limiter]
     a.variant = variant
+    a.flags = (_lib.STEP_KEEP_NONFINITE | _lib.STEP_NO_SPEED_OUT) if accumulate else 0
     a.dt = dt
     a.dtdx = dt / spec0.dx
     a.dtdy = dt / spec0.dy if store.ndim == 2 else 0.0
@@ -615,6 +711,49 @@ def restrict_rects(coarse_store, fine_store, rects_np, ratio, swe, stream=None):
     _lib.check(_lib.lib().adj_restrict(_lib.C.byref(a)), "adj_restrict")
 
 
+def flag_axis_tables(store: LevelStore, ring_shape, a_origin, a_dx, a_dy, level_origin, level_dx, level_dy):
+    """Per patch row/column bilinear weights into the adjoint grid, computed
+    once with interpolate_uniform's arithmetic (geometry.py:248-290) and its
+    bounds check (raises OutOfRangeError), plus _adjoint_dry_at indices
+    (adjoint.py:217-224).  Cached per store and adjoint geometry."""
+    key = ("flagtab", tuple(ring_shape), tuple(a_origin), a_dx, a_dy, tuple(level_origin), level_dx, level_dy)
+    hit = store._scratch.get(key)
+    if hit is not None:
+        return hit
+    from .geometry import OutOfRangeError
+    nd = store.ndim
+    n_a = [ring_shape[0]] + ([ring_shape[1]] if nd == 2 else [])
+    widths_a = [a_dx] + ([a_dy] if nd == 2 else [])
+    widths_f = [level_dx] + ([level_dy] if nd == 2 else [])
+    hi0 = a_origin[0] + n_a[0] * widths_a[0]
+    eps = 1e-12 * max(abs(hi0 - a_origin[0]), 1.0)
+    ws, iis, drys, offs = [], [], [], []
+    off = 0
+    for p in store.patches:
+        po = []
+        for ax in range(nd):
+            idx = np.arange(p.spec.lo[ax], p.spec.hi[ax] + 1)
+            coord = level_origin[ax] + (idx + 0.5) * widths_f[ax]
+            hi = a_origin[ax] + n_a[ax] * widths_a[ax]
+            if np.any(coord < a_origin[ax] - eps) or np.any(coord > hi + eps):
+                raise OutOfRangeError("interpolation point outside the adjoint domain")
+            i0, w = _axis_weights_np(coord, a_origin[ax], widths_a[ax], n_a[ax])
+            dry = np.clip(((coord - a_origin[ax]) / widths_a[ax]).astype(int), 0, n_a[ax] - 1)
+            ws.append(w)
+            iis.append(i0.astype(np.int32))
+            drys.append(dry.astype(np.int32))
+            po.append(off)
+            off += len(idx)
+        offs.extend(po if nd == 2 else [po[0], po[0]])
+    torch = _torch()
+    tabs = (torch.from_numpy(np.concatenate(ws).astype(np.float64)).to("cuda"),
+            torch.from_numpy(np.concatenate(iis)).to("cuda"),
+            torch.from_numpy(np.concatenate(drys)).to("cuda"),
+            torch.from_numpy(np.array(offs, dtype=np.int64)).to("cuda"))
+    store._scratch[key] = tabs
+    return tabs
+
+
 def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level_origin, level_dx, level_dy,
                 snap_index, tolerance, adj_wet=None, interp_w=None, want_best=False, stream=None):
     """K3 on every patch of the store.  ring: (N, m, nxa[, nya]) float64 CUDA
@@ -649,13 +788,15 @@ def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level
     a.best = _ptr(best)
     a.best_offset = _ptr(best_off)
     a.status = _ptr(status)
+    tw, ti, tdry, toff = flag_axis_tables(store, ring_shape, a_origin, a_dx, a_dy, level_origin, level_dx, level_dy)
+    a.axis_w, a.axis_i, a.axis_dry, a.axis_off = _ptr(tw), _ptr(ti), _ptr(tdry), _ptr(toff)
     a.comp_stride = store.plane
     a.aux_stride = store.plane
     a.npatch = npatch
     a.ndim = store.ndim
     a.m = store.m
     a.ghost = store.g
-    a.swe = int(store.swe)
+    a.swe = int(store.swe and store.any_dry())   # the forward wet test only matters with dry cells
     a.mode = mode
     a.nidx = len(snap_index)
     a.nxa = ring_shape[0]

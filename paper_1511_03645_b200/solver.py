@@ -202,15 +202,30 @@ def step_patch(patch: Patch, dt: float, equation: EquationSet, limiter: str = "M
 
 
 def _launch_single(st, slot, dt, equation, limiter, variant, out):
-    """Step one patch of a multi-patch store (tile subset)."""
+    """Step one patch of a multi-patch store (work tables restricted to it)."""
     if variant == _lib.VARIANT_FAST and st.any_dry():
         variant = _lib.VARIANT_EXACT
     key = ("single", variant, slot)
     if key not in st._tiles:
-        tiles, _ = st.tiles(variant)
-        allrows = np.frombuffer(tiles.cpu().numpy().tobytes(), dtype=_lib.TILE_DTYPE)
-        sub = allrows[allrows["patch"] == slot]
-        st._tiles[key] = (device._dev_table(sub), len(sub))
+        tiles, ntile, jobs, njob = st.tiles(variant)
+        allrows = np.frombuffer(tiles.cpu().numpy().tobytes(), dtype=_lib.TILE_DTYPE)[:ntile]
+        if jobs is None:
+            sub = allrows[allrows["patch"] == slot]
+            st._tiles[key] = (device._dev_table(sub), len(sub), None, len(sub))
+        else:
+            offs = jobs.cpu().numpy()
+            rows, new_offs = [], [0]
+            for j in range(len(offs) - 1):
+                seg = allrows[offs[j]:offs[j + 1]]
+                seg = seg[seg["patch"] == slot]
+                for r in seg:
+                    r = r.copy()
+                    r["pad"] = 0
+                    rows.append(r)
+                    new_offs.append(len(rows))
+            arr = np.array(rows, dtype=_lib.TILE_DTYPE)
+            st._tiles[key] = (device._dev_table(arr), len(arr),
+                              device._torch().from_numpy(np.array(new_offs, dtype=np.int32)).to("cuda"), len(arr))
     saved = st._tiles[variant]
     st._tiles[variant] = st._tiles[key]
     try:
