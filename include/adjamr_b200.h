@@ -120,6 +120,8 @@ typedef struct AdjStepArgs {
 /* AdjStepArgs.flags */
 #define ADJ_STEP_KEEP_NONFINITE 1   /* do not zero nonfinite: accumulate over launches */
 #define ADJ_STEP_NO_SPEED_OUT   2   /* do not write speed_max (caller uses static_speed) */
+#define ADJ_STEP_TWO_ROWS       4   /* FAST + static_speed: tiles are 64-row strips (<= 60 outputs),
+                                       two rows per lane; no job_offsets */
 int adj_step_level(const AdjStepArgs* a);
 
 /* Tile shape (ni, nj) the given variant expects in AdjStepArgs.tiles. */

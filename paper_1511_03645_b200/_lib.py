@@ -23,7 +23,7 @@ VARIANT_EXACT, VARIANT_FAST = 0, 1
 EDGE_XLO, EDGE_XHI, EDGE_YLO, EDGE_YHI = 1, 2, 4, 8
 BC_WALL, BC_OUTFLOW = 0, 1
 RECT_COPY, RECT_COARSE = 0, 1
-STEP_KEEP_NONFINITE, STEP_NO_SPEED_OUT = 1, 2
+STEP_KEEP_NONFINITE, STEP_NO_SPEED_OUT, STEP_TWO_ROWS = 1, 2, 4
 
 
 class NativeUnavailableError(RuntimeError):

@@ -28,11 +28,23 @@
 #ifndef K1_MIN_BLOCKS
 #define K1_MIN_BLOCKS 3   // CTAs of 128 threads per SM the register budget targets
 #endif
+#ifndef K1_TILE_NI
+#define K1_TILE_NI 128    // columns per strip (march length)
+#endif
+#ifndef K1_GROUPS
+#define K1_GROUPS 2       // cp.async groups of 3 columns in flight
+#endif
+#ifndef K1_FINITE_INT
+#define K1_FINITE_INT 0   // 1: non-finite test on the exponent bits (integer pipe)
+#endif
+#ifndef K1_KY_RECOMPUTE
+#define K1_KY_RECOMPUTE 0 // 1: recompute the neighbour's y coefficient instead of shuffling it
+#endif
 
 namespace adj {
 
 void fast_tile_shape(int ndim, int32_t* ni, int32_t* nj) {
-    if (ndim == 2) { *ni = 128; *nj = 28; } else { *ni = 256; *nj = 1; }
+    if (ndim == 2) { *ni = K1_TILE_NI; *nj = 28; } else { *ni = 256; *nj = 1; }
 }
 
 namespace fast {
@@ -199,7 +211,7 @@ ADJ_D void transverse(double f0, double h, const Mat& b, const Mat& a,
 
 struct Raw { double q0, q1, q2, c, z; };
 
-constexpr int GROUPS = 2;          // cp.async groups (of 3 columns) in flight per warp
+constexpr int GROUPS = K1_GROUPS;  // cp.async groups (of 3 columns) in flight per warp
 constexpr int RING = 3 * GROUPS;   // column slots of the per-warp ring
 
 // One warp's march along x over an output strip.  Every carried quantity
@@ -281,7 +293,11 @@ struct Strip {
         mu.m = SWE ? mu.c : sh_dn(m[C].m);
         mu.k1i = sh_dn(m[C].k1i);
         mu.k1 = fma(mu.m, mu.m, 1.0);
+#if K1_KY_RECOMPUTE
+        mu.ky = (FORM == ADJ_FORM_FWAVE ? 1.0 : mu.c) * (0.5 * fma(-dtdy, mu.c, 1.0));
+#else
         mu.ky = sh_dn(m[C].ky);
+#endif
         mu.kx = 0.0;
         mu.tr = SWE ? mu.c * mu.c : mu.c * mu.m;
         mu.fx = FORM == ADJ_FORM_FWAVE ? sh_dn(m[C].fx) : 0.0;
@@ -337,7 +353,13 @@ struct Strip {
             const double n0 = q0[PP] + d0, n1 = q1[PP] + d1, n2 = q2[PP] + d2;
             const int64_t o = (int64_t)(colbase + s - 2) * pitch;
             qout[o] = n0; qout[cs + o] = n1; qout[2 * cs + o] = n2;
+#if K1_FINITE_INT
+            const int ex = 0x7ff00000;
+            const int e0 = __double2hiint(n0) & ex, e1 = __double2hiint(n1) & ex, e2 = __double2hiint(n2) & ex;
+            bad |= (max(max(e0, e1), e2) == ex);
+#else
             bad |= !(isfinite(n0) && isfinite(n1) && isfinite(n2));
+#endif
         }
     }
 
@@ -445,6 +467,274 @@ __global__ void __launch_bounds__(128, K1_MIN_BLOCKS) k1_fast(AdjStepArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Two rows per lane: a warp owns 64 rows (60 outputs).  Lane l holds rows
+// a = 2l and b = 2l+1 of the strip (relative to j0-2); the y-face between
+// them is local, the one above b needs lane l+1's row a.  Each lane carries
+// two independent dependency chains (more ILP at the same occupancy) and the
+// shuffles per cell halve.  Used with the static CFL bound only.
+template <int SYS, int FORM, bool REV, int LIM>
+struct Strip2 {
+    static constexpr bool SWE = SYS == ADJ_SYS_SWE2D;
+    static constexpr int NARR = SWE ? 4 : 5;
+    const double* __restrict__ qin[2];
+    const double* __restrict__ aux[2];
+    double* __restrict__ qout[2];
+    int64_t cs, as;
+    int pitch, g, ni, s_last, colbase;
+    bool out[2];
+    double dtdx, dtdy, hx, hy;
+    double* ring;                  // [RING][NARR][64]
+    int lane;
+
+    Mat m[3][2];
+    double q0[3][2], q1[3][2], q2[3][2];
+    Face xf[3][2];
+    double sy0[3][2], sy2[3][2];
+    double gt0[3][2], gt2[3][2];   // gtil at the row's top face (row a: a|b, row b: b|a')
+    double cy0[3][2], cy2[3][2];
+    double bpy0[3][2], bpy1[3][2];
+    double ft0[3][2], ft1[3][2];
+    double sx0[3][2], sx1[3][2];
+    double cup[3], mup[3];         // next lane's row a material (row above b)
+    bool bad;
+
+    ADJ_D void prefetch(int s, int slot) const {
+        if (s <= s_last) {
+            const int64_t o = (int64_t)(colbase + s) * pitch;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const double* src[5] = {qin[r] + o, qin[r] + cs + o, qin[r] + 2 * cs + o, aux[r] + o, aux[r] + as + o};
+#pragma unroll
+                for (int k = 0; k < NARR; ++k) {
+                    const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + (slot * NARR + k) * 64 + 2 * lane + r);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src[k]) : "memory");
+                }
+            }
+        }
+    }
+
+    ADJ_D static void commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+    ADJ_D void read(int slot, Raw& A, Raw& B) const {
+        const double2* r = reinterpret_cast<const double2*>(ring + slot * NARR * 64) + lane;
+        const double2 v0 = r[0], v1 = r[32], v2 = r[64], v3 = r[96];
+        A.q0 = v0.x; B.q0 = v0.y; A.q1 = v1.x; B.q1 = v1.y; A.q2 = v2.x; B.q2 = v2.y; A.c = v3.x; B.c = v3.y;
+        if (!SWE) { const double2 v4 = r[128]; A.z = v4.x; B.z = v4.y; } else { A.z = 0.0; B.z = 0.0; }
+    }
+
+    template <int K>
+    ADJ_D void column(int s, const Raw& RA, const Raw& RB) {
+        constexpr int C = K, P = (K + 2) % 3, PP = (K + 1) % 3;
+        m[C][0] = make_mat<SYS, FORM>(RA.c, RA.z, dtdx, dtdy);
+        m[C][1] = make_mat<SYS, FORM>(RB.c, RB.z, dtdx, dtdy);
+        q0[C][0] = RA.q0; q1[C][0] = RA.q1; q2[C][0] = RA.q2;
+        q0[C][1] = RB.q0; q1[C][1] = RB.q1; q2[C][1] = RB.q2;
+
+        // ---- x-faces s-1/2, both rows
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            xf[C][r] = solve_face<SYS, FORM, REV>(q0[P][r], q1[P][r], q0[C][r], q1[C][r], m[P][r], m[C][r]);
+
+        // ---- y-faces: F1 = a|b (local), F2 = b|a' (a' = next lane's row a)
+        const Face F1 = solve_face<SYS, FORM, REV>(RA.q0, RA.q2, RB.q0, RB.q2, m[C][0], m[C][1]);
+        const double uq0 = sh_dn(RA.q0), uq2 = sh_dn(RA.q2);
+        Mat mu{};
+        mu.c = sh_dn(m[C][0].c);
+        mu.m = SWE ? mu.c : sh_dn(m[C][0].m);
+        mu.k1i = sh_dn(m[C][0].k1i);
+        mu.k1 = fma(mu.m, mu.m, 1.0);
+        mu.ky = sh_dn(m[C][0].ky);
+        mu.tr = SWE ? mu.c * mu.c : mu.c * mu.m;
+        mu.fx = FORM == ADJ_FORM_FWAVE ? sh_dn(m[C][0].fx) : 0.0;
+        const Face F2 = solve_face<SYS, FORM, REV>(RB.q0, RB.q2, uq0, uq2, m[C][1], mu);
+        {
+            // F1: previous face = lane-1's F2, next face = own F2
+            const double s0n = REV ? sh_up(F2.s0) : F2.s0;
+            const double s1n = REV ? F2.s1 : sh_up(F2.s1);
+            const double P0n = REV ? sh_up(F2.P) : 0.0;
+            const double P1n = REV ? F2.P : 0.0;
+            correction<SYS, FORM, REV, LIM>(F1, s0n, P0n, s1n, P1n, m[C][0], m[C][1], m[C][0].ky, m[C][1].ky,
+                                            cy0[C][0], cy2[C][0]);
+        }
+        {
+            // F2: previous face = own F1, next face = lane+1's F1
+            const double s0n = REV ? F1.s0 : sh_dn(F1.s0);
+            const double s1n = REV ? sh_dn(F1.s1) : F1.s1;
+            const double P0n = REV ? F1.P : 0.0;
+            const double P1n = REV ? sh_dn(F1.P) : 0.0;
+            correction<SYS, FORM, REV, LIM>(F2, s0n, P0n, s1n, P1n, m[C][1], mu, m[C][1].ky, mu.ky,
+                                            cy0[C][1], cy2[C][1]);
+        }
+        sy0[C][0] = F1.am0 + sh_up(F2.ap0);
+        sy2[C][0] = F1.am1 + sh_up(F2.ap1);
+        sy0[C][1] = F2.am0 + F1.ap0;
+        sy2[C][1] = F2.am1 + F1.ap1;
+        cup[C] = mu.c;
+        mup[C] = mu.m;
+
+        // ---- Sx(s-1) and its transverse split (rows above / below, column s-1)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            sx0[P][r] = xf[P][r].ap0 + xf[C][r].am0;
+            sx1[P][r] = xf[P][r].ap1 + xf[C][r].am1;
+        }
+        {
+            Mat mb{};                       // row a-1 = lane-1's row b
+            mb.c = sh_up(m[P][1].c);
+            mb.m = SWE ? mb.c : sh_up(m[P][1].m);
+            mb.tr = SWE ? mb.c * mb.c : mb.c * mb.m;
+            Mat ma{};                       // row b+1 = lane+1's row a
+            ma.c = cup[P]; ma.m = mup[P];
+            ma.tr = SWE ? ma.c * ma.c : ma.c * ma.m;
+            double amA0, amAv, apA0, apAv, amB0, amBv, apB0, apBv;
+            transverse<SYS, FORM, REV>(sx0[P][0], hx, mb, m[P][1], amA0, amAv, apA0, apAv);
+            transverse<SYS, FORM, REV>(sx0[P][1], hx, m[P][0], ma, amB0, amBv, apB0, apBv);
+            gt0[P][0] = cy0[P][0] - (apA0 + amB0);
+            gt2[P][0] = cy2[P][0] - (apAv + amBv);
+            gt0[P][1] = cy0[P][1] - (apB0 + sh_dn(amA0));
+            gt2[P][1] = cy2[P][1] - (apBv + sh_dn(amAv));
+        }
+
+        // ---- transverse of Sy(s-1) with columns s-2, s; x-limiter of face s-3/2
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            double bm0, bmv, bp0, bpv;
+            transverse<SYS, FORM, REV>(sy0[P][r], hy, m[PP][r], m[C][r], bm0, bmv, bp0, bpv);
+            double fc0, fc1;
+            correction<SYS, FORM, REV, LIM>(xf[P][r], REV ? xf[PP][r].s0 : xf[C][r].s0, xf[PP][r].P,
+                                            REV ? xf[C][r].s1 : xf[PP][r].s1, xf[C][r].P,
+                                            m[PP][r], m[P][r], m[PP][r].kx, m[P][r].kx, fc0, fc1);
+            ft0[P][r] = fc0 - (bpy0[PP][r] + bm0);
+            ft1[P][r] = fc1 - (bpy1[PP][r] + bmv);
+            bpy0[P][r] = bp0; bpy1[P][r] = bpv;
+        }
+
+        // ---- update cells of column s-2
+        const double gb0 = sh_up(gt0[PP][1]), gb2 = sh_up(gt2[PP][1]);   // face below row a
+        if (s >= 2 && s <= s_last) {
+            const int64_t o = (int64_t)(colbase + s - 2) * pitch;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                if (!out[r]) continue;
+                const double b0 = r == 0 ? gb0 : gt0[PP][0], b2 = r == 0 ? gb2 : gt2[PP][0];
+                const double d0 = -dtdx * ((sx0[PP][r] + ft0[P][r]) - ft0[PP][r]) - dtdy * ((sy0[PP][r] + gt0[PP][r]) - b0);
+                const double d1 = -dtdx * ((sx1[PP][r] + ft1[P][r]) - ft1[PP][r]);
+                const double d2 = -dtdy * ((sy2[PP][r] + gt2[PP][r]) - b2);
+                const double n0 = q0[PP][r] + d0, n1 = q1[PP][r] + d1, n2 = q2[PP][r] + d2;
+                qout[r][o] = n0; qout[r][cs + o] = n1; qout[r][2 * cs + o] = n2;
+                bad |= !(isfinite(n0) && isfinite(n1) && isfinite(n2));
+            }
+        }
+    }
+
+    ADJ_D void setup(const AdjTile& T, const AdjPatch& p, const AdjStepArgs& a, int lane_, double* ring_) {
+        lane = lane_;
+        ring = ring_;
+        g = a.ghost;
+        const int NY = p.ny + 2 * g;
+        cs = a.comp_stride; as = a.aux_stride;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int l = 2 * lane + r;                 // row within the 64-row strip
+            const int jj = g + T.j0 - 2 + l;
+            const int jl = jj < 0 ? 0 : (jj > NY - 1 ? NY - 1 : jj);
+            out[r] = l >= 2 && l < 2 + T.nj;
+            qin[r] = a.q_in + p.offset + jl;
+            aux[r] = a.aux + p.offset + jl;
+            qout[r] = a.q_out + p.offset + jl;
+        }
+        pitch = p.pitch;
+        dtdx = a.dtdx; dtdy = a.dtdy;
+        hx = 0.5 * dtdx; hy = 0.5 * dtdy;
+        colbase = g + T.i0;
+        ni = T.ni;
+    }
+
+    ADJ_D void run() {
+        const int s_first = -2;
+        s_last = ni + 1;
+        for (int gI = 0; gI < GROUPS; ++gI) {
+            for (int k = 0; k < 3; ++k) prefetch(s_first + 3 * gI + k, 3 * gI + k);
+            commit();
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                m[k][r] = Mat{}; xf[k][r] = Face{};
+                q0[k][r] = q1[k][r] = q2[k][r] = 0.0;
+                sy0[k][r] = sy2[k][r] = gt0[k][r] = gt2[k][r] = cy0[k][r] = cy2[k][r] = 0.0;
+                bpy0[k][r] = bpy1[k][r] = ft0[k][r] = ft1[k][r] = sx0[k][r] = sx1[k][r] = 0.0;
+            }
+            cup[k] = mup[k] = 0.0;
+        }
+        int base = 0;
+#pragma unroll 1
+        for (int s = s_first; s <= s_last; s += 3) {
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(GROUPS - 1) : "memory");
+            Raw a0, b0, a1, b1, a2, b2;
+            read(base, a0, b0);
+            read(base + 1, a1, b1);
+            read(base + 2, a2, b2);
+            prefetch(s + RING, base);
+            prefetch(s + RING + 1, base + 1);
+            prefetch(s + RING + 2, base + 2);
+            commit();
+            column<0>(s, a0, b0);
+            column<1>(s + 1, a1, b1);
+            column<2>(s + 2, a2, b2);
+            base = base + 3 == RING ? 0 : base + 3;
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
+};
+
+#ifndef K1_MIN_BLOCKS2
+#define K1_MIN_BLOCKS2 2
+#endif
+
+template <int SYS, int FORM, bool REV, int LIM>
+__global__ void __launch_bounds__(128, K1_MIN_BLOCKS2) k1_fast2(AdjStepArgs a) {
+    const int lane = threadIdx.x & 31;
+    __shared__ int s_tile[4];
+    constexpr int NARR = Strip2<SYS, FORM, REV, LIM>::NARR;
+    extern __shared__ __align__(16) double s_ring2[];            // [4 warps][RING][NARR][64]
+    const int warp = threadIdx.x >> 5;
+    for (;;) {
+        if (lane == 0) s_tile[warp] = atomicAdd(a.work_counter, 1);
+        __syncwarp();
+        const int job = s_tile[warp];
+        __syncwarp();
+        if (job >= a.ntile) break;
+        const AdjTile T = a.tiles[job];
+        const AdjPatch p = a.patches[T.patch];
+        Strip2<SYS, FORM, REV, LIM> S;
+        S.bad = false;
+        S.setup(T, p, a, lane, s_ring2 + warp * RING * NARR * 64);
+        S.run();
+        if (S.bad) a.nonfinite[T.patch] = 1;
+    }
+}
+
+template <int SYS, int FORM, bool REV, int LIM>
+static void launch_two_rows(const AdjStepArgs& a, cudaStream_t st) {
+    static int blocks_per_sm = 0, sms = 0;
+    constexpr int smem = 4 * RING * Strip2<SYS, FORM, REV, LIM>::NARR * 64 * (int)sizeof(double);
+    if (blocks_per_sm == 0) {
+        cudaFuncSetAttribute(k1_fast2<SYS, FORM, REV, LIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast2<SYS, FORM, REV, LIM>, 128, smem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    int blocks = blocks_per_sm * sms;
+    const int need = (a.ntile + 3) / 4;
+    if (blocks > need) blocks = need;
+    k1_fast2<SYS, FORM, REV, LIM><<<blocks, 128, smem, st>>>(a);
+}
+
 template <int SYS, int FORM, bool REV, int LIM, bool CFL>
 static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     static int blocks_per_sm = 0, sms = 0;
@@ -463,7 +753,8 @@ static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
 
 template <int SYS, int FORM, bool REV, int LIM>
 static void launch_kernel(const AdjStepArgs& a, cudaStream_t st) {
-    if (a.static_speed) launch_cfl<SYS, FORM, REV, LIM, false>(a, st);
+    if ((a.flags & ADJ_STEP_TWO_ROWS) && a.static_speed && !a.job_offsets) launch_two_rows<SYS, FORM, REV, LIM>(a, st);
+    else if (a.static_speed) launch_cfl<SYS, FORM, REV, LIM, false>(a, st);
     else if (!a.job_offsets) launch_cfl<SYS, FORM, REV, LIM, true>(a, st);
 }
 

@@ -331,6 +331,15 @@ class LevelStore:
         self.edges_table(level_shape)
         return bool(np.all(self.table_np["edges"] == full))
 
+    def two_rows(self) -> bool:
+        """Use the two-rows-per-lane fast kernel (64-row strips; 2D, no dry
+        cells) -- opt-in with ADJAMR_K1_ROWS=2: measured slower on B200 than
+        the one-row kernel (255 registers with spills, 8 warps/SM)."""
+        import os
+        if self.ndim != 2 or self.any_dry():
+            return False
+        return os.environ.get("ADJAMR_K1_ROWS") == "2"
+
     def tiles(self, variant):
         """Work tables of a step variant: (tiles, ntile, job_offsets, njob).
         FAST 2D: strips of <= 28 rows x <= 128 columns; full strips are one warp
@@ -343,6 +352,9 @@ class LevelStore:
             _lib.check(_lib.lib().adj_step_tile_shape(variant, self.ndim, _lib.C.byref(ni_t), _lib.C.byref(nj_t)),
                        "adj_step_tile_shape")
             ti, tj = ni_t.value, nj_t.value
+            two = variant == _lib.VARIANT_FAST and self.two_rows()
+            if two:
+                tj = 60
             full, short = [], {}
             for k, p in enumerate(self.patches):
                 nx = p.spec.shape[0]
@@ -351,11 +363,15 @@ class LevelStore:
                     ni = min(ti, nx - i0)
                     for j0 in range(0, ny, tj):
                         nj = min(tj, ny - j0)
-                        if variant == _lib.VARIANT_FAST and self.ndim == 2 and nj < tj and nj + 4 <= 16:
+                        if variant == _lib.VARIANT_FAST and self.ndim == 2 and not two and nj < tj and nj + 4 <= 16:
                             short.setdefault(ni, []).append((k, i0, j0, ni, nj, 0))
                         else:
                             full.append((k, i0, j0, ni, nj, 0))
-            if variant == _lib.VARIANT_FAST and self.ndim == 2:
+            if two:
+                full.sort(key=lambda r: (r[0], r[1], r[2]))
+                arr = np.array(full, dtype=_lib.TILE_DTYPE)
+                self._tiles[variant] = (_dev_table(arr), len(full), None, len(full))
+            elif variant == _lib.VARIANT_FAST and self.ndim == 2:
                 # x-segment major, then strips: concurrently running warps are
                 # y-neighbours and share halo rows through L2
                 full.sort(key=lambda r: (r[0], r[1], r[2]))
@@ -446,8 +462,10 @@ class RectTable:
     interpolation weights of every COARSE rect are precomputed per row and
     column (``axis_weights``) and stored alongside."""
 
+    MAX_CELLS = 256     # one warp per rectangle: large rectangles are split
+
     def __init__(self, rects_np, coarse_geom=None):
-        rects_np = np.array(rects_np, dtype=_lib.RECT_DTYPE)
+        rects_np = self._split(np.array(rects_np, dtype=_lib.RECT_DTYPE))
         self.n = len(rects_np)
         self.max_cells = int(np.max(rects_np["ni"] * rects_np["nj"])) if self.n else 0
         self.axis_w = self.axis_i = None
@@ -458,6 +476,32 @@ class RectTable:
             self.axis_i = torch.from_numpy(i).to("cuda")
         self.dev = _dev_table(rects_np) if self.n else None
         self.np = rects_np
+
+    @classmethod
+    def _split(cls, rects):
+        """Split rectangles larger than MAX_CELLS into row / column chunks
+        (same cells, so the result is unchanged)."""
+        if len(rects) == 0 or int(np.max(rects["ni"] * rects["nj"])) <= cls.MAX_CELLS:
+            return rects
+        out = []
+        for r in rects:
+            ni, nj = int(r["ni"]), int(r["nj"])
+            if ni * nj <= cls.MAX_CELLS:
+                out.append(r.copy())
+                continue
+            cj = min(nj, cls.MAX_CELLS)
+            ci = max(1, cls.MAX_CELLS // cj)
+            for a in range(0, ni, ci):
+                for b in range(0, nj, cj):
+                    s = r.copy()
+                    s["di0"] = r["di0"] + a
+                    s["dj0"] = r["dj0"] + b
+                    s["si0"] = r["si0"] + a
+                    s["sj0"] = r["sj0"] + b
+                    s["ni"] = min(ci, ni - a)
+                    s["nj"] = min(cj, nj - b)
+                    out.append(s)
+        return np.array(out, dtype=_lib.RECT_DTYPE)
 
 
 def _axis_weights_np(coord, origin, width, n):
@@ -673,6 +717,8 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     a.limiter = _lib.LIMITERS[limiter]
     a.variant = variant
     a.flags = (_lib.STEP_KEEP_NONFINITE | _lib.STEP_NO_SPEED_OUT) if accumulate else 0
+    if variant == _lib.VARIANT_FAST and store.ndim == 2 and store.two_rows():
+        a.flags |= _lib.STEP_TWO_ROWS
     a.dt = dt
     a.dtdx = dt / spec0.dx
     a.dtdy = dt / spec0.dy if store.ndim == 2 else 0.0

@@ -72,3 +72,16 @@ def test_bad_args():
         solver.step_patch(p, 0.0, eq)
     with pytest.raises(ValueError):
         solver.step_patch(p, d["dt"], eq, "vanleer")
+
+
+@pytest.mark.parametrize("rows", ["1", "2"])
+@pytest.mark.parametrize("case", [c for c in sorted(STEP) if not STEP[c]["name"].startswith("ac1d")
+                                  and STEP[c]["name"] != "swe_dry" and STEP[c]["name"] != "swe_adj_rev"])
+def test_fast_kernel_rows_per_lane(case, rows, monkeypatch):
+    """Both fast kernels (one and two rows per lane) on every golden 2D case
+    without dry cells, forced through ADJAMR_K1_ROWS."""
+    from paper_1511_03645_b200 import _lib
+    monkeypatch.setenv("ADJAMR_K1_ROWS", rows)
+    d = STEP[case]
+    q, cfl = _run(d, _lib.VARIANT_FAST)
+    assert norm_rel(q, d["q_out"]) <= 1e-12
