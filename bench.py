@@ -429,6 +429,7 @@ def main():
     # ---- e2e through the public API with host buffers
     e2e = bench_e2e(p, eq, bc, shape, dt, variant, min(args.steps, 5))
     c5 = None if args.no_c5 else bench_c5(min(args.steps, 10), 3, variant)
+    c3 = None if args.no_c5 else bench_c3(min(args.steps, 20), variant)
 
     line = {
         "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
@@ -445,6 +446,7 @@ def main():
                      "kernel_cell_updates_per_s": N * N / (k1 * 1e-3)},
         "flagging": flag,
         "c5_batched_patches": c5,
+        "c3_heterogeneous_acoustics": c3,
         "e2e": e2e,
         "gpu_launches": args.steps * 4,
         "clocks": clk.summary(),
@@ -455,6 +457,101 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def build_c3(n=2048):
+    """C3: 2048^2 two-layer acoustics on [0,1]^2 (K=4, rho=1 where y < 0.2x,
+    else K=1, rho=1.5), 8 Gaussians (width 0.05, centres/amplitudes U[0.5,1],
+    seed 0).  Periodic x has no reference oracle: outflow in x,
+    walls in y."""
+    from paper_1511_03645_b200 import equations as E
+    from paper_1511_03645_b200 import solver
+    from paper_1511_03645_b200.geometry import Patch, PatchHierarchy
+    lower = lambda x, y: np.asarray(y) < 0.2 * np.asarray(x)                      # noqa: E731
+    eq = E.Acoustics2D(E.AcousticsMaterialModel(lambda x, y: np.where(lower(x, y), 4.0, 1.0),
+                                                lambda x, y: np.where(lower(x, y), 1.0, 1.5)))
+    bc = solver.BoundarySpec("outflow", "outflow", "wall", "wall")
+    h = PatchHierarchy(xlim=(0.0, 1.0), ylim=(0.0, 1.0), base_shape=(n, n), ratios=[])
+    p = Patch(h.make_spec(1, (0, 0), (n - 1, n - 1)), 3)
+    solver.sample_patch_material(p, eq, bc, (n, n))
+    rng = np.random.default_rng(0)
+    cx, cy, amp = rng.uniform(0.5, 1.0, 8), rng.uniform(0.5, 1.0, 8), rng.uniform(0.5, 1.0, 8)
+    xs = (np.arange(n) + 0.5) / n
+    X, Y = np.meshgrid(xs, xs, indexing="ij")
+    q = np.zeros((n, n))
+    for k in range(8):
+        q += amp[k] * np.exp(-((X - cx[k]) ** 2 + (Y - cy[k]) ** 2) / 0.05 ** 2)
+    p.interior()[0] = q
+    h.levels = [[p]]
+    dt = 0.9 * p.spec.dx / 2.0
+    return h, p, eq, bc, dt
+
+
+def adjoint_ring_c3(nsnap, n, device="cuda"):
+    """50 snapshots of a 2048^2 adjoint field from seed 1 with the same
+    Gaussian recipe on p (u = v = 0), shifted in time."""
+    import torch
+    rng = np.random.default_rng(1)
+    cx, cy, amp = rng.uniform(0.5, 1.0, 8), rng.uniform(0.5, 1.0, 8), rng.uniform(0.5, 1.0, 8)
+    xs = (torch.arange(n, dtype=torch.float64, device=device) + 0.5) / n
+    X, Y = torch.meshgrid(xs, xs, indexing="ij")
+    ring = torch.zeros(nsnap, 3, n, n, dtype=torch.float64, device=device)
+    for s in range(nsnap):
+        w = 0.05 * (1.0 + 3.0 * (nsnap - 1 - s) / max(nsnap - 1, 1))
+        for k in range(8):
+            ring[s, 0] += amp[k] * torch.exp(-((X - cx[k]) ** 2 + (Y - cy[k]) ** 2) / w ** 2)
+    return ring
+
+
+def bench_c3(steps, variant):
+    import torch
+    from paper_1511_03645_b200 import adjoint, device, solver
+    n = 2048
+    h, p, eq, bc, dt = build_c3(n)
+    st = solver.store_of(p)
+    solver.advance_uniform(p, eq, bc, (n, n), dt, 4, "MC", variant)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    solver.advance_uniform(p, eq, bc, (n, n), dt, steps, "MC", variant)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    k1 = []
+    for _ in range(8):
+        st.fold_ghosts()
+        out = st._free(st.cur, -1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        device.launch_step(st, dt, eq, "MC", variant, out)
+        b.record()
+        st.ghost_src = st.cur
+        st.cur = out
+        k1.append((a, b))
+    torch.cuda.synchronize()
+    k1ms = statistics.median([a.elapsed_time(b) for a, b in k1])
+    # flagging every 10 steps against 50 snapshots, full-span window (TimeWindow(0, T))
+    nsnap = 50
+    ring = adjoint_ring_c3(nsnap, n)
+    T = 200 * dt
+    times = np.linspace(0.0, T, nsnap)
+    idx = adjoint.window_indices(100 * dt, adjoint.TimeWindow(0.0, T), times)
+    args = ((n, n), (0.0, 0.0), 1.0 / n, 1.0 / n, (0.0, 0.0), 1.0 / n, 1.0 / n, idx, 0.05)
+    device.launch_flag(st, ring, *args)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(5):
+        _, counts, _, _ = device.launch_flag(st, ring, *args)
+    b.record()
+    torch.cuda.synchronize()
+    fms = a.elapsed_time(b) / 5
+    return {"value": n * n / (ms * 1e-3), "unit": "cell-updates/s", "ms_per_step": ms,
+            "k1_ms": k1ms, "k1_achieved_GBps": 64 * n * n / (k1ms * 1e-3) / 1e9, "bytes_per_cell_update": 64,
+            "flagging": {"value": n * n / (fms * 1e-3), "unit": "flagged cells/s", "snapshots": len(idx),
+                         "kernel_ms": fms, "flagged": int(counts[0].item()), "tolerance": 0.05},
+            "workload": "C3: 2048^2 two-layer acoustics (y<0.2x), 8 Gaussians seed 0, outflow x (periodic "
+                        "has no oracle, SURVEY D3) / wall y, CFL 0.9, MC; flagging: 50 snapshots (seed 1), "
+                        "full-span window at step 100"}
 
 
 def bench_flagging(p, st, dt, stream):

@@ -331,6 +331,23 @@ class LevelStore:
         self.edges_table(level_shape)
         return bool(np.all(self.table_np["edges"] == full))
 
+    def _strip_length(self, ti_max, tj, warps_per_sm=12):
+        """Strip march length: balance the last wave of the persistent warp
+        queue against the 4 priming columns per strip."""
+        torch = _torch()
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        slots = sms * warps_per_sm
+        best, best_score = ti_max, -1.0
+        for ti in (ti_max, 112, 96, 80, 64, 48):
+            if ti > ti_max:
+                continue
+            jobs = sum(-(-p.spec.shape[0] // ti) * -(-p.spec.shape[1] // tj) for p in self.patches)
+            waves = jobs / slots
+            score = (waves / np.ceil(waves)) * (ti / (ti + 4.0))
+            if score > best_score + 1e-9:
+                best, best_score = ti, score
+        return best
+
     def two_rows(self) -> bool:
         """Use the two-rows-per-lane fast kernel (64-row strips; 2D, no dry
         cells) -- opt-in with ADJAMR_K1_ROWS=2: measured slower on B200 than
@@ -355,6 +372,8 @@ class LevelStore:
             two = variant == _lib.VARIANT_FAST and self.two_rows()
             if two:
                 tj = 60
+            if variant == _lib.VARIANT_FAST and self.ndim == 2:
+                ti = self._strip_length(ti, tj)
             full, short = [], {}
             for k, p in enumerate(self.patches):
                 nx = p.spec.shape[0]

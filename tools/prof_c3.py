@@ -1,0 +1,18 @@
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import bench
+from paper_1511_03645_b200 import _lib, device, solver
+h, p, eq, bc, dt = bench.build_c3(2048)
+st = solver.store_of(p)
+solver.advance_uniform(p, eq, bc, (2048, 2048), dt, 2, "MC", _lib.VARIANT_FAST, graph=False)
+torch.cuda.synchronize()
+ts = []
+for _ in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
+    out = st._free(st.cur, -1)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); device.launch_step(st, dt, eq, "MC", _lib.VARIANT_FAST, out); b.record()
+    st.ghost_src = st.cur; st.cur = out
+    ts.append((a, b))
+torch.cuda.synchronize()
+print("k1 ms", [round(a.elapsed_time(b), 4) for a, b in ts])
