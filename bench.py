@@ -193,6 +193,43 @@ def bench_c5(steps, warmup, variant):
             "patches_per_level": npatch, "setup_s": setup, "workload": C5_STEPS_NOTE}
 
 
+def bench_c5_full(coarse_steps, variant):
+    """C5 as BASELINE states it: device adjoint solve on 1024^2 (64 snapshot
+    intervals), time-interpolated adjoint flagging (K3 mode 1) and a regrid
+    every 4 coarse steps (host clustering, device regrid fill), then the
+    level sweep.  Wall-clock per coarse step, split into regrid and sweep."""
+    import torch
+    from paper_1511_03645_b200 import adjoint, amr, solver
+    h, eq, ctx, dt = build_c5(variant)
+    T = coarse_steps * dt
+    window = adjoint.TimeWindow(0.0, T)
+    t0 = time.perf_counter()
+    store = adjoint.solve_adjoint(eq, ctx.boundary, adjoint.FunctionalSpec("box", (0.6, 0.7, 0.3, 0.4), (1.0, 0.0, 0.0)),
+                                  window, (0.0, 1.0), (0.0, 1.0), (1024, 1024), t0=0.0, dt_snap=T / 64,
+                                  keep_on_device=True)
+    torch.cuda.synchronize()
+    t_adj = time.perf_counter() - t0
+    ctx.strategy = adjoint.AdjointFlagging(store, window, 1e-9, time_interp=True)
+    ctx.regrid_interval = 4
+    ctx.max_patch_edge = 64
+    w0 = time.perf_counter()
+    regrid_s = 0.0
+    for step in range(coarse_steps):
+        r0 = time.perf_counter()
+        due = step > 0 and step % ctx.regrid_interval == 0
+        amr.advance_hierarchy(h, 1, dt, ctx)
+        torch.cuda.synchronize()
+        if due:
+            regrid_s += time.perf_counter() - r0
+    wall = time.perf_counter() - w0
+    return {"coarse_steps": coarse_steps, "adjoint_solve_s": t_adj, "snapshots": len(store.times),
+            "wall_ms_per_coarse_step": 1e3 * wall / coarse_steps,
+            "regrid_step_ms": 1e3 * regrid_s / max(1, (coarse_steps - 1) // 4),
+            "flagged_per_regrid": ctx.flagged_per_regrid[-4:],
+            "patches_per_level": [len(h.patches(l)) for l in (1, 2, 3)],
+            "cell_updates": int(sum(ctx.cell_steps.values()))}
+
+
 def adjoint_ring(nsnap, na=1024, device="cuda"):
     """Synthetic adjoint snapshots on the 1024^2 grid (seeded shapes, no
     dataset): a ring leaving the 20x20-cell coastal box near x'=0.9 and
@@ -361,6 +398,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", default="fast", choices=["fast", "exact"])
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--c5-full", type=int, default=0, help="run the full C5 workflow for this many coarse steps")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -430,6 +468,7 @@ def main():
     e2e = bench_e2e(p, eq, bc, shape, dt, variant, min(args.steps, 5))
     c5 = None if args.no_c5 else bench_c5(min(args.steps, 10), 3, variant)
     c3 = None if args.no_c5 else bench_c3(min(args.steps, 20), variant)
+    c5_full = bench_c5_full(args.c5_full, variant) if args.c5_full else None
 
     line = {
         "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
@@ -447,6 +486,7 @@ def main():
         "flagging": flag,
         "c5_batched_patches": c5,
         "c3_heterogeneous_acoustics": c3,
+        "c5_full_workflow": c5_full,
         "e2e": e2e,
         "gpu_launches": args.steps * 4,
         "clocks": clk.summary(),

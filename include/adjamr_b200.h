@@ -243,6 +243,14 @@ typedef struct AdjFlagArgs {
 } AdjFlagArgs;
 int adj_flag_adjoint(const AdjFlagArgs* a);
 
+/* Host (no GPU): signature-bisection clustering of a flag mask, identical
+ * to cluster() (amr.py:244-309).  mask: uint8 (nx, ny) row-major (ny = 1 in
+ * 1D); max_edge <= 0: no cap.  boxes: 4 ints per box (lo_x, lo_y, hi_x,
+ * hi_y) in emission order, effs: efficiency per box.  Returns
+ * ADJ_ERR_BAD_ARG (nboxes = -1) when max_boxes is too small. */
+int adj_cluster(const uint8_t* mask, int ndim, int nx, int ny, double efficiency, int max_edge,
+                int32_t* boxes, double* effs, int max_boxes, int32_t* nboxes);
+
 /* Last CUDA error string of the calling thread (diagnostics). */
 const char* adj_last_error(void);
 int adj_abi_version(void);

@@ -104,6 +104,8 @@ EXPORTS = {
     "adj_fill_ghost_rects": ([C.POINTER(AdjGhostArgs)], C.c_int),
     "adj_restrict": ([C.POINTER(AdjRestrictArgs)], C.c_int),
     "adj_flag_adjoint": ([C.POINTER(AdjFlagArgs)], C.c_int),
+    "adj_cluster": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p,
+                     C.c_int, C.POINTER(I32)], C.c_int),
 }
 
 _lib = None

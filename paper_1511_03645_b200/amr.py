@@ -241,8 +241,13 @@ def _tight_efficiency(mask, box):
     return float(core.sum()) / core.size
 
 
-def cluster(flags, efficiency_threshold: float, max_edge: int | None = None) -> list[ClusterBox]:
-    """Cover all flagged cells with efficient rectangles (amr.py:244-309)."""
+def cluster(flags, efficiency_threshold: float, max_edge: int | None = None,
+            native: bool | None = None) -> list[ClusterBox]:
+    """Cover all flagged cells with efficient rectangles (amr.py:244-309).
+
+    Runs the host-native C++ port (``adj_cluster`` in libadjamr_b200.so,
+    O(perimeter) per candidate box via prefix sums) when the library is
+    built, else the same algorithm in numpy; both produce identical boxes."""
     if not 0.0 < efficiency_threshold <= 1.0:
         raise ValueError("efficiency_threshold must be in (0, 1]")
     if isinstance(flags, FlagField):
@@ -250,6 +255,40 @@ def cluster(flags, efficiency_threshold: float, max_edge: int | None = None) -> 
     else:
         mask = np.asarray(flags, dtype=bool)
         offset = (0,) * mask.ndim
+    if native is not False:
+        out = _cluster_native(mask, offset, efficiency_threshold, max_edge)
+        if out is not None:
+            return out
+        if native:
+            raise RuntimeError("native clustering unavailable")
+    return _cluster_py(mask, offset, efficiency_threshold, max_edge)
+
+
+def _cluster_native(mask, offset, eff, max_edge):
+    try:
+        lib = _lib.load_library()
+    except _lib.NativeUnavailableError:
+        return None
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    nd = m.ndim
+    nx, ny = m.shape[0], (m.shape[1] if nd == 2 else 1)
+    cap = max(16, int(m.sum()) + 1)
+    boxes = np.zeros((cap, 4), dtype=np.int32)
+    effs = np.zeros(cap, dtype=np.float64)
+    n = _lib.I32()
+    rc = lib.adj_cluster(m.ctypes.data, nd, nx, ny, float(eff), -1 if max_edge is None else int(max_edge),
+                         boxes.ctypes.data, effs.ctypes.data, cap, _lib.C.byref(n))
+    _lib.check(rc, "adj_cluster")
+    out = []
+    for k in range(n.value):
+        b = boxes[k]
+        lo = (int(b[0]) + offset[0],) if nd == 1 else (int(b[0]) + offset[0], int(b[1]) + offset[1])
+        hi = (int(b[2]) + offset[0],) if nd == 1 else (int(b[2]) + offset[0], int(b[3]) + offset[1])
+        out.append(ClusterBox(lo=lo, hi=hi, efficiency=float(effs[k])))
+    return out
+
+
+def _cluster_py(mask, offset, efficiency_threshold, max_edge):
     boxes: list[ClusterBox] = []
     top = _bbox(mask)
     if top is None:

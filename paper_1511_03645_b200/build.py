@@ -23,6 +23,7 @@ UNITS = {
     "k2_ghost.cu": ["-fmad=false"],
     "k3_flag.cu": ["-fmad=false"],
     "k1_fast.cu": [],
+    "host_cluster.cpp": [],
 }
 
 
@@ -52,7 +53,7 @@ def build(verbose: bool = False, ptxas_info: bool = False, lib: str = LIB, build
     procs = []
     for src, flags in UNITS.items():
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(BUILD, src.replace(".cu", ".o").replace(".cpp", ".o"))
         objs.append(o)
         if _stale(o, [s, *headers, __file__]):
             cmd = [nvcc(), *ARCH, *COMMON, *flags, *(extra or []), "-c", s, "-o", o]

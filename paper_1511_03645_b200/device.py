@@ -499,28 +499,29 @@ class RectTable:
     @classmethod
     def _split(cls, rects):
         """Split rectangles larger than MAX_CELLS into row / column chunks
-        (same cells, so the result is unchanged)."""
+        (same cells, so the result is unchanged).  Vectorised: rect r becomes
+        ceil(ni/ci) x ceil(nj/cj) chunks in row-major chunk order."""
         if len(rects) == 0 or int(np.max(rects["ni"] * rects["nj"])) <= cls.MAX_CELLS:
             return rects
-        out = []
-        for r in rects:
-            ni, nj = int(r["ni"]), int(r["nj"])
-            if ni * nj <= cls.MAX_CELLS:
-                out.append(r.copy())
-                continue
-            cj = min(nj, cls.MAX_CELLS)
-            ci = max(1, cls.MAX_CELLS // cj)
-            for a in range(0, ni, ci):
-                for b in range(0, nj, cj):
-                    s = r.copy()
-                    s["di0"] = r["di0"] + a
-                    s["dj0"] = r["dj0"] + b
-                    s["si0"] = r["si0"] + a
-                    s["sj0"] = r["sj0"] + b
-                    s["ni"] = min(ci, ni - a)
-                    s["nj"] = min(cj, nj - b)
-                    out.append(s)
-        return np.array(out, dtype=_lib.RECT_DTYPE)
+        ni = rects["ni"].astype(np.int64)
+        nj = rects["nj"].astype(np.int64)
+        cj = np.minimum(nj, cls.MAX_CELLS)
+        ci = np.maximum(1, cls.MAX_CELLS // cj)
+        na = -(-ni // ci)
+        nb = -(-nj // cj)
+        cnt = na * nb
+        src = np.repeat(np.arange(len(rects)), cnt)
+        k = np.arange(int(cnt.sum())) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+        a = (k // nb[src]) * ci[src]
+        b = (k % nb[src]) * cj[src]
+        out = rects[src].copy()
+        out["di0"] += a.astype(np.int32)
+        out["dj0"] += b.astype(np.int32)
+        out["si0"] += a.astype(np.int32)
+        out["sj0"] += b.astype(np.int32)
+        out["ni"] = np.minimum(ci[src], ni[src] - a)
+        out["nj"] = np.minimum(cj[src], nj[src] - b)
+        return out
 
 
 def _axis_weights_np(coord, origin, width, n):
@@ -537,34 +538,51 @@ def _axis_weights_np(coord, origin, width, n):
 
 def axis_weight_tables(rects, fine_store, coarse_store, hierarchy):
     """Per COARSE rect: x weights of its rows then y weights of its columns;
-    sets rects["pad"] to the rect's offset into the tables."""
+    sets rects["pad"] to the rect's offset into the tables.  Vectorised over
+    all rects; every element sees the same IEEE operations as
+    ``_axis_weights_np`` (geometry.py:248-260)."""
     level = fine_store.patches[0].spec.level
     wf = hierarchy.widths(level)
     wc = hierarchy.widths(level - 1)
     org = hierarchy.origin
     gf, gc = fine_store.g, coarse_store.g
-    ws, js = [], []
-    off = 0
-    for r in rects:
-        if r["kind"] != _lib.RECT_COARSE:
-            continue
-        dp = fine_store.patches[int(r["dst_patch"])].spec
-        sp = coarse_store.patches[int(r["src_patch"])].spec
-        axes = [(0, int(r["di0"]), int(r["ni"]))]
-        if fine_store.ndim == 2:
-            axes.append((1, int(r["dj0"]), int(r["nj"])))
-        r["pad"] = off
-        for ax, d0, n in axes:
-            gidx = dp.lo[ax] - gf + d0 + np.arange(n)
-            coord = org[ax] + (gidx + 0.5) * wf[ax]
-            lo_phys = org[ax] + (sp.lo[ax] - gc) * wc[ax]
-            i0, w = _axis_weights_np(coord, lo_phys, wc[ax], sp.shape[ax] + 2 * gc)
-            ws.append(w)
-            js.append(i0.astype(np.int32))
-            off += n
-    if not ws:
+    sel = np.nonzero(rects["kind"] == _lib.RECT_COARSE)[0]
+    if len(sel) == 0:
         return np.zeros(1), np.zeros(1, np.int32)
-    return np.concatenate(ws).astype(np.float64), np.concatenate(js).astype(np.int32)
+    nd = fine_store.ndim
+    dlo = np.array([p.spec.lo for p in fine_store.patches], dtype=np.int64).reshape(-1, nd)
+    slo = np.array([p.spec.lo for p in coarse_store.patches], dtype=np.int64).reshape(-1, nd)
+    sshape = np.array([p.spec.shape for p in coarse_store.patches], dtype=np.int64).reshape(-1, nd)
+    r = rects[sel]
+    dpi = r["dst_patch"].astype(np.int64)
+    spi = r["src_patch"].astype(np.int64)
+    lens = [r["ni"].astype(np.int64)] + ([r["nj"].astype(np.int64)] if nd == 2 else [])
+    d0s = [r["di0"].astype(np.int64)] + ([r["dj0"].astype(np.int64)] if nd == 2 else [])
+    per_rect = lens[0] + (lens[1] if nd == 2 else 0)
+    offs = np.cumsum(per_rect) - per_rect
+    rects["pad"][sel] = offs.astype(rects["pad"].dtype)
+    total = int(per_rect.sum())
+    W = np.empty(total, np.float64)
+    I = np.empty(total, np.int32)
+    for ax in range(nd):
+        n = lens[ax]
+        base = offs + (lens[0] if ax == 1 else 0)
+        rid = np.repeat(np.arange(len(sel)), n)
+        t = np.arange(int(n.sum())) - np.repeat(np.cumsum(n) - n, n)
+        gidx = dlo[dpi[rid], ax] - gf + d0s[ax][rid] + t
+        coord = org[ax] + (gidx + 0.5) * wf[ax]
+        lo_phys = org[ax] + (slo[spi[rid], ax] - gc) * wc[ax]
+        ncell = sshape[spi[rid], ax] + 2 * gc
+        s = (coord - lo_phys) / wc[ax] - 0.5
+        i0 = np.floor(s).astype(np.int64)
+        w = s - i0
+        w = np.where(i0 < 0, 0.0, np.where(i0 > ncell - 2, 1.0, w))
+        i0 = np.clip(i0, 0, np.maximum(ncell - 2, 0))
+        w = np.where(ncell == 1, 0.0, w)
+        pos = base[rid] + t
+        W[pos] = w
+        I[pos] = i0.astype(np.int32)
+    return W, I
 
 
 def _as_table(rects):

@@ -56,3 +56,30 @@ def test_ghost_rect_cover_is_exact():
                 cell = (key, r[3] + i, r[4] + j)
                 assert cell not in seen
                 seen[cell] = 1
+
+
+@pytest.mark.parametrize("case", CL)
+def test_native_and_python_clustering_agree_with_reference(case):
+    d = H[case]
+    mask = d["mask"].astype(bool)
+    nd = mask.ndim
+    me = None if d["max_edge"] < 0 else int(d["max_edge"])
+    for native in (True, False):
+        boxes = amr.cluster(mask, float(d["eff"]), max_edge=me, native=native)
+        got = np.array([[*b.lo, *b.hi, b.efficiency] for b in boxes], dtype=float).reshape(-1, 2 * nd + 1)
+        assert np.array_equal(got, d["boxes"]), native
+
+
+def test_native_clustering_matches_python_on_large_masks():
+    rng = np.random.default_rng(11)
+    for n, cover, me in ((300, 0.2, 12), (512, 0.35, 30), (257, 0.5, None)):
+        yy, xx = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+        m = np.zeros((n, n), bool)
+        while m.mean() < cover:
+            cx, cy = rng.uniform(0, n, 2)
+            r = rng.uniform(3, n / 8)
+            m |= (xx - cx) ** 2 + (yy - cy) ** 2 <= r * r
+        m ^= rng.random((n, n)) < 0.01
+        a = amr.cluster(m, 0.7, max_edge=me, native=True)
+        b = amr.cluster(m, 0.7, max_edge=me, native=False)
+        assert [(x.lo, x.hi, x.efficiency) for x in a] == [(x.lo, x.hi, x.efficiency) for x in b]
