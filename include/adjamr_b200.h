@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define ADJ_ABI_VERSION 1
+#define ADJ_ABI_VERSION 2
 
 /* status codes (mapped to the reference's exception classes by the host) */
 #define ADJ_OK                 0
@@ -102,7 +102,8 @@ typedef struct AdjStepArgs {
     const AdjTile* tiles;      /* device */
     double* speed_max;         /* device, 2*npatch (x, y), zeroed by the call */
     int32_t* nonfinite;        /* device, npatch, zeroed by the call          */
-    int32_t* work_counter;     /* device, 1 int tile queue head, zeroed by the call */
+    int32_t* work_counter;     /* device, 2 ints (tile queue head, exit count), zeroed by the call
+                                  unless ADJ_STEP_COUNTER_ZERO */
     const double* static_speed;/* optional device (x, y) per patch: material speed bound over the
                                   CFL ranges; when given, the FAST variant (no dry cells) copies it
                                   to speed_max instead of reducing per face (same values) */
@@ -122,6 +123,8 @@ typedef struct AdjStepArgs {
 #define ADJ_STEP_NO_SPEED_OUT   2   /* do not write speed_max (caller uses static_speed) */
 #define ADJ_STEP_TWO_ROWS       4   /* FAST + static_speed: tiles are 64-row strips (<= 60 outputs),
                                        two rows per lane; no job_offsets */
+#define ADJ_STEP_COUNTER_ZERO   8   /* FAST 2D: work_counter holds 2 ints that are zero on entry; the
+                                       kernel leaves them zero (no memset node per launch) */
 int adj_step_level(const AdjStepArgs* a);
 
 /* Tile shape (ni, nj) the given variant expects in AdjStepArgs.tiles. */
@@ -183,6 +186,59 @@ typedef struct AdjGhostArgs {
     void* stream;
 } AdjGhostArgs;
 int adj_fill_ghost_rects(const AdjGhostArgs* a);
+
+/* K2, planned form of a whole level fill (fill_level_ghosts, amr.py:479-491:
+ * coarse interpolation, same-level copy, then physical boundaries) as ONE
+ * gather launch.  The plan is built once per regrid on the device from the
+ * level's disjoint COARSE + COPY rectangles (COARSE rects first) and its
+ * boundary patches; every ghost cell the fill writes gets one entry.
+ * Out-of-domain (physical) cells are resolved at build time to the entry
+ * (or interior cell) their mirrored / extrapolated source ends up holding
+ * (solver.py:84-146 applied after the in-domain phases), with the normal
+ * component's sign flips as a bit mask, so the fill has no ordering
+ * between entries.  Values are bitwise those of the three phases. */
+typedef struct AdjGhostPlan {
+    int32_t* dst;                /* [n] destination offset in the fine level plane               */
+    int32_t* src;                /* [n] COPY: source offset (same plane); COARSE: coarse entry   */
+    uint32_t* meta;              /* [n] bit 0: COARSE; bit 1+c: negate component c               */
+    int32_t* c_base;             /* [nc] offset of (i0, j0) in the coarse level plane            */
+    int32_t* c_step;             /* [nc] (i1-i0)*pitch | (j1-j0) << 30                          */
+    double* c_wx;                /* [nc] x weight (geometry.py:248-260)                          */
+    double* c_wy;                /* [nc] y weight (2D)                                           */
+    int32_t n;                   /* entries                                                      */
+    int32_t nc;                  /* COARSE rect cells = entries [0, nc), src == own index        */
+} AdjGhostPlan;
+typedef struct AdjGhostPlanBuildArgs {
+    AdjGhostPlan plan;           /* arrays sized by the caller; n = rect cells + physical cells  */
+    const AdjRect* rects;        /* COARSE rects first, then COPY rects (disjoint)               */
+    const int32_t* rect_cell0;   /* [nrect+1] first entry of each rect (prefix of ni*nj)         */
+    const AdjPatch* patches;     /* fine level table                                             */
+    const AdjPatch* coarse_patches;
+    const double* axis_w;        /* per-rect axis tables as in AdjGhostArgs                      */
+    const int32_t* axis_i;
+    const AdjPatch* edge_patches;/* fine patches touching the domain boundary (edges set)        */
+    int32_t* owner;              /* [plane] scratch filled with -1 (entry writing each cell)     */
+    int32_t* counter;            /* one int, zeroed: physical entries are appended after it      */
+    int32_t nrect, rect_cells;   /* rect_cells = rect_cell0[nrect]: physical entries start here  */
+    int32_t nedge, ndim, m;
+    int32_t ghost, ghost_coarse, max_ghost_cells;
+    int32_t bc[4];               /* x-lo, x-hi, y-lo, y-hi: ADJ_BC_*                             */
+    int32_t normal_comp[2];
+    void* stream;
+} AdjGhostPlanBuildArgs;
+int adj_ghost_plan_build(const AdjGhostPlanBuildArgs* a);
+typedef struct AdjGhostPlanFillArgs {
+    AdjGhostPlan plan;
+    double* q;                   /* fine level state (COPY sources are read from it too)         */
+    const double* q_coarse_old;  /* coarse state at t0 / t1 (may be NULL when nc == 0)           */
+    const double* q_coarse_new;
+    int64_t comp_stride, coarse_comp_stride;
+    int32_t ndim, m, time_mode, pad;
+    double w_time;
+    const double* w_time_dev;    /* optional device weight (< 0: old only), as in AdjGhostArgs  */
+    void* stream;
+} AdjGhostPlanFillArgs;
+int adj_fill_ghost_plan(const AdjGhostPlanFillArgs* a);
 
 /* K4: conservative fine-to-coarse averaging.  Replaces
  * restrict_fine_to_coarse (amr.py:399-450); one AdjRect per (coarse patch,

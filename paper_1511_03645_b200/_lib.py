@@ -23,7 +23,7 @@ VARIANT_EXACT, VARIANT_FAST = 0, 1
 EDGE_XLO, EDGE_XHI, EDGE_YLO, EDGE_YHI = 1, 2, 4, 8
 BC_WALL, BC_OUTFLOW = 0, 1
 RECT_COPY, RECT_COARSE = 0, 1
-STEP_KEEP_NONFINITE, STEP_NO_SPEED_OUT, STEP_TWO_ROWS = 1, 2, 4
+STEP_KEEP_NONFINITE, STEP_NO_SPEED_OUT, STEP_TWO_ROWS, STEP_COUNTER_ZERO = 1, 2, 4, 8
 
 
 class NativeUnavailableError(RuntimeError):
@@ -74,6 +74,26 @@ class AdjGhostArgs(C.Structure):
                 ("max_rect_cells", I32), ("stream", P)]
 
 
+class AdjGhostPlan(C.Structure):
+    _fields_ = [("dst", P), ("src", P), ("meta", P), ("c_base", P), ("c_step", P), ("c_wx", P), ("c_wy", P),
+                ("n", I32), ("nc", I32)]
+
+
+class AdjGhostPlanBuildArgs(C.Structure):
+    _fields_ = [("plan", AdjGhostPlan), ("rects", P), ("rect_cell0", P), ("patches", P), ("coarse_patches", P),
+                ("axis_w", P), ("axis_i", P), ("edge_patches", P), ("owner", P), ("counter", P),
+                ("nrect", I32), ("rect_cells", I32), ("nedge", I32), ("ndim", I32), ("m", I32),
+                ("ghost", I32), ("ghost_coarse", I32), ("max_ghost_cells", I32),
+                ("bc", I32 * 4), ("normal_comp", I32 * 2), ("stream", P)]
+
+
+class AdjGhostPlanFillArgs(C.Structure):
+    _fields_ = [("plan", AdjGhostPlan), ("q", P), ("q_coarse_old", P), ("q_coarse_new", P),
+                ("comp_stride", I64), ("coarse_comp_stride", I64),
+                ("ndim", I32), ("m", I32), ("time_mode", I32), ("pad", I32),
+                ("w_time", D), ("w_time_dev", P), ("stream", P)]
+
+
 class AdjRestrictArgs(C.Structure):
     _fields_ = [("q_coarse", P), ("q_fine", P), ("aux_coarse", P), ("aux_fine", P),
                 ("coarse_patches", P), ("fine_patches", P), ("rects", P),
@@ -95,6 +115,8 @@ class AdjFlagArgs(C.Structure):
                 ("tolerance", D), ("stream", P)]
 
 
+ABI_VERSION = 2
+
 EXPORTS = {
     "adj_abi_version": ([], C.c_int),
     "adj_last_error": ([], C.c_char_p),
@@ -102,6 +124,8 @@ EXPORTS = {
     "adj_step_level": ([C.POINTER(AdjStepArgs)], C.c_int),
     "adj_fill_physical": ([C.POINTER(AdjPhysArgs)], C.c_int),
     "adj_fill_ghost_rects": ([C.POINTER(AdjGhostArgs)], C.c_int),
+    "adj_ghost_plan_build": ([C.POINTER(AdjGhostPlanBuildArgs)], C.c_int),
+    "adj_fill_ghost_plan": ([C.POINTER(AdjGhostPlanFillArgs)], C.c_int),
     "adj_restrict": ([C.POINTER(AdjRestrictArgs)], C.c_int),
     "adj_flag_adjoint": ([C.POINTER(AdjFlagArgs)], C.c_int),
     "adj_cluster": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p,
@@ -124,7 +148,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = argtypes
         fn.restype = restype
-    if lib.adj_abi_version() != 1:
+    if lib.adj_abi_version() != ABI_VERSION:
         raise NativeUnavailableError("ABI version mismatch")
     _lib = lib
     return lib

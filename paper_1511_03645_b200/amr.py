@@ -628,6 +628,10 @@ def _fill_physical_subset(st, slots, boundary, equation, level_shape):
     device.fill_physical(st, boundary, equation, level_shape, slots=slots)
 
 
+# planned whole-level ghost fill (device.GhostPlan); False: the three-phase launches
+USE_GHOST_PLAN = True
+
+
 class LevelPlan:
     """Launch plan of one level for the batched sweep: its store, the coarse
     store, device-resident ghost / restriction rectangle tables and the
@@ -655,6 +659,24 @@ class LevelPlan:
         self.full = all(covered[k] + _ring_and_physical(p.spec, shape)[1] >= _ring_and_physical(p.spec, shape)[0]
                         for k, p in enumerate(patches))
         self.restrict_to = None      # (coarse store, RectTable) for restriction into level-1
+        self._gather = {}            # (boundary, normals, level shape) -> device.GhostPlan
+
+    def gather(self, hierarchy, level, ctx):
+        """The level's whole fill as one planned gather (built once, on first use)."""
+        if not USE_GHOST_PLAN:
+            return None
+        eq, bd = ctx.equation, ctx.boundary
+        key = (device._bc_codes(bd), eq.normal_component(0), eq.normal_component(1) if hierarchy.ndim == 2 else -1,
+               tuple(hierarchy.level_shape(level)))
+        gp = self._gather.get(key)
+        if gp is None:
+            if not device.GhostPlan.usable(self.st, self.cst):
+                return None
+            rects = self.combined if self.coarse_all.n else self.copies
+            gp = device.GhostPlan(self.st, rects, self.cst if self.coarse_all.n else None, bd, eq,
+                                  hierarchy.level_shape(level))
+            self._gather[key] = gp
+        return gp
 
     def valid(self, hierarchy, level) -> bool:
         ps = hierarchy.levels[level - 1] if level - 1 < len(hierarchy.levels) else None
@@ -699,12 +721,24 @@ def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrC
     st.sync_in()
     st.prepare_write(full_ghosts=pl.full)
     copies_done = False
-    if level >= 2 and pl.coarse_all.n:
+    coarse_in = level >= 2 and pl.coarse_all.n
+    if coarse_in:
         cst = pl.cst
         cst.sync_in()
         cst.fold_ghosts()
         old_buf = _coarse_old_buffer(cst)
         mw = _store_time_mode(cst, t)
+    if not coarse_in or mw is not None:
+        # level-synchronised times: coarse, copy and physical phases in one gather
+        gp = pl.gather(hierarchy, level, ctx)
+        if gp is not None:
+            if coarse_in:
+                gp.fill(st, old_buf, cst.buf[cst.cur], cst, mw[1], mw[0])
+            else:
+                gp.fill(st)
+            st.ghost_src = st.cur
+            return
+    if coarse_in:
         r = hierarchy.ratio_to_finer(level - 1)
         if mw is not None:
             # disjoint coarse + copy rectangles in one launch

@@ -2,6 +2,7 @@
 #include "adj_common.cuh"
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 
 namespace adj {
 
@@ -15,11 +16,23 @@ int record_cuda(cudaError_t e, const char* where) {
 
 int check_launch(const char* where) { return record_cuda(cudaGetLastError(), where); }
 
+// ADJAMR_PDL=0 disables programmatic dependent launch (A/B measurements).
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("ADJAMR_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
 int step_exact(const AdjStepArgs& a, cudaStream_t st);
 int step_fast(const AdjStepArgs& a, cudaStream_t st);
 void fast_tile_shape(int ndim, int32_t* ni, int32_t* nj);
 int fill_physical(const AdjPhysArgs& a);
 int fill_ghost_rects(const AdjGhostArgs& a);
+int ghost_plan_build(const AdjGhostPlanBuildArgs& a, int rect_cells);
+int fill_ghost_plan(const AdjGhostPlanFillArgs& a);
 int restrict_level(const AdjRestrictArgs& a);
 int flag_adjoint(const AdjFlagArgs& a);
 
@@ -72,8 +85,11 @@ int adj_step_level(const AdjStepArgs* a) {
         rc = adj::record_cuda(cudaMemsetAsync(a->nonfinite, 0, sizeof(int32_t) * a->npatch, st), "memset nonfinite");
         if (rc) return rc;
     }
-    rc = adj::record_cuda(cudaMemsetAsync(a->work_counter, 0, sizeof(int32_t), st), "memset work_counter");
-    if (rc) return rc;
+    const bool counter_zero = (a->flags & ADJ_STEP_COUNTER_ZERO) && a->variant == ADJ_VARIANT_FAST && a->ndim == 2;
+    if (!counter_zero) {
+        rc = adj::record_cuda(cudaMemsetAsync(a->work_counter, 0, 2 * sizeof(int32_t), st), "memset work_counter");
+        if (rc) return rc;
+    }
     if (a->variant == ADJ_VARIANT_EXACT) return adj::step_exact(*a, st);
     if (a->variant == ADJ_VARIANT_FAST) return adj::step_fast(*a, st);
     return adj::bad("unknown variant");
@@ -90,6 +106,31 @@ int adj_fill_ghost_rects(const AdjGhostArgs* a) {
         return adj::bad("null pointer");
     if (a->time_mode < 0 || a->time_mode > 2) return adj::bad("time_mode");
     return adj::fill_ghost_rects(*a);
+}
+
+int adj_ghost_plan_build(const AdjGhostPlanBuildArgs* a) {
+    if (!a || !a->patches || !a->counter) return adj::bad("null pointer");
+    if (!a->plan.dst || !a->plan.src || !a->plan.meta) return adj::bad("null plan arrays");
+    if (a->nrect > 0 && !(a->rects && a->rect_cell0)) return adj::bad("rects need rect_cell0");
+    if (a->plan.nc > 0 && !(a->coarse_patches && a->axis_w && a->axis_i && a->plan.c_base && a->plan.c_step &&
+                            a->plan.c_wx && a->plan.c_wy))
+        return adj::bad("COARSE entries need coarse patches, axis tables and coarse arrays");
+    if (a->nedge > 0 && !a->edge_patches) return adj::bad("null edge patches");
+    if (a->ghost < 2) return adj::bad("ghost width must be >= 2");
+    if (a->m < 1 || a->m > 3) return adj::bad("m must be 1..3");
+    cudaStream_t st = (cudaStream_t)a->stream;
+    int rc = adj::record_cuda(cudaMemsetAsync(a->counter, 0, sizeof(int32_t), st), "memset counter");
+    if (rc) return rc;
+    return adj::ghost_plan_build(*a, a->rect_cells);
+}
+
+int adj_fill_ghost_plan(const AdjGhostPlanFillArgs* a) {
+    if (!a || !a->q) return adj::bad("null pointer");
+    if (a->plan.n > 0 && !(a->plan.dst && a->plan.src && a->plan.meta)) return adj::bad("null plan arrays");
+    if (a->plan.nc > 0 && !(a->q_coarse_old && a->q_coarse_new && a->plan.c_base)) return adj::bad("null coarse state");
+    if (a->m < 1 || a->m > 3) return adj::bad("m must be 1..3");
+    if (a->time_mode < 0 || a->time_mode > 2) return adj::bad("time_mode");
+    return adj::fill_ghost_plan(*a);
 }
 
 int adj_restrict(const AdjRestrictArgs* a) {

@@ -10,6 +10,32 @@
 
 namespace adj {
 
+// Programmatic dependent launch: kernels of a level sweep are launched with
+// programmatic stream serialisation so a grid is scheduled while its
+// predecessor drains; every such kernel waits for the predecessor's memory
+// (griddepcontrol.wait) before touching anything, then lets its own
+// successor launch.  Without the launch attribute both are no-ops.
+ADJ_D void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+ADJ_D void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" :::); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+
 // Record the last CUDA error for adj_last_error(); returns ADJ_ERR_CUDA on error.
 int record_cuda(cudaError_t e, const char* where);
 int check_launch(const char* where);

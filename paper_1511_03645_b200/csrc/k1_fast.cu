@@ -28,14 +28,17 @@
 #ifndef K1_MIN_BLOCKS
 #define K1_MIN_BLOCKS 3   // CTAs of 128 threads per SM the register budget targets
 #endif
+#ifndef K1_WARPS
+#define K1_WARPS 4        // warps per CTA of the single-row kernel
+#endif
 #ifndef K1_TILE_NI
 #define K1_TILE_NI 128    // columns per strip (march length)
 #endif
 #ifndef K1_GROUPS
 #define K1_GROUPS 2       // cp.async groups of 3 columns in flight
 #endif
-#ifndef K1_FINITE_INT
-#define K1_FINITE_INT 0   // 1: non-finite test on the exponent bits (integer pipe)
+#ifndef K1_PREFETCH_CLAMP
+#define K1_PREFETCH_CLAMP 1   // 1: branch-free prefetch (re-read the last column)
 #endif
 #ifndef K1_KY_RECOMPUTE
 #define K1_KY_RECOMPUTE 0 // 1: recompute the neighbour's y coefficient instead of shuffling it
@@ -50,6 +53,16 @@ void fast_tile_shape(int ndim, int32_t* ni, int32_t* nj) {
 namespace fast {
 
 constexpr unsigned FULL = 0xffffffffu;
+
+// ADJ_STEP_COUNTER_ZERO: the last warp to leave the job queue zeroes it (and
+// the exit count) for the next launch, so no memset precedes a launch.
+ADJ_D void release_counter(const AdjStepArgs& a, int lane, int warps) {
+    if (!(a.flags & ADJ_STEP_COUNTER_ZERO) || lane != 0) return;
+    if (atomicAdd(a.work_counter + 1, 1) == warps - 1) {
+        a.work_counter[0] = 0;
+        a.work_counter[1] = 0;
+    }
+}
 
 ADJ_D double rcp(double x) {  // x > 0, normal: MUFU seed + one cubic Newton step
     double r;
@@ -242,14 +255,20 @@ struct Strip {
     double sx0[3], sx1[3];         // Sx(column)
     double cup[3], mup[3];         // row j+1 materials of column
     double smx, smy;
-    bool bad;
+    unsigned bad;
 
     static constexpr int NARR = SWE ? 4 : 5;
 
     // issue the cp.async copies of column s into ring slot `slot`
     ADJ_D void prefetch(int s, int slot) const {
+#if K1_PREFETCH_CLAMP   // branch-free: columns past the strip re-read its last column, unused
+        {
+            const int sc = s < s_last ? s : s_last;
+#else
         if (s <= s_last) {
-            const int64_t o = (int64_t)(colbase + s) * pitch;
+            const int sc = s;
+#endif
+            const int64_t o = (int64_t)(colbase + sc) * pitch;
             const double* src[5] = {qin + o, qin + cs + o, qin + 2 * cs + o, aux + o, aux + as + o};
 #pragma unroll
             for (int k = 0; k < NARR; ++k) {
@@ -353,13 +372,10 @@ struct Strip {
             const double n0 = q0[PP] + d0, n1 = q1[PP] + d1, n2 = q2[PP] + d2;
             const int64_t o = (int64_t)(colbase + s - 2) * pitch;
             qout[o] = n0; qout[cs + o] = n1; qout[2 * cs + o] = n2;
-#if K1_FINITE_INT
-            const int ex = 0x7ff00000;
-            const int e0 = __double2hiint(n0) & ex, e1 = __double2hiint(n1) & ex, e2 = __double2hiint(n2) & ex;
-            bad |= (max(max(e0, e1), e2) == ex);
-#else
-            bad |= !(isfinite(n0) && isfinite(n1) && isfinite(n2));
-#endif
+            // non-finite <=> exponent bits all set (integer pipe)
+            const unsigned ex = 0x7ff00000u;
+            bad |= (((unsigned)__double2hiint(n0) & ex) == ex) | (((unsigned)__double2hiint(n1) & ex) == ex) |
+                   (((unsigned)__double2hiint(n2) & ex) == ex);
         }
     }
 
@@ -424,12 +440,18 @@ struct Strip {
 };
 
 template <int SYS, int FORM, bool REV, int LIM, bool CFL>
-__global__ void __launch_bounds__(128, K1_MIN_BLOCKS) k1_fast(AdjStepArgs a) {
+#ifdef K1_MAXREG
+__global__ void __maxnreg__(K1_MAXREG) k1_fast(AdjStepArgs a) {
+#else
+__global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepArgs a) {
+#endif
     const int lane = threadIdx.x & 31;
-    __shared__ int s_tile[4];
+    __shared__ int s_tile[K1_WARPS];
     constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL>::NARR;
-    __shared__ __align__(16) double s_ring[4][RING * NARR * 32];
+    __shared__ __align__(16) double s_ring[K1_WARPS][RING * NARR * 32];
     const int warp = threadIdx.x >> 5;
+    pdl_wait();
+    pdl_trigger();
     // persistent warps: pull strip tiles from a global queue until empty
     const int njob = a.job_offsets ? a.njob : a.ntile;
     for (;;) {
@@ -437,7 +459,10 @@ __global__ void __launch_bounds__(128, K1_MIN_BLOCKS) k1_fast(AdjStepArgs a) {
         __syncwarp();
         const int job = s_tile[warp];
         __syncwarp();
-        if (job >= njob) break;
+        if (job >= njob) {
+            release_counter(a, lane, gridDim.x * K1_WARPS);
+            break;
+        }
         // this lane's strip: single-strip jobs use all lanes; packed jobs
         // stack up to four short strips (same ni) along the lanes
         int tix = job, lane0 = 0;
@@ -453,7 +478,7 @@ __global__ void __launch_bounds__(128, K1_MIN_BLOCKS) k1_fast(AdjStepArgs a) {
         const AdjTile T = a.tiles[tix];
         const AdjPatch p = a.patches[T.patch];
         Strip<SYS, FORM, REV, LIM, CFL> S;
-        S.smx = 0.0; S.smy = 0.0; S.bad = false;
+        S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
         S.setup(T, p, a, lane, lane0, s_ring[warp]);
         S.run();
         if (CFL) {   // single-strip jobs only (packed jobs require static_speed)
@@ -701,12 +726,17 @@ __global__ void __launch_bounds__(128, K1_MIN_BLOCKS2) k1_fast2(AdjStepArgs a) {
     constexpr int NARR = Strip2<SYS, FORM, REV, LIM>::NARR;
     extern __shared__ __align__(16) double s_ring2[];            // [4 warps][RING][NARR][64]
     const int warp = threadIdx.x >> 5;
+    pdl_wait();
+    pdl_trigger();
     for (;;) {
         if (lane == 0) s_tile[warp] = atomicAdd(a.work_counter, 1);
         __syncwarp();
         const int job = s_tile[warp];
         __syncwarp();
-        if (job >= a.ntile) break;
+        if (job >= a.ntile) {
+            release_counter(a, lane, gridDim.x * 4);
+            break;
+        }
         const AdjTile T = a.tiles[job];
         const AdjPatch p = a.patches[T.patch];
         Strip2<SYS, FORM, REV, LIM> S;
@@ -732,23 +762,23 @@ static void launch_two_rows(const AdjStepArgs& a, cudaStream_t st) {
     int blocks = blocks_per_sm * sms;
     const int need = (a.ntile + 3) / 4;
     if (blocks > need) blocks = need;
-    k1_fast2<SYS, FORM, REV, LIM><<<blocks, 128, smem, st>>>(a);
+    launch_pdl(k1_fast2<SYS, FORM, REV, LIM>, dim3(blocks), dim3(128), smem, st, a);
 }
 
 template <int SYS, int FORM, bool REV, int LIM, bool CFL>
 static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     static int blocks_per_sm = 0, sms = 0;
     if (blocks_per_sm == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL>, 128, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL>, 32 * K1_WARPS, 0);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     int blocks = blocks_per_sm * sms;
-    const int need = ((a.job_offsets ? a.njob : a.ntile) + 3) / 4;
+    const int need = ((a.job_offsets ? a.njob : a.ntile) + K1_WARPS - 1) / K1_WARPS;
     if (blocks > need) blocks = need;
-    k1_fast<SYS, FORM, REV, LIM, CFL><<<blocks, 128, 0, st>>>(a);
+    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL>, dim3(blocks), dim3(32 * K1_WARPS), 0, st, a);
 }
 
 template <int SYS, int FORM, bool REV, int LIM>

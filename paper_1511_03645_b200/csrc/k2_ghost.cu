@@ -190,6 +190,172 @@ int fill_ghost_rects(const AdjGhostArgs& a) {
 }
 
 // ---------------------------------------------------------------------------
+// Planned level fill.  Build (once per regrid): one entry per ghost cell the
+// fill writes, rect cells first (COARSE rects, then COPY rects, at the
+// caller's prefix offsets), then the physical cells, each resolved to the
+// entry or interior cell its composite source reads.  Fill: a flat gather.
+
+__global__ void __launch_bounds__(32 * RECTS_PER_CTA) k2_plan_rects(AdjGhostPlanBuildArgs a) {
+    const int rid = blockIdx.x * RECTS_PER_CTA + (threadIdx.x >> 5);
+    if (rid >= a.nrect) return;
+    const int lane = threadIdx.x & 31;
+    const AdjRect R = a.rects[rid];
+    const AdjPatch dp = a.patches[R.dst_patch];
+    const bool coarse = R.kind == ADJ_RECT_COARSE;
+    const AdjPatch sp = coarse ? a.coarse_patches[R.src_patch] : a.patches[R.src_patch];
+    const int base = a.rect_cell0[rid];
+    const int n = R.ni * R.nj;
+    for (int t = lane; t < n; t += 32) {
+        const int di = t / R.nj, dj = t - di * R.nj;
+        const int pos = base + t;
+        const int dst = (int)(dp.offset + (int64_t)(R.di0 + di) * dp.pitch + (R.dj0 + dj));
+        a.plan.dst[pos] = dst;
+        if (coarse) {
+            const int gc = a.ghost_coarse;
+            const int ncx = sp.nx + 2 * gc;
+            const int i0 = a.axis_i[R.pad + di];
+            int j0 = 0, j1 = 0;
+            double wy = 0.0;
+            if (a.ndim == 2) {
+                j0 = a.axis_i[R.pad + R.ni + dj];
+                wy = a.axis_w[R.pad + R.ni + dj];
+                j1 = min(j0 + 1, sp.ny + 2 * gc - 1);
+            }
+            const int i1 = min(i0 + 1, ncx - 1);
+            a.plan.c_base[pos] = (int)(sp.offset + (int64_t)i0 * sp.pitch + j0);
+            a.plan.c_step[pos] = (i1 - i0) * sp.pitch | ((j1 - j0) << 30);
+            a.plan.c_wx[pos] = a.axis_w[R.pad + di];
+            a.plan.c_wy[pos] = wy;
+            a.plan.src[pos] = pos;
+            a.plan.meta[pos] = 1u;
+        } else {
+            a.plan.src[pos] = (int)(sp.offset + (int64_t)(R.si0 + di) * sp.pitch + (R.sj0 + dj));
+            a.plan.meta[pos] = 0u;
+        }
+        if (a.owner) a.owner[dst] = pos;
+    }
+}
+
+__global__ void k2_plan_physical(AdjGhostPlanBuildArgs a, int first) {
+    const AdjPatch p = a.edge_patches[blockIdx.y];
+    const int g = a.ghost;
+    const int NX = p.nx + 2 * g;
+    const int gy = a.ndim == 2 ? g : 0;
+    const int NY = p.ny + 2 * gy;
+    const int ring = NX * NY - p.nx * p.ny;
+    const bool xlo = p.edges & ADJ_EDGE_XLO, xhi = p.edges & ADJ_EDGE_XHI;
+    const bool ylo = a.ndim == 2 && (p.edges & ADJ_EDGE_YLO), yhi = a.ndim == 2 && (p.edges & ADJ_EDGE_YHI);
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ring; r += gridDim.x * blockDim.x) {
+        int ii, jj;
+        const int band = g * NY;
+        if (r < band) { ii = r / NY; jj = r % NY; }
+        else if (r < 2 * band) { const int s = r - band; ii = NX - g + s / NY; jj = s % NY; }
+        else {
+            const int s = r - 2 * band;
+            ii = g + s / (2 * gy);
+            const int k = s % (2 * gy);
+            jj = k < gy ? k : NY - 2 * gy + k;
+        }
+        bool nx_, hx, ny_ = false, hy = false;
+        const int sx = phys_src(ii, NX, g, xlo, xhi, a.bc[0], a.bc[1], &nx_, &hx);
+        int sy = jj;
+        if (a.ndim == 2) sy = phys_src(jj, NY, g, ylo, yhi, a.bc[2], a.bc[3], &ny_, &hy);
+        if (!hx && !hy) continue;
+        unsigned sign = 0u;
+        if (nx_ && a.normal_comp[0] >= 0) sign ^= 2u << a.normal_comp[0];
+        if (ny_ && a.normal_comp[1] >= 0) sign ^= 2u << a.normal_comp[1];
+        const int dst = (int)(p.offset + (int64_t)ii * p.pitch + jj);
+        const int src = (int)(p.offset + (int64_t)sx * p.pitch + sy);
+        const int pos = first + atomicAdd(a.counter, 1);
+        const int o = a.owner ? a.owner[src] : -1;
+        a.plan.dst[pos] = dst;
+        if (o >= 0) {               // source is a ghost the in-domain phases write
+            a.plan.src[pos] = a.plan.src[o];
+            a.plan.meta[pos] = a.plan.meta[o] ^ sign;
+        } else {                    // interior (or untouched) cell of the same patch
+            a.plan.src[pos] = src;
+            a.plan.meta[pos] = sign;
+        }
+    }
+}
+
+int ghost_plan_build(const AdjGhostPlanBuildArgs& a, int rect_cells) {
+    cudaStream_t st = (cudaStream_t)a.stream;
+    if (a.nrect > 0) {
+        const int blocks = (a.nrect + RECTS_PER_CTA - 1) / RECTS_PER_CTA;
+        k2_plan_rects<<<blocks, 32 * RECTS_PER_CTA, 0, st>>>(a);
+        int rc = check_launch("k2_plan_rects");
+        if (rc) return rc;
+    }
+    if (a.nedge > 0 && a.max_ghost_cells > 0) {
+        int bx = (a.max_ghost_cells + 255) / 256;
+        if (bx > 4096) bx = 4096;
+        k2_plan_physical<<<dim3(bx, a.nedge), 256, 0, st>>>(a, rect_cells);
+        return check_launch("k2_plan_physical");
+    }
+    return ADJ_OK;
+}
+
+__global__ void __launch_bounds__(256) k2_gather(AdjGhostPlanFillArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    double wt = a.w_time;
+    int tmode = a.time_mode;
+    if (a.w_time_dev) {           // graph replays: negative weight = old state only
+        wt = *a.w_time_dev;
+        tmode = wt < 0.0 ? 0 : 1;
+    }
+    const int64_t cs = a.comp_stride, ccs = a.coarse_comp_stride;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < a.plan.n; t += gridDim.x * blockDim.x) {
+        const int dst = a.plan.dst[t], src = a.plan.src[t];
+        const unsigned meta = a.plan.meta[t];
+        double v[3];
+        if (meta & 1u) {
+            const int cb = a.plan.c_base[src];
+            const int step = a.plan.c_step[src];
+            const int di = step & 0x3fffffff, dj = (int)((unsigned)step >> 30);
+            const double wx = a.plan.c_wx[src], wy = a.plan.c_wy[src];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (c >= a.m) break;
+                const double* po = a.q_coarse_old + c * ccs + cb;
+                const double* pn = a.q_coarse_new + c * ccs + cb;
+                double vo = 0.0, vn = 0.0;
+                if (a.ndim == 2) {      // interpolate_patch, geometry.py:302-327 (reference order)
+                    if (tmode != 2)
+                        vo = po[0] * (1.0 - wx) * (1.0 - wy) + po[di] * wx * (1.0 - wy) + po[dj] * (1.0 - wx) * wy +
+                             po[di + dj] * wx * wy;
+                    if (tmode != 0)
+                        vn = pn[0] * (1.0 - wx) * (1.0 - wy) + pn[di] * wx * (1.0 - wy) + pn[dj] * (1.0 - wx) * wy +
+                             pn[di + dj] * wx * wy;
+                } else {
+                    if (tmode != 2) vo = po[0] * (1.0 - wx) + po[di] * wx;
+                    if (tmode != 0) vn = pn[0] * (1.0 - wx) + pn[di] * wx;
+                }
+                v[c] = tmode == 0 ? vo : (tmode == 2 ? vn : (1.0 - wt) * vo + wt * vn);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                if (c < a.m) v[c] = a.q[c * cs + src];
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (c >= a.m) break;
+            a.q[c * cs + dst] = (meta >> (1 + c)) & 1u ? v[c] * -1.0 : v[c];
+        }
+    }
+}
+
+int fill_ghost_plan(const AdjGhostPlanFillArgs& a) {
+    if (a.plan.n <= 0) return ADJ_OK;
+    int blocks = (a.plan.n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    launch_pdl(k2_gather, dim3(blocks), dim3(256), 0, (cudaStream_t)a.stream, a);
+    return check_launch("k2_gather");
+}
+
+// ---------------------------------------------------------------------------
 // K4 restriction.  numpy's mean over the (r, r) child block (amr.py:440-450)
 // sums each child row sequentially and adds the row sums in order, then
 // divides by r*r -- except when the coarse box is one cell wide in y: numpy
@@ -228,6 +394,8 @@ ADJ_D double block_sum(const double* f, const double* wet, int64_t pitch, int fi
 }
 
 __global__ void k4_restrict(AdjRestrictArgs a) {
+    pdl_wait();
+    pdl_trigger();
     const AdjRect R = a.rects[blockIdx.x];
     const AdjPatch cp = a.coarse_patches[R.dst_patch];
     const AdjPatch fp = a.fine_patches[R.src_patch];
@@ -268,7 +436,7 @@ __global__ void k4_restrict(AdjRestrictArgs a) {
 int restrict_level(const AdjRestrictArgs& a) {
     if (a.nrect <= 0) return ADJ_OK;
     int threads = a.max_rect_cells >= 256 ? 256 : (a.max_rect_cells >= 128 ? 128 : 64);
-    k4_restrict<<<a.nrect, threads, 0, (cudaStream_t)a.stream>>>(a);
+    launch_pdl(k4_restrict, dim3(a.nrect), dim3(threads), 0, (cudaStream_t)a.stream, a);
     return check_launch("k4_restrict");
 }
 

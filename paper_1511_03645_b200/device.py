@@ -665,6 +665,126 @@ def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ra
     _lib.check(_lib.lib().adj_fill_ghost_rects(_lib.C.byref(a)), "adj_fill_ghost_rects")
 
 
+def _bc_codes(boundary):
+    return tuple(_lib.BC_WALL if sd == "wall" else _lib.BC_OUTFLOW
+                 for sd in (boundary.left, boundary.right, boundary.bottom, boundary.top))
+
+
+def physical_cell_count(store: LevelStore, level_shape) -> int:
+    """Out-of-domain ghost cells of every patch (what the physical phase writes)."""
+    g = store.g
+    tot = 0
+    for p in store.patches:
+        s = p.spec
+        full = 1
+        ind = 1
+        for ax in range(store.ndim):
+            full *= s.shape[ax] + 2 * g
+            ind *= min(s.hi[ax] + g, level_shape[ax] - 1) - max(s.lo[ax] - g, 0) + 1
+        tot += full - ind
+    return int(tot)
+
+
+class GhostPlan:
+    """Whole-level ghost fill as one gather launch (adj_ghost_plan_build /
+    adj_fill_ghost_plan): the level's disjoint COARSE + COPY rectangles and
+    its physical boundary cells, compiled on the device once per regrid.
+    Same values as the coarse -> copy -> physical phases
+    (fill_level_ghosts, amr.py:479-491)."""
+
+    def __init__(self, store: LevelStore, rects: RectTable, coarse_store, boundary, equation, level_shape):
+        torch = _torch()
+        r = rects.np if rects.n else np.zeros(0, dtype=_lib.RECT_DTYPE)
+        kinds = r["kind"]
+        is_c = kinds == _lib.RECT_COARSE
+        if len(r) > 1 and np.any(is_c[1:] & ~is_c[:-1]):
+            raise ValueError("GhostPlan needs COARSE rects before COPY rects")
+        cells = (r["ni"].astype(np.int64) * r["nj"].astype(np.int64))
+        cell0 = np.zeros(len(r) + 1, dtype=np.int64)
+        np.cumsum(cells, out=cell0[1:])
+        rect_cells = int(cell0[-1])
+        nc = int(cells[kinds == _lib.RECT_COARSE].sum())
+        store.edges_table(level_shape)
+        edge_tab, nedge = store._edge_tab
+        nphys = physical_cell_count(store, level_shape) if nedge else 0
+        n = rect_cells + nphys
+        self.n, self.nc = n, nc
+        i32, f64 = torch.int32, torch.float64
+        self.dst = torch.empty(max(n, 1), dtype=i32, device="cuda")
+        self.src = torch.empty(max(n, 1), dtype=i32, device="cuda")
+        self.meta = torch.empty(max(n, 1), dtype=i32, device="cuda")
+        self.c_base = torch.empty(max(nc, 1), dtype=i32, device="cuda")
+        self.c_step = torch.empty(max(nc, 1), dtype=i32, device="cuda")
+        self.c_wx = torch.empty(max(nc, 1), dtype=f64, device="cuda")
+        self.c_wy = torch.empty(max(nc, 1), dtype=f64, device="cuda")
+        self.plan = _lib.AdjGhostPlan()
+        for k in ("dst", "src", "meta", "c_base", "c_step", "c_wx", "c_wy"):
+            setattr(self.plan, k, _ptr(getattr(self, k)))
+        self.plan.n, self.plan.nc = n, nc
+        if n == 0:
+            return
+        counter = torch.zeros(1, dtype=i32, device="cuda")
+        owner = torch.full((store.plane,), -1, dtype=i32, device="cuda") if nphys else None
+        cell0_dev = torch.from_numpy(cell0.astype(np.int32)).to("cuda")
+        a = _lib.AdjGhostPlanBuildArgs()
+        a.plan = self.plan
+        a.rects = _ptr(rects.dev) if rects.n else 0
+        a.rect_cell0 = _ptr(cell0_dev)
+        a.patches = _ptr(store.table)
+        a.coarse_patches = _ptr(coarse_store.table) if coarse_store is not None else 0
+        a.axis_w = _ptr(rects.axis_w)
+        a.axis_i = _ptr(rects.axis_i)
+        a.edge_patches = _ptr(edge_tab) if nedge else 0
+        a.owner = _ptr(owner)
+        a.counter = _ptr(counter)
+        a.nrect = rects.n
+        a.rect_cells = rect_cells
+        a.nedge = nedge
+        a.ndim = store.ndim
+        a.m = store.m
+        a.ghost = store.g
+        a.ghost_coarse = coarse_store.g if coarse_store is not None else 0
+        a.max_ghost_cells = store.max_ghost_cells
+        for k, code in enumerate(_bc_codes(boundary)):
+            a.bc[k] = code
+        a.normal_comp[0] = equation.normal_component(0)
+        a.normal_comp[1] = equation.normal_component(1) if store.ndim == 2 else -1
+        a.stream = _lib.stream_ptr(None)
+        _lib.check(_lib.lib().adj_ghost_plan_build(_lib.C.byref(a)), "adj_ghost_plan_build")
+        got = int(counter.item())
+        if got != nphys:
+            raise RuntimeError(f"ghost plan: {got} physical cells, expected {nphys}")
+
+    @staticmethod
+    def usable(store: LevelStore, coarse_store) -> bool:
+        """Entries are 32-bit plane offsets."""
+        lim = 2 ** 31 - 1
+        return store.plane < lim and (coarse_store is None or coarse_store.plane < lim)
+
+    def fill(self, store: LevelStore, q_old=None, q_new=None, coarse_store=None, w_time=0.0, mode=0, stream=None):
+        wptr = 0
+        if PARAMS is not None and self.nc:      # captured sweep: weight read from device memory
+            if mode == 2:
+                raise RuntimeError("coarse patches without saved state cannot be graph-replayed")
+            wptr = PARAMS.take(w_time if mode == 1 else -1.0)
+        if SHADOW or self.n == 0:
+            return
+        a = _lib.AdjGhostPlanFillArgs()
+        a.plan = self.plan
+        a.q = _ptr(store.buf[store.cur])
+        a.q_coarse_old = _ptr(q_old)
+        a.q_coarse_new = _ptr(q_new)
+        a.comp_stride = store.plane
+        a.coarse_comp_stride = coarse_store.plane if coarse_store is not None else 0
+        a.ndim = store.ndim
+        a.m = store.m
+        a.time_mode = mode
+        a.w_time = w_time
+        a.w_time_dev = wptr
+        a.stream = _lib.stream_ptr(stream)
+        _lib.check(_lib.lib().adj_fill_ghost_plan(_lib.C.byref(a)), "adj_fill_ghost_plan")
+
+
 def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=None, slots=None):
     """K2 physical phase on every patch of the store (solver.py:125-146);
     ``slots`` restricts it to a subset of patches."""
@@ -727,7 +847,7 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
         bad = store.nonfinite_acc
     else:
         bad = store.scratch("nonfinite", npatch, torch.int32)
-    counter = store.scratch("work_counter", 1, torch.int32)
+    counter = store.scratch("work_counter", 2, torch.int32)   # zero; kept zero by the FAST kernel
     if SHADOW:
         return smax[: 2 * npatch].view(npatch, 2), bad[:npatch]
     system, form, rev = equation.kernel_spec()
@@ -754,8 +874,10 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     a.limiter = _lib.LIMITERS[limiter]
     a.variant = variant
     a.flags = (_lib.STEP_KEEP_NONFINITE | _lib.STEP_NO_SPEED_OUT) if accumulate else 0
-    if variant == _lib.VARIANT_FAST and store.ndim == 2 and store.two_rows():
-        a.flags |= _lib.STEP_TWO_ROWS
+    if variant == _lib.VARIANT_FAST and store.ndim == 2:
+        a.flags |= _lib.STEP_COUNTER_ZERO
+        if store.two_rows():
+            a.flags |= _lib.STEP_TWO_ROWS
     a.dt = dt
     a.dtdx = dt / spec0.dx
     a.dtdy = dt / spec0.dy if store.ndim == 2 else 0.0

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.load_library()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.adj_abi_version() == 1
+    assert lib.adj_abi_version() == _lib.ABI_VERSION
     ni, nj = C.c_int32(), C.c_int32()
     assert lib.adj_step_tile_shape(1, 2, C.byref(ni), C.byref(nj)) == 0 and nj.value == 28
     assert lib.adj_step_tile_shape(7, 2, C.byref(ni), C.byref(nj)) == _lib.ADJ_ERR_BAD_ARG
@@ -44,6 +44,8 @@ def test_null_args_rejected_without_gpu():
     a = _lib.AdjStepArgs()
     assert lib.adj_step_level(C.byref(a)) == _lib.ADJ_ERR_BAD_ARG
     assert lib.adj_flag_adjoint(C.byref(_lib.AdjFlagArgs())) == _lib.ADJ_ERR_BAD_ARG
+    assert lib.adj_ghost_plan_build(C.byref(_lib.AdjGhostPlanBuildArgs())) == _lib.ADJ_ERR_BAD_ARG
+    assert lib.adj_fill_ghost_plan(C.byref(_lib.AdjGhostPlanFillArgs())) == _lib.ADJ_ERR_BAD_ARG
 
 
 def _struct_fields(name):
@@ -52,7 +54,7 @@ def _struct_fields(name):
     body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
     fields = []
     typewords = {"const", "unsigned", "long", "double", "int32_t", "int64_t", "uint32_t", "uint8_t", "void", "char",
-                 "AdjPatch", "AdjTile", "AdjRect"}
+                 "AdjPatch", "AdjTile", "AdjRect", "AdjGhostPlan"}
     for decl in body.split(";"):
         toks = decl.replace("*", " ").replace(",", " , ").split()
         if not toks:
@@ -65,7 +67,8 @@ def _struct_fields(name):
     return fields
 
 
-@pytest.mark.parametrize("name", ["AdjStepArgs", "AdjPhysArgs", "AdjGhostArgs", "AdjRestrictArgs", "AdjFlagArgs"])
+@pytest.mark.parametrize("name", ["AdjStepArgs", "AdjPhysArgs", "AdjGhostArgs", "AdjRestrictArgs", "AdjFlagArgs",
+                                  "AdjGhostPlan", "AdjGhostPlanBuildArgs", "AdjGhostPlanFillArgs"])
 def test_ctypes_structs_mirror_header(name):
     from paper_1511_03645_b200 import _lib
     assert [f[0] for f in getattr(_lib, name)._fields_] == _struct_fields(name)

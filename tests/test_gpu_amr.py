@@ -22,6 +22,23 @@ def build_eq(case):
 
 
 def run(name, variant, adjoint_from_golden=True):
+    from paper_1511_03645_b200 import amr
+    h, ctx, dt, case = setup(name, variant, adjoint_from_golden)
+    out = []
+    for step in range(case["steps"]):
+        amr.advance_hierarchy(h, 1, dt, ctx)
+        snap = {"nlev": h.num_levels(), "flagged": list(ctx.flagged_per_regrid),
+                "cell_steps": [ctx.cell_steps.get(lv, 0) for lv in range(1, 5)]}
+        for lev in range(1, h.num_levels() + 1):
+            ps = h.patches(lev)
+            snap[f"L{lev}_boxes"] = np.array([[*p.spec.lo, *p.spec.hi] for p in ps])
+            snap[f"L{lev}_q"] = np.concatenate([p.interior().reshape(p.num_components, -1) for p in ps], axis=1)
+        out.append(snap)
+    return out
+
+
+def setup(name, variant, adjoint_from_golden=True):
+    """The case's initial hierarchy (init regrids + IC), context and dt."""
     from paper_1511_03645_b200 import adjoint, amr, solver
     from paper_1511_03645_b200.geometry import PatchHierarchy, UniformField
     case = CASES[name]
@@ -74,17 +91,7 @@ def run(name, variant, adjoint_from_golden=True):
     assert ctx.flagged_per_regrid == list(g["init_flagged"])
     dt = solver.select_dt(h, eq, 0.9)
     assert dt == g["dt"]
-    out = []
-    for step in range(case["steps"]):
-        amr.advance_hierarchy(h, 1, dt, ctx)
-        snap = {"nlev": h.num_levels(), "flagged": list(ctx.flagged_per_regrid),
-                "cell_steps": [ctx.cell_steps.get(lv, 0) for lv in range(1, 5)]}
-        for lev in range(1, h.num_levels() + 1):
-            ps = h.patches(lev)
-            snap[f"L{lev}_boxes"] = np.array([[*p.spec.lo, *p.spec.hi] for p in ps])
-            snap[f"L{lev}_q"] = np.concatenate([p.interior().reshape(p.num_components, -1) for p in ps], axis=1)
-        out.append(snap)
-    return out
+    return h, ctx, dt, case
 
 
 def check(name, out, exact):

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+python tools/c5_graph_time.py > gpurun_out/c5_graph.log 2>&1
+NCU_ONE=1 ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none --csv --log-file gpurun_out/launches_c5_warm.csv python tools/c5_graph_time.py > gpurun_out/ncu32.log 2>&1
+echo done

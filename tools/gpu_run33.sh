@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+python -m pytest tests -q -m gpu -x > gpurun_out/pytest33.log 2>&1
+python tools/c5_graph_time.py > gpurun_out/c5_graph33.log 2>&1
+NCU_ONE=1 ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none --csv --log-file gpurun_out/launches_c5_warm33.csv python tools/c5_graph_time.py > gpurun_out/ncu33.log 2>&1
+echo done

@@ -35,7 +35,8 @@ for _ in range(a.launches):
     st.cur = out
     times.append((e0, e1))
 torch.cuda.synchronize()
-print("k1 ms:", [round(x.elapsed_time(y), 4) for x, y in times])
+ms = [x.elapsed_time(y) for x, y in times]
+print("k1 ms:", [round(v, 4) for v in ms], "median", round(sorted(ms)[len(ms) // 2], 4), os.environ.get("ADJAMR_LIB", "default"))
 if a.flag:
     ring = bench.adjoint_ring(41)
     device.launch_flag(st, ring, (1024, 1024), (0.0, 0.0), bench.L / 1024, bench.L / 1024, (0.0, 0.0),
