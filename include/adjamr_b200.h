@@ -256,6 +256,13 @@ typedef struct AdjRestrictArgs {
     int64_t coarse_aux_stride, fine_aux_stride;
     int32_t nrect, ndim, m, ratio, swe, max_rect_cells;
     int32_t ghost_coarse, ghost_fine;
+    /* optional planned form (built per regrid): one entry per covered coarse
+       cell, used instead of rects when cell_dst != NULL */
+    const int32_t* cell_dst;     /* coarse cell offset in the coarse plane                        */
+    const int32_t* cell_src;     /* offset of its first fine child in the fine plane              */
+    const int32_t* cell_meta;    /* bit 0: numpy flat order (overlap box one cell wide in y);
+                                    bits 1..: fine patch pitch                                    */
+    int32_t ncell, pad;
     void* stream;
 } AdjRestrictArgs;
 int adj_restrict(const AdjRestrictArgs* a);

@@ -100,7 +100,8 @@ class AdjRestrictArgs(C.Structure):
                 ("coarse_comp_stride", I64), ("fine_comp_stride", I64),
                 ("coarse_aux_stride", I64), ("fine_aux_stride", I64),
                 ("nrect", I32), ("ndim", I32), ("m", I32), ("ratio", I32), ("swe", I32),
-                ("max_rect_cells", I32), ("ghost_coarse", I32), ("ghost_fine", I32), ("stream", P)]
+                ("max_rect_cells", I32), ("ghost_coarse", I32), ("ghost_fine", I32),
+                ("cell_dst", P), ("cell_src", P), ("cell_meta", P), ("ncell", I32), ("pad", I32), ("stream", P)]
 
 
 class AdjFlagArgs(C.Structure):

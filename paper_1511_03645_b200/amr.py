@@ -630,6 +630,8 @@ def _fill_physical_subset(st, slots, boundary, equation, level_shape):
 
 # planned whole-level ghost fill (device.GhostPlan); False: the three-phase launches
 USE_GHOST_PLAN = True
+# planned restriction (device.RestrictPlan, one thread per coarse cell); False: per-rect blocks
+USE_RESTRICT_PLAN = True
 
 
 class LevelPlan:
@@ -803,7 +805,12 @@ def restrict_fine_to_coarse(hierarchy: PatchHierarchy, level: int):
     cst.sync_in()
     fst.sync_in()
     if fpl.restrict_to is None or fpl.restrict_to[0] is not cst:
-        fpl.restrict_to = (cst, device.RectTable(_restrict_rects(coarse, fine, r)))
+        rects = _restrict_rects(coarse, fine, r)
+        if USE_RESTRICT_PLAN and device.RestrictPlan.usable(cst, fst):
+            tab = device.RestrictPlan(cst, fst, rects, r)
+        else:
+            tab = device.RectTable(rects)
+        fpl.restrict_to = (cst, tab)
     cst._unalias()
     device.restrict_rects(cst, fst, fpl.restrict_to[1], r, cst.swe)
 

@@ -134,7 +134,8 @@ int adj_fill_ghost_plan(const AdjGhostPlanFillArgs* a) {
 }
 
 int adj_restrict(const AdjRestrictArgs* a) {
-    if (!a || !a->q_coarse || !a->q_fine || !a->rects) return adj::bad("null pointer");
+    if (!a || !a->q_coarse || !a->q_fine || !(a->rects || (a->cell_dst && a->cell_src && a->cell_meta)))
+        return adj::bad("null pointer");
     if (a->ratio < 1) return adj::bad("ratio");
     if (a->swe && (!a->aux_coarse || !a->aux_fine)) return adj::bad("swe restriction needs aux");
     return adj::restrict_level(*a);

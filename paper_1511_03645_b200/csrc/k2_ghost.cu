@@ -296,6 +296,17 @@ int ghost_plan_build(const AdjGhostPlanBuildArgs& a, int rect_cells) {
     return ADJ_OK;
 }
 
+// interpolate_patch (geometry.py:302-327) / linear in 1D, reference order,
+// at (i0, j0) with row step di and column step dj
+template <int NDIM>
+ADJ_D double interp_at(const double* p, int di, int dj, double wx, double wy) {
+    if (NDIM == 2)
+        return p[0] * (1.0 - wx) * (1.0 - wy) + p[di] * wx * (1.0 - wy) + p[dj] * (1.0 - wx) * wy +
+               p[di + dj] * wx * wy;
+    return p[0] * (1.0 - wx) + p[di] * wx;
+}
+
+template <int NDIM, int M>
 __global__ void __launch_bounds__(256) k2_gather(AdjGhostPlanFillArgs a) {
     pdl_wait();
     pdl_trigger();
@@ -306,44 +317,35 @@ __global__ void __launch_bounds__(256) k2_gather(AdjGhostPlanFillArgs a) {
         tmode = wt < 0.0 ? 0 : 1;
     }
     const int64_t cs = a.comp_stride, ccs = a.coarse_comp_stride;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < a.plan.n; t += gridDim.x * blockDim.x) {
+    const int n = a.plan.n, nc = a.plan.nc;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        // rect COARSE entries [0, nc) own coarse entry t: load it alongside the plan entry
+        const bool spec = t < nc;
+        int cb = 0, step = 0;
+        double wx = 0.0, wy = 0.0;
+        if (spec) { cb = a.plan.c_base[t]; step = a.plan.c_step[t]; wx = a.plan.c_wx[t]; wy = a.plan.c_wy[t]; }
         const int dst = a.plan.dst[t], src = a.plan.src[t];
         const unsigned meta = a.plan.meta[t];
-        double v[3];
+        double v[M];
         if (meta & 1u) {
-            const int cb = a.plan.c_base[src];
-            const int step = a.plan.c_step[src];
+            if (!spec) {          // physical cell mirroring a coarse-interpolated ghost
+                cb = a.plan.c_base[src]; step = a.plan.c_step[src]; wx = a.plan.c_wx[src]; wy = a.plan.c_wy[src];
+            }
             const int di = step & 0x3fffffff, dj = (int)((unsigned)step >> 30);
-            const double wx = a.plan.c_wx[src], wy = a.plan.c_wy[src];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                if (c >= a.m) break;
+            for (int c = 0; c < M; ++c) {
                 const double* po = a.q_coarse_old + c * ccs + cb;
                 const double* pn = a.q_coarse_new + c * ccs + cb;
-                double vo = 0.0, vn = 0.0;
-                if (a.ndim == 2) {      // interpolate_patch, geometry.py:302-327 (reference order)
-                    if (tmode != 2)
-                        vo = po[0] * (1.0 - wx) * (1.0 - wy) + po[di] * wx * (1.0 - wy) + po[dj] * (1.0 - wx) * wy +
-                             po[di + dj] * wx * wy;
-                    if (tmode != 0)
-                        vn = pn[0] * (1.0 - wx) * (1.0 - wy) + pn[di] * wx * (1.0 - wy) + pn[dj] * (1.0 - wx) * wy +
-                             pn[di + dj] * wx * wy;
-                } else {
-                    if (tmode != 2) vo = po[0] * (1.0 - wx) + po[di] * wx;
-                    if (tmode != 0) vn = pn[0] * (1.0 - wx) + pn[di] * wx;
-                }
+                const double vo = tmode != 2 ? interp_at<NDIM>(po, di, dj, wx, wy) : 0.0;
+                const double vn = tmode != 0 ? interp_at<NDIM>(pn, di, dj, wx, wy) : 0.0;
                 v[c] = tmode == 0 ? vo : (tmode == 2 ? vn : (1.0 - wt) * vo + wt * vn);
             }
         } else {
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-                if (c < a.m) v[c] = a.q[c * cs + src];
+            for (int c = 0; c < M; ++c) v[c] = a.q[c * cs + src];
         }
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            if (c >= a.m) break;
-            a.q[c * cs + dst] = (meta >> (1 + c)) & 1u ? v[c] * -1.0 : v[c];
-        }
+        for (int c = 0; c < M; ++c) a.q[c * cs + dst] = (meta >> (1 + c)) & 1u ? v[c] * -1.0 : v[c];
     }
 }
 
@@ -351,7 +353,15 @@ int fill_ghost_plan(const AdjGhostPlanFillArgs& a) {
     if (a.plan.n <= 0) return ADJ_OK;
     int blocks = (a.plan.n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    launch_pdl(k2_gather, dim3(blocks), dim3(256), 0, (cudaStream_t)a.stream, a);
+    const cudaStream_t st = (cudaStream_t)a.stream;
+    const dim3 g(blocks), b(256);
+    if (a.ndim == 2 && a.m == 3) launch_pdl(k2_gather<2, 3>, g, b, 0, st, a);
+    else if (a.ndim == 1 && a.m == 2) launch_pdl(k2_gather<1, 2>, g, b, 0, st, a);
+    else if (a.ndim == 2 && a.m == 2) launch_pdl(k2_gather<2, 2>, g, b, 0, st, a);
+    else if (a.ndim == 1 && a.m == 3) launch_pdl(k2_gather<1, 3>, g, b, 0, st, a);
+    else if (a.ndim == 1 && a.m == 1) launch_pdl(k2_gather<1, 1>, g, b, 0, st, a);
+    else if (a.ndim == 2 && a.m == 1) launch_pdl(k2_gather<2, 1>, g, b, 0, st, a);
+    else return ADJ_ERR_BAD_ARG;
     return check_launch("k2_gather");
 }
 
@@ -433,7 +443,51 @@ __global__ void k4_restrict(AdjRestrictArgs a) {
     }
 }
 
+// Planned form: one thread per covered coarse cell, no rect / patch lookups.
+template <int M, bool SWE>
+__global__ void __launch_bounds__(256) k4_cells(AdjRestrictArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    const int r = a.ratio;
+    const int rj = a.ndim == 2 ? r : 1;
+    const double cnt = (double)(r * rj);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < a.ncell; t += gridDim.x * blockDim.x) {
+        const int cdst = a.cell_dst[t], fsrc = a.cell_src[t], meta = a.cell_meta[t];
+        const bool flat = meta & 1;
+        const int fpitch = meta >> 1;
+        if (!SWE) {
+#pragma unroll
+            for (int c = 0; c < M; ++c)
+                a.q_coarse[c * a.coarse_comp_stride + cdst] =
+                    block_sum(a.q_fine + c * a.fine_comp_stride + fsrc, nullptr, fpitch, 0, 0, r, rj, flat) / cnt;
+        } else {
+            const double* fd = a.aux_fine + a.fine_aux_stride + fsrc;   // depth plane
+            double ws = 0.0;
+            for (int p = 0; p < r; ++p)
+                for (int q = 0; q < rj; ++q) ws = ws + (fd[(int64_t)p * fpitch + q] > 0.0 ? 1.0 : 0.0);
+            const bool wetc = a.aux_coarse[a.coarse_aux_stride + cdst] > 0.0;
+            if (!(ws > 0.0 && wetc)) continue;
+#pragma unroll
+            for (int c = 0; c < M; ++c)
+                a.q_coarse[c * a.coarse_comp_stride + cdst] =
+                    block_sum(a.q_fine + c * a.fine_comp_stride + fsrc, fd, fpitch, 0, 0, r, rj, flat) / ws;
+        }
+    }
+}
+
 int restrict_level(const AdjRestrictArgs& a) {
+    if (a.cell_dst) {
+        if (a.ncell <= 0) return ADJ_OK;
+        int blocks = (a.ncell + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        const cudaStream_t st = (cudaStream_t)a.stream;
+        const dim3 g(blocks), b(256);
+        if (a.m == 3 && !a.swe) launch_pdl(k4_cells<3, false>, g, b, 0, st, a);
+        else if (a.m == 3) launch_pdl(k4_cells<3, true>, g, b, 0, st, a);
+        else if (a.m == 2 && !a.swe) launch_pdl(k4_cells<2, false>, g, b, 0, st, a);
+        else return ADJ_ERR_BAD_ARG;
+        return check_launch("k4_cells");
+    }
     if (a.nrect <= 0) return ADJ_OK;
     int threads = a.max_rect_cells >= 256 ? 256 : (a.max_rect_cells >= 128 ? 128 : 64);
     launch_pdl(k4_restrict, dim3(a.nrect), dim3(threads), 0, (cudaStream_t)a.stream, a);

@@ -887,29 +887,80 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     return smax[: 2 * npatch].view(npatch, 2), bad[:npatch]
 
 
+def restrict_cells(coarse_store, fine_store, rects, ratio):
+    """Planned restriction: per covered coarse cell (row-major within each
+    overlap rect) its coarse offset, the offset of its first fine child and
+    meta = flat | fine pitch << 1, from the UNSPLIT overlap rects (numpy's
+    flat reduction order depends on the overlap box, amr.py:440-450)."""
+    nd = coarse_store.ndim
+    gC, gF = coarse_store.g, fine_store.g
+    gCy, gFy = (gC, gF) if nd == 2 else (0, 0)
+    rj = ratio if nd == 2 else 1
+    ni = rects["ni"].astype(np.int64)
+    nj = rects["nj"].astype(np.int64)
+    cnt = ni * nj
+    rid = np.repeat(np.arange(len(rects)), cnt)
+    k = np.arange(int(cnt.sum())) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    a = k // nj[rid]
+    b = k % nj[rid]
+    ct = coarse_store.table_np
+    ft = fine_store.table_np
+    cp = rects["dst_patch"].astype(np.int64)[rid]
+    fp = rects["src_patch"].astype(np.int64)[rid]
+    cdst = ct["offset"][cp] + (gC + rects["di0"].astype(np.int64)[rid] + a) * ct["pitch"][cp].astype(np.int64) + \
+        (gCy + rects["dj0"].astype(np.int64)[rid] + b)
+    fpitch = ft["pitch"][fp].astype(np.int64)
+    fsrc = ft["offset"][fp] + (gF + rects["si0"].astype(np.int64)[rid] + a * ratio) * fpitch + \
+        (gFy + rects["sj0"].astype(np.int64)[rid] + b * rj)
+    flat = (nd == 2) & (nj[rid] == 1)
+    meta = flat.astype(np.int64) | (fpitch << 1)
+    return cdst.astype(np.int32), fsrc.astype(np.int32), meta.astype(np.int32)
+
+
+class RestrictPlan:
+    """Device copy of restrict_cells (built once per regrid)."""
+
+    def __init__(self, coarse_store, fine_store, rects_np, ratio):
+        torch = _torch()
+        d, s_, m = restrict_cells(coarse_store, fine_store, rects_np, ratio)
+        self.n = len(d)
+        self.dst = torch.from_numpy(d if self.n else np.zeros(1, np.int32)).to("cuda")
+        self.src = torch.from_numpy(s_ if self.n else np.zeros(1, np.int32)).to("cuda")
+        self.meta = torch.from_numpy(m if self.n else np.zeros(1, np.int32)).to("cuda")
+
+    @staticmethod
+    def usable(coarse_store, fine_store) -> bool:
+        lim = 2 ** 31 - 1
+        return coarse_store.plane < lim and fine_store.plane < lim
+
+
 def restrict_rects(coarse_store, fine_store, rects_np, ratio, swe, stream=None):
-    tab = _as_table(rects_np)
-    if tab.n == 0 or SHADOW:
+    plan = rects_np if isinstance(rects_np, RestrictPlan) else None
+    tab = None if plan is not None else _as_table(rects_np)
+    if (plan.n if plan is not None else tab.n) == 0 or SHADOW:
         return
-    rects = tab.dev
     a = _lib.AdjRestrictArgs()
+    if plan is not None:
+        a.cell_dst, a.cell_src, a.cell_meta = _ptr(plan.dst), _ptr(plan.src), _ptr(plan.meta)
+        a.ncell = plan.n
+    else:
+        a.rects = _ptr(tab.dev)
+        a.nrect = tab.n
+        a.max_rect_cells = tab.max_cells
     a.q_coarse = _ptr(coarse_store.buf[coarse_store.cur])
     a.q_fine = _ptr(fine_store.buf[fine_store.cur])
     a.aux_coarse = _ptr(coarse_store.aux)
     a.aux_fine = _ptr(fine_store.aux)
     a.coarse_patches = _ptr(coarse_store.table)
     a.fine_patches = _ptr(fine_store.table)
-    a.rects = _ptr(rects)
     a.coarse_comp_stride = coarse_store.plane
     a.fine_comp_stride = fine_store.plane
     a.coarse_aux_stride = coarse_store.plane
     a.fine_aux_stride = fine_store.plane
-    a.nrect = tab.n
     a.ndim = coarse_store.ndim
     a.m = coarse_store.m
     a.ratio = ratio
     a.swe = int(swe)
-    a.max_rect_cells = tab.max_cells
     a.ghost_coarse = coarse_store.g
     a.ghost_fine = fine_store.g
     a.stream = _lib.stream_ptr(stream)

@@ -63,3 +63,31 @@ def test_plan_counts_physical_cells():
     assert gp.n == gp.nc + int((amr._plan(h, 1).copies.np["ni"] * amr._plan(h, 1).copies.np["nj"]).sum()) + \
         device.physical_cell_count(st, h.level_shape(1))
     assert np.isfinite(gp.n)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_planned_restrict_equals_rect_restrict(name):
+    import torch
+    from paper_1511_03645_b200 import _lib, amr
+    h, ctx, dt, case = setup(name, _lib.VARIANT_EXACT)
+    amr.advance_hierarchy(h, 1, dt, ctx)
+    done = 0
+    for lev in range(h.num_levels() - 1, 0, -1):
+        if not h.patches(lev + 1):
+            continue
+        fpl = amr._plan(h, lev + 1)
+        outs = []
+        for plan in (False, True):
+            amr.USE_RESTRICT_PLAN = plan
+            fpl.restrict_to = None
+            try:
+                before = fpl.cst.buf[fpl.cst.cur].clone()
+                amr.restrict_fine_to_coarse(h, lev)
+                outs.append(fpl.cst.buf[fpl.cst.cur].clone())
+                fpl.cst.buf[fpl.cst.cur].copy_(before)
+            finally:
+                amr.USE_RESTRICT_PLAN = True
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], outs[1]), (name, lev, int((outs[0] != outs[1]).sum()))
+        done += 1
+    assert done

@@ -91,3 +91,42 @@ def test_axis_weight_tables_match_loop():
         assert w.tobytes() == w0.tobytes()
         assert np.array_equal(i, i0)
         assert r1.tobytes() == r2.tobytes()
+
+
+def test_restrict_cells_match_rect_loop():
+    """device.restrict_cells flattens restriction rects exactly as k4_restrict
+    walks them (amr.py:440-450 order flag from the unsplit overlap box)."""
+    rng = np.random.default_rng(2)
+    for nd in (1, 2):
+        r = 4
+        ct = np.zeros(3, dtype=_lib.PATCH_DTYPE)
+        ft = np.zeros(4, dtype=_lib.PATCH_DTYPE)
+        ct["offset"] = [0, 5000, 9000]
+        ct["pitch"] = [12, 20, 8] if nd == 2 else 1
+        ft["offset"] = [0, 30000, 70000, 99000]
+        ft["pitch"] = [36, 68, 20, 44] if nd == 2 else 1
+        cs = types.SimpleNamespace(ndim=nd, g=2, table_np=ct)
+        fs = types.SimpleNamespace(ndim=nd, g=2, table_np=ft)
+        rects = np.zeros(30, dtype=_lib.RECT_DTYPE)
+        rects["dst_patch"] = rng.integers(0, 3, 30)
+        rects["src_patch"] = rng.integers(0, 4, 30)
+        rects["di0"] = rng.integers(0, 5, 30)
+        rects["si0"] = rng.integers(0, 5, 30)
+        rects["ni"] = rng.integers(1, 9, 30)
+        if nd == 2:
+            rects["dj0"] = rng.integers(0, 5, 30)
+            rects["sj0"] = rng.integers(0, 5, 30)
+            rects["nj"] = rng.choice([1, 2, 7], 30)
+        else:
+            rects["nj"] = 1
+        d, s, m = device.restrict_cells(cs, fs, rects, r)
+        want = []
+        for R in rects:
+            cp, fp = ct[R["dst_patch"]], ft[R["src_patch"]]
+            gy = 2 if nd == 2 else 0
+            for a in range(R["ni"]):
+                for b in range(R["nj"]):
+                    cd = cp["offset"] + (2 + R["di0"] + a) * cp["pitch"] + gy + R["dj0"] + b
+                    fsrc = fp["offset"] + (2 + R["si0"] + a * r) * fp["pitch"] + gy + R["sj0"] + b * (r if nd == 2 else 1)
+                    want.append((cd, fsrc, int(nd == 2 and R["nj"] == 1) | (int(fp["pitch"]) << 1)))
+        assert [tuple(map(int, x)) for x in zip(d, s, m)] == want
