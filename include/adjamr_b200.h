@@ -306,6 +306,32 @@ typedef struct AdjFlagArgs {
 } AdjFlagArgs;
 int adj_flag_adjoint(const AdjFlagArgs* a);
 
+/* K5: regrid flag post-processing on the device.  Replaces, for one parent
+ * level, the per-patch region overrides of flag_cells (amr.py:137-154), the
+ * box dilation of buffer_flags clipped to each patch (amr.py:157-179), the OR
+ * into the level mask and the proper-nesting clip by the one-cell erosion of
+ * the level's occupancy with edge padding (allowed_region_mask,
+ * geometry.py:341-368; amr.py:580-581).  Input: K3's packed flags.  Output:
+ * one byte per cell of the level index space (x-major, level_ny contiguous):
+ * bit 0 = clipped flag, bit 1 = allowed; only this mask goes to the host
+ * clusterer.  raw_count = flags after region overrides (amr.py:575). */
+typedef struct AdjFlagMaskArgs {
+    const uint32_t* flag_bits;   /* K3 flag words (AdjPatch.flag_word, row-major interior)          */
+    const AdjPatch* patches;     /* parent level */
+    const uint8_t* region_rows;  /* optional: bit k = row centre inside region k's x range          */
+    const uint8_t* region_cols;  /*           bit k = column centre inside region k's y range       */
+    const int32_t* region_row_off;  /* [npatch] first row entry of each patch                       */
+    const int32_t* region_col_off;  /* [npatch] first column entry of each patch                    */
+    uint8_t* mask;               /* level_nx * level_ny bytes, fully written                        */
+    uint8_t* occupancy;          /* scratch, level_nx * level_ny bytes                               */
+    unsigned long long* raw_count;  /* one counter, zeroed by the call                              */
+    int32_t npatch, ndim, level_nx, level_ny, buffer, max_cells;
+    uint32_t force_regions;      /* regions active at t with level+1 <= min_level (flags |= region) */
+    uint32_t clear_regions;      /* regions active at t with level+1 >  max_level (flags &= ~region) */
+    void* stream;
+} AdjFlagMaskArgs;
+int adj_flag_level_mask(const AdjFlagMaskArgs* a);
+
 /* Host (no GPU): signature-bisection clustering of a flag mask, identical
  * to cluster() (amr.py:244-309).  mask: uint8 (nx, ny) row-major (ny = 1 in
  * 1D); max_edge <= 0: no cap.  boxes: 4 ints per box (lo_x, lo_y, hi_x,

@@ -118,6 +118,13 @@ class AdjFlagArgs(C.Structure):
 
 ABI_VERSION = 2
 
+class AdjFlagMaskArgs(C.Structure):
+    _fields_ = [("flag_bits", P), ("patches", P), ("region_rows", P), ("region_cols", P),
+                ("region_row_off", P), ("region_col_off", P), ("mask", P), ("occupancy", P), ("raw_count", P),
+                ("npatch", I32), ("ndim", I32), ("level_nx", I32), ("level_ny", I32), ("buffer", I32),
+                ("max_cells", I32), ("force_regions", C.c_uint32), ("clear_regions", C.c_uint32), ("stream", P)]
+
+
 EXPORTS = {
     "adj_abi_version": ([], C.c_int),
     "adj_last_error": ([], C.c_char_p),
@@ -128,6 +135,7 @@ EXPORTS = {
     "adj_ghost_plan_build": ([C.POINTER(AdjGhostPlanBuildArgs)], C.c_int),
     "adj_fill_ghost_plan": ([C.POINTER(AdjGhostPlanFillArgs)], C.c_int),
     "adj_restrict": ([C.POINTER(AdjRestrictArgs)], C.c_int),
+    "adj_flag_level_mask": ([C.POINTER(AdjFlagMaskArgs)], C.c_int),
     "adj_flag_adjoint": ([C.POINTER(AdjFlagArgs)], C.c_int),
     "adj_cluster": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p,
                      C.c_int, C.POINTER(I32)], C.c_int),

@@ -219,9 +219,10 @@ def _adjoint_geometry(store):
 
 
 def flag_level(patches: list[Patch], t: float, store: AdjointSnapshotStore, window: TimeWindow,
-               tolerance: float, want_best: bool = False, time_interp: bool = False):
+               tolerance: float, want_best: bool = False, time_interp: bool = False, device_bits: bool = False):
     """K3 over every patch of a level in one launch.  Returns (flags: list of
-    bool arrays, raw counts: list of int, best: list of arrays or None)."""
+    bool arrays, raw counts: list of int, best: list of arrays or None);
+    ``device_bits``: (packed flag words on the device, level store) instead."""
     if store is None:
         raise ConfigurationError("adjoint flagging requires a snapshot store")
     from .solver import level_store
@@ -242,6 +243,8 @@ def flag_level(patches: list[Patch], t: float, store: AdjointSnapshotStore, wind
         idx, tolerance, adj_wet=store._wet_dev if spec.ndim == 2 else None, interp_w=w, want_best=want_best)
     if int(status[0].item()):
         raise OutOfRangeError("interpolation point outside the adjoint domain")
+    if device_bits:
+        return bits, st
     words = bits[: max(st.flag_words, 1)].cpu().numpy().view(np.uint32)
     cnt = counts[: len(st.patches)].cpu().numpy()[slots]
     flags = []
@@ -361,6 +364,11 @@ class AdjointFlagging:
         flags, _, _ = flag_level([patch], patch.time, self.store, self.window, self.tolerance,
                                  time_interp=self.time_interp)
         return flags[0]
+
+    def evaluate_level_bits(self, patches):
+        """One K3 launch -> (packed flag words on the device, level store)."""
+        return flag_level(patches, patches[0].time, self.store, self.window, self.tolerance,
+                          time_interp=self.time_interp, device_bits=True)
 
     def evaluate_level(self, patches):
         """All patches of a level in one K3 launch -> (flags list, raw counts)."""

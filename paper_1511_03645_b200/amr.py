@@ -834,6 +834,24 @@ def _flag_level(parents, ctx: AmrContext):
     return out
 
 
+# adjoint flags post-processed on the device (K5); False: host buffer / mask / clip
+USE_DEVICE_FLAG_MASK = True
+
+
+def _device_level_mask(hierarchy, parent, parents, t, ctx):
+    """K3 -> K5 on the device: (clipped, allowed, raw count), or None when the
+    strategy is not adjoint flagging or the level store does not match."""
+    from .adjoint import AdjointFlagging
+    if not USE_DEVICE_FLAG_MASK or not isinstance(ctx.strategy, AdjointFlagging):
+        return None
+    if len(ctx.regions) > 8:
+        return None
+    bits, st = ctx.strategy.evaluate_level_bits(parents)
+    if len(st.patches) != len(parents) or any(p._store is not st for p in parents):
+        return None
+    return device.flag_level_mask(st, bits, hierarchy.level_shape(parent), ctx.buffer_cells, ctx.regions, t)
+
+
 def regrid(hierarchy: PatchHierarchy, level: int, ctx: AmrContext, deepest: int | None = None):
     """Rebuild levels level..deepest from parent flags (amr.py:554-599)."""
     if level < 2:
@@ -849,16 +867,20 @@ def regrid(hierarchy: PatchHierarchy, level: int, ctx: AmrContext, deepest: int 
             continue
         t = parents[0].time
         fill_level_ghosts(hierarchy, parent, t, ctx)
-        mask = np.zeros(hierarchy.level_shape(parent), dtype=bool)
-        raw = 0
-        for ff in _flag_level(parents, ctx):
-            raw += int(ff.flags.sum())
-            bf = buffer_flags(ff, ctx.buffer_cells)
-            sl = _box_slice(ff.lo, tuple(l + n - 1 for l, n in zip(ff.lo, bf.flags.shape)))
-            mask[sl] |= bf.flags
+        dev = _device_level_mask(hierarchy, parent, parents, t, ctx)
+        if dev is not None:
+            clipped, allowed, raw = dev
+        else:
+            mask = np.zeros(hierarchy.level_shape(parent), dtype=bool)
+            raw = 0
+            for ff in _flag_level(parents, ctx):
+                raw += int(ff.flags.sum())
+                bf = buffer_flags(ff, ctx.buffer_cells)
+                sl = _box_slice(ff.lo, tuple(l + n - 1 for l, n in zip(ff.lo, bf.flags.shape)))
+                mask[sl] |= bf.flags
+            allowed = allowed_region_mask(hierarchy, parent)
+            clipped = mask & allowed
         ctx.flagged_per_regrid.append(raw)
-        allowed = allowed_region_mask(hierarchy, parent)
-        clipped = mask & allowed
         ratio = hierarchy.ratio_to_finer(parent)
         boxes = cluster(clipped, ctx.efficiency, max_edge=max(1, ctx.max_patch_edge // ratio))
         rects = [rb for b in boxes for rb in _allowed_rectangles(b, allowed, clipped)]

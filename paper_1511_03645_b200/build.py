@@ -23,6 +23,7 @@ UNITS = {
     "k2_ghost.cu": ["-fmad=false"],
     "k3_flag.cu": ["-fmad=false"],
     "k1_fast.cu": [],
+    "k5_flagmask.cu": [],
     "host_cluster.cpp": [],
 }
 

@@ -35,6 +35,7 @@ int ghost_plan_build(const AdjGhostPlanBuildArgs& a, int rect_cells);
 int fill_ghost_plan(const AdjGhostPlanFillArgs& a);
 int restrict_level(const AdjRestrictArgs& a);
 int flag_adjoint(const AdjFlagArgs& a);
+int flag_level_mask(const AdjFlagMaskArgs& a);
 
 static int bad(const char* msg) {
     snprintf(g_err, sizeof(g_err), "bad argument: %s", msg);
@@ -152,6 +153,15 @@ int adj_flag_adjoint(const AdjFlagArgs* a) {
     rc = adj::record_cuda(cudaMemsetAsync(a->status, 0, sizeof(int32_t), st), "memset status");
     if (rc) return rc;
     return adj::flag_adjoint(*a);
+}
+
+int adj_flag_level_mask(const AdjFlagMaskArgs* a) {
+    if (!a || !a->mask || !a->occupancy || !a->raw_count) return adj::bad("null pointer");
+    if (a->npatch > 0 && !(a->flag_bits && a->patches)) return adj::bad("null flags / patches");
+    if (a->region_rows && (!a->region_row_off || (a->ndim == 2 && !(a->region_cols && a->region_col_off))))
+        return adj::bad("region tables incomplete");
+    if (a->level_nx < 1 || a->level_ny < 1 || a->buffer < 0) return adj::bad("level shape / buffer");
+    return adj::flag_level_mask(*a);
 }
 
 }  // extern "C"

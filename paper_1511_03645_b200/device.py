@@ -967,6 +967,80 @@ def restrict_rects(coarse_store, fine_store, rects_np, ratio, swe, stream=None):
     _lib.check(_lib.lib().adj_restrict(_lib.C.byref(a)), "adj_restrict")
 
 
+def region_tables(store: LevelStore, regions, t):
+    """Per-patch row / column bitmasks of the refinement regions that act at
+    time t on flags of this level (RefinementRegion.cell_mask and the
+    force / clear order of flag_cells, amr.py:137-154).  Returns None when no
+    region acts, else (rows, cols, row_off, col_off, force_bits, clear_bits);
+    raises ValueError beyond 8 regions."""
+    new_level = store.patches[0].spec.level + 1
+    force = clear = 0
+    for k, r in enumerate(regions):
+        if not r.contains_time(t):
+            continue
+        if new_level <= r.min_level:
+            force |= 1 << k
+        if new_level > r.max_level:
+            clear |= 1 << k
+    if not (force | clear):
+        return None
+    if len(regions) > 8:
+        raise ValueError("device region tables hold at most 8 regions")
+    rows, cols, roff, coff = [], [], [], []
+    nr = nc = 0
+    for p in store.patches:
+        cs = p.spec.cell_centers()
+        rb = np.zeros(len(cs[0]), dtype=np.uint8)
+        cb = np.zeros(len(cs[1]) if store.ndim == 2 else 0, dtype=np.uint8)
+        for k, r in enumerate(regions):
+            rb |= (((cs[0] >= r.rect[0]) & (cs[0] <= r.rect[1])).astype(np.uint8) << k)
+            if store.ndim == 2:
+                cb |= (((cs[1] >= r.rect[2]) & (cs[1] <= r.rect[3])).astype(np.uint8) << k)
+        roff.append(nr)
+        coff.append(nc)
+        rows.append(rb)
+        cols.append(cb)
+        nr += len(rb)
+        nc += len(cb)
+    cat = lambda xs: np.concatenate(xs) if xs and sum(len(x) for x in xs) else np.zeros(1, np.uint8)
+    return cat(rows), cat(cols), np.array(roff, np.int32), np.array(coff, np.int32), force, clear
+
+
+def flag_level_mask(store: LevelStore, bits, level_shape, buffer_cells, regions=(), t=0.0, stream=None):
+    """K5 on K3's packed flags of every patch of ``store``: -> (clipped bool
+    mask, allowed bool mask, raw flag count after region overrides), both
+    masks over the level's index space (amr.py:570-581)."""
+    torch = _torch()
+    nx = int(level_shape[0])
+    ny = int(level_shape[1]) if store.ndim == 2 else 1
+    mask = torch.empty(nx * ny, dtype=torch.uint8, device="cuda")
+    occ = torch.empty(nx * ny, dtype=torch.uint8, device="cuda")
+    raw = torch.empty(1, dtype=torch.int64, device="cuda")
+    tabs = region_tables(store, regions, t) if regions else None
+    keep = []
+    a = _lib.AdjFlagMaskArgs()
+    a.flag_bits = _ptr(bits)
+    a.patches = _ptr(store.table)
+    if tabs is not None:
+        rows, cols, roff, coff, force, clear = tabs
+        keep = [torch.from_numpy(x).to("cuda") for x in (rows, cols, roff, coff)]
+        a.region_rows, a.region_cols, a.region_row_off, a.region_col_off = (_ptr(x) for x in keep)
+        a.force_regions, a.clear_regions = force, clear
+    a.mask = _ptr(mask)
+    a.occupancy = _ptr(occ)
+    a.raw_count = _ptr(raw)
+    a.npatch = len(store.patches)
+    a.ndim = store.ndim
+    a.level_nx, a.level_ny = nx, ny
+    a.buffer = int(buffer_cells)
+    a.max_cells = max(int(np.prod(p.spec.shape)) for p in store.patches)
+    a.stream = _lib.stream_ptr(stream)
+    _lib.check(_lib.lib().adj_flag_level_mask(_lib.C.byref(a)), "adj_flag_level_mask")
+    m = mask.cpu().numpy().reshape((nx, ny) if store.ndim == 2 else (nx,))
+    del keep
+    return (m & 1).astype(bool), (m & 2).astype(bool), int(raw.item())
+
+
 def flag_axis_tables(store: LevelStore, ring_shape, a_origin, a_dx, a_dy, level_origin, level_dx, level_dy):
     """Per patch row/column bilinear weights into the adjoint grid, computed
     once with interpolate_uniform's arithmetic (geometry.py:248-290) and its

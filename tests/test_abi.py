@@ -46,6 +46,7 @@ def test_null_args_rejected_without_gpu():
     assert lib.adj_flag_adjoint(C.byref(_lib.AdjFlagArgs())) == _lib.ADJ_ERR_BAD_ARG
     assert lib.adj_ghost_plan_build(C.byref(_lib.AdjGhostPlanBuildArgs())) == _lib.ADJ_ERR_BAD_ARG
     assert lib.adj_fill_ghost_plan(C.byref(_lib.AdjGhostPlanFillArgs())) == _lib.ADJ_ERR_BAD_ARG
+    assert lib.adj_flag_level_mask(C.byref(_lib.AdjFlagMaskArgs())) == _lib.ADJ_ERR_BAD_ARG
 
 
 def _struct_fields(name):
@@ -68,7 +69,8 @@ def _struct_fields(name):
 
 
 @pytest.mark.parametrize("name", ["AdjStepArgs", "AdjPhysArgs", "AdjGhostArgs", "AdjRestrictArgs", "AdjFlagArgs",
-                                  "AdjGhostPlan", "AdjGhostPlanBuildArgs", "AdjGhostPlanFillArgs"])
+                                  "AdjGhostPlan", "AdjGhostPlanBuildArgs", "AdjGhostPlanFillArgs",
+                                  "AdjFlagMaskArgs"])
 def test_ctypes_structs_mirror_header(name):
     from paper_1511_03645_b200 import _lib
     assert [f[0] for f in getattr(_lib, name)._fields_] == _struct_fields(name)
