@@ -306,6 +306,54 @@ typedef struct AdjFlagArgs {
 } AdjFlagArgs;
 int adj_flag_adjoint(const AdjFlagArgs* a);
 
+/* Output path, on the device so only scalars / gauge values
+ * cross to the host at output times.
+ *
+ * evaluate_J (adjoint.py:299-336) over one level: per interior cell not
+ * covered by a finer patch (_uncovered_mask, adjoint.py:280-296) the signed
+ * inner product sum_c qhat_c q_c with qhat = interpolate_uniform of the
+ * store interpolated in time (interpolate_time, adjoint.py:98-110; the same
+ * per-cell arithmetic as K3).  Per-block sums go to partial[patch *
+ * blocks_x + block] (fixed order); the host multiplies each patch's sum by
+ * the cell area and accumulates in patch order as the reference does. */
+typedef struct AdjFunctionalArgs {
+    const double* q;             /* forward level store                                          */
+    const AdjPatch* patches;     /* device, the level's patches                                  */
+    const double* ring;          /* snapshots (nsnap, m, nxa, nya)                               */
+    const AdjPatch* finer;       /* optional: next finer level's patches (covered cells)         */
+    uint8_t* covered;            /* scratch level_nx * level_ny bytes when finer != NULL          */
+    double* partial;             /* [npatch * blocks_x]                                          */
+    int32_t* status;             /* 1 int, zeroed: 1 = point outside the adjoint grid            */
+    int64_t comp_stride;
+    int32_t npatch, nfiner, ratio, ndim, m, ghost;
+    int32_t nxa, nya, level_nx, level_ny, blocks_x, snap;   /* snap < 0: snapshot -snap-1;
+                                                               else blend snap, snap+1 with w */
+    double w;
+    double origin_x, origin_y, dx, dy;          /* the level's geometry           */
+    double a_origin_x, a_origin_y, a_dx, a_dy;  /* the adjoint grid's geometry    */
+    void* stream;
+} AdjFunctionalArgs;
+int adj_functional(const AdjFunctionalArgs* a);
+
+/* Gauges (record_gauge, runio.py:217-226): interpolate_patch with
+ * interior_only (geometry.py:302-327) for ngauge points at once.  Per gauge
+ * the host gives the patch's interior corner offset and pitch and the
+ * stencil (i0, i1, j0, j1, wx, wy) from _axis_weights; out[g*m + c]. */
+typedef struct AdjGauge {
+    int64_t base;                /* offset of interior cell (0, 0) in the level plane */
+    int32_t pitch, i0, i1, j0, j1, pad;
+    double wx, wy;
+} AdjGauge;
+typedef struct AdjGaugeArgs {
+    const double* q;
+    const AdjGauge* gauges;      /* device */
+    double* out;                 /* device, ngauge * m */
+    int64_t comp_stride;
+    int32_t ngauge, ndim, m, pad;
+    void* stream;
+} AdjGaugeArgs;
+int adj_gauges(const AdjGaugeArgs* a);
+
 /* K5: regrid flag post-processing on the device.  Replaces, for one parent
  * level, the per-patch region overrides of flag_cells (amr.py:137-154), the
  * box dilation of buffer_flags clipped to each patch (amr.py:157-179), the OR

@@ -506,3 +506,86 @@ def inner_product_interp(q_int, xc, yc, fields, times, t_eval, a_origin, a_dx, a
         qh = uniform_sample(vals, a_origin, a_dx, a_dy, xc, yc)
         best = np.maximum(best, np.abs(_seqsum([qh[c] * q_int[c] for c in range(q_int.shape[0])])))
     return best
+
+
+# ---------------------------------------------------------------------------
+# output path
+
+def interpolate_time(fields, times, t):
+    """AdjointSnapshotStore.interpolate_time (adjoint.py:98-110) on arrays."""
+    times = np.asarray(times, dtype=float)
+    eps = 1e-9 * max(abs(times[-1]), 1.0)
+    if t <= times[0] + eps:
+        return fields[0]
+    if t >= times[-1] - eps:
+        return fields[-1]
+    n = int(np.searchsorted(times, t) - 1)
+    w = (t - times[n]) / (times[n + 1] - times[n])
+    return (1 - w) * fields[n] + w * fields[n + 1]
+
+
+def evaluate_J(levels, ratios, origin, widths, qhat, a_origin, a_dx, a_dy):
+    """evaluate_J on a hierarchy (adjoint.py:299-336) with _uncovered_mask
+    (adjoint.py:280-296).  levels[l] = list of (lo, interior q (m, nx[, ny]));
+    widths[l] = (wx, wy) of level l+1; qhat = the (time-interpolated) adjoint
+    field values (m, nxa[, nya])."""
+    nd = len(origin)
+    total = 0.0
+    for li, plist in enumerate(levels):
+        wx, wy = widths[li]
+        area = wx if nd == 1 else wx * wy
+        finer = levels[li + 1] if li + 1 < len(levels) else []
+        for lo, q in plist:
+            shape = q.shape[1:]
+            hi = tuple(l + n - 1 for l, n in zip(lo, shape))
+            keep = np.ones(shape, dtype=bool)
+            if finer:
+                r = ratios[li]
+                for flo, fq in finer:
+                    fhi = tuple(l + n - 1 for l, n in zip(flo, fq.shape[1:]))
+                    clo = tuple(max(flo[a] // r, lo[a]) for a in range(nd))
+                    chi = tuple(min(fhi[a] // r, hi[a]) for a in range(nd))
+                    if any(a > b for a, b in zip(clo, chi)):
+                        continue
+                    keep[tuple(slice(a - l, b - l + 1) for a, b, l in zip(clo, chi, lo))] = False
+            cs = [origin[a] + (np.arange(lo[a], hi[a] + 1) + 0.5) * (wx, wy)[a] for a in range(nd)]
+            if nd == 1:
+                qh = uniform_sample(qhat, a_origin, a_dx, a_dy, cs[0])
+            else:
+                x = np.broadcast_to(cs[0][:, None], shape)
+                y = np.broadcast_to(cs[1][None, :], shape)
+                qh = uniform_sample(qhat, a_origin, a_dx, a_dy, x, y)
+            prod = np.sum(qh * q, axis=0)
+            total += float(np.sum(prod[keep]) * area)
+    return total
+
+
+def gauge_value(q_int, lo, origin, widths, point):
+    """interpolate_patch(interior_only=True) (geometry.py:302-327) at one point
+    of a patch's interior q (m, nx[, ny]) -- what record_gauge stores."""
+    nd = len(lo)
+    shape = q_int.shape[1:]
+    lo_phys = [origin[a] + lo[a] * widths[a] for a in range(nd)]
+    i0, wx = axis_weights(np.array([point[0]]), lo_phys[0], widths[0], shape[0])
+    if nd == 1:
+        return (q_int[:, i0] * (1 - wx) + q_int[:, np.minimum(i0 + 1, shape[0] - 1)] * wx)[:, 0]
+    j0, wy = axis_weights(np.array([point[1]]), lo_phys[1], widths[1], shape[1])
+    i1 = np.minimum(i0 + 1, shape[0] - 1)
+    j1 = np.minimum(j0 + 1, shape[1] - 1)
+    return (q_int[:, i0, j0] * (1 - wx) * (1 - wy) + q_int[:, i1, j0] * wx * (1 - wy)
+            + q_int[:, i0, j1] * (1 - wx) * wy + q_int[:, i1, j1] * wx * wy)[:, 0]
+
+
+def finest_patch_at(levels, origin, widths, level_shapes, point):
+    """PatchHierarchy.finest_patch_at (geometry.py:197-215): (level index,
+    patch index) of the finest patch containing the point, lowest index wins."""
+    found = None
+    for li, plist in enumerate(levels):
+        cell = tuple(int(np.clip(np.floor((point[a] - origin[a]) / widths[li][a]), 0, level_shapes[li][a] - 1))
+                     for a in range(len(origin)))
+        for k, (lo, q) in enumerate(plist):
+            hi = tuple(l + n - 1 for l, n in zip(lo, q.shape[1:]))
+            if all(l <= c <= h for l, c, h in zip(lo, cell, hi)):
+                found = (li, k)
+                break
+    return found

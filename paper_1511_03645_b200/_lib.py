@@ -118,6 +118,24 @@ class AdjFlagArgs(C.Structure):
 
 ABI_VERSION = 2
 
+class AdjFunctionalArgs(C.Structure):
+    _fields_ = [("q", P), ("patches", P), ("ring", P), ("finer", P), ("covered", P), ("partial", P), ("status", P),
+                ("comp_stride", I64), ("npatch", I32), ("nfiner", I32), ("ratio", I32), ("ndim", I32), ("m", I32),
+                ("ghost", I32), ("nxa", I32), ("nya", I32), ("level_nx", I32), ("level_ny", I32),
+                ("blocks_x", I32), ("snap", I32), ("w", D), ("origin_x", D), ("origin_y", D), ("dx", D), ("dy", D),
+                ("a_origin_x", D), ("a_origin_y", D), ("a_dx", D), ("a_dy", D), ("stream", P)]
+
+
+GAUGE_DTYPE = np.dtype([("base", np.int64), ("pitch", np.int32), ("i0", np.int32), ("i1", np.int32),
+                        ("j0", np.int32), ("j1", np.int32), ("pad", np.int32), ("wx", np.float64),
+                        ("wy", np.float64)], align=True)
+
+
+class AdjGaugeArgs(C.Structure):
+    _fields_ = [("q", P), ("gauges", P), ("out", P), ("comp_stride", I64), ("ngauge", I32), ("ndim", I32),
+                ("m", I32), ("pad", I32), ("stream", P)]
+
+
 class AdjFlagMaskArgs(C.Structure):
     _fields_ = [("flag_bits", P), ("patches", P), ("region_rows", P), ("region_cols", P),
                 ("region_row_off", P), ("region_col_off", P), ("mask", P), ("occupancy", P), ("raw_count", P),
@@ -136,6 +154,8 @@ EXPORTS = {
     "adj_fill_ghost_plan": ([C.POINTER(AdjGhostPlanFillArgs)], C.c_int),
     "adj_restrict": ([C.POINTER(AdjRestrictArgs)], C.c_int),
     "adj_flag_level_mask": ([C.POINTER(AdjFlagMaskArgs)], C.c_int),
+    "adj_functional": ([C.POINTER(AdjFunctionalArgs)], C.c_int),
+    "adj_gauges": ([C.POINTER(AdjGaugeArgs)], C.c_int),
     "adj_flag_adjoint": ([C.POINTER(AdjFlagArgs)], C.c_int),
     "adj_cluster": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p,
                      C.c_int, C.POINTER(I32)], C.c_int),

@@ -36,6 +36,8 @@ int fill_ghost_plan(const AdjGhostPlanFillArgs& a);
 int restrict_level(const AdjRestrictArgs& a);
 int flag_adjoint(const AdjFlagArgs& a);
 int flag_level_mask(const AdjFlagMaskArgs& a);
+int functional(const AdjFunctionalArgs& a);
+int gauges(const AdjGaugeArgs& a);
 
 static int bad(const char* msg) {
     snprintf(g_err, sizeof(g_err), "bad argument: %s", msg);
@@ -162,6 +164,18 @@ int adj_flag_level_mask(const AdjFlagMaskArgs* a) {
         return adj::bad("region tables incomplete");
     if (a->level_nx < 1 || a->level_ny < 1 || a->buffer < 0) return adj::bad("level shape / buffer");
     return adj::flag_level_mask(*a);
+}
+
+int adj_functional(const AdjFunctionalArgs* a) {
+    if (!a || !a->q || !a->patches || !a->ring || !a->partial || !a->status) return adj::bad("null pointer");
+    if (a->finer && a->nfiner > 0 && (!a->covered || a->ratio < 1)) return adj::bad("covered mask needs scratch and ratio");
+    if (a->blocks_x < 1 || a->npatch < 1) return adj::bad("empty launch");
+    return adj::functional(*a);
+}
+
+int adj_gauges(const AdjGaugeArgs* a) {
+    if (!a || !a->q || (a->ngauge > 0 && (!a->gauges || !a->out))) return adj::bad("null pointer");
+    return adj::gauges(*a);
 }
 
 }  // extern "C"

@@ -4,6 +4,8 @@
 //   interpolate_uniform / _axis_weights         geometry.py:248-290
 //   _adjoint_dry_at                             adjoint.py:217-224
 //   AdjointSnapshotStore.interpolate_time       adjoint.py:98-110  (mode 1)
+//   evaluate_J / _uncovered_mask               adjoint.py:280-336  (k3_functional)
+//   interpolate_patch (gauges)                  geometry.py:302-327 (k3_gauges)
 //
 // One thread per forward interior cell; a warp covers 32 consecutive cells of
 // one patch (row-major over the interior), so the warp's ballot is exactly
@@ -170,6 +172,141 @@ int flag_adjoint(const AdjFlagArgs& a) {
         else k3_flag<3, true, false><<<grid, threads, 0, st>>>(a);
     }
     return check_launch("k3_flag");
+}
+
+// ---------------------------------------------------------------------------
+// evaluate_J: signed inner products over uncovered cells, per-block sums.
+
+__global__ void k3_cover(AdjFunctionalArgs a) {
+    const AdjPatch f = a.finer[blockIdx.y];
+    const int r = a.ratio;
+    const int ci0 = f.lo_x / r, ci1 = (f.lo_x + f.nx - 1) / r;
+    const int cj0 = a.ndim == 2 ? f.lo_y / r : 0, cj1 = a.ndim == 2 ? (f.lo_y + f.ny - 1) / r : 0;
+    const int nj = cj1 - cj0 + 1;
+    const int n = (ci1 - ci0 + 1) * nj;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = ci0 + t / nj, j = cj0 + t % nj;
+        if (i < a.level_nx && j < a.level_ny) a.covered[(int64_t)i * a.level_ny + j] = 1;
+    }
+}
+
+template <int M, bool TWO_D>
+__global__ void __launch_bounds__(256) k3_functional(AdjFunctionalArgs a) {
+    __shared__ double s_part[8];
+    const int pidx = blockIdx.y;
+    const AdjPatch p = a.patches[pidx];
+    const int ny = TWO_D ? p.ny : 1;
+    const int ncell = p.nx * ny;
+    const int g = a.ghost, gy = TWO_D ? g : 0;
+    const unsigned plane = (unsigned)a.nxa * (unsigned)a.nya;
+    double acc = 0.0;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += a.blocks_x * blockDim.x) {
+        const int i = t / ny, j = t - (t / ny) * ny;
+        if (a.covered && a.covered[(int64_t)(p.lo_x + i) * a.level_ny + (TWO_D ? p.lo_y + j : 0)]) continue;
+        const int64_t o = p.offset + (int64_t)(i + g) * p.pitch + (j + gy);
+        // cell centre (PatchSpec.cell_centers) and interpolate_uniform's bounds check
+        const double x = a.origin_x + ((p.lo_x + i) + 0.5) * a.dx;
+        const double y = TWO_D ? a.origin_y + ((p.lo_y + j) + 0.5) * a.dy : 0.0;
+        const double hx = a.a_origin_x + a.nxa * a.a_dx;
+        const double eps = 1e-12 * fmax(fabs(hx - a.a_origin_x), 1.0);
+        bool oob = (x < a.a_origin_x - eps) || (x > hx + eps);
+        if (TWO_D) {
+            const double hy = a.a_origin_y + a.nya * a.a_dy;
+            oob |= (y < a.a_origin_y - eps) || (y > hy + eps);
+        }
+        if (oob) atomicOr(a.status, 1);
+        int i0, j0 = 0;
+        double wx, wy = 0.0;
+        uweights(x, a.a_origin_x, a.a_dx, a.nxa, &i0, &wx);
+        if (TWO_D) uweights(y, a.a_origin_y, a.a_dy, a.nya, &j0, &wy);
+        const int i1 = min(i0 + 1, a.nxa - 1);
+        const int j1 = TWO_D ? min(j0 + 1, a.nya - 1) : 0;
+        const unsigned o00 = (unsigned)i0 * a.nya + j0, o10 = (unsigned)i1 * a.nya + j0;
+        const unsigned o01 = (unsigned)i0 * a.nya + j1, o11 = (unsigned)i1 * a.nya + j1;
+        const double ux = 1.0 - wx, uy = 1.0 - wy;
+        double dot = 0.0;
+        const int k = a.snap;
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+            double qh;
+            if (k < 0) {
+                const double* fc = a.ring + ((int64_t)(-k - 1) * M + c) * plane;
+                qh = TWO_D ? fc[o00] * ux * uy + fc[o10] * wx * uy + fc[o01] * ux * wy + fc[o11] * wx * wy
+                           : fc[o00] * ux + fc[o10] * wx;
+            } else {   // interpolate_time, then the spatial stencil
+                const double* ac = a.ring + ((int64_t)k * M + c) * plane;
+                const double* bc = ac + (int64_t)plane * M;
+                const double v00 = (1.0 - a.w) * ac[o00] + a.w * bc[o00];
+                const double v10 = (1.0 - a.w) * ac[o10] + a.w * bc[o10];
+                if (TWO_D) {
+                    const double v01 = (1.0 - a.w) * ac[o01] + a.w * bc[o01];
+                    const double v11 = (1.0 - a.w) * ac[o11] + a.w * bc[o11];
+                    qh = v00 * ux * uy + v10 * wx * uy + v01 * ux * wy + v11 * wx * wy;
+                } else {
+                    qh = v00 * ux + v10 * wx;
+                }
+            }
+            const double qc = a.q[c * a.comp_stride + o];
+            dot = c == 0 ? qh * qc : dot + qh * qc;   // np.sum(qhat * q, axis=0)
+        }
+        acc = acc + dot;
+    }
+    // fixed-order block reduction
+    for (int off = 16; off > 0; off >>= 1) acc = acc + __shfl_down_sync(0xffffffffu, acc, off);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s_part[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = s_part[0];
+        for (int wi = 1; wi < (int)(blockDim.x >> 5); ++wi) s = s + s_part[wi];
+        a.partial[(int64_t)pidx * a.blocks_x + blockIdx.x] = s;
+    }
+}
+
+int functional(const AdjFunctionalArgs& a) {
+    cudaStream_t st = (cudaStream_t)a.stream;
+    int rc = record_cuda(cudaMemsetAsync(a.status, 0, sizeof(int32_t), st), "memset status");
+    if (rc) return rc;
+    if (a.finer && a.nfiner > 0) {
+        rc = record_cuda(cudaMemsetAsync(a.covered, 0, (size_t)a.level_nx * a.level_ny, st), "memset covered");
+        if (rc) return rc;
+        k3_cover<<<dim3(16, a.nfiner), 256, 0, st>>>(a);
+        rc = check_launch("k3_cover");
+        if (rc) return rc;
+    }
+    AdjFunctionalArgs b = a;
+    if (!(a.finer && a.nfiner > 0)) b.covered = nullptr;
+    const dim3 grid(a.blocks_x, a.npatch);
+    if (a.ndim == 2 && a.m == 3) k3_functional<3, true><<<grid, 256, 0, st>>>(b);
+    else if (a.ndim == 1 && a.m == 2) k3_functional<2, false><<<grid, 256, 0, st>>>(b);
+    else return ADJ_ERR_BAD_ARG;
+    return check_launch("k3_functional");
+}
+
+// gauges: interpolate_patch(interior_only=True), reference expression order
+__global__ void k3_gauges(AdjGaugeArgs a) {
+    const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= a.ngauge) return;
+    const AdjGauge G = a.gauges[gi];
+    for (int c = 0; c < a.m; ++c) {
+        const double* d = a.q + c * a.comp_stride + G.base;
+        double v;
+        if (a.ndim == 1) {
+            v = d[G.i0] * (1.0 - G.wx) + d[G.i1] * G.wx;
+        } else {
+            v = d[(int64_t)G.i0 * G.pitch + G.j0] * (1.0 - G.wx) * (1.0 - G.wy) +
+                d[(int64_t)G.i1 * G.pitch + G.j0] * G.wx * (1.0 - G.wy) +
+                d[(int64_t)G.i0 * G.pitch + G.j1] * (1.0 - G.wx) * G.wy +
+                d[(int64_t)G.i1 * G.pitch + G.j1] * G.wx * G.wy;
+        }
+        a.out[gi * a.m + c] = v;
+    }
+}
+
+int gauges(const AdjGaugeArgs& a) {
+    if (a.ngauge <= 0) return ADJ_OK;
+    k3_gauges<<<(a.ngauge + 127) / 128, 128, 0, (cudaStream_t)a.stream>>>(a);
+    return check_launch("k3_gauges");
 }
 
 }  // namespace adj

@@ -47,6 +47,8 @@ def test_null_args_rejected_without_gpu():
     assert lib.adj_ghost_plan_build(C.byref(_lib.AdjGhostPlanBuildArgs())) == _lib.ADJ_ERR_BAD_ARG
     assert lib.adj_fill_ghost_plan(C.byref(_lib.AdjGhostPlanFillArgs())) == _lib.ADJ_ERR_BAD_ARG
     assert lib.adj_flag_level_mask(C.byref(_lib.AdjFlagMaskArgs())) == _lib.ADJ_ERR_BAD_ARG
+    assert lib.adj_functional(C.byref(_lib.AdjFunctionalArgs())) == _lib.ADJ_ERR_BAD_ARG
+    assert lib.adj_gauges(C.byref(_lib.AdjGaugeArgs())) == _lib.ADJ_ERR_BAD_ARG
 
 
 def _struct_fields(name):
@@ -55,7 +57,7 @@ def _struct_fields(name):
     body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
     fields = []
     typewords = {"const", "unsigned", "long", "double", "int32_t", "int64_t", "uint32_t", "uint8_t", "void", "char",
-                 "AdjPatch", "AdjTile", "AdjRect", "AdjGhostPlan"}
+                 "AdjPatch", "AdjTile", "AdjRect", "AdjGhostPlan", "AdjGauge"}
     for decl in body.split(";"):
         toks = decl.replace("*", " ").replace(",", " , ").split()
         if not toks:
@@ -70,7 +72,7 @@ def _struct_fields(name):
 
 @pytest.mark.parametrize("name", ["AdjStepArgs", "AdjPhysArgs", "AdjGhostArgs", "AdjRestrictArgs", "AdjFlagArgs",
                                   "AdjGhostPlan", "AdjGhostPlanBuildArgs", "AdjGhostPlanFillArgs",
-                                  "AdjFlagMaskArgs"])
+                                  "AdjFlagMaskArgs", "AdjFunctionalArgs", "AdjGaugeArgs"])
 def test_ctypes_structs_mirror_header(name):
     from paper_1511_03645_b200 import _lib
     assert [f[0] for f in getattr(_lib, name)._fields_] == _struct_fields(name)
@@ -81,6 +83,8 @@ def test_table_dtypes_mirror_header():
     assert list(_lib.PATCH_DTYPE.names) == _struct_fields("AdjPatch")
     assert list(_lib.TILE_DTYPE.names) == _struct_fields("AdjTile")
     assert list(_lib.RECT_DTYPE.names) == _struct_fields("AdjRect")
+    assert list(_lib.GAUGE_DTYPE.names) == _struct_fields("AdjGauge")
+    assert _lib.GAUGE_DTYPE.itemsize == 48
 
 
 def test_product_refuses_cpu_fallback():
