@@ -390,6 +390,20 @@ int adj_cluster(const uint8_t* mask, int ndim, int nx, int ny, double efficiency
 
 /* Last CUDA error string of the calling thread (diagnostics). */
 const char* adj_last_error(void);
+/* Host (no GPU): ghost-fill rectangles of one level, identical to
+ * build_ghost_rects (the per-patch phases of fill_ghost_same_level /
+ * fill_ghost_from_coarse, solver.py:208-263, as rectangles).  Boxes are
+ * inclusive global (lo, hi), ndim ints each; coarse boxes in the coarse
+ * index space (ratio to this level).  For every patch (or only patch `only`
+ * >= 0) and ghost strip inside the domain: COPY rects from overlapping
+ * same-level patches, then COARSE rects (of the strip, or with `disjoint` of
+ * what the copies leave).  covered[k] = ghost cells of patch k the rects
+ * fill.  ADJ_ERR_BAD_ARG with *nrects = the count needed when max_rects is
+ * too small. */
+int adj_ghost_rects(int ndim, int ghost, const int32_t* level_shape, int npatch, const int32_t* lo,
+                    const int32_t* hi, int ncoarse, const int32_t* clo, const int32_t* chi, int ratio,
+                    int only, int disjoint, AdjRect* rects, int max_rects, int32_t* nrects, int64_t* covered);
+
 int adj_abi_version(void);
 
 #ifdef __cplusplus

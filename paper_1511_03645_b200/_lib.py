@@ -157,6 +157,9 @@ EXPORTS = {
     "adj_functional": ([C.POINTER(AdjFunctionalArgs)], C.c_int),
     "adj_gauges": ([C.POINTER(AdjGaugeArgs)], C.c_int),
     "adj_flag_adjoint": ([C.POINTER(AdjFlagArgs)], C.c_int),
+    "adj_ghost_rects": ([C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                         C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.POINTER(I32), C.c_void_p],
+                        C.c_int),
     "adj_cluster": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p,
                      C.c_int, C.POINTER(I32)], C.c_int),
 }

@@ -256,6 +256,15 @@ def cluster(flags, efficiency_threshold: float, max_edge: int | None = None,
         mask = np.asarray(flags, dtype=bool)
         offset = (0,) * mask.ndim
     if native is not False:
+        # the algorithm starts from the flags' bounding box (amr.py:258-262):
+        # clustering the cropped mask gives the same boxes
+        nz = [np.flatnonzero(mask.any(axis=tuple(b for b in range(mask.ndim) if b != a)))
+              for a in range(mask.ndim)]
+        if any(len(v) == 0 for v in nz):
+            return []
+        crop = tuple(slice(int(v[0]), int(v[-1]) + 1) for v in nz)
+        mask = mask[crop]
+        offset = tuple(o + int(v[0]) for o, v in zip(offset, nz))
         out = _cluster_native(mask, offset, efficiency_threshold, max_edge)
         if out is not None:
             return out
@@ -463,12 +472,60 @@ def _subtract(box, holes):
     return out
 
 
-def build_ghost_rects(hierarchy: PatchHierarchy, level: int, only=None, disjoint: bool = False):
+def build_ghost_rects(hierarchy: PatchHierarchy, level: int, only=None, disjoint: bool = False, native=None):
     """Rectangles for the in-domain ghost phases of one level:
     coarse rects grouped by coarse patch, then same-level copy rects.
     ``disjoint``: coarse rects exclude the cells a same-level copy overwrites
     (same final values, one launch, less interpolation).
-    Returns (coarse {coarse slot: [rect]}, copy [rect], covered cells per patch)."""
+    Returns (coarse {coarse slot: [rect]}, copy [rect], covered cells per patch).
+    Runs natively (adj_ghost_rects) when the library is present."""
+    if native is not False:
+        try:
+            return _build_ghost_rects_native(hierarchy, level, only, disjoint)
+        except _lib.NativeUnavailableError:
+            if native:
+                raise
+    return _build_ghost_rects_py(hierarchy, level, only, disjoint)
+
+
+def _build_ghost_rects_native(hierarchy, level, only, disjoint):
+    import ctypes as C
+    patches = hierarchy.patches(level)
+    nd = hierarchy.ndim
+    shape = np.array(hierarchy.level_shape(level), dtype=np.int32)
+    lo, hi = (np.ascontiguousarray(a, dtype=np.int32) for a in _boxes(patches))
+    coarse = hierarchy.patches(level - 1) if level >= 2 else []
+    if coarse:
+        clo, chi = (np.ascontiguousarray(a, dtype=np.int32) for a in _boxes(coarse))
+        r = hierarchy.ratio_to_finer(level - 1)
+    else:
+        clo = chi = np.zeros((1, nd), np.int32)
+        r = 1
+    k_only = -1 if only is None else next(k for k, p in enumerate(patches) if p is only)
+    g = patches[0].spec.ghost_width
+    cap = max(64, 16 * len(patches))
+    lib = _lib.load_library()
+    while True:
+        rects = np.zeros(cap, dtype=_lib.RECT_DTYPE)
+        covered = np.zeros(len(patches), dtype=np.int64)
+        n = _lib.I32()
+        rc = lib.adj_ghost_rects(nd, g, shape.ctypes.data, len(patches), lo.ctypes.data, hi.ctypes.data,
+                                 len(coarse), clo.ctypes.data, chi.ctypes.data, r, k_only, int(disjoint),
+                                 rects.ctypes.data, cap, C.byref(n), covered.ctypes.data)
+        if rc == 0:
+            break
+        if n.value <= cap:
+            raise ValueError("adj_ghost_rects: bad arguments")
+        cap = n.value
+    rects = rects[: n.value]
+    copy_rects = rects[rects["kind"] == _lib.RECT_COPY].tolist()
+    coarse_rects: dict[int, list] = {}
+    for r_ in rects[rects["kind"] == _lib.RECT_COARSE].tolist():
+        coarse_rects.setdefault(r_[2], []).append(r_)
+    return coarse_rects, copy_rects, covered
+
+
+def _build_ghost_rects_py(hierarchy: PatchHierarchy, level: int, only=None, disjoint: bool = False):
     patches = hierarchy.patches(level)
     shape = hierarchy.level_shape(level)
     dom_lo, dom_hi = (0,) * hierarchy.ndim, tuple(n - 1 for n in shape)
@@ -531,6 +588,16 @@ def _ring_and_physical(spec, level_shape):
         hi = min(spec.hi[a] + g, level_shape[a] - 1)
         ind *= hi - lo + 1
     return int(tot), int(np.prod([n + 2 * g for n in spec.shape]) - ind)
+
+
+def _ring_and_physical_all(patches, level_shape):
+    """_ring_and_physical of every patch, vectorised -> (ring, physical) arrays."""
+    lo, hi = _boxes(patches)
+    g = patches[0].spec.ghost_width
+    n = hi - lo + 1
+    full = np.prod(n + 2 * g, axis=1)
+    ind = np.prod(np.minimum(hi + g, np.array(level_shape) - 1) - np.maximum(lo - g, 0) + 1, axis=1)
+    return full - np.prod(n, axis=1), full - ind
 
 
 def _coarse_time_mode(cp: Patch, t: float):
@@ -658,8 +725,8 @@ class LevelPlan:
         # coarse (disjoint from the copies) + copies: one launch when times are synchronised
         self.combined = device.RectTable(allc + list(copies), geom if allc else None)
         shape = hierarchy.level_shape(level)
-        self.full = all(covered[k] + _ring_and_physical(p.spec, shape)[1] >= _ring_and_physical(p.spec, shape)[0]
-                        for k, p in enumerate(patches))
+        ring, phys = _ring_and_physical_all(patches, shape)
+        self.full = bool(np.all(covered + phys >= ring))
         self.restrict_to = None      # (coarse store, RectTable) for restriction into level-1
         self._gather = {}            # (boundary, normals, level shape) -> device.GhostPlan
 

@@ -25,6 +25,7 @@ UNITS = {
     "k1_fast.cu": [],
     "k5_flagmask.cu": [],
     "host_cluster.cpp": [],
+    "host_ghost.cpp": [],
 }
 
 

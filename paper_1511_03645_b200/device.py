@@ -144,8 +144,17 @@ class LevelStore:
                                    for (_, NX_, NY_, _) in self.boxes)
         self._phys_args = {}
         self.nonfinite_acc = None
+        # material planes of every patch assembled on the host, one upload
+        host_aux = np.zeros(self.naux * self.plane, dtype=np.float64)
         for k, p in enumerate(patches):
-            self._attach(p, k)
+            off, NX, NY, pitch = self.boxes[k]
+            v = np.lib.stride_tricks.as_strided(host_aux[off:], (self.naux, NX, NY), (8 * self.plane, 8 * pitch, 8),
+                                                writeable=True)
+            for a, pl in enumerate(p.aux.planes()):
+                v[a] = np.asarray(pl, dtype=float).reshape(NX, NY)
+        self.aux.copy_(torch.from_numpy(host_aux))
+        for k, p in enumerate(patches):
+            self._attach(p, k, upload=False)
 
     # ------------------------------------------------------------------ views
     def _view(self, t, slot, comps):
@@ -160,13 +169,13 @@ class LevelStore:
     def aux_view(self, slot):
         return self._view(self.aux, slot, self.naux)
 
-    def _attach(self, patch, slot):
+    def _attach(self, patch, slot, upload=True):
         if patch.aux is None:
             raise ValueError("patch has no material (call sample_patch_material first)")
-        planes = patch.aux.planes()
-        av = self.aux_view(slot)
-        for k, pl in enumerate(planes):
-            av[k].copy_(_torch().from_numpy(np.ascontiguousarray(pl, dtype=float)))
+        if upload:
+            av = self.aux_view(slot)
+            for k, pl in enumerate(patch.aux.planes()):
+                av[k].copy_(_torch().from_numpy(np.ascontiguousarray(pl, dtype=float)))
         patch._time = patch.time          # detach level-synchronised fields of a previous store
         patch._time_old = patch.time_old
         patch._loc_own = "host"           # uploaded by sync_in
@@ -1057,24 +1066,33 @@ def flag_axis_tables(store: LevelStore, ring_shape, a_origin, a_dx, a_dy, level_
     widths_f = [level_dx] + ([level_dy] if nd == 2 else [])
     hi0 = a_origin[0] + n_a[0] * widths_a[0]
     eps = 1e-12 * max(abs(hi0 - a_origin[0]), 1.0)
-    ws, iis, drys, offs = [], [], [], []
-    off = 0
-    for p in store.patches:
-        po = []
-        for ax in range(nd):
-            idx = np.arange(p.spec.lo[ax], p.spec.hi[ax] + 1)
-            coord = level_origin[ax] + (idx + 0.5) * widths_f[ax]
-            hi = a_origin[ax] + n_a[ax] * widths_a[ax]
-            if np.any(coord < a_origin[ax] - eps) or np.any(coord > hi + eps):
-                raise OutOfRangeError("interpolation point outside the adjoint domain")
-            i0, w = _axis_weights_np(coord, a_origin[ax], widths_a[ax], n_a[ax])
-            dry = np.clip(((coord - a_origin[ax]) / widths_a[ax]).astype(int), 0, n_a[ax] - 1)
-            ws.append(w)
-            iis.append(i0.astype(np.int32))
-            drys.append(dry.astype(np.int32))
-            po.append(off)
-            off += len(idx)
-        offs.extend(po if nd == 2 else [po[0], po[0]])
+    # vectorised over patches; layout per patch: its rows (x), then its columns (y)
+    los = np.array([p.spec.lo for p in store.patches], dtype=np.int64).reshape(-1, nd)
+    his = np.array([p.spec.hi for p in store.patches], dtype=np.int64).reshape(-1, nd)
+    ext = his - los + 1
+    per = ext.sum(axis=1)
+    poff = np.cumsum(per) - per
+    total = int(per.sum())
+    W = np.empty(total, np.float64)
+    I = np.empty(total, np.int32)
+    Dr = np.empty(total, np.int32)
+    for ax in range(nd):
+        n = ext[:, ax]
+        pid = np.repeat(np.arange(len(n)), n)
+        t = np.arange(int(n.sum())) - np.repeat(np.cumsum(n) - n, n)
+        idx = los[pid, ax] + t
+        coord = level_origin[ax] + (idx + 0.5) * widths_f[ax]
+        hi = a_origin[ax] + n_a[ax] * widths_a[ax]
+        if np.any(coord < a_origin[ax] - eps) or np.any(coord > hi + eps):
+            raise OutOfRangeError("interpolation point outside the adjoint domain")
+        i0, w = _axis_weights_np(coord, a_origin[ax], widths_a[ax], n_a[ax])
+        dry = np.clip(((coord - a_origin[ax]) / widths_a[ax]).astype(int), 0, n_a[ax] - 1)
+        pos = poff[pid] + (ext[pid, 0] if ax == 1 else 0) + t
+        W[pos] = w
+        I[pos] = i0
+        Dr[pos] = dry
+    offs = np.stack([poff, poff + ext[:, 0]] if nd == 2 else [poff, poff], axis=1).reshape(-1)
+    ws, iis, drys = [W], [I], [Dr]
     torch = _torch()
     tabs = (torch.from_numpy(np.concatenate(ws).astype(np.float64)).to("cuda"),
             torch.from_numpy(np.concatenate(iis)).to("cuda"),

@@ -81,6 +81,17 @@ def _fix_aux_ghosts(arr: np.ndarray, axis: int, high: bool, g: int, wall: bool):
     arr[tuple(idx)] = arr[tuple(src)]
 
 
+_FIELDS: dict = {}
+
+
+def _field_names(cls):
+    names = _FIELDS.get(cls)
+    if names is None:
+        import dataclasses
+        names = _FIELDS[cls] = tuple(f.name for f in dataclasses.fields(cls))
+    return names
+
+
 def sample_patch_material(patch: Patch, equation: EquationSet, boundary: BoundarySpec,
                           level_shape: tuple[int, ...]):
     """Sample the material at cell centres (incl. ghosts), then mirror (wall)
@@ -92,9 +103,8 @@ def sample_patch_material(patch: Patch, equation: EquationSet, boundary: Boundar
     else:
         xx, yy = np.meshgrid(cs[0], cs[1], indexing="ij")
         mat = equation.sample_material(xx, yy)
-    import dataclasses
-    arrays = {f.name: np.array(getattr(mat, f.name), copy=True) for f in dataclasses.fields(mat)
-              if isinstance(getattr(mat, f.name), np.ndarray)}
+    names = _field_names(type(mat))
+    arrays = {n: np.array(getattr(mat, n), copy=True) for n in names if isinstance(getattr(mat, n), np.ndarray)}
     g = spec.ghost_width
     for axis in range(spec.ndim):
         for high in (False, True):
@@ -103,7 +113,7 @@ def sample_patch_material(patch: Patch, equation: EquationSet, boundary: Boundar
                 wall = boundary.side(axis, high) == "wall"
                 for arr in arrays.values():
                     _fix_aux_ghosts(arr, axis, high, g, wall)
-    others = {f.name: getattr(mat, f.name) for f in dataclasses.fields(mat) if f.name not in arrays}
+    others = {n: getattr(mat, n) for n in names if n not in arrays}
     patch.aux = type(mat)(**arrays, **others)
     if patch._store is not None:
         patch._store._dry = None

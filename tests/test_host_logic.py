@@ -83,3 +83,40 @@ def test_native_clustering_matches_python_on_large_masks():
         a = amr.cluster(m, 0.7, max_edge=me, native=True)
         b = amr.cluster(m, 0.7, max_edge=me, native=False)
         assert [(x.lo, x.hi, x.efficiency) for x in a] == [(x.lo, x.hi, x.efficiency) for x in b]
+
+
+def _random_hierarchy(rng, nd):
+    """Coarse level tiled into boxes, fine level from clustering a random blob
+    mask (disjoint boxes), some touching the domain edge."""
+    if nd == 2:
+        h = PatchHierarchy(xlim=(0, 1), ylim=(0, 1), base_shape=(24, 20), ratios=[2])
+        coarse = [Patch(h.make_spec(1, (x, y), (min(x + 7, 23), min(y + 9, 19))), 3)
+                  for x in range(0, 24, 8) for y in range(0, 20, 10)]
+        mask = np.zeros((48, 40), dtype=bool)
+        for _ in range(6):
+            cx, cy, r = rng.integers(0, 48), rng.integers(0, 40), rng.integers(2, 9)
+            X, Y = np.meshgrid(np.arange(48), np.arange(40), indexing="ij")
+            mask |= (X - cx) ** 2 + (Y - cy) ** 2 < r * r
+    else:
+        h = PatchHierarchy(xlim=(0, 1), ylim=None, base_shape=(40,), ratios=[2])
+        coarse = [Patch(h.make_spec(1, (x,), (min(x + 9, 39),)), 2) for x in range(0, 40, 10)]
+        mask = rng.random(80) < 0.3
+    boxes = amr.cluster(mask, 0.7, max_edge=12)
+    fine = [Patch(h.make_spec(2, b.lo, b.hi), 3 if nd == 2 else 2) for b in boxes]
+    h.levels = [coarse, fine]
+    return h
+
+
+@pytest.mark.parametrize("nd", [1, 2])
+def test_native_ghost_rects_equal_python(nd):
+    rng = np.random.default_rng(7 + nd)
+    for _ in range(8):
+        h = _random_hierarchy(rng, nd)
+        for level in (1, 2):
+            for disjoint in (False, True):
+                for only in (None, h.patches(level)[len(h.patches(level)) // 2]):
+                    a = amr.build_ghost_rects(h, level, only=only, disjoint=disjoint, native=True)
+                    b = amr.build_ghost_rects(h, level, only=only, disjoint=disjoint, native=False)
+                    assert a[0] == b[0]
+                    assert a[1] == b[1]
+                    assert np.array_equal(a[2], b[2])
