@@ -298,6 +298,20 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def k1_traffic():
+    """DRAM bytes (read + write) per K1 launch on C4 from the committed ncu
+    --set full capture (profiles/r01_k1_traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_k1_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return {"bytes_per_launch": d["dram_bytes_read"] + d["dram_bytes_write"],
+                "algorithmic_bytes": d["algorithmic_bytes"],
+                "ratio": (d["dram_bytes_read"] + d["dram_bytes_write"]) / d["algorithmic_bytes"], "source": d["source"]}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -479,7 +493,8 @@ def main():
                    "l2": "inputs (537 MB/step) larger than the 126 MB L2; no flush"},
         "max_courant": cfl,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": (k1_traffic() or {}).get("bytes_per_launch"),
+                     "traffic_detail": k1_traffic(), "peak_kind": peak_kind,
                      "kernel": "k1_fast (SWE, MC)", "kernel_ms": k1,
                      "bytes_per_cell_update": BYTES_PER_CELL_SWE, "cells_per_launch": N * N,
                      "kernel_cell_updates_per_s": N * N / (k1 * 1e-3)},

@@ -94,3 +94,12 @@ def test_product_refuses_cpu_fallback():
         pytest.skip("GPU present")
     with pytest.raises(_lib.NativeUnavailableError):
         _lib.lib()
+
+
+def test_integration_stub_matches_header():
+    """The ctypes binding shown in INTEGRATION.md mirrors AdjStepArgs."""
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = text[text.index("class AdjStepArgs"):text.index("lib.adj_step_level.argtypes")]
+    assert re.findall(r'\("(\w+)"', block) == _struct_fields("AdjStepArgs")
+    for name in declared_functions():
+        assert name in text, name
