@@ -1167,3 +1167,151 @@ def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level
             best_list.append(best[o:o + n])
             o += n
     return bits, counts, best_list, status
+
+
+# ---------------------------------------------------------------------------
+# streamed step of a host-resident patch state
+
+def _slab_bounds(NX, g, slabs, ti):
+    """Output-row partition o_0 = g < ... < o_S = NX - g on multiples of the
+    strip length ti, so every strip starts where the whole-patch step's strips
+    start (the fast kernel's last bits depend on a column's place in its
+    strip's 3-way unrolled march)."""
+    nint = NX - 2 * g
+    nstrip = -(-nint // ti)
+    S = max(1, min(int(slabs), nstrip))
+    cuts = sorted({min(nint, ti * ((nstrip * k) // S)) for k in range(S + 1)})
+    return [g + c for c in cuts]
+
+
+def _fast_tile_shape():
+    ni_t, nj_t = _lib.I32(), _lib.I32()
+    _lib.check(_lib.lib().adj_step_tile_shape(_lib.VARIANT_FAST, 2, _lib.C.byref(ni_t), _lib.C.byref(nj_t)),
+               "adj_step_tile_shape")
+    return ni_t.value, nj_t.value
+
+
+def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, limiter, slabs=8):
+    """fill_ghost_physical + the fast step of the single patch of ``store``
+    on a state held in host memory ``host`` (m, NX, NY), updated in place.
+
+    Row slabs run on three streams: the H2D copy of slab k+1, the physical
+    fill + K1 of slab k and the D2H copy of slab k-1 overlap.  Each slab is a
+    virtual patch over the real one (its rows with a g-row halo; x edge bits
+    only on the first / last slab), so K1 and the fill run unchanged; the
+    halo rows come from the neighbouring chunk, which is copied first.
+    Leaves the new state (interior and filled ghosts) in the store's ``cur``."""
+    torch = _torch()
+    p = store.patches[0]
+    off, NX, NY, pitch = store.boxes[0]
+    g, m = store.g, store.m
+    store.edges_table(level_shape)
+    edges = int(store.table_np["edges"][0])
+    inb = store.cur
+    outb = store._free(store.cur, store.ghost_src, -1 if store.old is None else store.old)
+    ti, tj = _fast_tile_shape()
+    ti = store._strip_length(ti, tj)
+    o = _slab_bounds(NX, g, slabs, ti)
+    S = len(o) - 1
+    r = [0] + [o[k] + g for k in range(1, S)] + [NX]      # H2D chunks: slab k needs rows < o[k+1] + g
+    d = [0] + o[1:S] + [NX]                                # D2H chunks
+    if not hasattr(store, "_streams"):
+        store._streams = tuple(torch.cuda.Stream() for _ in range(3))
+        store._stream_scratch = torch.zeros(4, dtype=torch.int32, device="cuda")
+    s_in, s_cmp, s_out = store._streams
+    scratch = store._stream_scratch
+    main = torch.cuda.current_stream()
+    start = torch.cuda.Event()
+    start.record(main)
+    for s in (s_in, s_cmp, s_out):
+        s.wait_event(start)
+    dev_in = store.buf[inb].as_strided((m, NX, NY), (store.plane, pitch, 1), off)
+    dev_out = store.buf[outb].as_strided((m, NX, NY), (store.plane, pitch, 1), off)
+    # per-slab virtual patch tables and tiles (cached per geometry)
+    key = ("stream", tuple(o), edges, ti)
+    cached = store._scratch.get(key)
+    if cached is None:
+        tabs, tiles = [], []
+        for k in range(S):
+            v = store.table_np[:1].copy()
+            v["offset"] = off + (o[k] - g) * pitch
+            v["nx"] = o[k + 1] - o[k]
+            e = edges & ~(_lib.EDGE_XLO | _lib.EDGE_XHI)
+            if k == 0:
+                e |= edges & _lib.EDGE_XLO
+            if k == S - 1:
+                e |= edges & _lib.EDGE_XHI
+            v["edges"] = e
+            nxv, ny = int(v["nx"][0]), int(v["ny"][0])
+            t = [(0, i0, j0, min(ti, nxv - i0), min(tj, ny - j0), 0)
+                 for i0 in range(0, nxv, ti) for j0 in range(0, ny, tj)]
+            tabs.append(_dev_table(v))
+            tiles.append((_dev_table(np.array(t, dtype=_lib.TILE_DTYPE)), len(t)))
+        cached = (tabs, tiles)
+        store._scratch[key] = cached
+    tabs, tiles = cached
+    system, form, rev = equation.kernel_spec()
+    spec = p.spec
+    sides = _bc_codes(boundary)
+    ev_in = [torch.cuda.Event() for _ in range(S)]
+    ev_cmp = [torch.cuda.Event() for _ in range(S)]
+    with torch.cuda.stream(s_cmp):
+        scratch.zero_()
+    for k in range(S):
+        with torch.cuda.stream(s_in):
+            for c in range(m):     # per component: contiguous rows on both sides
+                dev_in[c, r[k]:r[k + 1]].copy_(host[c, r[k]:r[k + 1]], non_blocking=True)
+            ev_in[k].record(s_in)
+        with torch.cuda.stream(s_cmp):
+            s_cmp.wait_event(ev_in[k])
+            a = _lib.AdjPhysArgs()
+            a.q = _ptr(store.buf[inb])
+            a.patches = _ptr(tabs[k])
+            a.comp_stride = store.plane
+            a.npatch, a.ndim, a.ghost, a.m = 1, 2, g, m
+            for i, code in enumerate(sides):
+                a.bc[i] = code
+            a.normal_comp[0] = equation.normal_component(0)
+            a.normal_comp[1] = equation.normal_component(1)
+            a.max_ghost_cells = (o[k + 1] - o[k] + 2 * g) * NY
+            a.stream = _lib.stream_ptr(s_cmp)
+            _lib.check(_lib.lib().adj_fill_physical(_lib.C.byref(a)), "adj_fill_physical")
+            b = _lib.AdjStepArgs()
+            b.q_in = _ptr(store.buf[inb])
+            b.q_out = _ptr(store.buf[outb])
+            b.aux = _ptr(store.aux)
+            b.patches = _ptr(tabs[k])
+            b.tiles = _ptr(tiles[k][0])
+            b.speed_max = _ptr(store.scratch("smax", 2, torch.float64))
+            b.nonfinite = _ptr(scratch)
+            b.work_counter = _ptr(scratch[2:])
+            b.static_speed = _ptr(store.static_speed())
+            b.comp_stride = store.plane
+            b.aux_stride = store.plane
+            b.npatch, b.ntile, b.ndim, b.ghost = 1, tiles[k][1], 2, g
+            b.system, b.form, b.reversed = system, form, rev
+            b.limiter = _lib.LIMITERS[limiter]
+            b.variant = _lib.VARIANT_FAST
+            b.flags = _lib.STEP_KEEP_NONFINITE | _lib.STEP_NO_SPEED_OUT | _lib.STEP_COUNTER_ZERO
+            b.dt, b.dtdx, b.dtdy, b.gravity = dt, dt / spec.dx, dt / spec.dy, equation.gravity
+            b.stream = _lib.stream_ptr(s_cmp)
+            _lib.check(_lib.lib().adj_step_level(_lib.C.byref(b)), "adj_step_level")
+            # the output keeps the filled ghosts (the reference's step leaves ghosts untouched)
+            lo, hi = d[k], d[k + 1]
+            dev_out[:, lo:hi, :g].copy_(dev_in[:, lo:hi, :g])
+            dev_out[:, lo:hi, NY - g:].copy_(dev_in[:, lo:hi, NY - g:])
+            if k == 0:
+                dev_out[:, :g].copy_(dev_in[:, :g])
+            if k == S - 1:
+                dev_out[:, NX - g:].copy_(dev_in[:, NX - g:])
+            ev_cmp[k].record(s_cmp)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_cmp[k])
+            for c in range(m):
+                host[c, d[k]:d[k + 1]].copy_(dev_out[c, d[k]:d[k + 1]], non_blocking=True)
+    for s in (s_in, s_cmp, s_out):
+        main.wait_stream(s)
+    s_out.synchronize()
+    store.ghost_src = outb
+    store.cur = outb
+    return bool(scratch[0].item())

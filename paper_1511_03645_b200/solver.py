@@ -211,6 +211,36 @@ def step_patch(patch: Patch, dt: float, equation: EquationSet, limiter: str = "M
     return StepResult(lambda: patch.state, cfl)
 
 
+def step_patch_host(patch: Patch, host_state, dt: float, equation: EquationSet, boundary: BoundarySpec,
+                    level_shape: tuple[int, ...], limiter: str = "MC", slabs: int = 8) -> StepResult:
+    """fill_ghost_physical + step_patch (solver.py:125-146, 515-522) on a state
+    that lives in host memory, as the reference keeps it: ``host_state``
+    (m, nx+2g, ny+2g) -- a torch CPU tensor, pinned for full overlap -- is
+    read, advanced by dt and overwritten in place; the patch's device copy
+    holds the same state afterwards.  Row slabs stream through the device
+    with the host-to-device copy, the step and the device-to-host copy of
+    consecutive slabs overlapping.  Needs the fast 2D path (static CFL bound,
+    no dry cells); raises CflViolationError before any mutation."""
+    if dt <= 0:
+        raise ValueError("dt must be positive")
+    if limiter not in LIMITERS:
+        raise ValueError(f"unknown limiter {limiter!r}")
+    st = store_of(patch)
+    if len(st.patches) != 1 or st.ndim != 2 or st.any_dry():
+        raise ValueError("step_patch_host needs a single 2D patch store without dry cells")
+    spec = patch.spec
+    dtdx, dtdy = dt / spec.dx, dt / spec.dy
+    cfl = float(_cfl(st.static_speed_np(), dtdx, dtdy, 2)[0])
+    if cfl > 1.0 + 1e-12:
+        raise CflViolationError(f"Courant number {cfl:.4f} > 1")
+    bad = device.stream_step(st, host_state, dt, equation, boundary, level_shape, limiter, slabs)
+    patch._loc = "device"
+    patch.time += dt
+    if bad:
+        raise NumericalBlowupError(f"non-finite state at t={patch.time}")
+    return StepResult(lambda: patch.state, cfl)
+
+
 def _launch_single(st, slot, dt, equation, limiter, variant, out):
     """Step one patch of a multi-patch store (work tables restricted to it)."""
     if variant == _lib.VARIANT_FAST and st.any_dry():
