@@ -155,6 +155,122 @@ __global__ void __launch_bounds__(256) k3_flag(AdjFlagArgs a) {
     if (lane == 0 && cnt) atomicAdd(&a.counts[pidx], cnt);
 }
 
+// ---------------------------------------------------------------------------
+// Table path, v2: the same per-cell arithmetic as cell_best<.., TABLES=true>
+// (bitwise), restructured for issue efficiency -- mode as a template
+// parameter, the window's snapshot list staged in shared memory, one
+// division per thread (cells then advance by 32), per-snapshot component
+// base pointers with 32-bit corner indices (one IMAD.WIDE per load).
+constexpr int K3_MAXN = 256;
+
+// 8-byte load at a 32-bit byte offset from a (warp-uniform) base
+ADJ_D double ld(const char* base, unsigned off) { return *reinterpret_cast<const double*>(base + off); }
+
+template <int M, bool TWO_D, bool MODE1>
+__global__ void __launch_bounds__(256) k3_flag_t(AdjFlagArgs a) {
+    __shared__ int s_k[K3_MAXN];
+    __shared__ double s_w[K3_MAXN];
+    const int nidx = a.nidx;
+    for (int n = threadIdx.x; n < nidx; n += blockDim.x) {
+        s_k[n] = a.snap_index[n];
+        if (MODE1) s_w[n] = a.interp_w[n];
+    }
+    __syncthreads();
+    const int pidx = blockIdx.y;
+    const AdjPatch p = a.patches[pidx];
+    const unsigned ny = TWO_D ? (unsigned)p.ny : 1u;
+    const unsigned ncell = (unsigned)p.nx * ny;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned base = (blockIdx.x * (blockDim.x >> 5) + warp) * (32u * NC);
+    if (base >= ncell) return;
+    const int g = a.ghost, gy = TWO_D ? g : 0;
+    const unsigned nxa = (unsigned)a.nxa, nya = (unsigned)a.nya;
+    const int64_t plane_b = (int64_t)nxa * nya * 8;        // one snapshot component, bytes
+    const int64_t snap_b = plane_b * M;                    // one snapshot, bytes
+    const char* ring = reinterpret_cast<const char*>(a.ring);
+    const int64_t rowoff = a.axis_off[2 * pidx], coloff = a.axis_off[2 * pidx + 1];
+    unsigned i = TWO_D ? (base + lane) / ny : base + lane;
+    unsigned j = TWO_D ? (base + lane) - i * ny : 0u;
+    unsigned long long cnt = 0;
+#pragma unroll
+    for (int kk = 0; kk < NC; ++kk) {
+        const unsigned wbase = base + 32u * kk;
+        if (wbase >= ncell) break;                     // warp-uniform
+        const unsigned cidx = wbase + lane;
+        bool flag = false;
+        if (cidx < ncell) {
+            const int64_t o = p.offset + (int64_t)(i + g) * p.pitch + (j + gy);
+            double q[M];
+#pragma unroll
+            for (int c = 0; c < M; ++c) q[c] = a.q[c * a.comp_stride + o];
+            const int64_t ro = rowoff + i, co = coloff + j;
+            const int i0 = a.axis_i[ro];
+            const double wx = a.axis_w[ro];
+            int j0 = 0;
+            double wy = 0.0;
+            if (TWO_D) { j0 = a.axis_i[co]; wy = a.axis_w[co]; }
+            const unsigned i1 = min((unsigned)i0 + 1u, nxa - 1u);
+            const unsigned j1 = TWO_D ? min((unsigned)j0 + 1u, nya - 1u) : 0u;
+            // corner byte offsets within one snapshot component (plane * 8 < 2^32)
+            const unsigned b00 = ((unsigned)i0 * nya + (unsigned)j0) * 8u, b10 = (i1 * nya + (unsigned)j0) * 8u;
+            const unsigned b01 = ((unsigned)i0 * nya + j1) * 8u, b11 = (i1 * nya + j1) * 8u;
+            const double ux = 1.0 - wx, uy = 1.0 - wy;
+            double best = 0.0;
+            for (int n = 0; n < nidx; ++n) {
+                const int k = s_k[n];
+                double dot = 0.0;
+                if (!MODE1 || k < 0) {
+                    const char* f = ring + (int64_t)(k < 0 ? -k - 1 : k) * snap_b;
+#pragma unroll
+                    for (int c = 0; c < M; ++c) {
+                        const char* fc = f + c * plane_b;
+                        double qh;
+                        if (TWO_D)
+                            qh = ld(fc, b00) * ux * uy + ld(fc, b10) * wx * uy + ld(fc, b01) * ux * wy +
+                                 ld(fc, b11) * wx * wy;
+                        else
+                            qh = ld(fc, b00) * ux + ld(fc, b10) * wx;
+                        dot = c == 0 ? qh * q[c] : dot + qh * q[c];
+                    }
+                } else {
+                    const double w = s_w[n];
+                    const char* fa = ring + (int64_t)k * snap_b;
+#pragma unroll
+                    for (int c = 0; c < M; ++c) {
+                        const char* ac = fa + c * plane_b;
+                        const char* bc = ac + snap_b;
+                        const double v00 = (1.0 - w) * ld(ac, b00) + w * ld(bc, b00);
+                        const double v10 = (1.0 - w) * ld(ac, b10) + w * ld(bc, b10);
+                        double qh;
+                        if (TWO_D) {
+                            const double v01 = (1.0 - w) * ld(ac, b01) + w * ld(bc, b01);
+                            const double v11 = (1.0 - w) * ld(ac, b11) + w * ld(bc, b11);
+                            qh = v00 * ux * uy + v10 * wx * uy + v01 * ux * wy + v11 * wx * wy;
+                        } else {
+                            qh = v00 * ux + v10 * wx;
+                        }
+                        dot = c == 0 ? qh * q[c] : dot + qh * q[c];
+                    }
+                }
+                best = fmax(best, fabs(dot));
+            }
+            if (a.swe && !(a.aux[a.aux_stride + o] > 0.0)) best = 0.0;   // forward dry cell
+            if (TWO_D && a.adj_wet != nullptr && a.axis_dry) {
+                const int ia = a.axis_dry[ro], ja = a.axis_dry[co];
+                if (!a.adj_wet[(unsigned)ia * nya + ja]) best = 0.0;
+            }
+            flag = best > a.tolerance;
+            if (a.best != nullptr) a.best[a.best_offset[pidx] + cidx] = best;
+        }
+        const unsigned word = __ballot_sync(0xffffffffu, flag);
+        if (lane == 0) a.flag_bits[p.flag_word + (wbase >> 5)] = word;
+        cnt += __popc(word);
+        // next cell of this lane: 32 further in row-major order
+        if (TWO_D) { j += 32u; while (j >= ny) { j -= ny; ++i; } } else { i += 32u; }
+    }
+    if (lane == 0 && cnt) atomicAdd(&a.counts[pidx], cnt);
+}
+
 int flag_adjoint(const AdjFlagArgs& a) {
     if (a.npatch <= 0 || a.max_cells <= 0) return ADJ_OK;
     const int threads = 256;
@@ -162,6 +278,19 @@ int flag_adjoint(const AdjFlagArgs& a) {
     dim3 grid((unsigned)bx, (unsigned)a.npatch);
     cudaStream_t st = (cudaStream_t)a.stream;
     const bool tab = a.axis_w && a.axis_i && a.axis_off;
+    if (tab && a.nidx <= K3_MAXN && !(a.ndim == 2 && a.adj_wet && !a.axis_dry)) {
+        const bool m1 = a.mode == 1;
+        if (a.ndim == 1 && a.m == 2) {
+            if (m1) k3_flag_t<2, false, true><<<grid, threads, 0, st>>>(a);
+            else k3_flag_t<2, false, false><<<grid, threads, 0, st>>>(a);
+        } else if (a.ndim == 2 && a.m == 3) {
+            if (m1) k3_flag_t<3, true, true><<<grid, threads, 0, st>>>(a);
+            else k3_flag_t<3, true, false><<<grid, threads, 0, st>>>(a);
+        } else {
+            return ADJ_ERR_BAD_ARG;
+        }
+        return check_launch("k3_flag_t");
+    }
     if (a.ndim == 1) {
         if (a.m != 2) return ADJ_ERR_BAD_ARG;
         if (tab) k3_flag<2, false, true><<<grid, threads, 0, st>>>(a);
