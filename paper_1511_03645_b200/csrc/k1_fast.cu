@@ -40,9 +40,6 @@
 #ifndef K1_PREFETCH_CLAMP
 #define K1_PREFETCH_CLAMP 1   // 1: branch-free prefetch (re-read the last column)
 #endif
-#ifndef K1_KY_RECOMPUTE
-#define K1_KY_RECOMPUTE 0 // 1: recompute the neighbour's y coefficient instead of shuffling it
-#endif
 
 namespace adj {
 
@@ -99,25 +96,29 @@ ADJ_D double limab2(double A, double B) {
 }
 
 // Per-cell material quantities.  m: eigen material (z for acoustics, c for
-// shallow water); k1i = 1/(1+m^2); kx, ky: correction magnitudes
+// shallow water); k1i = 1/(2(1+m^2)); kx, ky: correction magnitudes
 // (wave: 0.5 c (1 - dtd c); f-wave: 0.5 (1 - dtd c)); tr: transverse helper
 // (acoustics K = c z, shallow water c^2); fx: f-wave flux factor (acoustics
 // 1/rho, shallow water g h = c^2).
 struct Mat {
-    double c, m, k1, k1i, kx, ky, tr, fx;   // k1 = 1+m^2, k1i = 1/(2 k1)
+    double c, m, k1, k1i, kx, ky, tr, fx;   // k1 = 1+m^2, k1i = 1/(2 k1); kx, ky include k1i when limited
 };
 
-template <int SYS, int FORM>
+template <int SYS, int FORM, int LIM>
 ADJ_D Mat make_mat(double c, double z, double dtdx, double dtdy) {
     constexpr bool SWE = SYS == ADJ_SYS_SWE2D, FW = FORM == ADJ_FORM_FWAVE;
     Mat t;
     t.c = c;
     t.m = SWE ? c : z;
     t.k1 = fma(t.m, t.m, 1.0);
-    t.k1i = rcp(t.k1 + t.k1);
     const double hx = 0.5 * fma(-dtdx, c, 1.0), hy = 0.5 * fma(-dtdy, c, 1.0);
     t.kx = FW ? hx : c * hx;
     t.ky = FW ? hy : c * hy;
+    if (LIM != ADJ_LIM_NONE) {   // the limited strength is only ever used scaled by k / (2 (1 + m^2))
+        t.k1i = rcp(t.k1 + t.k1);
+        t.kx *= t.k1i;
+        t.ky *= t.k1i;
+    }
     t.tr = SWE ? c * c : c * z;
     t.fx = FW ? (SWE ? c * c : c / z) : 0.0;
     return t;
@@ -191,8 +192,8 @@ ADJ_D void correction(const Face& f, double s0_nb, double P0_nb, double s1_nb, d
         const double A1 = f.s1 * R.k1;
         const double B0 = s0_nb * (REV ? P0_nb : f.P);
         const double B1 = s1_nb * (REV ? P1_nb : f.P);
-        p0 = limab2<LIM>(A0, B0) * L.k1i;
-        p1 = limab2<LIM>(A1, B1) * R.k1i;
+        p0 = limab2<LIM>(A0, B0);     // 1 / (2 (1 + m^2)) is folded into kL, kR (make_mat)
+        p1 = limab2<LIM>(A1, B1);
     }
     // coefficients: wave 0.5|s|(1-dtd|s|) for both; f-wave sign(s) 0.5(1-dtd|s|)
     const double u0 = (FW ? -kL : kL) * p0;
@@ -234,6 +235,7 @@ constexpr int RING = 3 * GROUPS;   // column slots of the per-warp ring
 template <int SYS, int FORM, bool REV, int LIM, bool CFL>
 struct Strip {
     static constexpr bool SWE = SYS == ADJ_SYS_SWE2D;
+    static constexpr bool FWD_WAVE = FORM == ADJ_FORM_WAVE && !REV;
     const double* __restrict__ qin;
     const double* __restrict__ aux;
     double* __restrict__ qout;
@@ -291,7 +293,7 @@ struct Strip {
     template <int K>
     ADJ_D void column(int s, const Raw& cr) {
         constexpr int C = K, P = (K + 2) % 3, PP = (K + 1) % 3;
-        m[C] = make_mat<SYS, FORM>(cr.c, cr.z, dtdx, dtdy);
+        m[C] = make_mat<SYS, FORM, LIM>(cr.c, cr.z, dtdx, dtdy);
         // CFL: max |speed| of the faces is the max material speed of the cells
         // they touch (fast path = no dry cells): x-faces of this strip touch
         // columns [i0-1, i0+ni] of the output rows, y-faces rows j0-1..j0+nj
@@ -310,13 +312,8 @@ struct Strip {
         Mat mu{};
         mu.c = sh_dn(m[C].c);
         mu.m = SWE ? mu.c : sh_dn(m[C].m);
-        mu.k1i = sh_dn(m[C].k1i);
         mu.k1 = fma(mu.m, mu.m, 1.0);
-#if K1_KY_RECOMPUTE
-        mu.ky = (FORM == ADJ_FORM_FWAVE ? 1.0 : mu.c) * (0.5 * fma(-dtdy, mu.c, 1.0));
-#else
         mu.ky = sh_dn(m[C].ky);
-#endif
         mu.kx = 0.0;
         mu.tr = SWE ? mu.c * mu.c : mu.c * mu.m;
         mu.fx = FORM == ADJ_FORM_FWAVE ? sh_dn(m[C].fx) : 0.0;
@@ -328,14 +325,29 @@ struct Strip {
             const double P1n = REV ? sh_dn(yf.P) : 0.0;
             correction<SYS, FORM, REV, LIM>(yf, s0n, P0n, s1n, P1n, m[C], mu, m[C].ky, mu.ky, cy0[C], cy2[C]);
         }
-        sy0[C] = yf.am0 + sh_up(yf.ap0);
-        sy2[C] = yf.am1 + sh_up(yf.ap1);
+        if (FWD_WAVE) {
+            // Sy(cell) = apdq(face below, R = cell) + amdq(own face, L = cell): the
+            // cell's own material times the two strengths (s1 below is the
+            // limiter neighbour the correction above already shuffled)
+            const double s1b = sh_up(yf.s1);
+            if (SWE) { sy0[C] = m[C].c * (s1b - yf.s0); sy2[C] = m[C].tr * (s1b + yf.s0); }
+            else { sy0[C] = m[C].tr * (s1b + yf.s0); sy2[C] = m[C].c * (s1b - yf.s0); }
+        } else {
+            sy0[C] = yf.am0 + sh_up(yf.ap0);
+            sy2[C] = yf.am1 + sh_up(yf.ap1);
+        }
         cup[C] = mu.c;
         mup[C] = mu.m;
 
         // ---- Sx(s-1) and its transverse split with rows j-1, j+1 of column s-1
-        sx0[P] = xf[P].ap0 + xf[C].am0;
-        sx1[P] = xf[P].ap1 + xf[C].am1;
+        if (FWD_WAVE) {   // Sx(s-1) from the strengths of its two x-faces and its own material
+            const double sl = xf[P].s1, sr = xf[C].s0;
+            if (SWE) { sx0[P] = m[P].c * (sl - sr); sx1[P] = m[P].tr * (sl + sr); }
+            else { sx0[P] = m[P].tr * (sl + sr); sx1[P] = m[P].c * (sl - sr); }
+        } else {
+            sx0[P] = xf[P].ap0 + xf[C].am0;
+            sx1[P] = xf[P].ap1 + xf[C].am1;
+        }
         {
             Mat mb{};
             mb.c = sh_up(m[P].c);
@@ -551,8 +563,8 @@ struct Strip2 {
     template <int K>
     ADJ_D void column(int s, const Raw& RA, const Raw& RB) {
         constexpr int C = K, P = (K + 2) % 3, PP = (K + 1) % 3;
-        m[C][0] = make_mat<SYS, FORM>(RA.c, RA.z, dtdx, dtdy);
-        m[C][1] = make_mat<SYS, FORM>(RB.c, RB.z, dtdx, dtdy);
+        m[C][0] = make_mat<SYS, FORM, LIM>(RA.c, RA.z, dtdx, dtdy);
+        m[C][1] = make_mat<SYS, FORM, LIM>(RB.c, RB.z, dtdx, dtdy);
         q0[C][0] = RA.q0; q1[C][0] = RA.q1; q2[C][0] = RA.q2;
         q0[C][1] = RB.q0; q1[C][1] = RB.q1; q2[C][1] = RB.q2;
 
@@ -567,7 +579,6 @@ struct Strip2 {
         Mat mu{};
         mu.c = sh_dn(m[C][0].c);
         mu.m = SWE ? mu.c : sh_dn(m[C][0].m);
-        mu.k1i = sh_dn(m[C][0].k1i);
         mu.k1 = fma(mu.m, mu.m, 1.0);
         mu.ky = sh_dn(m[C][0].ky);
         mu.tr = SWE ? mu.c * mu.c : mu.c * mu.m;
