@@ -503,7 +503,8 @@ def main():
         "c3_heterogeneous_acoustics": c3,
         "c5_full_workflow": c5_full,
         "e2e": e2e,
-        "gpu_launches": args.steps * 4,
+        # per step: k2_physical + k1_fast (graph replay; no memset nodes, fold is a no-op)
+        "gpu_launches": args.steps * 2,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
