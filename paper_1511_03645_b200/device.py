@@ -1111,9 +1111,19 @@ def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level
     torch = _torch()
     npatch = len(store.patches)
     mode = 0 if interp_w is None else 1
-    idx = torch.tensor(list(snap_index) if len(snap_index) else [0], dtype=torch.int32, device="cuda")
-    w = torch.tensor(list(interp_w) if interp_w is not None and len(interp_w) else [0.0],
-                     dtype=torch.float64, device="cuda")
+    # window lists cached on the device (no blocking pageable copy per launch)
+    wkey = ("flagwin", tuple(int(k) for k in snap_index),
+            None if interp_w is None else tuple(float(x) for x in interp_w))
+    cached = store._scratch.get(wkey)
+    if cached is None:
+        if len(store._scratch) > 256:
+            for k in [k for k in store._scratch if isinstance(k, tuple) and k and k[0] == "flagwin"]:
+                del store._scratch[k]
+        idx = torch.tensor(list(snap_index) if len(snap_index) else [0], dtype=torch.int32, device="cuda")
+        w = torch.tensor(list(interp_w) if interp_w is not None and len(interp_w) else [0.0],
+                         dtype=torch.float64, device="cuda")
+        cached = store._scratch[wkey] = (idx, w)
+    idx, w = cached
     bits = store.scratch("flag_bits", max(store.flag_words, 1), torch.int32)
     counts = store.scratch("flag_counts", npatch, torch.int64)
     status = store.scratch("flag_status", 1, torch.int32)

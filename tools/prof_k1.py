@@ -16,6 +16,7 @@ ap.add_argument("--launches", type=int, default=3)
 ap.add_argument("--n", type=int, default=4096)
 ap.add_argument("--variant", default="fast")
 ap.add_argument("--flag", action="store_true")
+ap.add_argument("--flag1", action="store_true", help="single-snapshot window")
 a = ap.parse_args()
 bench.N = a.n
 h, p, eq, bc, dt = bench.build_c4(a.n)
@@ -37,9 +38,9 @@ for _ in range(a.launches):
 torch.cuda.synchronize()
 ms = [x.elapsed_time(y) for x, y in times]
 print("k1 ms:", [round(v, 4) for v in ms], "median", round(sorted(ms)[len(ms) // 2], 4), os.environ.get("ADJAMR_LIB", "default"))
-if a.flag:
+if a.flag or a.flag1:
     ring = bench.adjoint_ring(41)
     device.launch_flag(st, ring, (1024, 1024), (0.0, 0.0), bench.L / 1024, bench.L / 1024, (0.0, 0.0),
-                       bench.L / a.n, bench.L / a.n, [19, 20], 1e-4)
+                       bench.L / a.n, bench.L / a.n, [20] if a.flag1 else [19, 20], 1e-4)
     torch.cuda.synchronize()
 print("ok")
