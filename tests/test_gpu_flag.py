@@ -81,3 +81,19 @@ def test_out_of_range_raises():
     st2 = adjoint.AdjointSnapshotStore(times=store.times, fields=small, window=store.window)
     with pytest.raises(OutOfRangeError):
         adjoint.inner_product_field(p, 0.5, st2, st2.window)
+
+
+def test_empty_window_gives_no_flags():
+    """t beyond the last snapshot: query_window_times is empty (adjoint.py:
+    192-214) and inner_product_field is zero everywhere (adjoint.py:227-249)."""
+    from paper_1511_03645_b200 import adjoint
+    d = FLAG["flag0"]
+    p, store = _setup(d)
+    t = float(d["times"][-1]) + 0.5
+    assert adjoint.query_window_times(t, store.window, store) == []
+    best = adjoint.inner_product_field(p, t, store, store.window)
+    assert not np.any(best)
+    ff = adjoint.inner_product_flags(p, t, store, store.window, 0.0)
+    assert not ff.flags.any()
+    _, counts, _ = adjoint.flag_level([p], t, store, store.window, 0.0)
+    assert counts[0] == 0
