@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define ADJ_ABI_VERSION 2
+#define ADJ_ABI_VERSION 3
 
 /* status codes (mapped to the reference's exception classes by the host) */
 #define ADJ_OK                 0
@@ -86,72 +86,7 @@ typedef struct AdjTile {
     int32_t patch, i0, j0, ni, nj, pad;
 } AdjTile;
 
-/* K1: wave-propagation step of every patch of a level.
- * Replaces step_patch / step_patch_1d / step_patch_2d (solver.py:415-522), the
- * Riemann and transverse solvers (equations.py:98-349), TimeReversed
- * (equations.py:496-534) and the limiter (solver.py:65-77, 317-348).
- * Reads q_in (ghosts filled), writes the interior of q_out (ping-pong buffers
- * replace Patch.save_old, geometry.py:123).  Outputs per patch: the maximum
- * |speed| over the reference's CFL interface ranges, x and y separately
- * (solver.py:425, 457-460), and a non-finite flag (solver.py:437, 510). */
-typedef struct AdjStepArgs {
-    const double* q_in;
-    double* q_out;
-    const double* aux;
-    const AdjPatch* patches;   /* device */
-    const AdjTile* tiles;      /* device */
-    double* speed_max;         /* device, 2*npatch (x, y), zeroed by the call */
-    int32_t* nonfinite;        /* device, npatch, zeroed by the call          */
-    int32_t* work_counter;     /* device, 2 ints (tile queue head, exit count), zeroed by the call
-                                  unless ADJ_STEP_COUNTER_ZERO */
-    const double* static_speed;/* optional device (x, y) per patch: material speed bound over the
-                                  CFL ranges; when given, the FAST variant (no dry cells) copies it
-                                  to speed_max instead of reducing per face (same values) */
-    const int32_t* job_offsets;/* optional (FAST + static_speed): warp job j = tiles[job_offsets[j],
-                                  job_offsets[j+1]); each tile of a job is a row strip placed at
-                                  lanes [pad, pad + nj + 4) of the warp, all with the same ni */
-    int32_t njob, pad2;
-    int64_t comp_stride, aux_stride;
-    int32_t npatch, ntile;
-    int32_t ndim, ghost;
-    int32_t system, form, reversed, limiter, variant, flags;   /* ADJ_STEP_* bits */
-    double dt, dtdx, dtdy, gravity;
-    void* stream;              /* cudaStream_t */
-} AdjStepArgs;
-/* AdjStepArgs.flags */
-#define ADJ_STEP_KEEP_NONFINITE 1   /* do not zero nonfinite: accumulate over launches */
-#define ADJ_STEP_NO_SPEED_OUT   2   /* do not write speed_max (caller uses static_speed) */
-#define ADJ_STEP_TWO_ROWS       4   /* FAST + static_speed: tiles are 64-row strips (<= 60 outputs),
-                                       two rows per lane; no job_offsets */
-#define ADJ_STEP_COUNTER_ZERO   8   /* FAST 2D: work_counter holds 2 ints that are zero on entry; the
-                                       kernel leaves them zero (no memset node per launch) */
-int adj_step_level(const AdjStepArgs* a);
-
-/* Tile shape (ni, nj) the given variant expects in AdjStepArgs.tiles. */
-int adj_step_tile_shape(int variant, int ndim, int32_t* ni, int32_t* nj);
-
-/* K2 (physical phase): wall / outflow ghost fill of every patch edge that
- * meets the domain boundary.  Replaces fill_ghost_physical (solver.py:125-146)
- * with its x-then-y, low-then-high slab order folded into one gather. */
-typedef struct AdjPhysArgs {
-    double* q;
-    const AdjPatch* patches;   /* device */
-    int64_t comp_stride;
-    int32_t npatch, ndim, ghost, m;
-    int32_t bc[4];             /* left, right, bottom, top: ADJ_BC_*          */
-    int32_t normal_comp[2];    /* component negated at a wall, per axis      */
-    int32_t max_ghost_cells;   /* max ghost cells of any patch (grid sizing) */
-    int32_t pad;
-    void* stream;
-} AdjPhysArgs;
-int adj_fill_physical(const AdjPhysArgs* a);
-
-/* K2 (in-domain phase): same-level copies and coarse-to-fine space-time
- * interpolation over rectangles of ghost cells.  Replaces
- * fill_ghost_from_coarse + space_time_interp (solver.py:227-286),
- * interpolate_patch (geometry.py:302-327) and fill_ghost_same_level
- * (solver.py:208-224); rectangles are built on the host once per regrid.
- * Also used for regrid data movement (amr.py:504-551, kind 2/3). */
+/* Rectangle of ghost cells (K2 rect fills and plans; K4 overlaps). */
 #define ADJ_RECT_COPY        0   /* dst cells <- src patch cells (same level)          */
 #define ADJ_RECT_COARSE      1   /* dst cells <- bilinear/linear-in-time coarse interp */
 typedef struct AdjRect {
@@ -162,30 +97,6 @@ typedef struct AdjRect {
     int32_t si0, sj0;     /* src start (COPY), ghost-inclusive local coords    */
     int32_t pad;
 } AdjRect;
-typedef struct AdjGhostArgs {
-    double* q_dst;               /* destination level store                        */
-    const double* q_src;         /* COPY source level store (may == q_dst)          */
-    const double* q_coarse_old;  /* COARSE: coarse level state at t0                */
-    const double* q_coarse_new;  /* COARSE: coarse level state at t1                */
-    const AdjPatch* dst_patches; /* device */
-    const AdjPatch* src_patches; /* device, COPY sources                            */
-    const AdjPatch* coarse_patches; /* device, COARSE sources                       */
-    const AdjRect* rects;        /* device; COPY and COARSE rects may be mixed when disjoint */
-    int64_t dst_comp_stride, src_comp_stride, coarse_comp_stride;
-    int32_t nrect, ndim, m, ghost_dst, ghost_src, ratio;
-    double origin_x, origin_y;   /* hierarchy.origin                              */
-    double dx_f, dy_f;           /* fine widths                                   */
-    double dx_c, dy_c;           /* coarse widths                                 */
-    double w_time;               /* clip((t-t0)/(t1-t0),0,1)                      */
-    const double* w_time_dev;    /* optional: read w from device memory (graph replay) */
-    const double* axis_w;        /* optional per-rect axis weights: COARSE rect r has its ni x-weights at
-                                    axis_w[rect.pad], then its nj y-weights (geometry.py:248-260) */
-    const int32_t* axis_i;       /* matching lower stencil indices (same layout)               */
-    int32_t time_mode;           /* 0: old only, 1: blend old/new, 2: new only    */
-    int32_t max_rect_cells;
-    void* stream;
-} AdjGhostArgs;
-int adj_fill_ghost_rects(const AdjGhostArgs* a);
 
 /* K2, planned form of a whole level fill (fill_level_ghosts, amr.py:479-491:
  * coarse interpolation, same-level copy, then physical boundaries) as ONE
@@ -239,6 +150,102 @@ typedef struct AdjGhostPlanFillArgs {
     void* stream;
 } AdjGhostPlanFillArgs;
 int adj_fill_ghost_plan(const AdjGhostPlanFillArgs* a);
+
+/* K1: wave-propagation step of every patch of a level.
+ * Replaces step_patch / step_patch_1d / step_patch_2d (solver.py:415-522), the
+ * Riemann and transverse solvers (equations.py:98-349), TimeReversed
+ * (equations.py:496-534) and the limiter (solver.py:65-77, 317-348).
+ * Reads q_in (ghosts filled), writes the interior of q_out (ping-pong buffers
+ * replace Patch.save_old, geometry.py:123).  Outputs per patch: the maximum
+ * |speed| over the reference's CFL interface ranges, x and y separately
+ * (solver.py:425, 457-460), and a non-finite flag (solver.py:437, 510). */
+typedef struct AdjStepArgs {
+    const double* q_in;
+    double* q_out;
+    const double* aux;
+    const AdjPatch* patches;   /* device */
+    const AdjTile* tiles;      /* device */
+    double* speed_max;         /* device, 2*npatch (x, y), zeroed by the call */
+    int32_t* nonfinite;        /* device, npatch, zeroed by the call          */
+    int32_t* work_counter;     /* device, 2 ints (tile queue head, exit count), zeroed by the call
+                                  unless ADJ_STEP_COUNTER_ZERO */
+    const double* static_speed;/* optional device (x, y) per patch: material speed bound over the
+                                  CFL ranges; when given, the FAST variant (no dry cells) copies it
+                                  to speed_max instead of reducing per face (same values) */
+    const int32_t* job_offsets;/* optional (FAST + static_speed): warp job j = tiles[job_offsets[j],
+                                  job_offsets[j+1]); each tile of a job is a row strip placed at
+                                  lanes [pad, pad + nj + 4) of the warp, all with the same ni */
+    int32_t njob, pad2;
+    int64_t comp_stride, aux_stride;
+    int32_t npatch, ntile;
+    int32_t ndim, ghost;
+    int32_t system, form, reversed, limiter, variant, flags;   /* ADJ_STEP_* bits */
+    double dt, dtdx, dtdy, gravity;
+    void* stream;              /* cudaStream_t */
+    AdjGhostPlanFillArgs prefill;  /* optional (prefill.plan.n > 0; FAST 2D with static_speed and
+                                  ADJ_STEP_COUNTER_ZERO): the level's planned ghost fill of q_in runs
+                                  inside this launch before the step (a grid barrier separates them);
+                                  work_counter then holds 3 zeroed ints */
+} AdjStepArgs;
+/* AdjStepArgs.flags */
+#define ADJ_STEP_KEEP_NONFINITE 1   /* do not zero nonfinite: accumulate over launches */
+#define ADJ_STEP_NO_SPEED_OUT   2   /* do not write speed_max (caller uses static_speed) */
+#define ADJ_STEP_TWO_ROWS       4   /* FAST + static_speed: tiles are 64-row strips (<= 60 outputs),
+                                       two rows per lane; no job_offsets */
+#define ADJ_STEP_COUNTER_ZERO   8   /* FAST 2D: work_counter holds 2 ints that are zero on entry; the
+                                       kernel leaves them zero (no memset node per launch) */
+int adj_step_level(const AdjStepArgs* a);
+
+/* Tile shape (ni, nj) the given variant expects in AdjStepArgs.tiles. */
+int adj_step_tile_shape(int variant, int ndim, int32_t* ni, int32_t* nj);
+
+/* K2 (physical phase): wall / outflow ghost fill of every patch edge that
+ * meets the domain boundary.  Replaces fill_ghost_physical (solver.py:125-146)
+ * with its x-then-y, low-then-high slab order folded into one gather. */
+typedef struct AdjPhysArgs {
+    double* q;
+    const AdjPatch* patches;   /* device */
+    int64_t comp_stride;
+    int32_t npatch, ndim, ghost, m;
+    int32_t bc[4];             /* left, right, bottom, top: ADJ_BC_*          */
+    int32_t normal_comp[2];    /* component negated at a wall, per axis      */
+    int32_t max_ghost_cells;   /* max ghost cells of any patch (grid sizing) */
+    int32_t pad;
+    void* stream;
+} AdjPhysArgs;
+int adj_fill_physical(const AdjPhysArgs* a);
+
+/* K2 (in-domain phase): same-level copies and coarse-to-fine space-time
+ * interpolation over rectangles of ghost cells.  Replaces
+ * fill_ghost_from_coarse + space_time_interp (solver.py:227-286),
+ * interpolate_patch (geometry.py:302-327) and fill_ghost_same_level
+ * (solver.py:208-224); rectangles are built on the host once per regrid.
+ * Also used for regrid data movement (amr.py:504-551, kind 2/3). */
+typedef struct AdjGhostArgs {
+    double* q_dst;               /* destination level store                        */
+    const double* q_src;         /* COPY source level store (may == q_dst)          */
+    const double* q_coarse_old;  /* COARSE: coarse level state at t0                */
+    const double* q_coarse_new;  /* COARSE: coarse level state at t1                */
+    const AdjPatch* dst_patches; /* device */
+    const AdjPatch* src_patches; /* device, COPY sources                            */
+    const AdjPatch* coarse_patches; /* device, COARSE sources                       */
+    const AdjRect* rects;        /* device; COPY and COARSE rects may be mixed when disjoint */
+    int64_t dst_comp_stride, src_comp_stride, coarse_comp_stride;
+    int32_t nrect, ndim, m, ghost_dst, ghost_src, ratio;
+    double origin_x, origin_y;   /* hierarchy.origin                              */
+    double dx_f, dy_f;           /* fine widths                                   */
+    double dx_c, dy_c;           /* coarse widths                                 */
+    double w_time;               /* clip((t-t0)/(t1-t0),0,1)                      */
+    const double* w_time_dev;    /* optional: read w from device memory (graph replay) */
+    const double* axis_w;        /* optional per-rect axis weights: COARSE rect r has its ni x-weights at
+                                    axis_w[rect.pad], then its nj y-weights (geometry.py:248-260) */
+    const int32_t* axis_i;       /* matching lower stencil indices (same layout)               */
+    int32_t time_mode;           /* 0: old only, 1: blend old/new, 2: new only    */
+    int32_t max_rect_cells;
+    void* stream;
+} AdjGhostArgs;
+int adj_fill_ghost_rects(const AdjGhostArgs* a);
+
 
 /* K4: conservative fine-to-coarse averaging.  Replaces
  * restrict_fine_to_coarse (amr.py:399-450); one AdjRect per (coarse patch,

@@ -48,32 +48,6 @@ assert PATCH_DTYPE.itemsize == 48 and TILE_DTYPE.itemsize == 24 and RECT_DTYPE.i
 P, D, I32, I64 = C.c_void_p, C.c_double, C.c_int32, C.c_int64
 
 
-class AdjStepArgs(C.Structure):
-    _fields_ = [("q_in", P), ("q_out", P), ("aux", P), ("patches", P), ("tiles", P),
-                ("speed_max", P), ("nonfinite", P), ("work_counter", P), ("static_speed", P), ("job_offsets", P),
-                ("njob", I32), ("pad2", I32), ("comp_stride", I64), ("aux_stride", I64),
-                ("npatch", I32), ("ntile", I32), ("ndim", I32), ("ghost", I32),
-                ("system", I32), ("form", I32), ("reversed", I32), ("limiter", I32),
-                ("variant", I32), ("flags", I32),
-                ("dt", D), ("dtdx", D), ("dtdy", D), ("gravity", D), ("stream", P)]
-
-
-class AdjPhysArgs(C.Structure):
-    _fields_ = [("q", P), ("patches", P), ("comp_stride", I64), ("npatch", I32), ("ndim", I32),
-                ("ghost", I32), ("m", I32), ("bc", I32 * 4), ("normal_comp", I32 * 2),
-                ("max_ghost_cells", I32), ("pad", I32), ("stream", P)]
-
-
-class AdjGhostArgs(C.Structure):
-    _fields_ = [("q_dst", P), ("q_src", P), ("q_coarse_old", P), ("q_coarse_new", P),
-                ("dst_patches", P), ("src_patches", P), ("coarse_patches", P), ("rects", P),
-                ("dst_comp_stride", I64), ("src_comp_stride", I64), ("coarse_comp_stride", I64),
-                ("nrect", I32), ("ndim", I32), ("m", I32), ("ghost_dst", I32), ("ghost_src", I32),
-                ("ratio", I32), ("origin_x", D), ("origin_y", D), ("dx_f", D), ("dy_f", D),
-                ("dx_c", D), ("dy_c", D), ("w_time", D), ("w_time_dev", P), ("axis_w", P), ("axis_i", P), ("time_mode", I32),
-                ("max_rect_cells", I32), ("stream", P)]
-
-
 class AdjGhostPlan(C.Structure):
     _fields_ = [("dst", P), ("src", P), ("meta", P), ("c_base", P), ("c_step", P), ("c_wx", P), ("c_wy", P),
                 ("n", I32), ("nc", I32)]
@@ -92,6 +66,32 @@ class AdjGhostPlanFillArgs(C.Structure):
                 ("comp_stride", I64), ("coarse_comp_stride", I64),
                 ("ndim", I32), ("m", I32), ("time_mode", I32), ("pad", I32),
                 ("w_time", D), ("w_time_dev", P), ("stream", P)]
+
+
+class AdjStepArgs(C.Structure):
+    _fields_ = [("q_in", P), ("q_out", P), ("aux", P), ("patches", P), ("tiles", P),
+                ("speed_max", P), ("nonfinite", P), ("work_counter", P), ("static_speed", P), ("job_offsets", P),
+                ("njob", I32), ("pad2", I32), ("comp_stride", I64), ("aux_stride", I64),
+                ("npatch", I32), ("ntile", I32), ("ndim", I32), ("ghost", I32),
+                ("system", I32), ("form", I32), ("reversed", I32), ("limiter", I32),
+                ("variant", I32), ("flags", I32),
+                ("dt", D), ("dtdx", D), ("dtdy", D), ("gravity", D), ("stream", P), ("prefill", AdjGhostPlanFillArgs)]
+
+
+class AdjPhysArgs(C.Structure):
+    _fields_ = [("q", P), ("patches", P), ("comp_stride", I64), ("npatch", I32), ("ndim", I32),
+                ("ghost", I32), ("m", I32), ("bc", I32 * 4), ("normal_comp", I32 * 2),
+                ("max_ghost_cells", I32), ("pad", I32), ("stream", P)]
+
+
+class AdjGhostArgs(C.Structure):
+    _fields_ = [("q_dst", P), ("q_src", P), ("q_coarse_old", P), ("q_coarse_new", P),
+                ("dst_patches", P), ("src_patches", P), ("coarse_patches", P), ("rects", P),
+                ("dst_comp_stride", I64), ("src_comp_stride", I64), ("coarse_comp_stride", I64),
+                ("nrect", I32), ("ndim", I32), ("m", I32), ("ghost_dst", I32), ("ghost_src", I32),
+                ("ratio", I32), ("origin_x", D), ("origin_y", D), ("dx_f", D), ("dy_f", D),
+                ("dx_c", D), ("dy_c", D), ("w_time", D), ("w_time_dev", P), ("axis_w", P), ("axis_i", P), ("time_mode", I32),
+                ("max_rect_cells", I32), ("stream", P)]
 
 
 class AdjRestrictArgs(C.Structure):
@@ -116,7 +116,7 @@ class AdjFlagArgs(C.Structure):
                 ("tolerance", D), ("stream", P)]
 
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 class AdjFunctionalArgs(C.Structure):
     _fields_ = [("q", P), ("patches", P), ("ring", P), ("finer", P), ("covered", P), ("partial", P), ("status", P),

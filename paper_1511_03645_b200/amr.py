@@ -699,6 +699,14 @@ def _fill_physical_subset(st, slots, boundary, equation, level_shape):
 USE_GHOST_PLAN = True
 # planned restriction (device.RestrictPlan, one thread per coarse cell); False: per-rect blocks
 USE_RESTRICT_PLAN = True
+# fast static-CFL levels: run the planned fill inside the step launch (prefill + grid barrier).
+# Off: measured slower on C5 (0.94-0.96 vs 0.75 ms per coarse step) -- the persistent step grid
+# has ~57K threads for ~400K gather entries, the standalone gather ~300K
+USE_FUSED_FILL = False
+
+
+def _static_fast(st, ctx) -> bool:
+    return ctx.variant == _lib.VARIANT_FAST and st.ndim == 2 and not st.any_dry() and not st.two_rows()
 
 
 class LevelPlan:
@@ -779,9 +787,12 @@ def _store_time_mode(cst, t):
     return None
 
 
-def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrContext):
+def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrContext, defer: bool = False):
     """Coarse interpolation, then same-level copies, then physical boundaries
-    (amr.py:479-491), each a batched device launch over the whole level."""
+    (amr.py:479-491), each a batched device launch over the whole level.
+    ``defer``: on the fast static-CFL path return the planned fill as step
+    prefill arguments instead of launching it (the next launch_step on this
+    level runs it; nothing may touch the level in between)."""
     patches = hierarchy.patches(level)
     if not patches:
         return
@@ -801,12 +812,17 @@ def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrC
         # level-synchronised times: coarse, copy and physical phases in one gather
         gp = pl.gather(hierarchy, level, ctx)
         if gp is not None:
+            if defer and USE_FUSED_FILL and gp.n and _static_fast(st, ctx):
+                args = (gp.fill_args(st, old_buf, cst.buf[cst.cur], cst, mw[1], mw[0]) if coarse_in
+                        else gp.fill_args(st))
+                st.ghost_src = st.cur
+                return args
             if coarse_in:
                 gp.fill(st, old_buf, cst.buf[cst.cur], cst, mw[1], mw[0])
             else:
                 gp.fill(st)
             st.ghost_src = st.cur
-            return
+            return None
     if coarse_in:
         r = hierarchy.ratio_to_finer(level - 1)
         if mw is not None:
@@ -1019,7 +1035,7 @@ def _retry_half_steps(st, slot, patch, dt, ctx):
     del torch
 
 
-def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext):
+def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext, prefill=None):
     """save_old + step of every patch of the level in one K1 launch, with the
     reference's per-patch CFL retry and cell-step accounting (amr.py:620-631).
 
@@ -1034,7 +1050,10 @@ def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext
     st.set_level_times(t, t)
     out = st._free(st.cur)
     static = ctx.variant == _lib.VARIANT_FAST and st.ndim == 2 and not st.any_dry()
-    smax, bad = device.launch_step(st, dt, ctx.equation, ctx.limiter, ctx.variant, out, accumulate=static)
+    if prefill is not None and not static:
+        raise RuntimeError("a deferred ghost fill needs the fast static-CFL step")
+    smax, bad = device.launch_step(st, dt, ctx.equation, ctx.limiter, ctx.variant, out, accumulate=static,
+                                   prefill=prefill)
     spec = patches[0].spec
     dtdx = dt / spec.dx
     dtdy = dt / spec.dy if spec.ndim == 2 else 0.0
@@ -1095,8 +1114,8 @@ def _advance(hierarchy, level, dt, ctx):
     if not patches:
         return
     t = patches[0].time
-    fill_level_ghosts(hierarchy, level, t, ctx)
-    step_level(hierarchy, level, dt, ctx)
+    pre = fill_level_ghosts(hierarchy, level, t, ctx, defer=True)
+    step_level(hierarchy, level, dt, ctx, prefill=pre)
     t_new = t + dt
     st = patches[0]._store
     st.set_level_times(t_new, t)

@@ -73,6 +73,16 @@ int adj_step_level(const AdjStepArgs* a) {
     if (a->ndim == 2 && a->system == ADJ_SYS_AC1D) return adj::bad("2D requires a 2D system");
     if (a->limiter < ADJ_LIM_NONE || a->limiter > ADJ_LIM_SUPERBEE) return adj::bad("limiter");
     if (!(a->dt > 0.0)) return adj::bad("dt must be positive");
+    if (a->prefill.plan.n > 0) {
+        if (!(a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed && (a->flags & ADJ_STEP_COUNTER_ZERO) &&
+              !(a->flags & ADJ_STEP_TWO_ROWS)))
+            return adj::bad("prefill needs the FAST 2D static-CFL path with ADJ_STEP_COUNTER_ZERO");
+        if (a->prefill.q != a->q_in || a->prefill.ndim != 2 || a->prefill.m != 3)
+            return adj::bad("prefill must fill q_in (2D, m = 3)");
+        if (!(a->prefill.plan.dst && a->prefill.plan.src && a->prefill.plan.meta)) return adj::bad("null prefill plan");
+        if (a->prefill.plan.nc > 0 && !(a->prefill.q_coarse_old && a->prefill.q_coarse_new && a->prefill.plan.c_base))
+            return adj::bad("null prefill coarse state");
+    }
     cudaStream_t st = (cudaStream_t)a->stream;
     int rc = ADJ_OK;
     const bool static_cfl = a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed;

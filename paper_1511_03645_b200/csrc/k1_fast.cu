@@ -52,13 +52,109 @@ namespace fast {
 constexpr unsigned FULL = 0xffffffffu;
 
 // ADJ_STEP_COUNTER_ZERO: the last warp to leave the job queue zeroes it (and
-// the exit count) for the next launch, so no memset precedes a launch.
+// the exit count, and the prefill barrier) for the next launch, so no memset
+// precedes a launch.
 ADJ_D void release_counter(const AdjStepArgs& a, int lane, int warps) {
     if (!(a.flags & ADJ_STEP_COUNTER_ZERO) || lane != 0) return;
     if (atomicAdd(a.work_counter + 1, 1) == warps - 1) {
         a.work_counter[0] = 0;
         a.work_counter[1] = 0;
+        if (a.prefill.plan.n > 0) a.work_counter[2] = 0;
     }
+}
+
+// ---- prefill: the level's planned ghost fill inside the step launch.
+// Same entries and arithmetic as k2_gather (k2_ghost.cu, -fmad=false):
+// unfused _rn multiplies / adds keep the values bitwise; loads bypass L1
+// (ld.global.cg) so the step phase's cached loads never see a stale line.
+ADJ_D double ip2(const double* p, int di, int dj, double wx, double wy) {
+    const double ux = __dsub_rn(1.0, wx), uy = __dsub_rn(1.0, wy);
+    double s = __dmul_rn(__dmul_rn(__ldcg(p), ux), uy);
+    s = __dadd_rn(s, __dmul_rn(__dmul_rn(__ldcg(p + di), wx), uy));
+    s = __dadd_rn(s, __dmul_rn(__dmul_rn(__ldcg(p + dj), ux), wy));
+    return __dadd_rn(s, __dmul_rn(__dmul_rn(__ldcg(p + di + dj), wx), wy));
+}
+
+ADJ_D void prefill_gather(const AdjGhostPlanFillArgs& a) {
+    double wt = a.w_time;
+    int tmode = a.time_mode;
+    if (a.w_time_dev) {           // graph replays: negative weight = old state only
+        wt = __ldcg(a.w_time_dev);
+        tmode = wt < 0.0 ? 0 : 1;
+    }
+    const int64_t cs = a.comp_stride, ccs = a.coarse_comp_stride;
+    const int n = a.plan.n, nc = a.plan.nc;
+    constexpr int U = 4;          // entries per thread in flight (the persistent grid is small)
+    const int stride = gridDim.x * blockDim.x;
+    for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < n; t0 += U * stride) {
+        int dst[U], src[U], cb[U], step[U];
+        unsigned meta[U];
+        double wx[U], wy[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + u * stride;
+            const bool ok = t < n;
+            const int tt = ok ? t : 0;
+            dst[u] = ok ? __ldcg(a.plan.dst + tt) : -1;
+            src[u] = __ldcg(a.plan.src + tt);
+            meta[u] = ok ? __ldcg(a.plan.meta + tt) : 0u;
+            const int ci = tt < nc ? tt : 0;
+            cb[u] = nc ? __ldcg(a.plan.c_base + ci) : 0;
+            step[u] = nc ? __ldcg(a.plan.c_step + ci) : 0;
+            wx[u] = nc ? __ldcg(a.plan.c_wx + ci) : 0.0;
+            wy[u] = nc ? __ldcg(a.plan.c_wy + ci) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + u * stride;
+            if ((meta[u] & 1u) && t >= nc) {     // physical cell mirroring a coarse-interpolated ghost
+                const int c0 = src[u];
+                cb[u] = __ldcg(a.plan.c_base + c0); step[u] = __ldcg(a.plan.c_step + c0);
+                wx[u] = __ldcg(a.plan.c_wx + c0); wy[u] = __ldcg(a.plan.c_wy + c0);
+            }
+        }
+        double v[U][3];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (meta[u] & 1u) {
+                const int di = step[u] & 0x3fffffff, dj = (int)((unsigned)step[u] >> 30);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double vo = tmode != 2 ? ip2(a.q_coarse_old + c * ccs + cb[u], di, dj, wx[u], wy[u]) : 0.0;
+                    const double vn = tmode != 0 ? ip2(a.q_coarse_new + c * ccs + cb[u], di, dj, wx[u], wy[u]) : 0.0;
+                    v[u][c] = tmode == 0 ? vo
+                            : (tmode == 2 ? vn : __dadd_rn(__dmul_rn(__dsub_rn(1.0, wt), vo), __dmul_rn(wt, vn)));
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) v[u][c] = dst[u] >= 0 ? __ldcg(a.q + c * cs + src[u]) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (dst[u] < 0) continue;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                a.q[c * cs + dst[u]] = (meta[u] >> (1 + c)) & 1u ? __dmul_rn(v[u][c], -1.0) : v[u][c];
+        }
+    }
+}
+
+// Software grid barrier: the persistent grid is sized to be co-resident.
+ADJ_D void grid_barrier(int* counter, int nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(counter, 1);
+        for (;;) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+            if (v >= nblocks) break;
+            __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
 }
 
 ADJ_D double rcp(double x) {  // x > 0, normal: MUFU seed + one cubic Newton step
@@ -464,6 +560,10 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
     const int warp = threadIdx.x >> 5;
     pdl_wait();
     pdl_trigger();
+    if (!CFL && a.prefill.plan.n > 0) {      // the level's ghost fill, then every CTA waits for it
+        prefill_gather(a.prefill);
+        grid_barrier(a.work_counter + 2, gridDim.x);
+    }
     // persistent warps: pull strip tiles from a global queue until empty
     const int njob = a.job_offsets ? a.njob : a.ntile;
     for (;;) {

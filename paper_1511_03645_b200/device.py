@@ -770,6 +770,30 @@ class GhostPlan:
         lim = 2 ** 31 - 1
         return store.plane < lim and (coarse_store is None or coarse_store.plane < lim)
 
+    def fill_args(self, store: LevelStore, q_old=None, q_new=None, coarse_store=None, w_time=0.0, mode=0,
+                  stream=None):
+        """The fill as an argument struct (for a standalone launch or a step
+        prefill); takes the captured-sweep weight slot like fill()."""
+        wptr = 0
+        if PARAMS is not None and self.nc:      # captured sweep: weight read from device memory
+            if mode == 2:
+                raise RuntimeError("coarse patches without saved state cannot be graph-replayed")
+            wptr = PARAMS.take(w_time if mode == 1 else -1.0)
+        a = _lib.AdjGhostPlanFillArgs()
+        a.plan = self.plan
+        a.q = _ptr(store.buf[store.cur])
+        a.q_coarse_old = _ptr(q_old)
+        a.q_coarse_new = _ptr(q_new)
+        a.comp_stride = store.plane
+        a.coarse_comp_stride = coarse_store.plane if coarse_store is not None else 0
+        a.ndim = store.ndim
+        a.m = store.m
+        a.time_mode = mode
+        a.w_time = w_time
+        a.w_time_dev = wptr
+        a.stream = _lib.stream_ptr(stream)
+        return a
+
     def fill(self, store: LevelStore, q_old=None, q_new=None, coarse_store=None, w_time=0.0, mode=0, stream=None):
         wptr = 0
         if PARAMS is not None and self.nc:      # captured sweep: weight read from device memory
@@ -835,7 +859,7 @@ def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=Non
 
 
 def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index, stream=None,
-                accumulate=False):
+                accumulate=False, prefill=None):
     """K1 on every patch: reads buf[cur], writes buf[out_buf_index].
     Returns (speed_max (npatch, 2) tensor, nonfinite (npatch,) tensor).
     ``accumulate`` (static-CFL fast path only): no per-launch memsets; the
@@ -856,7 +880,7 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
         bad = store.nonfinite_acc
     else:
         bad = store.scratch("nonfinite", npatch, torch.int32)
-    counter = store.scratch("work_counter", 2, torch.int32)   # zero; kept zero by the FAST kernel
+    counter = store.scratch("work_counter", 4, torch.int32)   # zero; kept zero by the FAST kernel
     if SHADOW:
         return smax[: 2 * npatch].view(npatch, 2), bad[:npatch]
     system, form, rev = equation.kernel_spec()
@@ -892,6 +916,8 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     a.dtdy = dt / spec0.dy if store.ndim == 2 else 0.0
     a.gravity = equation.gravity
     a.stream = _lib.stream_ptr(stream)
+    if prefill is not None:
+        a.prefill = prefill
     _lib.check(_lib.lib().adj_step_level(_lib.C.byref(a)), "adj_step_level")
     return smax[: 2 * npatch].view(npatch, 2), bad[:npatch]
 

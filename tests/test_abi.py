@@ -57,7 +57,7 @@ def _struct_fields(name):
     body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
     fields = []
     typewords = {"const", "unsigned", "long", "double", "int32_t", "int64_t", "uint32_t", "uint8_t", "void", "char",
-                 "AdjPatch", "AdjTile", "AdjRect", "AdjGhostPlan", "AdjGauge"}
+                 "AdjPatch", "AdjTile", "AdjRect", "AdjGhostPlan", "AdjGauge", "AdjGhostPlanFillArgs"}
     for decl in body.split(";"):
         toks = decl.replace("*", " ").replace(",", " , ").split()
         if not toks:

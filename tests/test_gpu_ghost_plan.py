@@ -91,3 +91,25 @@ def test_planned_restrict_equals_rect_restrict(name):
         assert torch.equal(outs[0], outs[1]), (name, lev, int((outs[0] != outs[1]).sum()))
         done += 1
     assert done
+
+
+@pytest.mark.parametrize("name", ["ac2d_adjoint", "ac2d_hetero", "ac2d_everywhere"])
+def test_fused_fill_equals_separate_fill(name):
+    """The planned fill run inside the step launch (prefill + grid barrier)
+    gives bitwise the states of the separate gather launch (FAST variant,
+    several coarse steps incl. regrids)."""
+    from paper_1511_03645_b200 import _lib, amr
+    from tests.test_gpu_amr import run
+    outs = []
+    for fused in (False, True):
+        old = amr.USE_FUSED_FILL
+        amr.USE_FUSED_FILL = fused
+        try:
+            outs.append(run(name, _lib.VARIANT_FAST))
+        finally:
+            amr.USE_FUSED_FILL = old
+    for step, (a, b) in enumerate(zip(*outs)):
+        assert a["nlev"] == b["nlev"] and a["flagged"] == b["flagged"]
+        for lev in range(1, a["nlev"] + 1):
+            assert np.array_equal(a[f"L{lev}_boxes"], b[f"L{lev}_boxes"])
+            assert np.array_equal(a[f"L{lev}_q"], b[f"L{lev}_q"]), (name, step, lev)
