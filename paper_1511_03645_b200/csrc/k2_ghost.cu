@@ -8,6 +8,7 @@
 //   interpolate_patch / _axis_weights           geometry.py:248-260, 302-327
 //   restrict_fine_to_coarse                     amr.py:399-450
 #include "adj_common.cuh"
+#include <stdlib.h>
 
 namespace adj {
 
@@ -306,7 +307,7 @@ ADJ_D double interp_at(const double* p, int di, int dj, double wx, double wy) {
     return p[0] * (1.0 - wx) + p[di] * wx;
 }
 
-template <int NDIM, int M>
+template <int NDIM, int M, int U>
 __global__ void __launch_bounds__(256) k2_gather(AdjGhostPlanFillArgs a) {
     pdl_wait();
     pdl_trigger();
@@ -318,49 +319,91 @@ __global__ void __launch_bounds__(256) k2_gather(AdjGhostPlanFillArgs a) {
     }
     const int64_t cs = a.comp_stride, ccs = a.coarse_comp_stride;
     const int n = a.plan.n, nc = a.plan.nc;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        // rect COARSE entries [0, nc) own coarse entry t: load it alongside the plan entry
-        const bool spec = t < nc;
-        int cb = 0, step = 0;
-        double wx = 0.0, wy = 0.0;
-        if (spec) { cb = a.plan.c_base[t]; step = a.plan.c_step[t]; wx = a.plan.c_wx[t]; wy = a.plan.c_wy[t]; }
-        const int dst = a.plan.dst[t], src = a.plan.src[t];
-        const unsigned meta = a.plan.meta[t];
-        double v[M];
-        if (meta & 1u) {
-            if (!spec) {          // physical cell mirroring a coarse-interpolated ghost
-                cb = a.plan.c_base[src]; step = a.plan.c_step[src]; wx = a.plan.c_wx[src]; wy = a.plan.c_wy[src];
-            }
-            const int di = step & 0x3fffffff, dj = (int)((unsigned)step >> 30);
+    const int stride = gridDim.x * blockDim.x;
+    // U entries per thread with all their loads issued before any use
+    for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < n; t0 += U * stride) {
+        int dst[U], src[U], cb[U], step[U];
+        unsigned meta[U];
+        double wx[U], wy[U];
 #pragma unroll
-            for (int c = 0; c < M; ++c) {
-                const double* po = a.q_coarse_old + c * ccs + cb;
-                const double* pn = a.q_coarse_new + c * ccs + cb;
-                const double vo = tmode != 2 ? interp_at<NDIM>(po, di, dj, wx, wy) : 0.0;
-                const double vn = tmode != 0 ? interp_at<NDIM>(pn, di, dj, wx, wy) : 0.0;
-                v[c] = tmode == 0 ? vo : (tmode == 2 ? vn : (1.0 - wt) * vo + wt * vn);
-            }
-        } else {
-#pragma unroll
-            for (int c = 0; c < M; ++c) v[c] = a.q[c * cs + src];
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + u * stride;
+            const bool ok = t < n;
+            const int tt = ok ? t : 0;
+            dst[u] = ok ? a.plan.dst[tt] : -1;
+            src[u] = a.plan.src[tt];
+            meta[u] = ok ? a.plan.meta[tt] : 0u;
+            // rect COARSE entries [0, nc) own coarse entry t: load it alongside the plan entry
+            const int ci = tt < nc ? tt : 0;
+            cb[u] = nc ? a.plan.c_base[ci] : 0;
+            step[u] = nc ? a.plan.c_step[ci] : 0;
+            wx[u] = nc ? a.plan.c_wx[ci] : 0.0;
+            wy[u] = nc ? a.plan.c_wy[ci] : 0.0;
         }
 #pragma unroll
-        for (int c = 0; c < M; ++c) a.q[c * cs + dst] = (meta >> (1 + c)) & 1u ? v[c] * -1.0 : v[c];
+        for (int u = 0; u < U; ++u) {
+            if ((meta[u] & 1u) && t0 + u * stride >= nc) {   // physical cell mirroring a coarse-interpolated ghost
+                const int c0 = src[u];
+                cb[u] = a.plan.c_base[c0]; step[u] = a.plan.c_step[c0];
+                wx[u] = a.plan.c_wx[c0]; wy[u] = a.plan.c_wy[c0];
+            }
+        }
+        double v[U][M];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (meta[u] & 1u) {
+                const int di = step[u] & 0x3fffffff, dj = (int)((unsigned)step[u] >> 30);
+#pragma unroll
+                for (int c = 0; c < M; ++c) {
+                    const double* po = a.q_coarse_old + c * ccs + cb[u];
+                    const double* pn = a.q_coarse_new + c * ccs + cb[u];
+                    const double vo = tmode != 2 ? interp_at<NDIM>(po, di, dj, wx[u], wy[u]) : 0.0;
+                    const double vn = tmode != 0 ? interp_at<NDIM>(pn, di, dj, wx[u], wy[u]) : 0.0;
+                    v[u][c] = tmode == 0 ? vo : (tmode == 2 ? vn : (1.0 - wt) * vo + wt * vn);
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < M; ++c) v[u][c] = dst[u] >= 0 ? a.q[c * cs + src[u]] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (dst[u] < 0) continue;
+#pragma unroll
+            for (int c = 0; c < M; ++c) a.q[c * cs + dst[u]] = (meta[u] >> (1 + c)) & 1u ? v[u][c] * -1.0 : v[u][c];
+        }
     }
+}
+
+static int gather_batch() {
+    static int u = -1;
+    if (u < 0) {
+        const char* e = getenv("ADJAMR_GATHER_U");
+        u = (e && (e[0] == '1' || e[0] == '2' || e[0] == '4')) ? e[0] - '0' : 2;   // 2: measured best on C5
+    }
+    return u;
+}
+
+template <int NDIM, int M>
+static void launch_gather(const AdjGhostPlanFillArgs& a, cudaStream_t st) {
+    const int U = gather_batch();
+    int blocks = (a.plan.n + 256 * U - 1) / (256 * U);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    const dim3 g(blocks), b(256);
+    if (U == 4) launch_pdl(k2_gather<NDIM, M, 4>, g, b, 0, st, a);
+    else if (U == 2) launch_pdl(k2_gather<NDIM, M, 2>, g, b, 0, st, a);
+    else launch_pdl(k2_gather<NDIM, M, 1>, g, b, 0, st, a);
 }
 
 int fill_ghost_plan(const AdjGhostPlanFillArgs& a) {
     if (a.plan.n <= 0) return ADJ_OK;
-    int blocks = (a.plan.n + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
     const cudaStream_t st = (cudaStream_t)a.stream;
-    const dim3 g(blocks), b(256);
-    if (a.ndim == 2 && a.m == 3) launch_pdl(k2_gather<2, 3>, g, b, 0, st, a);
-    else if (a.ndim == 1 && a.m == 2) launch_pdl(k2_gather<1, 2>, g, b, 0, st, a);
-    else if (a.ndim == 2 && a.m == 2) launch_pdl(k2_gather<2, 2>, g, b, 0, st, a);
-    else if (a.ndim == 1 && a.m == 3) launch_pdl(k2_gather<1, 3>, g, b, 0, st, a);
-    else if (a.ndim == 1 && a.m == 1) launch_pdl(k2_gather<1, 1>, g, b, 0, st, a);
-    else if (a.ndim == 2 && a.m == 1) launch_pdl(k2_gather<2, 1>, g, b, 0, st, a);
+    if (a.ndim == 2 && a.m == 3) launch_gather<2, 3>(a, st);
+    else if (a.ndim == 1 && a.m == 2) launch_gather<1, 2>(a, st);
+    else if (a.ndim == 2 && a.m == 2) launch_gather<2, 2>(a, st);
+    else if (a.ndim == 1 && a.m == 3) launch_gather<1, 3>(a, st);
+    else if (a.ndim == 1 && a.m == 1) launch_gather<1, 1>(a, st);
+    else if (a.ndim == 2 && a.m == 1) launch_gather<2, 1>(a, st);
     else return ADJ_ERR_BAD_ARG;
     return check_launch("k2_gather");
 }
