@@ -411,6 +411,14 @@ int adj_ghost_rects(int ndim, int ghost, const int32_t* level_shape, int npatch,
                     const int32_t* hi, int ncoarse, const int32_t* clo, const int32_t* chi, int ratio,
                     int only, int disjoint, AdjRect* rects, int max_rects, int32_t* nrects, int64_t* covered);
 
+/* Host (no GPU): pairwise overlaps of dst boxes with src boxes (refined by
+ * ratio) as rectangles in dst ghost-inclusive coordinates (kind COPY adds
+ * src coordinates): the regrid fill of a new level from its parents and
+ * the old level (amr.py:504-551).  Order: dst ascending, then src. */
+int adj_box_overlaps(int ndim, int kind, int ndst, const int32_t* dlo, const int32_t* dhi, int gdst,
+                     int nsrc, const int32_t* slo, const int32_t* shi, int gsrc, int ratio,
+                     AdjRect* rects, int max_rects, int32_t* nrects);
+
 int adj_abi_version(void);
 
 #ifdef __cplusplus

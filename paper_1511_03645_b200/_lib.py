@@ -160,6 +160,8 @@ EXPORTS = {
     "adj_ghost_rects": ([C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                          C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.POINTER(I32), C.c_void_p],
                         C.c_int),
+    "adj_box_overlaps": ([C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                          C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.POINTER(I32)], C.c_int),
     "adj_cluster": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p,
                      C.c_int, C.POINTER(I32)], C.c_int),
 }

@@ -844,6 +844,15 @@ def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrC
     st.ghost_src = st.cur
 
 
+def make_patches(hierarchy: PatchHierarchy, level: int, boxes, ctx: AmrContext, time: float) -> list:
+    """make_patch for every (lo, hi) box of a regrid, materials sampled in one batch."""
+    from .solver import sample_patches_material
+    ps = [Patch(hierarchy.make_spec(level, lo, hi), ctx.equation.m, time=time) for lo, hi in boxes]
+    if ps:
+        sample_patches_material(ps, ctx.equation, ctx.boundary, hierarchy.level_shape(level))
+    return ps
+
+
 def make_patch(hierarchy: PatchHierarchy, level: int, lo, hi, ctx: AmrContext, time: float) -> Patch:
     spec = hierarchy.make_spec(level, lo, hi)
     p = Patch(spec, ctx.equation.m, time=time)
@@ -968,8 +977,8 @@ def regrid(hierarchy: PatchHierarchy, level: int, ctx: AmrContext, deepest: int 
         boxes = cluster(clipped, ctx.efficiency, max_edge=max(1, ctx.max_patch_edge // ratio))
         rects = [rb for b in boxes for rb in _allowed_rectangles(b, allowed, clipped)]
         old = hierarchy.patches(lev)
-        new = [make_patch(hierarchy, lev, tuple(l * ratio for l in rb.lo),
-                          tuple((h + 1) * ratio - 1 for h in rb.hi), ctx, t) for rb in rects]
+        new = make_patches(hierarchy, lev, [(tuple(l * ratio for l in rb.lo), tuple((h + 1) * ratio - 1 for h in rb.hi))
+                                            for rb in rects], ctx, t)
         if new:
             _fill_new_level(hierarchy, lev, new, old, parents, t)
         hierarchy.levels[lev - 1] = new
@@ -985,16 +994,16 @@ def _fill_new_level(hierarchy, lev, new, old, parents, t):
     cst.sync_in()
     cst.fold_ghosts()
     r = hierarchy.ratio_to_finer(lev - 1)
-    c_lo, c_hi = _boxes(parents)
-    cf_lo, cf_hi = c_lo * r, (c_hi + 1) * r - 1
+    g = new[0].spec.ghost_width
     groups: dict = {}
-    for k, p in enumerate(new):
-        for c in _candidates(cf_lo, cf_hi, p.spec.lo, p.spec.hi):
-            ib = _intersect(p.spec.lo, p.spec.hi, tuple(cf_lo[c]), tuple(cf_hi[c]))
-            if ib is not None:
-                ext = [h - l + 1 for l, h in zip(*ib)]
-                groups.setdefault(_coarse_time_mode(parents[c], t), []).append(
-                    _rect(_lib.RECT_COARSE, k, int(c), ib[0], p.spec, ext))
+    crects = _box_overlaps(_lib.RECT_COARSE, new, parents, g, parents[0].spec.ghost_width, r)
+    mw = _store_time_mode(cst, t)
+    if mw is not None:              # level-synchronised parents: one time mode
+        if len(crects):
+            groups[mw] = crects
+    else:
+        for row in crects.tolist():
+            groups.setdefault(_coarse_time_mode(parents[row[2]], t), []).append(row)
     old_buf = _coarse_old_buffer(cst)
     for (mode, w), rl in groups.items():
         device.coarse_rects(st, cst, device.RectTable(rl, (st, cst, hierarchy)), old_buf, cst.buf[cst.cur],
@@ -1002,16 +1011,31 @@ def _fill_new_level(hierarchy, lev, new, old, parents, t):
     if old:
         ost = level_store(old)
         ost.sync_in()
-        o_lo, o_hi = _boxes(old)
-        copies = []
-        for k, p in enumerate(new):
-            for o in _candidates(o_lo, o_hi, p.spec.lo, p.spec.hi):
-                ib = _intersect(p.spec.lo, p.spec.hi, tuple(o_lo[o]), tuple(o_hi[o]))
-                if ib is not None:
-                    ext = [h - l + 1 for l, h in zip(*ib)]
-                    copies.append(_rect(_lib.RECT_COPY, k, int(o), ib[0], p.spec, ext, ib[0], old[o].spec))
-        if copies:
-            device.copy_rects(st, ost, np.array(copies, dtype=_lib.RECT_DTYPE), ost.buf[ost.cur], st.buf[st.cur])
+        copies = _box_overlaps(_lib.RECT_COPY, new, old, g, old[0].spec.ghost_width, 1)
+        if len(copies):
+            device.copy_rects(st, ost, copies, ost.buf[ost.cur], st.buf[st.cur])
+
+
+def _box_overlaps(kind, dst, src, gdst, gsrc, ratio):
+    """Rects of every dst box's overlap with the (ratio-refined) src boxes
+    (native adj_box_overlaps; same rects, same order as the per-patch scan
+    of amr.py:504-551)."""
+    import ctypes as C
+    nd = dst[0].spec.ndim
+    dlo, dhi = (np.ascontiguousarray(a, dtype=np.int32) for a in _boxes(dst))
+    slo, shi = (np.ascontiguousarray(a, dtype=np.int32) for a in _boxes(src))
+    lib = _lib.load_library()
+    cap = max(64, 4 * len(dst) + 4 * len(src))
+    while True:
+        rects = np.zeros(cap, dtype=_lib.RECT_DTYPE)
+        n = _lib.I32()
+        rc = lib.adj_box_overlaps(nd, kind, len(dst), dlo.ctypes.data, dhi.ctypes.data, gdst, len(src),
+                                  slo.ctypes.data, shi.ctypes.data, gsrc, ratio, rects.ctypes.data, cap, C.byref(n))
+        if rc == 0:
+            return rects[: n.value]
+        if n.value <= cap:
+            raise ValueError("adj_box_overlaps: bad arguments")
+        cap = n.value
 
 
 # ---------------------------------------------------------------------------

@@ -249,3 +249,62 @@ extern "C" int adj_ghost_rects(int ndim, int ghost, const int32_t* level_shape, 
     *nrects = n;
     return overflow ? ADJ_ERR_BAD_ARG : ADJ_OK;
 }
+
+// Pairwise overlaps of dst boxes with (optionally refined) src boxes, as
+// rectangles in dst ghost-inclusive coordinates (COPY: also src
+// coordinates) -- the regrid fill of a new level from its parents (COARSE,
+// src boxes refined by `ratio`) and from the old level (COPY),
+// amr.py:504-551.  Order: dst ascending, then src ascending.
+extern "C" int adj_box_overlaps(int ndim, int kind, int ndst, const int32_t* dlo, const int32_t* dhi, int gdst,
+                                int nsrc, const int32_t* slo, const int32_t* shi, int gsrc, int ratio,
+                                AdjRect* rects, int max_rects, int32_t* nrects) {
+    if ((ndim != 1 && ndim != 2) || ndst < 0 || nsrc < 0 || ratio < 1 || !nrects || (max_rects > 0 && !rects) ||
+        (ndst && (!dlo || !dhi)) || (nsrc && (!slo || !shi)))
+        return ADJ_ERR_BAD_ARG;
+    const int nd = ndim;
+    std::vector<Box> dst(ndst), src(nsrc), orig(nsrc);
+    int ex = 1, ey = 1;
+    for (int k = 0; k < ndst; ++k)
+        for (int d = 0; d < 2; ++d) {
+            dst[k].lo[d] = d < nd ? dlo[k * nd + d] : 0;
+            dst[k].hi[d] = d < nd ? dhi[k * nd + d] : 0;
+        }
+    for (int c = 0; c < nsrc; ++c)
+        for (int d = 0; d < 2; ++d) {
+            orig[c].lo[d] = d < nd ? slo[c * nd + d] : 0;
+            orig[c].hi[d] = d < nd ? shi[c * nd + d] : 0;
+            src[c].lo[d] = d < nd ? orig[c].lo[d] * ratio : 0;
+            src[c].hi[d] = d < nd ? (orig[c].hi[d] + 1) * ratio - 1 : 0;
+            ex = std::max(ex, src[c].hi[0] + 1);
+            if (nd == 2) ey = std::max(ey, src[c].hi[1] + 1);
+        }
+    for (const Box& b : dst) { ex = std::max(ex, b.hi[0] + 1); if (nd == 2) ey = std::max(ey, b.hi[1] + 1); }
+    Index idx;
+    idx.build(src, nd, ex, ey);
+    std::vector<int> cand;
+    int n = 0;
+    bool overflow = false;
+    for (int k = 0; k < ndst; ++k) {
+        idx.query(dst[k], cand);
+        for (int c : cand) {
+            Box ib;
+            if (!intersect(dst[k], src[c], nd, ib)) continue;
+            if (n >= max_rects) { overflow = true; ++n; continue; }
+            AdjRect& r = rects[n++];
+            memset(&r, 0, sizeof(r));
+            r.kind = kind;
+            r.dst_patch = k;
+            r.src_patch = c;
+            r.di0 = ib.lo[0] - (dst[k].lo[0] - gdst);
+            r.ni = ib.hi[0] - ib.lo[0] + 1;
+            r.nj = nd == 2 ? ib.hi[1] - ib.lo[1] + 1 : 1;
+            if (nd == 2) r.dj0 = ib.lo[1] - (dst[k].lo[1] - gdst);
+            if (kind == ADJ_RECT_COPY) {
+                r.si0 = ib.lo[0] - (orig[c].lo[0] - gsrc);
+                if (nd == 2) r.sj0 = ib.lo[1] - (orig[c].lo[1] - gsrc);
+            }
+        }
+    }
+    *nrects = n;
+    return overflow ? ADJ_ERR_BAD_ARG : ADJ_OK;
+}

@@ -105,20 +105,26 @@ class LevelStore:
             raise ValueError("patches of one store must share ghost width and dimension")
         self.m = patches[0].num_components
         self.naux = len(patches[0].aux.planes())
+        # patch table, vectorised: boxes of nx+2g rows x pitch, each 32-element aligned
+        nd, g = self.ndim, self.g
+        lo = np.array([s.lo for s in specs], dtype=np.int64).reshape(len(specs), nd)
+        shp = np.array([s.shape for s in specs], dtype=np.int64).reshape(len(specs), nd)
+        nx = shp[:, 0]
+        ny = shp[:, 1] if nd == 2 else np.ones_like(nx)
+        NXa = nx + 2 * g
+        NYa = ny + 2 * g if nd == 2 else np.ones_like(nx)
+        pitch_a = (NYa + 3) // 4 * 4 if nd == 2 else np.ones_like(nx)
+        size = (NXa * pitch_a + 31) // 32 * 32
+        offs = np.cumsum(size) - size
+        words = (nx * ny + 31) // 32
+        fws = np.cumsum(words) - words
         tab = np.zeros(len(specs), dtype=_lib.PATCH_DTYPE)
-        off = 0
-        fw = 0
-        self.boxes = []
-        for k, s in enumerate(specs):
-            nx = s.shape[0]
-            ny = s.shape[1] if self.ndim == 2 else 1
-            NX = nx + 2 * self.g
-            NY = ny + 2 * self.g if self.ndim == 2 else 1
-            pitch = (NY + 3) // 4 * 4 if self.ndim == 2 else 1
-            tab[k] = (off, fw, nx, ny, pitch, s.lo[0], s.lo[1] if self.ndim == 2 else 0, 0, 0, 0)
-            self.boxes.append((off, NX, NY, pitch))
-            off += (NX * pitch + 31) // 32 * 32
-            fw += (nx * ny + 31) // 32
+        tab["offset"], tab["flag_word"], tab["nx"], tab["ny"], tab["pitch"] = offs, fws, nx, ny, pitch_a
+        tab["lo_x"] = lo[:, 0]
+        tab["lo_y"] = lo[:, 1] if nd == 2 else 0
+        self.boxes = list(zip(offs.tolist(), NXa.tolist(), NYa.tolist(), pitch_a.tolist()))
+        off = int(size.sum())
+        fw = int(words.sum())
         self.plane = off + _SLACK
         self.flag_words = fw
         self.table_np = tab
@@ -139,19 +145,27 @@ class LevelStore:
         self.time_synced = False
         self.level_time = 0.0
         self.level_time_old = None
-        self.total_cells = int(sum(int(np.prod(p.spec.shape)) for p in patches))
-        self.max_ghost_cells = max(NX_ * NY_ - (NX_ - 2 * self.g) * (NY_ - 2 * self.g if self.ndim == 2 else NY_)
-                                   for (_, NX_, NY_, _) in self.boxes)
+        self.total_cells = int((nx * ny).sum())
+        self.max_ghost_cells = int((NXa * NYa - nx * ny).max())
         self._phys_args = {}
         self.nonfinite_acc = None
         # material planes of every patch assembled on the host, one upload
         host_aux = np.zeros(self.naux * self.plane, dtype=np.float64)
-        for k, p in enumerate(patches):
-            off, NX, NY, pitch = self.boxes[k]
-            v = np.lib.stride_tricks.as_strided(host_aux[off:], (self.naux, NX, NY), (8 * self.plane, 8 * pitch, 8),
-                                                writeable=True)
-            for a, pl in enumerate(p.aux.planes()):
-                v[a] = np.asarray(pl, dtype=float).reshape(NX, NY)
+        if len({(b[1], b[2], b[3]) for b in self.boxes}) == 1:
+            # one box shape (e.g. uniform 32^2 patches): one scatter for all patches
+            _, NX0, NY0, P0 = self.boxes[0]
+            stacked = np.stack([np.stack([np.asarray(pl, dtype=float).reshape(NX0, NY0) for pl in p.aux.planes()])
+                                for p in patches])                          # (npatch, naux, NX, NY)
+            cell = (np.arange(NX0)[:, None] * P0 + np.arange(NY0)[None, :]).reshape(-1)
+            dst = (np.arange(self.naux)[None, :, None] * self.plane + offs[:, None, None] + cell[None, None, :])
+            host_aux[dst.reshape(-1)] = stacked.reshape(-1)
+        else:
+            for k, p in enumerate(patches):
+                off_k, NX, NY, pitch = self.boxes[k]
+                v = np.lib.stride_tricks.as_strided(host_aux[off_k:], (self.naux, NX, NY),
+                                                    (8 * self.plane, 8 * pitch, 8), writeable=True)
+                for a, pl in enumerate(p.aux.planes()):
+                    v[a] = np.asarray(pl, dtype=float).reshape(NX, NY)
         self.aux.copy_(torch.from_numpy(host_aux))
         for k, p in enumerate(patches):
             self._attach(p, k, upload=False)

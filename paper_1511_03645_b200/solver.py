@@ -125,6 +125,62 @@ def sample_patch_material(patch: Patch, equation: EquationSet, boundary: Boundar
     return patch.aux
 
 
+def _finish_material(patch, mat_cls, arrays, others, boundary, level_shape):
+    spec = patch.spec
+    g = spec.ghost_width
+    for axis in range(spec.ndim):
+        for high in (False, True):
+            at_edge = spec.hi[axis] == level_shape[axis] - 1 if high else spec.lo[axis] == 0
+            if at_edge:
+                wall = boundary.side(axis, high) == "wall"
+                for arr in arrays.values():
+                    _fix_aux_ghosts(arr, axis, high, g, wall)
+    patch.aux = mat_cls(**arrays, **others)
+
+
+def sample_patches_material(patches, equation: EquationSet, boundary: BoundarySpec, level_shape: tuple[int, ...]):
+    """sample_patch_material for many new patches of one level.  When they
+    share a shape the material model is called once on the stacked
+    cell-centre arrays; each patch's values are then those of its own call
+    (verified exactly against a per-patch call on the first patch; any
+    difference or error falls back to one call per patch)."""
+    P = len(patches)
+    if P < 4 or len({p.spec.shape for p in patches}) != 1 or any(p._store is not None for p in patches):
+        for p in patches:
+            sample_patch_material(p, equation, boundary, level_shape)
+        return
+    nd = patches[0].spec.ndim
+    cs = [p.spec.cell_centers(include_ghost=True) for p in patches]
+    try:
+        if nd == 1:
+            mat = equation.sample_material(np.stack([c[0] for c in cs]))
+            mat0 = equation.sample_material(cs[0][0])
+        else:
+            NX, NY = len(cs[0][0]), len(cs[0][1])
+            X = np.repeat(np.stack([c[0] for c in cs])[:, :, None], NY, axis=2)
+            Y = np.repeat(np.stack([c[1] for c in cs])[:, None, :], NX, axis=1)
+            mat = equation.sample_material(X, Y)
+            xx, yy = np.meshgrid(cs[0][0], cs[0][1], indexing="ij")
+            mat0 = equation.sample_material(xx, yy)
+        names = _field_names(type(mat))
+        arr_names = [n for n in names if isinstance(getattr(mat0, n), np.ndarray)]
+        ok = type(mat0) is type(mat) and all(
+            isinstance(getattr(mat, n), np.ndarray) and getattr(mat, n).shape == (P, *getattr(mat0, n).shape)
+            and np.array_equal(getattr(mat, n)[0], getattr(mat0, n)) for n in arr_names)
+        ok = ok and all(getattr(mat, n) == getattr(mat0, n) for n in names if n not in arr_names)
+    except Exception:
+        ok = False
+    if not ok:
+        for p in patches:
+            sample_patch_material(p, equation, boundary, level_shape)
+        return
+    others = {n: getattr(mat, n) for n in names if n not in arr_names}
+    fields = {n: getattr(mat, n) for n in arr_names}
+    for k, p in enumerate(patches):
+        _finish_material(p, type(mat), {n: np.array(f[k], copy=True) for n, f in fields.items()}, others, boundary,
+                         level_shape)
+
+
 # ---------------------------------------------------------------------------
 # store helpers
 

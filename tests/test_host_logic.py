@@ -2,7 +2,7 @@
 import numpy as np
 import pytest
 
-from paper_1511_03645_b200 import amr
+from paper_1511_03645_b200 import _lib, amr
 from paper_1511_03645_b200.geometry import Patch, PatchHierarchy, allowed_region_mask
 from tests.golden_io import load
 
@@ -120,3 +120,69 @@ def test_native_ghost_rects_equal_python(nd):
                     assert a[0] == b[0]
                     assert a[1] == b[1]
                     assert np.array_equal(a[2], b[2])
+
+
+@pytest.mark.parametrize("nd", [1, 2])
+def test_native_box_overlaps_equal_python_scan(nd):
+    """adj_box_overlaps gives the rects (and order) of the per-patch scan of
+    the regrid fill (amr.py:504-551): parents refined by the ratio (COARSE)
+    and old patches (COPY)."""
+    rng = np.random.default_rng(11 + nd)
+    for _ in range(6):
+        h = _random_hierarchy(rng, nd)
+        parents, new = h.patches(1), h.patches(2)
+        g = new[0].spec.ghost_width
+        r = h.ratio_to_finer(1)
+        got = amr._box_overlaps(_lib.RECT_COARSE, new, parents, g, g, r).tolist()
+        c_lo, c_hi = amr._boxes(parents)
+        cf_lo, cf_hi = c_lo * r, (c_hi + 1) * r - 1
+        want = []
+        for k, p in enumerate(new):
+            for c in amr._candidates(cf_lo, cf_hi, p.spec.lo, p.spec.hi):
+                ib = amr._intersect(p.spec.lo, p.spec.hi, tuple(cf_lo[c]), tuple(cf_hi[c]))
+                if ib is not None:
+                    ext = [hh - ll + 1 for ll, hh in zip(*ib)]
+                    want.append(amr._rect(_lib.RECT_COARSE, k, int(c), ib[0], p.spec, ext))
+        assert got == want
+        old = [Patch(h.make_spec(2, b.lo, b.hi), 3 if nd == 2 else 2)
+               for b in amr.cluster(rng.random(tuple(h.level_shape(2))) < 0.2, 0.6, max_edge=10)]
+        got = amr._box_overlaps(_lib.RECT_COPY, new, old, g, g, 1).tolist()
+        o_lo, o_hi = amr._boxes(old)
+        want = []
+        for k, p in enumerate(new):
+            for o in amr._candidates(o_lo, o_hi, p.spec.lo, p.spec.hi):
+                ib = amr._intersect(p.spec.lo, p.spec.hi, tuple(o_lo[o]), tuple(o_hi[o]))
+                if ib is not None:
+                    ext = [hh - ll + 1 for ll, hh in zip(*ib)]
+                    want.append(amr._rect(_lib.RECT_COPY, k, int(o), ib[0], p.spec, ext, ib[0], old[o].spec))
+        assert got == want
+
+
+def test_batched_material_sampling_equals_per_patch():
+    """solver.sample_patches_material (one model call on stacked cell
+    centres) gives each patch exactly sample_patch_material's aux,
+    including wall / outflow ghost treatment (solver.py:180-205)."""
+    from paper_1511_03645_b200 import equations as E, solver
+    h = PatchHierarchy(xlim=(0.0, 1.0), ylim=(0.0, 1.0), base_shape=(64, 64), ratios=[2])
+    bc = solver.BoundarySpec("wall", "outflow", "wall", "outflow")
+    eqs = (E.Acoustics2D(E.AcousticsMaterialModel(lambda x, y: 1.0 + 3.0 * (np.asarray(y) < 0.2 * np.asarray(x)),
+                                                  lambda x, y: np.where(np.asarray(y) < 0.2 * np.asarray(x), 1.0, 1.5))),
+           E.SweLinear2D(E.SweMaterialModel(lambda x, y: -50.0 + 80.0 * np.sin(3 * np.asarray(x)) * np.cos(2 * np.asarray(y)),
+                                            0.0, 9.81)))
+    boxes = [((0, 32 * k), (31, 32 * k + 31)) for k in range(4)] + [((96, 32 * k), (127, 32 * k + 31)) for k in range(4)]
+    for eq in eqs:
+        a = [Patch(h.make_spec(2, lo, hi), 3) for lo, hi in boxes]
+        b = [Patch(h.make_spec(2, lo, hi), 3) for lo, hi in boxes]
+        solver.sample_patches_material(a, eq, bc, (128, 128))
+        for p in b:
+            solver.sample_patch_material(p, eq, bc, (128, 128))
+        for pa, pb in zip(a, b):
+            assert type(pa.aux) is type(pb.aux)
+            for x, y in zip(pa.aux.planes(), pb.aux.planes()):
+                assert np.array_equal(x, y)
+    # a non-elementwise model falls back to per-patch calls
+    shape_dependent = E.Acoustics2D(E.AcousticsMaterialModel(lambda x, y: np.full(np.shape(x), 2.0 + np.asarray(x).ndim),
+                                                             lambda x, y: np.ones_like(np.asarray(x, float))))
+    a = [Patch(h.make_spec(2, lo, hi), 3) for lo, hi in boxes]
+    solver.sample_patches_material(a, shape_dependent, bc, (128, 128))
+    assert np.all(a[0].aux.bulk == 4.0)
