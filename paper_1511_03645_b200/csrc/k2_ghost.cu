@@ -35,6 +35,8 @@ ADJ_D int phys_src(int ii, int n, int g, bool lo_edge, bool hi_edge, int bc_lo, 
 }
 
 __global__ void k2_physical(AdjPhysArgs a) {
+    pdl_wait();
+    pdl_trigger();
     const AdjPatch p = a.patches[blockIdx.y];
     const int g = a.ghost;
     const int NX = p.nx + 2 * g;
@@ -77,7 +79,7 @@ int fill_physical(const AdjPhysArgs& a) {
     if (a.npatch <= 0 || a.max_ghost_cells <= 0) return ADJ_OK;
     int blocks = (a.max_ghost_cells + 255) / 256;
     if (blocks > 4096) blocks = 4096;
-    k2_physical<<<dim3(blocks, a.npatch), 256, 0, (cudaStream_t)a.stream>>>(a);
+    launch_pdl(k2_physical, dim3(blocks, a.npatch), dim3(256), 0, (cudaStream_t)a.stream, a);
     return check_launch("k2_physical");
 }
 
