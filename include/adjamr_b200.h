@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define ADJ_ABI_VERSION 3
+#define ADJ_ABI_VERSION 4
 
 /* status codes (mapped to the reference's exception classes by the host) */
 #define ADJ_OK                 0
@@ -285,6 +285,7 @@ int adj_restrict(const AdjRestrictArgs* a);
  *         adjoint.py:98-110) at each entry of interp_times, blended from
  *         snapshots interp_k[n] and interp_k[n]+1 with weight interp_w[n]
  *         (interp_k < 0: use snapshot -interp_k-1 unblended). */
+#define ADJ_FLAG_ROWS 1
 typedef struct AdjFlagArgs {
     const double* q;             /* forward level store                        */
     const double* aux;           /* forward aux (swe: depth plane 1)          */
@@ -306,6 +307,10 @@ typedef struct AdjFlagArgs {
     const int64_t* axis_off;     /* 2 per patch                                                  */
     int64_t comp_stride, aux_stride;
     int32_t npatch, ndim, m, ghost, swe, mode, nidx, nxa, nya, max_cells;
+    int32_t layout;              /* ADJ_FLAG_ROWS: every patch row is a multiple of 128 cells and
+                                    nxa, nya >= 2 (row-layout kernel for single-snapshot windows) */
+    int32_t max_rows, max_cols;  /* ADJ_FLAG_ROWS: largest patch nx, ny                            */
+    int32_t pad;
     double origin_x, origin_y, dx, dy;             /* forward level geometry   */
     double a_origin_x, a_origin_y, a_dx, a_dy;     /* adjoint grid geometry    */
     double tolerance;

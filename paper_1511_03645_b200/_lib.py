@@ -111,12 +111,14 @@ class AdjFlagArgs(C.Structure):
                 ("axis_off", P), ("comp_stride", I64), ("aux_stride", I64),
                 ("npatch", I32), ("ndim", I32), ("m", I32), ("ghost", I32), ("swe", I32),
                 ("mode", I32), ("nidx", I32), ("nxa", I32), ("nya", I32), ("max_cells", I32),
+                ("layout", I32), ("max_rows", I32), ("max_cols", I32), ("pad", I32),
                 ("origin_x", D), ("origin_y", D), ("dx", D), ("dy", D),
                 ("a_origin_x", D), ("a_origin_y", D), ("a_dx", D), ("a_dy", D),
                 ("tolerance", D), ("stream", P)]
 
 
-ABI_VERSION = 3
+ABI_VERSION = 4
+FLAG_ROWS = 1        # AdjFlagArgs.layout: ADJ_FLAG_ROWS
 
 class AdjFunctionalArgs(C.Structure):
     _fields_ = [("q", P), ("patches", P), ("ring", P), ("finer", P), ("covered", P), ("partial", P), ("status", P),

@@ -273,6 +273,222 @@ __global__ void __launch_bounds__(256) k3_flag_t(AdjFlagArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Row layout (patch rows a multiple of 32*NC cells, e.g. C3/C4 and any patch
+// of >=128-cell rows): a warp's 32*NC cells lie in one row i, so the row
+// weights are warp-uniform and each component's two adjoint rows are uniform
+// pointers; lane l's cells are columns j+32kk, whose state and column-table
+// entries sit at immediate offsets.  Every load is issued before the first
+// store.  Same per-cell arithmetic as k3_flag_t (bitwise); the adjoint axis
+// tables never give a corner past the last row/column when nxa, nya >= 2
+// (uweights clamps i0 <= n-2), which the host checks before choosing it.
+#ifndef K3_ROW_PIPE
+#define K3_ROW_PIPE 1
+#endif
+#ifndef K3_ROW_UNROLL
+#define K3_ROW_UNROLL 0   // 0: the compiler's choice
+#endif
+#ifndef K3_ROW_NC
+#define K3_ROW_NC 4
+#endif
+constexpr int K3_ROW_UNR = K3_ROW_UNROLL > 0 ? K3_ROW_UNROLL : 1;
+constexpr int RNC = K3_ROW_NC;     // cells per lane (a warp's segment is 32*RNC columns)
+constexpr int K3_ROW_WARPS = 4;   // warps per CTA
+#ifndef K3_ROW_RUN_ROWS
+#define K3_ROW_RUN_ROWS 16
+#endif
+constexpr int K3_ROW_RUN = K3_ROW_RUN_ROWS;   // rows one warp marches down (short runs: several waves, small tail)
+
+template <bool MODE1>
+#ifndef K3_ROW_MINB
+#define K3_ROW_MINB 1
+#endif
+__global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROW_MINB) k3_row(AdjFlagArgs a) {
+    // warp = one 32*RNC-column segment of K3_ROW_RUN consecutive rows.  The
+    // column tables load once; the next row's state streams into shared
+    // memory (cp.async) and its row-table entry into registers while this
+    // row is computed, so the corner loads depend on registers only, and
+    // rows sharing adjoint rows (refinement ratio >= 2) hit L1.
+    __shared__ double s_q[K3_ROW_WARPS][2][RNC * 3][32];
+    const int pidx = blockIdx.z;
+    const AdjPatch p = a.patches[pidx];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned seg = blockIdx.y * K3_ROW_WARPS + warp;          // column segment
+    const unsigned nseg = (unsigned)p.ny / (32u * RNC);
+    const unsigned r0 = blockIdx.x * K3_ROW_RUN;
+    if (seg >= nseg || r0 >= (unsigned)p.nx) return;               // warp-uniform
+    const unsigned r1 = min(r0 + K3_ROW_RUN, (unsigned)p.nx);
+    const unsigned ny = (unsigned)p.ny, j = seg * (32u * RNC) + lane;
+    const int g = a.ghost;
+    const int64_t cs = a.comp_stride;
+    const int64_t nya = a.nya;
+    const int64_t plane = (int64_t)a.nxa * nya;
+    const int k = __ldg(a.snap_index);
+    const bool interp = MODE1 && k >= 0;
+    const double* fa = a.ring + (int64_t)(k < 0 ? -k - 1 : k) * plane * 3;
+    const double w = interp ? __ldg(a.interp_w) : 0.0;
+    const int64_t rowoff = a.axis_off[2 * pidx], coloff = a.axis_off[2 * pidx + 1];
+    const double* qcol = a.q + p.offset + (int64_t)g * p.pitch + g + j;
+
+    auto prefetch = [&](unsigned i, int buf) {
+        const double* qp = qcol + (int64_t)i * p.pitch;
+#pragma unroll
+        for (int kk = 0; kk < RNC; ++kk)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_q[warp][buf][kk * 3 + cc][lane]);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(qp + cc * cs + 32 * kk)
+                             : "memory");
+            }
+    };
+    prefetch(r0, 0);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+
+    double wy[RNC], uy[RNC];
+    int j0[RNC], ja[RNC];
+#pragma unroll
+    for (int kk = 0; kk < RNC; ++kk) {
+        j0[kk] = __ldg(a.axis_i + coloff + j + 32 * kk);
+        wy[kk] = __ldg(a.axis_w + coloff + j + 32 * kk);
+        uy[kk] = 1.0 - wy[kk];
+        ja[kk] = a.axis_dry ? __ldg(a.axis_dry + coloff + j + 32 * kk) : 0;
+    }
+    auto row_epilogue = [&](unsigned i, double (&best)[RNC], unsigned long long& cnt) {
+        if (a.swe) {   // forward dry cells
+            const double* cp = a.aux + a.aux_stride + p.offset + (int64_t)(i + g) * p.pitch + (j + g);
+#pragma unroll
+            for (int kk = 0; kk < RNC; ++kk)
+                if (!(__ldg(cp + 32 * kk) > 0.0)) best[kk] = 0.0;
+        }
+        if (a.adj_wet != nullptr && a.axis_dry) {   // adjoint cell containing the centre is dry
+            const int ia = __ldg(a.axis_dry + rowoff + i);
+#pragma unroll
+            for (int kk = 0; kk < RNC; ++kk)
+                if (!a.adj_wet[(int64_t)ia * nya + ja[kk]]) best[kk] = 0.0;
+        }
+        const unsigned base = i * ny + seg * (32u * RNC);
+#pragma unroll
+        for (int kk = 0; kk < RNC; ++kk) {
+            if (a.best != nullptr) a.best[a.best_offset[pidx] + base + 32u * kk + lane] = best[kk];
+            const unsigned word = __ballot_sync(0xffffffffu, best[kk] > a.tolerance);
+            if (lane == 0) a.flag_bits[p.flag_word + ((base >> 5) + kk)] = word;
+            cnt += __popc(word);
+        }
+    };
+    int i0 = __ldg(a.axis_i + rowoff + r0);
+    double wx = __ldg(a.axis_w + rowoff + r0);
+    unsigned long long cnt = 0;
+    int buf = 0;
+#if K3_ROW_PIPE
+    if (!MODE1) {
+        // mode 0: the next row's corners load into registers as soon as this
+        // row's interpolation has consumed them, so they fly during the dot
+        // products, ballots and stores
+        double C[RNC][3][4];
+        auto corners = [&](int ii0) {
+#pragma unroll
+            for (int kk = 0; kk < RNC; ++kk)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double* q0 = fa + c * plane + (int64_t)ii0 * nya + j0[kk];
+                    C[kk][c][0] = __ldg(q0); C[kk][c][1] = __ldg(q0 + nya);
+                    C[kk][c][2] = __ldg(q0 + 1); C[kk][c][3] = __ldg(q0 + nya + 1);
+                }
+        };
+        corners(i0);
+        int i0n = r0 + 1 < r1 ? __ldg(a.axis_i + rowoff + r0 + 1) : 0;
+        double wxn = r0 + 1 < r1 ? __ldg(a.axis_w + rowoff + r0 + 1) : 0.0;
+#if K3_ROW_UNROLL > 0
+#pragma unroll K3_ROW_UNR
+#endif
+        for (unsigned i = r0; i < r1; ++i, buf ^= 1) {
+            const bool more = i + 1 < r1;
+            if (more) prefetch(i + 1, buf ^ 1);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+            const double ux = 1.0 - wx;
+            double qh[RNC][3];
+#pragma unroll
+            for (int kk = 0; kk < RNC; ++kk)
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    qh[kk][c] = C[kk][c][0] * ux * uy[kk] + C[kk][c][1] * wx * uy[kk] + C[kk][c][2] * ux * wy[kk] +
+                                C[kk][c][3] * wx * wy[kk];
+            if (more) corners(i0n);
+            const bool more2 = i + 2 < r1;
+            const int i0nn = more2 ? __ldg(a.axis_i + rowoff + i + 2) : 0;
+            const double wxnn = more2 ? __ldg(a.axis_w + rowoff + i + 2) : 0.0;
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            __syncwarp();
+            double best[RNC];
+#pragma unroll
+            for (int kk = 0; kk < RNC; ++kk) {
+                double dot = 0.0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double qc = s_q[warp][buf][kk * 3 + c][lane];
+                    dot = c == 0 ? qh[kk][c] * qc : dot + qh[kk][c] * qc;
+                }
+                best[kk] = fmax(0.0, fabs(dot));
+            }
+            __syncwarp();
+            row_epilogue(i, best, cnt);
+            wx = wxn; wxn = wxnn; i0n = i0nn;
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        if (lane == 0 && cnt) atomicAdd(&a.counts[pidx], cnt);
+        return;
+    }
+#endif
+    for (unsigned i = r0; i < r1; ++i, buf ^= 1) {
+        const bool more = i + 1 < r1;
+        if (more) prefetch(i + 1, buf ^ 1);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const int i0n = more ? __ldg(a.axis_i + rowoff + i + 1) : 0;
+        const double wxn = more ? __ldg(a.axis_w + rowoff + i + 1) : 0.0;
+
+        const double ux = 1.0 - wx;
+        double qh[RNC][3];
+#pragma unroll
+        for (int kk = 0; kk < RNC; ++kk) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double* q0 = fa + c * plane + (int64_t)i0 * nya + j0[kk];
+                const double* q1 = q0 + nya;
+                if (!interp) {
+                    qh[kk][c] = __ldg(q0) * ux * uy[kk] + __ldg(q1) * wx * uy[kk] + __ldg(q0 + 1) * ux * wy[kk] +
+                                __ldg(q1 + 1) * wx * wy[kk];
+                } else {   // interpolate_time, then the spatial stencil (k3_flag_t's order)
+                    const int64_t sb = plane * 3;
+                    const double v00 = (1.0 - w) * __ldg(q0) + w * __ldg(q0 + sb);
+                    const double v10 = (1.0 - w) * __ldg(q1) + w * __ldg(q1 + sb);
+                    const double v01 = (1.0 - w) * __ldg(q0 + 1) + w * __ldg(q0 + 1 + sb);
+                    const double v11 = (1.0 - w) * __ldg(q1 + 1) + w * __ldg(q1 + 1 + sb);
+                    qh[kk][c] = v00 * ux * uy[kk] + v10 * wx * uy[kk] + v01 * ux * wy[kk] + v11 * wx * wy[kk];
+                }
+            }
+        }
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // this row's state has landed
+        __syncwarp();
+        double best[RNC];
+#pragma unroll
+        for (int kk = 0; kk < RNC; ++kk) {
+            double dot = 0.0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double qc = s_q[warp][buf][kk * 3 + c][lane];
+                dot = c == 0 ? qh[kk][c] * qc : dot + qh[kk][c] * qc;
+            }
+            best[kk] = fmax(0.0, fabs(dot));
+        }
+        __syncwarp();                                          // buffer free for the row after next
+        row_epilogue(i, best, cnt);
+        i0 = i0n;
+        wx = wxn;
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (lane == 0 && cnt) atomicAdd(&a.counts[pidx], cnt);
+}
+
+// ---------------------------------------------------------------------------
 // 2D table path with two horizontally adjacent cells per lane: a warp covers
 // 64 consecutive cells (two flag words).  When every lane's pair lies in one
 // row with a common adjoint stencil (same j0 -- e.g. refinement ratio 4 on
@@ -444,6 +660,16 @@ static bool k3_pairs() {
     return on == 1;
 }
 
+// ADJAMR_K3_ROW=0 disables the row-layout kernel (A/B measurements)
+static bool k3_row_on() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("ADJAMR_K3_ROW");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
 int flag_adjoint(const AdjFlagArgs& a) {
     if (a.npatch <= 0 || a.max_cells <= 0) return ADJ_OK;
     const int threads = 256;
@@ -462,6 +688,13 @@ int flag_adjoint(const AdjFlagArgs& a) {
             if (k3_pairs() && a.nidx >= 2) {
                 if (m1) k3_pair<true><<<grid, threads, 0, st>>>(a);
                 else k3_pair<false><<<grid, threads, 0, st>>>(a);
+            } else if (a.nidx == 1 && (a.layout & ADJ_FLAG_ROWS) && k3_row_on()) {
+                // (row runs, column segments / warps per CTA, patches); max_rows = the tallest patch
+                const dim3 gr((unsigned)((a.max_rows + K3_ROW_RUN - 1) / K3_ROW_RUN),
+                              (unsigned)((a.max_cols / (32 * RNC) + K3_ROW_WARPS - 1) / K3_ROW_WARPS),
+                              (unsigned)a.npatch);
+                if (m1) k3_row<true><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a);
+                else k3_row<false><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a);
             } else {
                 if (m1) k3_flag_t<3, true, true><<<grid, threads, 0, st>>>(a);
                 else k3_flag_t<3, true, false><<<grid, threads, 0, st>>>(a);

@@ -1142,6 +1142,9 @@ def flag_axis_tables(store: LevelStore, ring_shape, a_origin, a_dx, a_dy, level_
     return tabs
 
 
+K3_ROW_CELLS = 128   # cells per warp of the K3 row-layout kernel (32 lanes x NC)
+
+
 def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level_origin, level_dx, level_dy,
                 snap_index, tolerance, adj_wet=None, interp_w=None, want_best=False, stream=None):
     """K3 on every patch of the store.  ring: (N, m, nxa[, nya]) float64 CUDA
@@ -1200,6 +1203,12 @@ def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level
     a.nxa = ring_shape[0]
     a.nya = ring_shape[1] if store.ndim == 2 else 1
     a.max_cells = max(ncell)
+    # row layout: whole 128-cell row segments per warp, interior adjoint corners
+    if (store.ndim == 2 and ring_shape[0] >= 2 and ring_shape[1] >= 2
+            and bool((store.table_np["ny"] % K3_ROW_CELLS == 0).all())):
+        a.layout = _lib.FLAG_ROWS
+        a.max_rows = int(store.table_np["nx"].max())
+        a.max_cols = int(store.table_np["ny"].max())
     a.origin_x = level_origin[0]
     a.origin_y = level_origin[1] if store.ndim == 2 else 0.0
     a.dx, a.dy = level_dx, level_dy

@@ -1,0 +1,98 @@
+"""K3 kernel layouts against the oracle (bitwise): the row-layout kernel
+(every patch row a multiple of 128 cells), the hoisted single-snapshot
+kernel (ragged rows) and the pair kernel (windows of >= 2 snapshots), on a
+multi-patch shallow-water level with dry forward and dry adjoint cells, in
+both window modes (adjoint.py:227-257, adjoint.py:98-110 for mode 1)."""
+import numpy as np
+import pytest
+
+from oracle import adjamr_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TIMES = np.linspace(0.0, 1.0, 6)
+NXA, NYA = 48, 100
+
+
+def _level(shapes_los, seed):
+    from paper_1511_03645_b200 import equations as E
+    from paper_1511_03645_b200.geometry import Patch, PatchHierarchy
+    rng = np.random.default_rng(seed)
+    h = PatchHierarchy(xlim=(0.0, 1.0), ylim=(0.0, 1.0), base_shape=(64, 512), ratios=[])
+    patches = []
+    for lo, shape in shapes_los:
+        spec = h.make_spec(1, lo, (lo[0] + shape[0] - 1, lo[1] + shape[1] - 1))
+        p = Patch(spec, 3)
+        G = (shape[0] + 4, shape[1] + 4)
+        depth = rng.uniform(-0.3, 1.0, G)
+        depth[depth < 0] = 0.0
+        p.aux = E.SweMaterial(bathymetry=-depth, depth=depth, wet=depth > 0, c=np.sqrt(9.81 * depth), gravity=9.81)
+        p.state = rng.standard_normal((3,) + G)
+        patches.append(p)
+    return h, patches
+
+
+def _store(seed, dry):
+    from paper_1511_03645_b200 import adjoint
+    from paper_1511_03645_b200.geometry import UniformField
+    rng = np.random.default_rng(seed)
+    vals = rng.standard_normal((len(TIMES), 3, NXA, NYA))
+    fields = [UniformField(values=vals[k], origin=(0.0, 0.0), dx=1.0 / NXA, dy=1.0 / NYA, time=t)
+              for k, t in enumerate(TIMES)]
+    wet = rng.uniform(size=(NXA, NYA)) > 0.1 if dry else None
+    return vals, wet, adjoint.AdjointSnapshotStore(times=TIMES, fields=fields, window=adjoint.TimeWindow(0.0, 1.0),
+                                                   wet=wet)
+
+
+def _oracle(p, vals, wet, t, window, interp):
+    from paper_1511_03645_b200 import adjoint
+    lo, shape, dx, dy = p.spec.lo, p.spec.shape, p.spec.dx, p.spec.dy
+    x = (np.arange(lo[0], lo[0] + shape[0]) + 0.5) * dx
+    y = (np.arange(lo[1], lo[1] + shape[1]) + 0.5) * dy
+    xc, yc = np.broadcast_to(x[:, None], shape), np.broadcast_to(y[None, :], shape)
+    qi = p.state[:, 2:-2, 2:-2]
+    fwd_wet = p.aux.wet[2:-2, 2:-2]
+    if not interp:
+        idx = adjoint.query_window_times(t, window, _FakeStore(window))
+        return O.inner_product(qi, xc, yc, vals, idx, (0.0, 0.0), 1.0 / NXA, 1.0 / NYA, fwd_wet, wet), len(idx)
+    upper = min(t + window.span, window.t_final)
+    t_eval = [t] + [float(s) for s in TIMES if t + 1e-9 < s < upper - 1e-9] + ([upper] if upper > t + 1e-9 else [])
+    best = O.inner_product_interp(qi, xc, yc, vals, TIMES, t_eval, (0.0, 0.0), 1.0 / NXA, 1.0 / NYA)
+    best = np.where(fwd_wet, best, 0.0)
+    if wet is not None:
+        i = np.clip((xc / (1.0 / NXA)).astype(int), 0, NXA - 1)
+        j = np.clip((yc / (1.0 / NYA)).astype(int), 0, NYA - 1)
+        best = np.where(~wet[i, j], 0.0, best)
+    return best, len(t_eval)
+
+
+class _FakeStore:
+    """query_window_times needs only times and the window."""
+    def __init__(self, window):
+        self.times = TIMES
+        self.window = window
+
+
+ROWS = [((0, 0), (20, 256)), ((20, 256), (17, 128)), ((40, 0), (8, 384))]
+RAGGED = [((0, 0), (20, 250)), ((20, 256), (17, 100)), ((40, 0), (8, 33))]
+
+
+@pytest.mark.parametrize("layout", ["rows", "ragged"])
+@pytest.mark.parametrize("interp", [False, True])
+@pytest.mark.parametrize("case", ["snapshot", "between", "span"])
+def test_layouts_bitwise(layout, interp, case):
+    from paper_1511_03645_b200 import adjoint
+    _, patches = _level(ROWS if layout == "rows" else RAGGED, seed=3)
+    vals, wet, store = _store(seed=4, dry=True)
+    t, window = {"snapshot": (0.6, adjoint.TimeWindow(0.6, 0.6)),
+                 "between": (0.5, adjoint.TimeWindow(0.5, 0.5)),
+                 "span": (0.3, adjoint.TimeWindow(0.0, 0.75))}[case]
+    tol = 0.7
+    flags, counts, best = adjoint.flag_level(patches, t, store, window, tol, want_best=True, time_interp=interp)
+    for p, f, c, b in zip(patches, flags, counts, best):
+        ref, n = _oracle(p, vals, wet, t, window, interp)
+        if case != "span":
+            assert n == 1 or not interp and case == "between"
+        assert np.array_equal(b, ref)
+        assert np.array_equal(f, ref > tol)
+        assert c == int((ref > tol).sum())
