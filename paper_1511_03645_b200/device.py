@@ -1132,11 +1132,10 @@ def flag_axis_tables(store: LevelStore, ring_shape, a_origin, a_dx, a_dy, level_
         I[pos] = i0
         Dr[pos] = dry
     offs = np.stack([poff, poff + ext[:, 0]] if nd == 2 else [poff, poff], axis=1).reshape(-1)
-    ws, iis, drys = [W], [I], [Dr]
     torch = _torch()
-    tabs = (torch.from_numpy(np.concatenate(ws).astype(np.float64)).to("cuda"),
-            torch.from_numpy(np.concatenate(iis)).to("cuda"),
-            torch.from_numpy(np.concatenate(drys)).to("cuda"),
+    tabs = (torch.from_numpy(W).to("cuda"),
+            torch.from_numpy(I).to("cuda"),
+            torch.from_numpy(Dr).to("cuda"),
             torch.from_numpy(np.array(offs, dtype=np.int64)).to("cuda"))
     store._scratch[key] = tabs
     return tabs

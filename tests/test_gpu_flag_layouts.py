@@ -1,8 +1,9 @@
-"""K3 kernel layouts against the oracle (bitwise): the row-layout kernel
-(every patch row a multiple of 128 cells), the hoisted single-snapshot
-kernel (ragged rows) and the pair kernel (windows of >= 2 snapshots), on a
-multi-patch shallow-water level with dry forward and dry adjoint cells, in
-both window modes (adjoint.py:227-257, adjoint.py:98-110 for mode 1)."""
+"""K3 kernel layouts against the oracle (bitwise) on a multi-patch
+shallow-water level with dry forward and dry adjoint cells, in both window
+modes (adjoint.py:227-257, adjoint.py:98-110 for mode 1): the row-layout
+kernel for single snapshots (every patch row a multiple of 128 cells), the
+one-cell-per-lane kernel (ragged rows) and the pair kernel (windows of >= 2
+snapshots)."""
 import numpy as np
 import pytest
 
@@ -11,7 +12,7 @@ from oracle import adjamr_oracle as O
 pytestmark = pytest.mark.gpu
 
 TIMES = np.linspace(0.0, 1.0, 6)
-NXA, NYA = 48, 100
+NXA = 48
 
 
 def _level(shapes_los, seed):
@@ -32,7 +33,7 @@ def _level(shapes_los, seed):
     return h, patches
 
 
-def _store(seed, dry):
+def _store(seed, dry, NYA):
     from paper_1511_03645_b200 import adjoint
     from paper_1511_03645_b200.geometry import UniformField
     rng = np.random.default_rng(seed)
@@ -44,7 +45,7 @@ def _store(seed, dry):
                                                    wet=wet)
 
 
-def _oracle(p, vals, wet, t, window, interp):
+def _oracle(p, vals, wet, t, window, interp, NYA):
     from paper_1511_03645_b200 import adjoint
     lo, shape, dx, dy = p.spec.lo, p.spec.shape, p.spec.dx, p.spec.dy
     x = (np.arange(lo[0], lo[0] + shape[0]) + 0.5) * dx
@@ -77,20 +78,22 @@ ROWS = [((0, 0), (20, 256)), ((20, 256), (17, 128)), ((40, 0), (8, 384))]
 RAGGED = [((0, 0), (20, 250)), ((20, 256), (17, 100)), ((40, 0), (8, 33))]
 
 
-@pytest.mark.parametrize("layout", ["rows", "ragged"])
+# adjoint widths: a 128-cell segment spans ~27 (100 columns) or ~102 (400)
+# adjoint columns
+@pytest.mark.parametrize("layout,nya", [("rows", 100), ("rows", 400), ("ragged", 100)])
 @pytest.mark.parametrize("interp", [False, True])
 @pytest.mark.parametrize("case", ["snapshot", "between", "span"])
-def test_layouts_bitwise(layout, interp, case):
+def test_layouts_bitwise(layout, nya, interp, case):
     from paper_1511_03645_b200 import adjoint
     _, patches = _level(ROWS if layout == "rows" else RAGGED, seed=3)
-    vals, wet, store = _store(seed=4, dry=True)
+    vals, wet, store = _store(seed=4, dry=True, NYA=nya)
     t, window = {"snapshot": (0.6, adjoint.TimeWindow(0.6, 0.6)),
                  "between": (0.5, adjoint.TimeWindow(0.5, 0.5)),
                  "span": (0.3, adjoint.TimeWindow(0.0, 0.75))}[case]
     tol = 0.7
     flags, counts, best = adjoint.flag_level(patches, t, store, window, tol, want_best=True, time_interp=interp)
     for p, f, c, b in zip(patches, flags, counts, best):
-        ref, n = _oracle(p, vals, wet, t, window, interp)
+        ref, n = _oracle(p, vals, wet, t, window, interp, nya)
         if case != "span":
             assert n == 1 or not interp and case == "between"
         assert np.array_equal(b, ref)
