@@ -286,6 +286,8 @@ int adj_restrict(const AdjRestrictArgs* a);
  *         snapshots interp_k[n] and interp_k[n]+1 with weight interp_w[n]
  *         (interp_k < 0: use snapshot -interp_k-1 unblended). */
 #define ADJ_FLAG_ROWS 1
+#define ADJ_FLAG_PAIRS 2   /* with ADJ_FLAG_ROWS: every even-aligned column pair of every patch
+                              shares its adjoint stencil column (ratio >= 2 on aligned grids) */
 typedef struct AdjFlagArgs {
     const double* q;             /* forward level store                        */
     const double* aux;           /* forward aux (swe: depth plane 1)          */

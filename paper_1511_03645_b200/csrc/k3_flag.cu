@@ -294,29 +294,33 @@ constexpr int K3_ROW_UNR = K3_ROW_UNROLL > 0 ? K3_ROW_UNROLL : 1;
 constexpr int RNC = K3_ROW_NC;     // cells per lane (a warp's segment is 32*RNC columns)
 constexpr int K3_ROW_WARPS = 4;   // warps per CTA
 #ifndef K3_ROW_RUN_ROWS
-#define K3_ROW_RUN_ROWS 16
+#define K3_ROW_RUN_ROWS 0
 #endif
-constexpr int K3_ROW_RUN = K3_ROW_RUN_ROWS;   // rows one warp marches down (short runs: several waves, small tail)
+constexpr int K3_ROW_RUN = K3_ROW_RUN_ROWS;   // rows one warp marches down (0: sized at launch to one wave)
+#ifndef K3_ROW_DEPTH
+#define K3_ROW_DEPTH 2
+#endif
+constexpr int RDEPTH = K3_ROW_DEPTH;          // state rows in flight per warp (shared-memory buffers)
 
 template <bool MODE1>
 #ifndef K3_ROW_MINB
 #define K3_ROW_MINB 1
 #endif
-__global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROW_MINB) k3_row(AdjFlagArgs a) {
+__global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROW_MINB) k3_row(AdjFlagArgs a, int run) {
     // warp = one 32*RNC-column segment of K3_ROW_RUN consecutive rows.  The
     // column tables load once; the next row's state streams into shared
     // memory (cp.async) and its row-table entry into registers while this
     // row is computed, so the corner loads depend on registers only, and
     // rows sharing adjoint rows (refinement ratio >= 2) hit L1.
-    __shared__ double s_q[K3_ROW_WARPS][2][RNC * 3][32];
+    __shared__ double s_q[K3_ROW_WARPS][RDEPTH][RNC * 3][32];
     const int pidx = blockIdx.z;
     const AdjPatch p = a.patches[pidx];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned seg = blockIdx.y * K3_ROW_WARPS + warp;          // column segment
     const unsigned nseg = (unsigned)p.ny / (32u * RNC);
-    const unsigned r0 = blockIdx.x * K3_ROW_RUN;
+    const unsigned r0 = blockIdx.x * (unsigned)run;
     if (seg >= nseg || r0 >= (unsigned)p.nx) return;               // warp-uniform
-    const unsigned r1 = min(r0 + K3_ROW_RUN, (unsigned)p.nx);
+    const unsigned r1 = min(r0 + (unsigned)run, (unsigned)p.nx);
     const unsigned ny = (unsigned)p.ny, j = seg * (32u * RNC) + lane;
     const int g = a.ghost;
     const int64_t cs = a.comp_stride;
@@ -340,8 +344,11 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROW_MINB) k3_row(AdjFlag
                              : "memory");
             }
     };
-    prefetch(r0, 0);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
+#pragma unroll
+    for (int d = 0; d < RDEPTH - 1; ++d) {       // rows r0 .. r0+RDEPTH-2 in flight
+        if (r0 + d < r1) prefetch(r0 + d, d);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
 
     double wy[RNC], uy[RNC];
     int j0[RNC], ja[RNC];
@@ -400,9 +407,9 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROW_MINB) k3_row(AdjFlag
 #if K3_ROW_UNROLL > 0
 #pragma unroll K3_ROW_UNR
 #endif
-        for (unsigned i = r0; i < r1; ++i, buf ^= 1) {
+        for (unsigned i = r0; i < r1; ++i, buf = buf + 1 == RDEPTH ? 0 : buf + 1) {
             const bool more = i + 1 < r1;
-            if (more) prefetch(i + 1, buf ^ 1);
+            if (i + RDEPTH - 1 < r1) prefetch(i + RDEPTH - 1, buf == 0 ? RDEPTH - 1 : buf - 1);
             asm volatile("cp.async.commit_group;\n" ::: "memory");
             const double ux = 1.0 - wx;
             double qh[RNC][3];
@@ -416,7 +423,7 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROW_MINB) k3_row(AdjFlag
             const bool more2 = i + 2 < r1;
             const int i0nn = more2 ? __ldg(a.axis_i + rowoff + i + 2) : 0;
             const double wxnn = more2 ? __ldg(a.axis_w + rowoff + i + 2) : 0.0;
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(RDEPTH - 1) : "memory");
             __syncwarp();
             double best[RNC];
 #pragma unroll
@@ -438,9 +445,9 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROW_MINB) k3_row(AdjFlag
         return;
     }
 #endif
-    for (unsigned i = r0; i < r1; ++i, buf ^= 1) {
+    for (unsigned i = r0; i < r1; ++i, buf = buf + 1 == RDEPTH ? 0 : buf + 1) {
         const bool more = i + 1 < r1;
-        if (more) prefetch(i + 1, buf ^ 1);
+        if (i + RDEPTH - 1 < r1) prefetch(i + RDEPTH - 1, buf == 0 ? RDEPTH - 1 : buf - 1);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         const int i0n = more ? __ldg(a.axis_i + rowoff + i + 1) : 0;
         const double wxn = more ? __ldg(a.axis_w + rowoff + i + 1) : 0.0;
@@ -466,7 +473,7 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROW_MINB) k3_row(AdjFlag
                 }
             }
         }
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // this row's state has landed
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(RDEPTH - 1) : "memory");   // this row's state has landed
         __syncwarp();
         double best[RNC];
 #pragma unroll
@@ -505,6 +512,178 @@ ADJ_D unsigned spread16(unsigned x) {   // bit k -> bit 2k
     x = (x | (x << 1)) & 0x55555555u;
     return x;
 }
+
+// ---------------------------------------------------------------------------
+// Row layout with column pairs (ADJ_FLAG_PAIRS; single-snapshot windows, mode
+// 0): lane l owns the cell pairs (64pp + 2l, 64pp + 2l + 1), pp = 0, 1, of its
+// warp's 128-column segment.  Both cells of a pair share the adjoint stencil
+// column, so a row needs 12 corner loads per pair instead of 12 per cell, the
+// corners prefetched a row ahead take half the registers, and the state row
+// streams in as 16-byte cp.async pieces read back with one LDS.128.  Each
+// cell's arithmetic is k3_row's (bitwise); the even/odd ballots are
+// interleaved into the standard flag words.
+#ifndef K3_ROWP_MINB
+#define K3_ROWP_MINB 3
+#endif
+constexpr int NPR = 2;   // pairs per lane
+
+__global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROWP_MINB) k3_rowp(AdjFlagArgs a, int run) {
+    __shared__ double2 s_q[K3_ROW_WARPS][RDEPTH][NPR * 3][32];
+    const int pidx = blockIdx.z;
+    const AdjPatch p = a.patches[pidx];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned seg = blockIdx.y * K3_ROW_WARPS + warp;
+    const unsigned nseg = (unsigned)p.ny / 128u;
+    const unsigned r0 = blockIdx.x * (unsigned)run;
+    if (seg >= nseg || r0 >= (unsigned)p.nx) return;               // warp-uniform
+    const unsigned r1 = min(r0 + (unsigned)run, (unsigned)p.nx);
+    const unsigned ny = (unsigned)p.ny, j = seg * 128u + 2u * lane;   // pair pp: columns j + 64pp, +1
+    const int g = a.ghost;
+    const int64_t cs = a.comp_stride;
+    const int64_t nya = a.nya;
+    const int64_t plane = (int64_t)a.nxa * nya;
+    const int k = __ldg(a.snap_index);
+    const double* fa = a.ring + (int64_t)k * plane * 3;
+    const int64_t rowoff = a.axis_off[2 * pidx], coloff = a.axis_off[2 * pidx + 1];
+    const double* qcol = a.q + p.offset + (int64_t)g * p.pitch + g + j;   // 16-byte aligned (even column)
+
+    auto prefetch = [&](unsigned i, int buf) {
+        const double* qp = qcol + (int64_t)i * p.pitch;
+#pragma unroll
+        for (int pp = 0; pp < NPR; ++pp)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_q[warp][buf][pp * 3 + cc][lane]);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(qp + cc * cs + 64 * pp)
+                             : "memory");
+            }
+    };
+#pragma unroll
+    for (int d = 0; d < RDEPTH - 1; ++d) {
+        if (r0 + d < r1) prefetch(r0 + d, d);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    double wy[NPR][2], uy[NPR][2];
+    int ja[NPR][2];
+    unsigned off[NPR][3];
+    const char* fab = reinterpret_cast<const char*>(fa);
+    const int64_t rowbytes = nya * 8;
+#pragma unroll
+    for (int pp = 0; pp < NPR; ++pp) {
+        const int jt = (int)(j + 64 * pp);
+        const int j0 = __ldg(a.axis_i + coloff + jt);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            wy[pp][e] = __ldg(a.axis_w + coloff + jt + e);
+            uy[pp][e] = 1.0 - wy[pp][e];
+            ja[pp][e] = a.axis_dry ? __ldg(a.axis_dry + coloff + jt + e) : 0;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) off[pp][c] = (unsigned)(((int64_t)c * plane + j0) * 8);
+    }
+    double C[NPR][3][4];
+    auto corners = [&](int ii0) {
+        const char* b0 = fab + ii0 * rowbytes;
+        const char* b1 = b0 + rowbytes;
+#pragma unroll
+        for (int pp = 0; pp < NPR; ++pp)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double* q0 = reinterpret_cast<const double*>(b0 + off[pp][c]);
+                const double* q1 = reinterpret_cast<const double*>(b1 + off[pp][c]);
+                C[pp][c][0] = __ldg(q0); C[pp][c][1] = __ldg(q1);
+                C[pp][c][2] = __ldg(q0 + 1); C[pp][c][3] = __ldg(q1 + 1);
+            }
+    };
+    double wx = __ldg(a.axis_w + rowoff + r0);
+    corners(__ldg(a.axis_i + rowoff + r0));
+    int i0n = r0 + 1 < r1 ? __ldg(a.axis_i + rowoff + r0 + 1) : 0;
+    double wxn = r0 + 1 < r1 ? __ldg(a.axis_w + rowoff + r0 + 1) : 0.0;
+    unsigned long long cnt = 0;
+    int buf = 0;
+    for (unsigned i = r0; i < r1; ++i, buf = buf + 1 == RDEPTH ? 0 : buf + 1) {
+        const bool more = i + 1 < r1;
+        if (i + RDEPTH - 1 < r1) prefetch(i + RDEPTH - 1, buf == 0 ? RDEPTH - 1 : buf - 1);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const double ux = 1.0 - wx;
+        double qh[NPR][2][3];
+#pragma unroll
+        for (int pp = 0; pp < NPR; ++pp)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    qh[pp][e][c] = C[pp][c][0] * ux * uy[pp][e] + C[pp][c][1] * wx * uy[pp][e] +
+                                   C[pp][c][2] * ux * wy[pp][e] + C[pp][c][3] * wx * wy[pp][e];
+        if (more) corners(i0n);
+        const bool more2 = i + 2 < r1;
+        const int i0nn = more2 ? __ldg(a.axis_i + rowoff + i + 2) : 0;
+        const double wxnn = more2 ? __ldg(a.axis_w + rowoff + i + 2) : 0.0;
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(RDEPTH - 1) : "memory");
+        __syncwarp();
+        double best[NPR][2];
+#pragma unroll
+        for (int pp = 0; pp < NPR; ++pp) {
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double2 qc = s_q[warp][buf][pp * 3 + c][lane];
+                d0 = c == 0 ? qh[pp][0][c] * qc.x : d0 + qh[pp][0][c] * qc.x;
+                d1 = c == 0 ? qh[pp][1][c] * qc.y : d1 + qh[pp][1][c] * qc.y;
+            }
+            best[pp][0] = fmax(0.0, fabs(d0));
+            best[pp][1] = fmax(0.0, fabs(d1));
+        }
+        __syncwarp();
+        if (a.swe) {   // forward dry cells
+            const double* cp = a.aux + a.aux_stride + p.offset + (int64_t)(i + g) * p.pitch + (j + g);
+#pragma unroll
+            for (int pp = 0; pp < NPR; ++pp)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (!(__ldg(cp + 64 * pp + e) > 0.0)) best[pp][e] = 0.0;
+        }
+        if (a.adj_wet != nullptr && a.axis_dry) {   // adjoint cell containing the centre is dry
+            const int ia = __ldg(a.axis_dry + rowoff + i);
+#pragma unroll
+            for (int pp = 0; pp < NPR; ++pp)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (!a.adj_wet[(int64_t)ia * nya + ja[pp][e]]) best[pp][e] = 0.0;
+        }
+        const unsigned base = i * ny + seg * 128u;
+        if (a.best != nullptr) {
+#pragma unroll
+            for (int pp = 0; pp < NPR; ++pp)
+                *reinterpret_cast<double2*>(a.best + a.best_offset[pidx] + base + 64u * pp + 2u * lane) =
+                    make_double2(best[pp][0], best[pp][1]);
+        }
+        // flag words: word 2pp+h, bit b is cell 64pp + 32h + b, held by lane
+        // 16h + b/2 as its pair element b%2.  Each lane fetches the 4 flag bits
+        // of lanes l/2 and 16 + l/2 and the four ballots are the words.
+        unsigned bits = 0;
+#pragma unroll
+        for (int pp = 0; pp < NPR; ++pp)
+            bits |= (best[pp][0] > a.tolerance ? 1u : 0u) << (2 * pp) | (best[pp][1] > a.tolerance ? 2u : 0u) << (2 * pp);
+        const unsigned t0 = __shfl_sync(0xffffffffu, bits, lane >> 1) >> (lane & 1);
+        const unsigned t1 = __shfl_sync(0xffffffffu, bits, 16 + (lane >> 1)) >> (lane & 1);
+        unsigned words[4];
+#pragma unroll
+        for (int pp = 0; pp < NPR; ++pp) {
+            words[2 * pp] = __ballot_sync(0xffffffffu, (t0 >> (2 * pp)) & 1u);
+            words[2 * pp + 1] = __ballot_sync(0xffffffffu, (t1 >> (2 * pp)) & 1u);
+        }
+        if (lane < 4) {
+            const unsigned wv = lane == 0 ? words[0] : (lane == 1 ? words[1] : (lane == 2 ? words[2] : words[3]));
+            a.flag_bits[p.flag_word + (base >> 5) + lane] = wv;
+        }
+        cnt += __popc(words[0]) + __popc(words[1]) + __popc(words[2]) + __popc(words[3]);
+        wx = wxn; wxn = wxnn; i0n = i0nn;
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (lane == 0 && cnt) atomicAdd(&a.counts[pidx], cnt);
+}
+
 
 template <bool MODE1, bool SHARED>
 ADJ_D void pair_window(const AdjFlagArgs& a, const int* s_k, const double* s_w, int nidx, const char* ring,
@@ -660,6 +839,16 @@ static bool k3_pairs() {
     return on == 1;
 }
 
+// ADJAMR_K3_ROWP=0 disables the paired row kernel (A/B measurements)
+static bool k3_rowp_on() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("ADJAMR_K3_ROWP");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
 // ADJAMR_K3_ROW=0 disables the row-layout kernel (A/B measurements)
 static bool k3_row_on() {
     static int on = -1;
@@ -668,6 +857,31 @@ static bool k3_row_on() {
         on = (e && e[0] == '0') ? 0 : 1;
     }
     return on == 1;
+}
+
+// Rows per warp of k3_row: K3_ROW_RUN, or (0) the run that makes the grid
+// about one wave of resident CTAs, so each warp's column tables and pipeline
+// fill amortise over as many rows as the device allows.
+static int k3_row_run(const AdjFlagArgs& a, bool m1, bool pairs) {
+    if (K3_ROW_RUN > 0) return K3_ROW_RUN;
+    static int resident[3] = {0, 0, 0};
+    int& res = resident[pairs ? 2 : (m1 ? 1 : 0)];
+    if (res == 0) {
+        int per_sm = 0, dev = 0, sms = 0;
+        if (pairs) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_rowp, 32 * K3_ROW_WARPS, 0);
+        else if (m1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_row<true>, 32 * K3_ROW_WARPS, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_row<false>, 32 * K3_ROW_WARPS, 0);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        res = (per_sm < 1 ? 1 : per_sm) * sms;
+    }
+    const int64_t segs = ((int64_t)a.max_cols / (32 * RNC) + K3_ROW_WARPS - 1) / K3_ROW_WARPS;
+    const int64_t ctas_per_run_row = segs * a.npatch;          // CTAs per row-run index
+    int64_t runs = res / (ctas_per_run_row > 0 ? ctas_per_run_row : 1);
+    if (runs < 1) runs = 1;
+    int64_t run = (a.max_rows + runs - 1) / runs;
+    if (run < 4) run = 4;
+    return (int)run;
 }
 
 int flag_adjoint(const AdjFlagArgs& a) {
@@ -690,11 +904,15 @@ int flag_adjoint(const AdjFlagArgs& a) {
                 else k3_pair<false><<<grid, threads, 0, st>>>(a);
             } else if (a.nidx == 1 && (a.layout & ADJ_FLAG_ROWS) && k3_row_on()) {
                 // (row runs, column segments / warps per CTA, patches); max_rows = the tallest patch
-                const dim3 gr((unsigned)((a.max_rows + K3_ROW_RUN - 1) / K3_ROW_RUN),
+                const bool pairs = !m1 && (a.layout & ADJ_FLAG_PAIRS) && k3_rowp_on() &&
+                                   (int64_t)a.nxa * a.nya * 3 * 8 < (int64_t(1) << 32);   // 32-bit corner offsets
+                const int run = k3_row_run(a, m1, pairs);
+                const dim3 gr((unsigned)((a.max_rows + run - 1) / run),
                               (unsigned)((a.max_cols / (32 * RNC) + K3_ROW_WARPS - 1) / K3_ROW_WARPS),
                               (unsigned)a.npatch);
-                if (m1) k3_row<true><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a);
-                else k3_row<false><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a);
+                if (pairs) k3_rowp<<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a, run);
+                else if (m1) k3_row<true><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a, run);
+                else k3_row<false><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a, run);
             } else {
                 if (m1) k3_flag_t<3, true, true><<<grid, threads, 0, st>>>(a);
                 else k3_flag_t<3, true, false><<<grid, threads, 0, st>>>(a);

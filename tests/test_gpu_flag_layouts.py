@@ -79,8 +79,9 @@ RAGGED = [((0, 0), (20, 250)), ((20, 256), (17, 100)), ((40, 0), (8, 33))]
 
 
 # adjoint widths: a 128-cell segment spans ~27 (100 columns) or ~102 (400)
-# adjoint columns
-@pytest.mark.parametrize("layout,nya", [("rows", 100), ("rows", 400), ("ragged", 100)])
+# adjoint columns; 128 columns = ratio 4, where every even-aligned column pair
+# shares its stencil column (the paired row kernel, k3_rowp)
+@pytest.mark.parametrize("layout,nya", [("rows", 100), ("rows", 400), ("rows", 128), ("ragged", 100)])
 @pytest.mark.parametrize("interp", [False, True])
 @pytest.mark.parametrize("case", ["snapshot", "between", "span"])
 def test_layouts_bitwise(layout, nya, interp, case):
@@ -99,3 +100,17 @@ def test_layouts_bitwise(layout, nya, interp, case):
         assert np.array_equal(b, ref)
         assert np.array_equal(f, ref > tol)
         assert c == int((ref > tol).sum())
+
+
+@pytest.mark.parametrize("nya,expect", [(128, True), (100, False), (256, False)])
+def test_pair_layout_detection(nya, expect):
+    """ADJ_FLAG_PAIRS is set exactly when every even-aligned column pair shares
+    its adjoint stencil column (ratio 4 yes; ratio 2 pairs straddle a centre)."""
+    from paper_1511_03645_b200 import adjoint, device, solver
+    _, patches = _level(ROWS, seed=3)
+    _, _, store = _store(seed=4, dry=False, NYA=nya)
+    adjoint.flag_level(patches, 0.6, store, adjoint.TimeWindow(0.6, 0.6), 0.7)
+    st = solver.store_of(patches[0])
+    tabs = device.flag_axis_tables(st, (NXA, nya), (0.0, 0.0), 1.0 / NXA, 1.0 / nya, (0.0, 0.0),
+                                   patches[0].spec.dx, patches[0].spec.dy)
+    assert tabs[4] is expect
