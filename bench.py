@@ -13,8 +13,10 @@ tolerance 1e-4) is measured in the same run and reported under "flagging".
 
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): independent replicas, one per GPU ("scaling": "weak"),
-value = all ranks' cell-updates / max-over-ranks device time.
+N > 1 (torchrun): the level is (N*4096) x 4096 on [0, N*1e6] x [0, 1e6],
+one 4096-row x-slab per GPU with a halo exchange (NCCL send/recv) every
+step (sharded.py; "scaling": "weak"), value = all ranks' cell-updates /
+max-over-ranks device time.
 """
 from __future__ import annotations
 
@@ -55,42 +57,54 @@ def fourier_modes():
     return modes, phases, amps
 
 
-def c4_fields(n=N, g=2, device="cuda"):
-    """Bathymetry (ghost-inclusive), computed on the device (setup only)."""
+def c4_fields(n=N, g=2, device="cuda", x_off=0):
+    """Bathymetry (ghost-inclusive), computed on the device (setup only).
+    x_off: first x cell of an n-row slab of a wider domain (sharded weak
+    scaling); the Fourier field keeps the scale of the C4 square."""
     import torch
     dx = L / n
     idx = torch.arange(-g, n + g, dtype=torch.float64, device=device)
     xp = ((idx + 0.5) * dx) / L
     modes, phases, amps = fourier_modes()
-    F = torch.zeros(n + 2 * g, n + 2 * g, dtype=torch.float64, device=device)
-    for (kx, ky), ph, a in zip(modes, phases, amps):
-        ax = 2 * np.pi * kx * xp
-        by = 2 * np.pi * ky * xp + ph
-        F += a * (torch.outer(torch.cos(ax), torch.cos(by)) - torch.outer(torch.sin(ax), torch.sin(by)))
-    F *= 200.0 / F[g:-g, g:-g].abs().max()
-    B = -4000.0 + 3000.0 * torch.tanh((xp[:, None] - 0.7) / 0.05) + F
+
+    def fourier(xq):
+        F = torch.zeros(n + 2 * g, n + 2 * g, dtype=torch.float64, device=device)
+        for (kx, ky), ph, a in zip(modes, phases, amps):
+            ax = 2 * np.pi * kx * xq
+            by = 2 * np.pi * ky * xp + ph
+            F += a * (torch.outer(torch.cos(ax), torch.cos(by)) - torch.outer(torch.sin(ax), torch.sin(by)))
+        return F
+    F = fourier(xp)
+    scale = 200.0 / F[g:-g, g:-g].abs().max()
+    xs = xp + x_off * dx / L
+    if x_off:
+        F = fourier(xs)
+    B = -4000.0 + 3000.0 * torch.tanh((xs[:, None] - 0.7) / 0.05) + F * scale
     return B
 
 
-def build_c4(n=N):
+def build_c4(n=N, rank=0, world=1):
+    """The C4 level; world > 1: rank's n-row x-slab of the (world*n) x n
+    level on [0, world*L] x [0, L] (weak scaling, sharded.py), dt from the
+    global select_dt."""
     import torch
     from paper_1511_03645_b200 import equations as E
-    from paper_1511_03645_b200 import solver
+    from paper_1511_03645_b200 import sharded, solver
     from paper_1511_03645_b200.geometry import Patch, PatchHierarchy
-    B = c4_fields(n)
+    B = c4_fields(n, x_off=rank * n)
     depth = (0.0 - B)
     c = torch.sqrt(GRAV * torch.clamp(depth, min=0.0))
     mat = E.SweMaterial(bathymetry=B.cpu().numpy(), depth=depth.cpu().numpy(), wet=(depth > 0).cpu().numpy(),
                         c=c.cpu().numpy(), gravity=GRAV)
     eq = E.SweLinear2D(E.SweMaterialModel(lambda x, y: np.zeros_like(x), 0.0, GRAV))
-    h = PatchHierarchy(xlim=(0.0, L), ylim=(0.0, L), base_shape=(n, n), ratios=[])
-    p = Patch(h.make_spec(1, (0, 0), (n - 1, n - 1)), 3)
+    h = PatchHierarchy(xlim=(0.0, world * L), ylim=(0.0, L), base_shape=(world * n, n), ratios=[])
+    p = Patch(h.make_spec(1, (rank * n, 0), ((rank + 1) * n - 1, n - 1)), 3)
     p.aux = mat
     xs = (np.arange(n) + 0.5) / n
-    X, Y = np.meshgrid(xs, xs, indexing="ij")
+    X, Y = np.meshgrid(xs + rank, xs, indexing="ij")
     p.interior()[0] = np.exp(-((X - 0.3) ** 2 + (Y - 0.5) ** 2) / 0.02 ** 2)
     h.levels = [[p]]
-    dt = solver.select_dt(h, eq, 0.9)
+    dt = solver.select_dt(h, eq, 0.9) if world == 1 else sharded.global_dt(h, eq, 0.9)
     bc = solver.BoundarySpec("outflow", "outflow", "outflow", "outflow")
     return h, p, eq, bc, dt
 
@@ -431,20 +445,32 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(torch.cuda.device_count(), 1))
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # ADJAMR_BENCH_BACKEND=gloo: functional check of the N > 1 path with several ranks
+        # on one device (host-staged exchange; not a measurement)
+        if os.environ.get("ADJAMR_BENCH_BACKEND") == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_1511_03645_b200 import _lib, device, solver
+    from paper_1511_03645_b200 import _lib, device, sharded, solver
     variant = _lib.VARIANT_FAST if args.variant == "fast" else _lib.VARIANT_EXACT
-    h, p, eq, bc, dt = build_c4()
-    shape = (N, N)
+    h, p, eq, bc, dt = build_c4(rank=rank, world=world)
+    shape = (world * N, N)
     st = solver.store_of(p)
     st.sync_in()
+    transport = sharded.DistTransport(rank, world) if world > 1 else None
+
+    def advance(nsteps):
+        if world == 1:    # fill+step pairs replayed from a CUDA graph
+            return solver.advance_uniform(p, eq, bc, shape, dt, nsteps, "MC", variant)
+        # rank's x-slab of the (world*N) x N level: fill, halo exchange (NCCL send/recv), step
+        return sharded.advance_sharded(p, eq, bc, shape, dt, nsteps, transport, "MC", variant)
 
     # warm-up (the kernels are prebuilt; this warms caches/clocks and
     # captures the CUDA graph of the fill+step pair, which needs >= 4 steps)
-    solver.advance_uniform(p, eq, bc, shape, dt, max(args.warmup, 4), "MC", variant)
+    advance(max(args.warmup, 4))
     torch.cuda.synchronize()
 
     def barrier():
@@ -458,7 +484,7 @@ def main():
     with Clocks(local) as clk:
         barrier()
         e0.record(stream)
-        cfl = solver.advance_uniform(p, eq, bc, shape, dt, args.steps, "MC", variant)
+        cfl = advance(args.steps)
         e1.record(stream)
         barrier()
     from paper_1511_03645_b200.replicas import aggregate
@@ -482,21 +508,23 @@ def main():
     peak, peak_kind = peaks()
     achieved = BYTES_PER_CELL_SWE * N * N / (k1 * 1e-3) / 1e9
 
-    # ---- K3 adjoint flagging on the same state
-    flag = bench_flagging(p, st, dt, stream)
+    # ---- K3 adjoint flagging on the same state (the adjoint grid covers rank 0's square)
+    flag = bench_flagging(p, st, dt, stream) if rank == 0 else None
 
     # ---- e2e through the public API with host buffers
-    e2e = bench_e2e(p, eq, bc, shape, dt, variant, min(args.steps, 5))
-    c5 = None if args.no_c5 else bench_c5(min(args.steps, 10), 3, variant)
-    c3 = None if args.no_c5 else bench_c3(min(args.steps, 20), variant)
-    c5_full = bench_c5_full(args.c5_full, variant) if args.c5_full and not args.no_c5 else None
+    e2e = bench_e2e(p, eq, bc, shape, dt, variant, min(args.steps, 5), world)
+    single = not args.no_c5 and world == 1     # C5 / C3 are single-GPU configurations
+    c5 = bench_c5(min(args.steps, 10), 3, variant) if single else None
+    c3 = bench_c3(min(args.steps, 20), variant) if single else None
+    c5_full = bench_c5_full(args.c5_full, variant) if args.c5_full and single else None
 
     line = {
         "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "grid": [N, N], "dt": dt, "limiter": "MC", "variant": args.variant,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": f"x-slabs{world} (halo exchange, NCCL send/recv)" if world > 1 else "single",
+                   "global_grid": [world * N, N],
                    "l2": "inputs (537 MB/step) larger than the 126 MB L2; no flush"},
         "max_courant": cfl,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -510,8 +538,9 @@ def main():
         "c3_heterogeneous_acoustics": c3,
         "c5_full_workflow": c5_full,
         "e2e": e2e,
-        # per step: k2_physical + k1_fast (graph replay; no memset nodes, fold is a no-op)
-        "gpu_launches": args.steps * 2,
+        # per step: k2_physical + k1_fast (graph replay; no memset nodes, fold is a no-op);
+        # sharded (N > 1): + the ghost-ring fold (k2_ring) before the exchange
+        "gpu_launches": args.steps * (2 if world == 1 else 3),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -659,9 +688,11 @@ def bench_flagging(p, st, dt, stream):
     return out
 
 
-def bench_e2e(p, eq, bc, shape, dt, variant, steps):
+def bench_e2e(p, eq, bc, shape, dt, variant, steps, world=1):
     """Public API with host buffers: state in pinned host memory -> H2D,
-    physical fill + step (solver.fill_ghost_physical / step_patch), D2H."""
+    physical fill + step (solver.fill_ghost_physical / step_patch), D2H.
+    world > 1: each rank's slab through sharded.advance_sharded (fill, halo
+    exchange, step), max wall time over ranks."""
     import torch
     from paper_1511_03645_b200 import solver
     st = p._store
@@ -669,6 +700,26 @@ def bench_e2e(p, eq, bc, shape, dt, variant, steps):
     host.copy_(st.view(p._slot))
     nbytes = host.numel() * 8
     torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        from paper_1511_03645_b200 import sharded
+        from paper_1511_03645_b200.replicas import aggregate
+        tr = sharded.DistTransport(dist.get_rank(), world)
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            st.prepare_write(full_ghosts=True)
+            st.view(p._slot).copy_(host, non_blocking=True)
+            p._loc = "device"
+            sharded.advance_sharded(p, eq, bc, shape, dt, 1, tr, "MC", variant)
+            st.fold_ghosts()
+            host.copy_(st.view(p._slot), non_blocking=True)
+        torch.cuda.synchronize()
+        el, cells = aggregate(time.perf_counter() - t0, N * N * steps, device="cuda")
+        return {"value": cells / el, "unit": "cell-updates/s", "h2d_bytes_per_step": nbytes * world,
+                "d2h_bytes_per_step": nbytes * world, "steps": steps,
+                "path": "per rank: pinned host slab -> H2D -> sharded.advance_sharded (fill, NCCL halo "
+                        "exchange, step) -> D2H; max wall time over ranks"}
     if variant == _lib_variant_fast():
         # streamed: H2D / physical fill + step / D2H of consecutive row slabs overlap
         solver.step_patch_host(p, host, dt, eq, bc, shape, "MC")       # warm-up (plans, streams)
