@@ -351,8 +351,15 @@ ADJ_D void transverse(double f0, double h, const Mat& b, const Mat& a,
 
 struct Raw { double q0, q1, q2, c, z; };
 
+#ifndef K1_LDSNB
+#define K1_LDSNB 0   // 1: y-neighbours' raw q and material read from the shared ring (LDS.64)
+                     // instead of warp shuffles; the ring keeps the current and previous
+                     // column groups resident, so it has GROUPS + 2 groups
+#endif
 constexpr int GROUPS = K1_GROUPS;  // cp.async groups (of 3 columns) in flight per warp
-constexpr int RING = 3 * GROUPS;   // column slots of the per-warp ring
+constexpr int RING = 3 * GROUPS;   // column slots of the two-row kernel's ring
+constexpr int NGRP = K1_LDSNB ? GROUPS + 2 : GROUPS;   // groups of the single-row kernel's ring
+constexpr int RING1 = 3 * NGRP;
 
 // One warp's march along x over an output strip.  Every carried quantity
 // lives in a 3-slot ring indexed by (column mod 3); column<K> is the body of
@@ -370,8 +377,8 @@ struct Strip {
     bool out_lane, yface_cfl;
     double dtdx, dtdy, hx, hy;
 
-    double* ring;                  // this warp's cp.async ring: [RING][NARR][32]
-    int lane;
+    double* ring;                  // this warp's cp.async ring: [RING1][NARR][32]
+    int lane, lup, ldn;            // lane, and the lanes of rows j+1, j-1 (clamped like the shuffles)
     Mat m[3];
     double q0[3], q1[3], q2[3];
     Face xf[3];                    // xf[k]: x-face left of column k
@@ -416,8 +423,10 @@ struct Strip {
         return v;
     }
 
+    // up: this column's ring slot at the lane of row j+1; dn: the previous
+    // column's slot at the lane of row j-1 (array k at +32k)
     template <int K>
-    ADJ_D void column(int s, const Raw& cr) {
+    ADJ_D void column(int s, const Raw& cr, const double* up, const double* dn) {
         constexpr int C = K, P = (K + 2) % 3, PP = (K + 1) % 3;
         m[C] = make_mat<SYS, FORM, LIM>(cr.c, cr.z, dtdx, dtdy);
         // CFL: max |speed| of the faces is the max material speed of the cells
@@ -434,10 +443,11 @@ struct Strip {
         xf[C] = solve_face<SYS, FORM, REV>(q0[P], q1[P], cr.q0, cr.q1, m[P], m[C]);
 
         // ---- y-face between rows j and j+1 at column s
-        const double uq0 = sh_dn(cr.q0), uq2 = sh_dn(cr.q2);
+        const double uq0 = K1_LDSNB ? up[0] : sh_dn(cr.q0);
+        const double uq2 = K1_LDSNB ? up[64] : sh_dn(cr.q2);
         Mat mu{};
-        mu.c = sh_dn(m[C].c);
-        mu.m = SWE ? mu.c : sh_dn(m[C].m);
+        mu.c = K1_LDSNB ? up[96] : sh_dn(m[C].c);
+        mu.m = SWE ? mu.c : (K1_LDSNB ? up[128] : sh_dn(m[C].m));
         mu.k1 = fma(mu.m, mu.m, 1.0);
         mu.ky = sh_dn(m[C].ky);
         mu.kx = 0.0;
@@ -476,8 +486,8 @@ struct Strip {
         }
         {
             Mat mb{};
-            mb.c = sh_up(m[P].c);
-            mb.m = SWE ? mb.c : sh_up(m[P].m);
+            mb.c = K1_LDSNB ? dn[96] : sh_up(m[P].c);
+            mb.m = SWE ? mb.c : (K1_LDSNB ? dn[128] : sh_up(m[P].m));
             mb.tr = SWE ? mb.c * mb.c : mb.c * mb.m;
             Mat ma{};
             ma.c = cup[P]; ma.m = mup[P];
@@ -528,6 +538,8 @@ struct Strip {
     ADJ_D void setup(const AdjTile& T, const AdjPatch& p, const AdjStepArgs& a, int lane_, int lane0,
                      double* ring_) {
         lane = lane_;
+        lup = lane < 31 ? lane + 1 : 31;
+        ldn = lane > 0 ? lane - 1 : 0;
         ring = ring_;
         g = a.ghost;
         const int l = lane - lane0;
@@ -567,18 +579,24 @@ struct Strip {
         int base = 0;
 #pragma unroll 1
         for (int s = s_first; s <= s_last; s += 3) {
-            // one wait per group of three columns, then the group's slots are
-            // refilled with the columns RING ahead
+            // one wait per group of three columns, then the columns 3*GROUPS
+            // ahead go to the group after the in-flight ones (with K1_LDSNB the
+            // current and previous groups stay resident for neighbour reads)
             asm volatile("cp.async.wait_group %0;\n" ::"n"(GROUPS - 1) : "memory");
             const Raw r0 = read(base), r1 = read(base + 1), r2 = read(base + 2);
-            prefetch(s + RING, base);
-            prefetch(s + RING + 1, base + 1);
-            prefetch(s + RING + 2, base + 2);
+            int pf = base + 3 * GROUPS;
+            if (pf >= RING1) pf -= RING1;
+            prefetch(s + 3 * GROUPS, pf);
+            prefetch(s + 3 * GROUPS + 1, pf + 1);
+            prefetch(s + 3 * GROUPS + 2, pf + 2);
             commit();
-            column<0>(s, r0);
-            column<1>(s + 1, r1);
-            column<2>(s + 2, r2);
-            base = base + 3 == RING ? 0 : base + 3;
+            constexpr int SL = NARR * 32;          // doubles per column slot
+            const double* rb = ring + base * SL;
+            const double* rp = (base == 0 ? ring + RING1 * SL : rb) - SL;   // slot before base
+            column<0>(s, r0, rb + lup, rp + ldn);
+            column<1>(s + 1, r1, rb + SL + lup, rb + ldn);
+            column<2>(s + 2, r2, rb + 2 * SL + lup, rb + SL + ldn);
+            base = base + 3 == RING1 ? 0 : base + 3;
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
     }
@@ -593,7 +611,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
     const int lane = threadIdx.x & 31;
     __shared__ int s_tile[K1_WARPS];
     constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL>::NARR;
-    __shared__ __align__(16) double s_ring[K1_WARPS][RING * NARR * 32];
+    extern __shared__ __align__(16) double s_ring1[];   // [K1_WARPS][RING1 * NARR * 32]
     const int warp = threadIdx.x >> 5;
     pdl_wait();
     pdl_trigger();
@@ -628,7 +646,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
         const AdjPatch p = a.patches[T.patch];
         Strip<SYS, FORM, REV, LIM, CFL> S;
         S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
-        S.setup(T, p, a, lane, lane0, s_ring[warp]);
+        S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32);
         S.run();
         if (CFL) {   // single-strip jobs only (packed jobs require static_speed)
             const double smx = warp_max(S.smx), smy = warp_max(S.smy);
@@ -916,8 +934,11 @@ static void launch_two_rows(const AdjStepArgs& a, cudaStream_t st) {
 template <int SYS, int FORM, bool REV, int LIM, bool CFL>
 static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     static int blocks_per_sm = 0, sms = 0;
+    constexpr int smem = K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL>::NARR * 32 * (int)sizeof(double);
     if (blocks_per_sm == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL>, 32 * K1_WARPS, 0);
+        cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL>, 32 * K1_WARPS,
+                                                      smem);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -926,7 +947,7 @@ static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     int blocks = blocks_per_sm * sms;
     const int need = ((a.job_offsets ? a.njob : a.ntile) + K1_WARPS - 1) / K1_WARPS;
     if (blocks > need) blocks = need;
-    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL>, dim3(blocks), dim3(32 * K1_WARPS), 0, st, a);
+    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL>, dim3(blocks), dim3(32 * K1_WARPS), smem, st, a);
 }
 
 template <int SYS, int FORM, bool REV, int LIM>
