@@ -648,7 +648,7 @@ def bench_c3(steps, variant):
 
 def bench_flagging(p, st, dt, stream):
     import torch
-    from paper_1511_03645_b200 import device
+    from paper_1511_03645_b200 import _lib, device
     nsnap = 41
     ring = adjoint_ring(nsnap)
     T = T_STEPS * dt
@@ -656,34 +656,43 @@ def bench_flagging(p, st, dt, stream):
     from paper_1511_03645_b200 import adjoint
     t = 150 * dt
     res = {}
-    for label, ts in (("single_point", T), ("full_span", 0.0)):
+    ref_bits = {}
+    for label, ts, variant in (("single_point", T, _lib.VARIANT_EXACT), ("full_span", 0.0, _lib.VARIANT_EXACT),
+                               ("full_span_fast", 0.0, _lib.VARIANT_FAST)):
         idx = adjoint.window_indices(t, adjoint.TimeWindow(ts, T), times)
-        device.launch_flag(st, ring, (1024, 1024), (0.0, 0.0), L / 1024, L / 1024, (0.0, 0.0), L / N, L / N,
-                           idx, FLAG_TOL)
+        args = (st, ring, (1024, 1024), (0.0, 0.0), L / 1024, L / 1024, (0.0, 0.0), L / N, L / N, idx, FLAG_TOL)
+        device.launch_flag(*args, variant=variant)
         torch.cuda.synchronize()
         reps = 10
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(reps):
-            _, counts, _, _ = device.launch_flag(st, ring, (1024, 1024), (0.0, 0.0), L / 1024, L / 1024,
-                                                 (0.0, 0.0), L / N, L / N, idx, FLAG_TOL)
+            bits, counts, _, _ = device.launch_flag(*args, variant=variant)
         b.record(stream)
         torch.cuda.synchronize()
         kms = a.elapsed_time(b) / reps
+        nwords = (N * N + 31) // 32
+        ref_bits.setdefault(ts, bits[:nwords].clone())
+        flag_diff = int((bits[:nwords] ^ ref_bits[ts]).ne(0).sum().item())   # words differing from EXACT
         nbytes = 24 * N * N + 24 * 1024 * 1024 * len(idx) + N * N / 8
         # north_star: cells whose inner product lies within 1e-12 relative of the
         # tolerance are reported separately (flags there may differ from the reference)
-        _, _, best, _ = device.launch_flag(st, ring, (1024, 1024), (0.0, 0.0), L / 1024, L / 1024, (0.0, 0.0),
-                                           L / N, L / N, idx, FLAG_TOL, want_best=True)
+        _, _, best, _ = device.launch_flag(*args, want_best=True, variant=variant)
         near = int(((best[0] - FLAG_TOL).abs() <= 1e-12 * FLAG_TOL).sum().item())
         del best
         peak, _ = peaks()
+        fp64 = 40 if variant == _lib.VARIANT_EXACT else 16      # FP64 instructions per cell-snapshot
         res[label] = {"value": N * N / (kms * 1e-3), "unit": "flagged cells/s", "snapshots": len(idx),
                       "kernel_ms": kms, "achieved_GBps": nbytes / (kms * 1e-3) / 1e9,
                       "hbm_frac": nbytes / (kms * 1e-3) / 1e9 / peak,
-                      "flagged": int(counts[0].item()), "near_tolerance_cells": near}
+                      "variant": "exact" if variant == _lib.VARIANT_EXACT else "fast",
+                      "fp64_per_cell_snapshot": fp64,
+                      "fp64_TFLOPs": fp64 * N * N * len(idx) / (kms * 1e-3) / 1e12,
+                      "flagged": int(counts[0].item()), "near_tolerance_cells": near,
+                      "flag_words_differing_from_exact": flag_diff}
     out = dict(res["single_point"])
     out["full_span"] = res["full_span"]
+    out["full_span_fast"] = res["full_span_fast"]
     out["tolerance"] = FLAG_TOL
     return out
 

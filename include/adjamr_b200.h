@@ -312,7 +312,10 @@ typedef struct AdjFlagArgs {
     int32_t layout;              /* ADJ_FLAG_ROWS: every patch row is a multiple of 128 cells and
                                     nxa, nya >= 2 (row-layout kernel for single-snapshot windows) */
     int32_t max_rows, max_cols;  /* ADJ_FLAG_ROWS: largest patch nx, ny                            */
-    int32_t pad;
+    int32_t variant;             /* ADJ_VARIANT_EXACT: the reference's arithmetic (bitwise flags);
+                                    ADJ_VARIANT_FAST: windows of >= 2 snapshots interpolate with
+                                    per-cell corner weights and FMAs (inner products within ~1e-16
+                                    relative; flags identical except within 1e-12 of the tolerance) */
     double origin_x, origin_y, dx, dy;             /* forward level geometry   */
     double a_origin_x, a_origin_y, a_dx, a_dy;     /* adjoint grid geometry    */
     double tolerance;

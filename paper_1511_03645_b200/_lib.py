@@ -111,7 +111,7 @@ class AdjFlagArgs(C.Structure):
                 ("axis_off", P), ("comp_stride", I64), ("aux_stride", I64),
                 ("npatch", I32), ("ndim", I32), ("m", I32), ("ghost", I32), ("swe", I32),
                 ("mode", I32), ("nidx", I32), ("nxa", I32), ("nya", I32), ("max_cells", I32),
-                ("layout", I32), ("max_rows", I32), ("max_cols", I32), ("pad", I32),
+                ("layout", I32), ("max_rows", I32), ("max_cols", I32), ("variant", I32),
                 ("origin_x", D), ("origin_y", D), ("dx", D), ("dy", D),
                 ("a_origin_x", D), ("a_origin_y", D), ("a_dx", D), ("a_dy", D),
                 ("tolerance", D), ("stream", P)]

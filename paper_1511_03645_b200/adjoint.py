@@ -219,10 +219,14 @@ def _adjoint_geometry(store):
 
 
 def flag_level(patches: list[Patch], t: float, store: AdjointSnapshotStore, window: TimeWindow,
-               tolerance: float, want_best: bool = False, time_interp: bool = False, device_bits: bool = False):
+               tolerance: float, want_best: bool = False, time_interp: bool = False, device_bits: bool = False,
+               variant: int | None = None):
     """K3 over every patch of a level in one launch.  Returns (flags: list of
     bool arrays, raw counts: list of int, best: list of arrays or None);
-    ``device_bits``: (packed flag words on the device, level store) instead."""
+    ``device_bits``: (packed flag words on the device, level store) instead.
+    ``variant``: VARIANT_EXACT (default; the reference's arithmetic, bitwise)
+    or VARIANT_FAST (multi-snapshot windows with FMA interpolation; flags
+    identical except for cells within 1e-12 relative of the tolerance)."""
     if store is None:
         raise ConfigurationError("adjoint flagging requires a snapshot store")
     from .solver import level_store
@@ -240,7 +244,8 @@ def flag_level(patches: list[Patch], t: float, store: AdjointSnapshotStore, wind
     spec = patches[0].spec
     bits, counts, best, status = device.launch_flag(
         st, ring, ashape, origin, adx, ady, spec.origin, spec.dx, spec.dy if spec.ndim == 2 else 0.0,
-        idx, tolerance, adj_wet=store._wet_dev if spec.ndim == 2 else None, interp_w=w, want_best=want_best)
+        idx, tolerance, adj_wet=store._wet_dev if spec.ndim == 2 else None, interp_w=w, want_best=want_best,
+        variant=variant)
     if int(status[0].item()):
         raise OutOfRangeError("interpolation point outside the adjoint domain")
     if device_bits:

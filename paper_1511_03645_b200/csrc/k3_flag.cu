@@ -685,11 +685,25 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROWP_MINB) k3_rowp(AdjFl
 }
 
 
-template <bool MODE1, bool SHARED>
+// qhat from the four corners: the reference's order (EXACT, bitwise) or, FAST,
+// per-cell corner weights W = (ux uy, wx uy, ux wy, wx wy) and FMAs
+template <bool FASTW>
+ADJ_D double corner_interp(double v00, double v10, double v01, double v11, double ux, double uy, double wx,
+                           double wy, const double (&W)[4]) {
+    if (FASTW) return fma(v11, W[3], fma(v01, W[2], fma(v10, W[1], v00 * W[0])));
+    return v00 * ux * uy + v10 * wx * uy + v01 * ux * wy + v11 * wx * wy;
+}
+
+template <bool MODE1, bool SHARED, bool FASTW>
 ADJ_D void pair_window(const AdjFlagArgs& a, const int* s_k, const double* s_w, int nidx, const char* ring,
                        int64_t plane_b, int64_t snap_b, const double (&q)[2][3], const unsigned (&b)[2][4],
                        const double (&ux)[2], const double (&uy)[2], const double (&wx)[2], const double (&wy)[2],
                        double (&best)[2]) {
+    double W[2][4];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        W[e][0] = ux[e] * uy[e]; W[e][1] = wx[e] * uy[e]; W[e][2] = ux[e] * wy[e]; W[e][3] = wx[e] * wy[e];
+    }
     for (int n = 0; n < nidx; ++n) {
         const int k = s_k[n];
         double dot[2] = {0.0, 0.0};
@@ -705,8 +719,8 @@ ADJ_D void pair_window(const AdjFlagArgs& a, const int* s_k, const double* s_w, 
                     if (!SHARED && e == 1) {
                         w00 = ld(fc, b[1][0]); w10 = ld(fc, b[1][1]); w01 = ld(fc, b[1][2]); w11 = ld(fc, b[1][3]);
                     }
-                    const double qh = w00 * ux[e] * uy[e] + w10 * wx[e] * uy[e] + w01 * ux[e] * wy[e] + w11 * wx[e] * wy[e];
-                    dot[e] = c == 0 ? qh * q[e][c] : dot[e] + qh * q[e][c];
+                    const double qh = corner_interp<FASTW>(w00, w10, w01, w11, ux[e], uy[e], wx[e], wy[e], W[e]);
+                    dot[e] = c == 0 ? qh * q[e][c] : (FASTW ? fma(qh, q[e][c], dot[e]) : dot[e] + qh * q[e][c]);
                 }
             }
         } else {   // interpolate_time, then the spatial stencil
@@ -728,8 +742,8 @@ ADJ_D void pair_window(const AdjFlagArgs& a, const int* s_k, const double* s_w, 
                         t01 = (1.0 - w) * ld(ac, b[1][2]) + w * ld(bc, b[1][2]);
                         t11 = (1.0 - w) * ld(ac, b[1][3]) + w * ld(bc, b[1][3]);
                     }
-                    const double qh = t00 * ux[e] * uy[e] + t10 * wx[e] * uy[e] + t01 * ux[e] * wy[e] + t11 * wx[e] * wy[e];
-                    dot[e] = c == 0 ? qh * q[e][c] : dot[e] + qh * q[e][c];
+                    const double qh = corner_interp<FASTW>(t00, t10, t01, t11, ux[e], uy[e], wx[e], wy[e], W[e]);
+                    dot[e] = c == 0 ? qh * q[e][c] : (FASTW ? fma(qh, q[e][c], dot[e]) : dot[e] + qh * q[e][c]);
                 }
             }
         }
@@ -738,7 +752,7 @@ ADJ_D void pair_window(const AdjFlagArgs& a, const int* s_k, const double* s_w, 
     }
 }
 
-template <bool MODE1>
+template <bool MODE1, bool FASTW>
 __global__ void __launch_bounds__(256, 3) k3_pair(AdjFlagArgs a) {
     __shared__ int s_k[K3_MAXN];
     __shared__ double s_w[K3_MAXN];
@@ -798,9 +812,9 @@ __global__ void __launch_bounds__(256, 3) k3_pair(AdjFlagArgs a) {
         // one stencil for both cells of every lane -> shared corner loads
         const bool share = !live[1] || (same_row && i0s[0] == i0s[1] && j0s[0] == j0s[1]);
         if (__all_sync(0xffffffffu, share))
-            pair_window<MODE1, true>(a, s_k, s_w, nidx, ring, plane_b, snap_b, q, b, ux, uy, wx, wy, best);
+            pair_window<MODE1, true, FASTW>(a, s_k, s_w, nidx, ring, plane_b, snap_b, q, b, ux, uy, wx, wy, best);
         else
-            pair_window<MODE1, false>(a, s_k, s_w, nidx, ring, plane_b, snap_b, q, b, ux, uy, wx, wy, best);
+            pair_window<MODE1, false, FASTW>(a, s_k, s_w, nidx, ring, plane_b, snap_b, q, b, ux, uy, wx, wy, best);
         bool flag[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -900,8 +914,11 @@ int flag_adjoint(const AdjFlagArgs& a) {
             // pairs pay off once a window has several snapshots (measured: 1.37 vs 1.69 ms at
             // 21 snapshots on C4; 0.23 vs 0.22 ms at one)
             if (k3_pairs() && a.nidx >= 2) {
-                if (m1) k3_pair<true><<<grid, threads, 0, st>>>(a);
-                else k3_pair<false><<<grid, threads, 0, st>>>(a);
+                const bool fw = a.variant == ADJ_VARIANT_FAST;
+                if (m1 && fw) k3_pair<true, true><<<grid, threads, 0, st>>>(a);
+                else if (m1) k3_pair<true, false><<<grid, threads, 0, st>>>(a);
+                else if (fw) k3_pair<false, true><<<grid, threads, 0, st>>>(a);
+                else k3_pair<false, false><<<grid, threads, 0, st>>>(a);
             } else if (a.nidx == 1 && (a.layout & ADJ_FLAG_ROWS) && k3_row_on()) {
                 // (row runs, column segments / warps per CTA, patches); max_rows = the tallest patch
                 const bool pairs = !m1 && (a.layout & ADJ_FLAG_PAIRS) && k3_rowp_on() &&

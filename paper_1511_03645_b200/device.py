@@ -1149,7 +1149,8 @@ K3_ROW_CELLS = 128   # cells per warp of the K3 row-layout kernel (32 lanes x NC
 
 
 def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level_origin, level_dx, level_dy,
-                snap_index, tolerance, adj_wet=None, interp_w=None, want_best=False, stream=None):
+                snap_index, tolerance, adj_wet=None, interp_w=None, want_best=False, stream=None,
+                variant=None):
     """K3 on every patch of the store.  ring: (N, m, nxa[, nya]) float64 CUDA
     tensor; snap_index: list of ints (mode 0) or (k, w) pairs (mode 1).
     Returns (flag_bits uint32 tensor, counts (npatch,) int64 tensor,
@@ -1220,6 +1221,7 @@ def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level
     a.a_origin_y = a_origin[1] if store.ndim == 2 else 0.0
     a.a_dx, a.a_dy = a_dx, a_dy
     a.tolerance = tolerance
+    a.variant = _lib.VARIANT_EXACT if variant is None else variant
     a.stream = _lib.stream_ptr(stream)
     _lib.check(_lib.lib().adj_flag_adjoint(_lib.C.byref(a)), "adj_flag_adjoint")
     best_list = None

@@ -114,3 +114,25 @@ def test_pair_layout_detection(nya, expect):
     tabs = device.flag_axis_tables(st, (NXA, nya), (0.0, 0.0), 1.0 / NXA, 1.0 / nya, (0.0, 0.0),
                                    patches[0].spec.dx, patches[0].spec.dy)
     assert tabs[4] is expect
+
+
+@pytest.mark.parametrize("layout,nya", [("rows", 100), ("rows", 128), ("ragged", 100)])
+@pytest.mark.parametrize("interp", [False, True])
+def test_fast_variant_multi_snapshot(layout, nya, interp):
+    """VARIANT_FAST (corner weights + FMAs) on a multi-snapshot window: inner
+    products within 1e-12 norm-relative of the reference, flags identical
+    except for cells within 1e-12 relative of the tolerance (north_star)."""
+    from paper_1511_03645_b200 import _lib, adjoint
+    _, patches = _level(ROWS if layout == "rows" else RAGGED, seed=5)
+    vals, wet, store = _store(seed=6, dry=True, NYA=nya)
+    t, window = 0.3, adjoint.TimeWindow(0.0, 0.75)
+    tol = 0.7
+    flags, counts, best = adjoint.flag_level(patches, t, store, window, tol, want_best=True, time_interp=interp,
+                                             variant=_lib.VARIANT_FAST)
+    for p, f, c, b in zip(patches, flags, counts, best):
+        ref, n = _oracle(p, vals, wet, t, window, interp, nya)
+        assert n >= 2
+        assert np.max(np.abs(b - ref)) <= 1e-12 * max(np.max(np.abs(ref)), 1e-300)
+        far = np.abs(ref - tol) > 1e-12 * tol
+        assert np.array_equal(f[far], (ref > tol)[far])
+        assert c == int(f.sum())
