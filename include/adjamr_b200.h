@@ -287,7 +287,9 @@ int adj_restrict(const AdjRestrictArgs* a);
  *         (interp_k < 0: use snapshot -interp_k-1 unblended). */
 #define ADJ_FLAG_ROWS 1
 #define ADJ_FLAG_PAIRS 2   /* with ADJ_FLAG_ROWS: every even-aligned column pair of every patch
-                              shares its adjoint stencil column (ratio >= 2 on aligned grids) */
+                              shares its adjoint stencil column (ratio >= 4 on aligned grids) */
+#define ADJ_FLAG_QUADS 4   /* with ADJ_FLAG_PAIRS: every even-aligned row pair shares its adjoint
+                              stencil row too, and every patch has an even number of rows */
 typedef struct AdjFlagArgs {
     const double* q;             /* forward level store                        */
     const double* aux;           /* forward aux (swe: depth plane 1)          */

@@ -843,6 +843,204 @@ __global__ void __launch_bounds__(256, 3) k3_pair(AdjFlagArgs a) {
     if (lane == 0 && cnt) atomicAdd(&a.counts[pidx], cnt);
 }
 
+// ---------------------------------------------------------------------------
+// Windows of >= 2 snapshots on the row layout with quads (ADJ_FLAG_QUADS:
+// even-aligned row pairs and column pairs share their adjoint stencil, e.g.
+// ratio 4 on aligned grids, C4).  Lane l owns the 2x2 cells (rows i, i+1;
+// columns 64 seg + 2l, +1): one snapshot's 12 corner loads serve 4 cells, the
+// next snapshot's corners load while this one is interpolated, the window
+// list sits in shared memory and the warp marches down row pairs with the
+// state streamed by cp.async.  EXACT: k3_row's per-cell arithmetic (bitwise);
+// FAST: per-cell corner weights and FMAs.
+#ifndef K3_QUAD_MINB
+#define K3_QUAD_MINB 3       // EXACT: 168 registers (a few spilled bytes), 3 CTAs/SM
+#endif
+#ifndef K3_QUAD_MINB_FAST
+#define K3_QUAD_MINB_FAST 2  // FAST: the corner weights need ~225 registers
+#endif
+
+#ifndef K3_QUAD_DEPTH
+#define K3_QUAD_DEPTH 3   // snapshots of corners in registers (2: one ahead, 3: two ahead)
+#endif
+
+template <bool FASTW>
+__global__ void __launch_bounds__(32 * K3_ROW_WARPS, FASTW ? K3_QUAD_MINB_FAST : K3_QUAD_MINB)
+    k3_quad(AdjFlagArgs a, int run) {
+    __shared__ const char* s_base[K3_MAXN];     // snapshot base addresses
+    __shared__ double2 s_q[K3_ROW_WARPS][RDEPTH][6][32];
+    const int nidx = a.nidx;
+    {
+        const int64_t snap_b = (int64_t)a.nxa * a.nya * 3 * 8;
+        for (int n = threadIdx.x; n < nidx; n += blockDim.x)
+            s_base[n] = reinterpret_cast<const char*>(a.ring) + (int64_t)a.snap_index[n] * snap_b;
+    }
+    __syncthreads();
+    const int pidx = blockIdx.z;
+    const AdjPatch p = a.patches[pidx];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned seg = blockIdx.y * K3_ROW_WARPS + warp;
+    const unsigned nseg = (unsigned)p.ny / 64u;
+    const unsigned r0 = blockIdx.x * (unsigned)run;               // run is even
+    if (seg >= nseg || r0 >= (unsigned)p.nx) return;               // warp-uniform; no barrier below
+    const unsigned r1 = min(r0 + (unsigned)run, (unsigned)p.nx);   // nx is even
+    const unsigned ny = (unsigned)p.ny, j = seg * 64u + 2u * lane;
+    const int g = a.ghost;
+    const int64_t cs = a.comp_stride;
+    const int64_t nya = a.nya;
+    const int64_t plane = (int64_t)a.nxa * nya;
+    const int64_t rowoff = a.axis_off[2 * pidx], coloff = a.axis_off[2 * pidx + 1];
+    const double* qcol = a.q + p.offset + (int64_t)g * p.pitch + g + j;   // 16-byte aligned (even column)
+
+    auto prefetch = [&](unsigned i, int buf) {   // rows i, i+1
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_q[warp][buf][r * 3 + cc][lane]);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
+                             "l"(qcol + (int64_t)(i + r) * p.pitch + cc * cs) : "memory");
+            }
+    };
+#pragma unroll
+    for (int d = 0; d < RDEPTH - 1; ++d) {
+        if (r0 + 2 * d < r1) prefetch(r0 + 2 * d, d);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    const int j0 = __ldg(a.axis_i + coloff + j);
+    double wy[2], uy[2];
+    int ja[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        wy[e] = __ldg(a.axis_w + coloff + j + e);
+        uy[e] = 1.0 - wy[e];
+        ja[e] = a.axis_dry ? __ldg(a.axis_dry + coloff + j + e) : 0;
+    }
+    unsigned off[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) off[c] = (unsigned)(((int64_t)c * plane + j0) * 8);
+    const int64_t rowbytes = nya * 8;
+
+    auto corners = [&](double (&C)[3][4], int n, int64_t rowb) {
+        const char* b0 = s_base[n] + rowb;
+        const char* b1 = b0 + rowbytes;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double* q0 = reinterpret_cast<const double*>(b0 + off[c]);
+            const double* q1 = reinterpret_cast<const double*>(b1 + off[c]);
+            C[c][0] = __ldg(q0); C[c][1] = __ldg(q1); C[c][2] = __ldg(q0 + 1); C[c][3] = __ldg(q1 + 1);
+        }
+    };
+    unsigned long long cnt = 0;
+    int buf = 0;
+    int i0n = __ldg(a.axis_i + rowoff + r0);
+    double wxn[2] = {__ldg(a.axis_w + rowoff + r0), __ldg(a.axis_w + rowoff + r0 + 1)};
+    for (unsigned i = r0; i < r1; i += 2, buf = buf + 1 == RDEPTH ? 0 : buf + 1) {
+        if (i + 2 * (RDEPTH - 1) < r1) prefetch(i + 2 * (RDEPTH - 1), buf == 0 ? RDEPTH - 1 : buf - 1);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const int64_t rowb = (int64_t)i0n * rowbytes;
+        double wx[2] = {wxn[0], wxn[1]}, ux[2];
+        ux[0] = 1.0 - wx[0]; ux[1] = 1.0 - wx[1];
+        double C0[3][4], C1[3][4], C2[3][4];
+        corners(C0, 0, rowb);
+        if (K3_QUAD_DEPTH > 2 && nidx > 1) corners(C1, 1, rowb);
+        if (i + 2 < r1) {   // the next row pair's stencil row and weights
+            i0n = __ldg(a.axis_i + rowoff + i + 2);
+            wxn[0] = __ldg(a.axis_w + rowoff + i + 2); wxn[1] = __ldg(a.axis_w + rowoff + i + 3);
+        }
+        double W[2][2][4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                W[r][e][0] = ux[r] * uy[e]; W[r][e][1] = wx[r] * uy[e];
+                W[r][e][2] = ux[r] * wy[e]; W[r][e][3] = wx[r] * wy[e];
+            }
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(RDEPTH - 1) : "memory");
+        __syncwarp();
+        double q[2][2][3];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double2 v = s_q[warp][buf][r * 3 + c][lane];
+                q[r][0][c] = v.x; q[r][1][c] = v.y;
+            }
+        __syncwarp();
+        double best[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        auto accumulate = [&](const double (&C)[3][4]) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    double d = 0.0;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const double qh = corner_interp<FASTW>(C[c][0], C[c][1], C[c][2], C[c][3], ux[r], uy[e],
+                                                               wx[r], wy[e], W[r][e]);
+                        d = c == 0 ? qh * q[r][e][c] : (FASTW ? fma(qh, q[r][e][c], d) : d + qh * q[r][e][c]);
+                    }
+                    best[r][e] = fmax(best[r][e], fabs(d));
+                }
+        };
+        if (K3_QUAD_DEPTH > 2) {                 // snapshots n+1, n+2 in flight during n's arithmetic
+            for (int n = 0; n < nidx; n += 3) {
+                if (n + 2 < nidx) corners(C2, n + 2, rowb);
+                accumulate(C0);
+                if (n + 1 >= nidx) break;
+                if (n + 3 < nidx) corners(C0, n + 3, rowb);
+                accumulate(C1);
+                if (n + 2 >= nidx) break;
+                if (n + 4 < nidx) corners(C1, n + 4, rowb);
+                accumulate(C2);
+            }
+        } else {
+            for (int n = 0; n < nidx; n += 2) {      // snapshot n+1's corners load during n's arithmetic
+                if (n + 1 < nidx) corners(C1, n + 1, rowb);
+                accumulate(C0);
+                if (n + 1 < nidx) {
+                    if (n + 2 < nidx) corners(C0, n + 2, rowb);
+                    accumulate(C1);
+                }
+            }
+        }
+        (void)C2;
+        unsigned bits = 0;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            if (a.swe) {   // forward dry cells
+                const double* cp = a.aux + a.aux_stride + p.offset + (int64_t)(i + r + g) * p.pitch + (j + g);
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (!(__ldg(cp + e) > 0.0)) best[r][e] = 0.0;
+            }
+            if (a.adj_wet != nullptr && a.axis_dry) {   // adjoint cell containing the centre is dry
+                const int ia = __ldg(a.axis_dry + rowoff + i + r);
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (!a.adj_wet[(int64_t)ia * nya + ja[e]]) best[r][e] = 0.0;
+            }
+            const unsigned base = (i + r) * ny + seg * 64u;
+            if (a.best != nullptr)
+                *reinterpret_cast<double2*>(a.best + a.best_offset[pidx] + base + 2u * lane) =
+                    make_double2(best[r][0], best[r][1]);
+            bits |= (best[r][0] > a.tolerance ? 1u : 0u) << (2 * r) | (best[r][1] > a.tolerance ? 2u : 0u) << (2 * r);
+        }
+        // word (row r, half h), bit b = cell 32h + b of the row, held by lane 16h + b/2 as element b%2
+        const unsigned t0 = __shfl_sync(0xffffffffu, bits, lane >> 1) >> (lane & 1);
+        const unsigned t1 = __shfl_sync(0xffffffffu, bits, 16 + (lane >> 1)) >> (lane & 1);
+        const unsigned w00 = __ballot_sync(0xffffffffu, t0 & 1u), w01 = __ballot_sync(0xffffffffu, t1 & 1u);
+        const unsigned w10 = __ballot_sync(0xffffffffu, (t0 >> 2) & 1u), w11 = __ballot_sync(0xffffffffu, (t1 >> 2) & 1u);
+        if (lane < 4) {
+            const unsigned r = lane >> 1, h = lane & 1u;
+            const unsigned wv = lane == 0 ? w00 : (lane == 1 ? w01 : (lane == 2 ? w10 : w11));
+            a.flag_bits[p.flag_word + (((i + r) * ny + seg * 64u) >> 5) + h] = wv;
+        }
+        cnt += __popc(w00) + __popc(w01) + __popc(w10) + __popc(w11);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (lane == 0 && cnt) atomicAdd(&a.counts[pidx], cnt);
+}
+
 // ADJAMR_K3_PAIRS=0 selects the one-cell-per-lane table kernel (A/B measurements)
 static bool k3_pairs() {
     static int on = -1;
@@ -851,6 +1049,37 @@ static bool k3_pairs() {
         on = (e && e[0] == '0') ? 0 : 1;
     }
     return on == 1;
+}
+
+// ADJAMR_K3_QUAD=0 disables the quad kernel for multi-snapshot windows (A/B measurements)
+static bool k3_quad_on() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("ADJAMR_K3_QUAD");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+// rows per warp of k3_quad: even, and the grid about one wave of resident CTAs
+static int k3_quad_run(const AdjFlagArgs& a) {
+    static int resident[2] = {0, 0};
+    const bool fw = a.variant == ADJ_VARIANT_FAST;
+    int& res = resident[fw ? 1 : 0];
+    if (res == 0) {
+        int per_sm = 0, dev = 0, sms = 0;
+        if (fw) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_quad<true>, 32 * K3_ROW_WARPS, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_quad<false>, 32 * K3_ROW_WARPS, 0);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        res = (per_sm < 1 ? 1 : per_sm) * sms;
+    }
+    const int64_t segs = ((int64_t)a.max_cols / 64 + K3_ROW_WARPS - 1) / K3_ROW_WARPS;
+    int64_t runs = res / (segs * a.npatch > 0 ? segs * a.npatch : 1);
+    if (runs < 1) runs = 1;
+    int64_t run = (a.max_rows + runs - 1) / runs;
+    run += run & 1;
+    return (int)(run < 2 ? 2 : run);
 }
 
 // ADJAMR_K3_ROWP=0 disables the paired row kernel (A/B measurements)
@@ -913,7 +1142,14 @@ int flag_adjoint(const AdjFlagArgs& a) {
         } else if (a.ndim == 2 && a.m == 3) {
             // pairs pay off once a window has several snapshots (measured: 1.37 vs 1.69 ms at
             // 21 snapshots on C4; 0.23 vs 0.22 ms at one)
-            if (k3_pairs() && a.nidx >= 2) {
+            if (!m1 && a.nidx >= 2 && (a.layout & ADJ_FLAG_ROWS) && (a.layout & ADJ_FLAG_QUADS) && k3_quad_on() &&
+                (int64_t)a.nxa * a.nya * 3 * 8 < (int64_t(1) << 32)) {
+                const int run = k3_quad_run(a);
+                const dim3 gr((unsigned)((a.max_rows + run - 1) / run),
+                              (unsigned)((a.max_cols / 64 + K3_ROW_WARPS - 1) / K3_ROW_WARPS), (unsigned)a.npatch);
+                if (a.variant == ADJ_VARIANT_FAST) k3_quad<true><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a, run);
+                else k3_quad<false><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a, run);
+            } else if (k3_pairs() && a.nidx >= 2) {
                 const bool fw = a.variant == ADJ_VARIANT_FAST;
                 if (m1 && fw) k3_pair<true, true><<<grid, threads, 0, st>>>(a);
                 else if (m1) k3_pair<true, false><<<grid, threads, 0, st>>>(a);

@@ -1131,16 +1131,21 @@ def flag_axis_tables(store: LevelStore, ring_shape, a_origin, a_dx, a_dy, level_
         W[pos] = w
         I[pos] = i0
         Dr[pos] = dry
-        if ax == 1:   # every even-aligned column pair shares its adjoint stencil (K3 paired row kernel)
-            ev = (t % 2 == 0) & (t + 1 < np.repeat(n, n))
-            pairs_ok = bool(np.all(I[pos[ev]] == I[pos[ev] + 1])) and bool(np.all(n % 2 == 0))
+        # every even-aligned pair along this axis shares its adjoint stencil index
+        # (K3 paired row kernel: columns; quad kernel: rows and columns)
+        ev = (t % 2 == 0) & (t + 1 < np.repeat(n, n))
+        ok = bool(np.all(I[pos[ev]] == I[pos[ev] + 1])) and bool(np.all(n % 2 == 0))
+        if ax == 1:
+            pairs_ok = ok
+        else:
+            rows_ok = ok
     offs = np.stack([poff, poff + ext[:, 0]] if nd == 2 else [poff, poff], axis=1).reshape(-1)
     torch = _torch()
     tabs = (torch.from_numpy(W).to("cuda"),
             torch.from_numpy(I).to("cuda"),
             torch.from_numpy(Dr).to("cuda"),
             torch.from_numpy(np.array(offs, dtype=np.int64)).to("cuda"),
-            nd == 2 and pairs_ok)
+            nd == 2 and pairs_ok, nd == 2 and pairs_ok and rows_ok)
     store._scratch[key] = tabs
     return tabs
 
@@ -1193,8 +1198,8 @@ def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level
     a.best = _ptr(best)
     a.best_offset = _ptr(best_off)
     a.status = _ptr(status)
-    tw, ti, tdry, toff, pairs_ok = flag_axis_tables(store, ring_shape, a_origin, a_dx, a_dy, level_origin, level_dx,
-                                                    level_dy)
+    tw, ti, tdry, toff, pairs_ok, quads_ok = flag_axis_tables(store, ring_shape, a_origin, a_dx, a_dy,
+                                                              level_origin, level_dx, level_dy)
     a.axis_w, a.axis_i, a.axis_dry, a.axis_off = _ptr(tw), _ptr(ti), _ptr(tdry), _ptr(toff)
     a.comp_stride = store.plane
     a.aux_stride = store.plane
@@ -1211,7 +1216,7 @@ def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level
     # row layout: whole 128-cell row segments per warp, interior adjoint corners
     if (store.ndim == 2 and ring_shape[0] >= 2 and ring_shape[1] >= 2
             and bool((store.table_np["ny"] % K3_ROW_CELLS == 0).all())):
-        a.layout = _lib.FLAG_ROWS | (_lib.FLAG_PAIRS if pairs_ok else 0)
+        a.layout = (_lib.FLAG_ROWS | (_lib.FLAG_PAIRS if pairs_ok else 0) | (_lib.FLAG_QUADS if quads_ok else 0))
         a.max_rows = int(store.table_np["nx"].max())
         a.max_cols = int(store.table_np["ny"].max())
     a.origin_x = level_origin[0]

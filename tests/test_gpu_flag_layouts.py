@@ -114,6 +114,7 @@ def test_pair_layout_detection(nya, expect):
     tabs = device.flag_axis_tables(st, (NXA, nya), (0.0, 0.0), 1.0 / NXA, 1.0 / nya, (0.0, 0.0),
                                    patches[0].spec.dx, patches[0].spec.dy)
     assert tabs[4] is expect
+    assert tabs[5] is False      # 48 adjoint rows over 64 forward rows: row pairs straddle centres
 
 
 @pytest.mark.parametrize("layout,nya", [("rows", 100), ("rows", 128), ("ragged", 100)])
@@ -135,4 +136,55 @@ def test_fast_variant_multi_snapshot(layout, nya, interp):
         assert np.max(np.abs(b - ref)) <= 1e-12 * max(np.max(np.abs(ref)), 1e-300)
         far = np.abs(ref - tol) > 1e-12 * tol
         assert np.array_equal(f[far], (ref > tol)[far])
+        assert c == int(f.sum())
+
+
+def _store_n(seed, nxa, nya, dry):
+    from paper_1511_03645_b200 import adjoint
+    from paper_1511_03645_b200.geometry import UniformField
+    rng = np.random.default_rng(seed)
+    vals = rng.standard_normal((len(TIMES), 3, nxa, nya))
+    fields = [UniformField(values=vals[k], origin=(0.0, 0.0), dx=1.0 / nxa, dy=1.0 / nya, time=t)
+              for k, t in enumerate(TIMES)]
+    wet = rng.uniform(size=(nxa, nya)) > 0.1 if dry else None
+    return vals, wet, adjoint.AdjointSnapshotStore(times=TIMES, fields=fields, window=adjoint.TimeWindow(0.0, 1.0),
+                                                   wet=wet)
+
+
+@pytest.mark.parametrize("variant", ["exact", "fast"])
+@pytest.mark.parametrize("dry", [False, True])
+def test_quad_kernel_multi_snapshot(variant, dry):
+    """Ratio 4 in both axes (adjoint 16 x 128 under the 64 x 512 level): every
+    even-aligned 2x2 quad shares its stencil, so windows of >= 2 snapshots run
+    the quad kernel (k3_quad).  EXACT: bitwise; FAST: 1e-12 norm-relative and
+    flags equal away from the tolerance."""
+    from paper_1511_03645_b200 import _lib, adjoint, device, solver
+    nxa, nya = 16, 128
+    shapes = [((0, 0), (20, 256)), ((20, 256), (18, 128)), ((40, 0), (8, 384))]
+    _, patches = _level(shapes, seed=8)
+    vals, wet, store = _store_n(9, nxa, nya, dry)
+    t, window = 0.3, adjoint.TimeWindow(0.0, 0.75)
+    tol = 0.7
+    var = _lib.VARIANT_EXACT if variant == "exact" else _lib.VARIANT_FAST
+    flags, counts, best = adjoint.flag_level(patches, t, store, window, tol, want_best=True, variant=var)
+    st = solver.store_of(patches[0])
+    tabs = device.flag_axis_tables(st, (nxa, nya), (0.0, 0.0), 1.0 / nxa, 1.0 / nya, (0.0, 0.0),
+                                   patches[0].spec.dx, patches[0].spec.dy)
+    assert tabs[5] is True
+    idx = adjoint.query_window_times(t, window, _FakeStore(window))
+    assert len(idx) >= 2
+    for p, f, c, b in zip(patches, flags, counts, best):
+        lo, shape, dx, dy = p.spec.lo, p.spec.shape, p.spec.dx, p.spec.dy
+        x = (np.arange(lo[0], lo[0] + shape[0]) + 0.5) * dx
+        y = (np.arange(lo[1], lo[1] + shape[1]) + 0.5) * dy
+        xc, yc = np.broadcast_to(x[:, None], shape), np.broadcast_to(y[None, :], shape)
+        ref = O.inner_product(p.state[:, 2:-2, 2:-2], xc, yc, vals, idx, (0.0, 0.0), 1.0 / nxa, 1.0 / nya,
+                              p.aux.wet[2:-2, 2:-2], wet)
+        if variant == "exact":
+            assert np.array_equal(b, ref)
+            assert np.array_equal(f, ref > tol)
+        else:
+            assert np.max(np.abs(b - ref)) <= 1e-12 * np.max(np.abs(ref))
+            far = np.abs(ref - tol) > 1e-12 * tol
+            assert np.array_equal(f[far], (ref > tol)[far])
         assert c == int(f.sum())
