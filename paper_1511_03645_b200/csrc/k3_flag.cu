@@ -1061,6 +1061,16 @@ static bool k3_quad_on() {
     return on == 1;
 }
 
+// ADJAMR_K3_QUAD1=1 also routes single-snapshot windows to k3_quad (A/B measurements)
+static bool k3_quad1() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("ADJAMR_K3_QUAD1");
+        on = (e && e[0] == '1') ? 1 : 0;
+    }
+    return on == 1;
+}
+
 // rows per warp of k3_quad: even, and the grid about one wave of resident CTAs
 static int k3_quad_run(const AdjFlagArgs& a) {
     static int resident[2] = {0, 0};
@@ -1142,7 +1152,8 @@ int flag_adjoint(const AdjFlagArgs& a) {
         } else if (a.ndim == 2 && a.m == 3) {
             // pairs pay off once a window has several snapshots (measured: 1.37 vs 1.69 ms at
             // 21 snapshots on C4; 0.23 vs 0.22 ms at one)
-            if (!m1 && a.nidx >= 2 && (a.layout & ADJ_FLAG_ROWS) && (a.layout & ADJ_FLAG_QUADS) && k3_quad_on() &&
+            if (!m1 && a.nidx >= (k3_quad1() ? 1 : 2) && (a.layout & ADJ_FLAG_ROWS) && (a.layout & ADJ_FLAG_QUADS) &&
+                k3_quad_on() &&
                 (int64_t)a.nxa * a.nya * 3 * 8 < (int64_t(1) << 32)) {
                 const int run = k3_quad_run(a);
                 const dim3 gr((unsigned)((a.max_rows + run - 1) / run),
