@@ -151,6 +151,21 @@ typedef struct AdjGhostPlanFillArgs {
 } AdjGhostPlanFillArgs;
 int adj_fill_ghost_plan(const AdjGhostPlanFillArgs* a);
 
+/* Restriction fused into the step of the finest level's last substep
+ * (restrict_fine_to_coarse, amr.py:399-450): every r x r block of new fine
+ * interior values is averaged into its covered coarse cell as the strip
+ * march produces it.  cell[base[patch] + (x/r) * (ny/r) + y/r] is the coarse
+ * cell's offset in the coarse plane (-1: not covered).  FAST 2D only, every
+ * tile's i0, j0, ni, nj a multiple of r; sum order differs from numpy's (the
+ * FAST tolerance). */
+typedef struct AdjStepRestrict {
+    double* q_coarse;            /* coarse level state written (cur)                              */
+    const int32_t* cell;         /* per fine r x r block: coarse cell offset or -1                */
+    const int32_t* base;         /* per fine patch: its first block in cell                       */
+    int64_t coarse_comp_stride;
+    int32_t ratio, pad;          /* ratio 2 or 4; 0: no fused restriction                          */
+} AdjStepRestrict;
+
 /* K1: wave-propagation step of every patch of a level.
  * Replaces step_patch / step_patch_1d / step_patch_2d (solver.py:415-522), the
  * Riemann and transverse solvers (equations.py:98-349), TimeReversed
@@ -186,6 +201,8 @@ typedef struct AdjStepArgs {
                                   ADJ_STEP_COUNTER_ZERO): the level's planned ghost fill of q_in runs
                                   inside this launch before the step (a grid barrier separates them);
                                   work_counter then holds 3 zeroed ints */
+    AdjStepRestrict fine_restrict; /* optional (ratio > 0): restriction into the coarse level fused
+                                  into this step (FAST 2D, static_speed, forward wave form) */
 } AdjStepArgs;
 /* AdjStepArgs.flags */
 #define ADJ_STEP_KEEP_NONFINITE 1   /* do not zero nonfinite: accumulate over launches */

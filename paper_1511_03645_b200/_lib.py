@@ -68,6 +68,11 @@ class AdjGhostPlanFillArgs(C.Structure):
                 ("w_time", D), ("w_time_dev", P), ("stream", P)]
 
 
+class AdjStepRestrict(C.Structure):
+    _fields_ = [("q_coarse", P), ("cell", P), ("base", P), ("coarse_comp_stride", I64), ("ratio", I32),
+                ("pad", I32)]
+
+
 class AdjStepArgs(C.Structure):
     _fields_ = [("q_in", P), ("q_out", P), ("aux", P), ("patches", P), ("tiles", P),
                 ("speed_max", P), ("nonfinite", P), ("work_counter", P), ("static_speed", P), ("job_offsets", P),
@@ -75,7 +80,8 @@ class AdjStepArgs(C.Structure):
                 ("npatch", I32), ("ntile", I32), ("ndim", I32), ("ghost", I32),
                 ("system", I32), ("form", I32), ("reversed", I32), ("limiter", I32),
                 ("variant", I32), ("flags", I32),
-                ("dt", D), ("dtdx", D), ("dtdy", D), ("gravity", D), ("stream", P), ("prefill", AdjGhostPlanFillArgs)]
+                ("dt", D), ("dtdx", D), ("dtdy", D), ("gravity", D), ("stream", P), ("prefill", AdjGhostPlanFillArgs),
+                ("fine_restrict", AdjStepRestrict)]
 
 
 class AdjPhysArgs(C.Structure):

@@ -699,6 +699,9 @@ def _fill_physical_subset(st, slots, boundary, equation, level_shape):
 USE_GHOST_PLAN = True
 # planned restriction (device.RestrictPlan, one thread per coarse cell); False: per-rect blocks
 USE_RESTRICT_PLAN = True
+# finest level's last substep on the fast static-CFL path: restriction into the coarser level
+# fused into the step launch (device.FusedRestrict); False: a separate K4 launch
+USE_FUSED_RESTRICT = True
 # fast static-CFL levels: run the planned fill inside the step launch (prefill + grid barrier).
 # Off: measured slower on C5 (0.94-0.96 vs 0.75 ms per coarse step) -- the persistent step grid
 # has ~57K threads for ~400K gather entries, the standalone gather ~300K
@@ -1059,13 +1062,39 @@ def _retry_half_steps(st, slot, patch, dt, ctx):
     del torch
 
 
-def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext, prefill=None):
+def _fused_restrict(hierarchy, level, pl, ctx, cfl_static):
+    """(FusedRestrict, coarse store) when this step may also restrict the
+    level into level-1: the finest level's last substep of the interval
+    (the caller asks), fast static path, no CFL retry, aligned tiles."""
+    if not USE_FUSED_RESTRICT or level < 2 or pl.cst is None or hierarchy.patches(level + 1):
+        return None
+    _, form, rev = ctx.equation.kernel_spec()
+    if cfl_static is None or np.any(cfl_static > 1.0 + 1e-12) or form != _lib.FORM_WAVE or rev:
+        return None
+    r = hierarchy.ratio_to_finer(level - 1)
+    cst, st = pl.cst, pl.st
+    if not device.FusedRestrict.usable(cst, st, r):
+        return None
+    fr = getattr(pl, "fused_restrict", None)
+    if fr is None or fr[0] is not cst:
+        fr = (cst, device.FusedRestrict(cst, st, _restrict_rects(hierarchy.patches(level - 1),
+                                                                 hierarchy.patches(level), r), r))
+        pl.fused_restrict = fr
+    cst.sync_in()
+    cst._unalias()
+    return fr[1], cst
+
+
+def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext, prefill=None,
+               restrict_into: bool = False) -> bool:
     """save_old + step of every patch of the level in one K1 launch, with the
     reference's per-patch CFL retry and cell-step accounting (amr.py:620-631).
 
     On the fast path (no dry cells) the CFL bound is the static per-patch
     material speed, so no device->host sync is needed; non-finite results are
-    accumulated on the device and raised at the end of the top-level advance."""
+    accumulated on the device and raised at the end of the top-level advance.
+    ``restrict_into``: this is the last substep of the interval, so the
+    restriction into level-1 may run inside the launch; returns whether it did."""
     patches = hierarchy.patches(level)
     pl = _plan(hierarchy, level)
     st = pl.st
@@ -1076,11 +1105,18 @@ def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext
     static = ctx.variant == _lib.VARIANT_FAST and st.ndim == 2 and not st.any_dry()
     if prefill is not None and not static:
         raise RuntimeError("a deferred ghost fill needs the fast static-CFL step")
-    smax, bad = device.launch_step(st, dt, ctx.equation, ctx.limiter, ctx.variant, out, accumulate=static,
-                                   prefill=prefill)
     spec = patches[0].spec
     dtdx = dt / spec.dx
     dtdy = dt / spec.dy if spec.ndim == 2 else 0.0
+    cfl_static = None
+    if static:
+        sm0 = st.static_speed_np()
+        cfl_static = np.maximum(sm0[:, 0] * dtdx, sm0[:, 1] * dtdy)
+    fused = _fused_restrict(hierarchy, level, pl, ctx, cfl_static) if restrict_into and prefill is None else None
+    if fused is not None:
+        ctx.__dict__["fused_restrictions"] = ctx.__dict__.get("fused_restrictions", 0) + 1
+    smax, bad = device.launch_step(st, dt, ctx.equation, ctx.limiter, ctx.variant, out, accumulate=static,
+                                   prefill=prefill, fine_restrict=fused)
     sm = st.static_speed_np() if static else smax.cpu().numpy()
     cfl = sm[:, 0] * dtdx if spec.ndim == 1 else np.maximum(sm[:, 0] * dtdx, sm[:, 1] * dtdy)
     st.ghost_src = st.cur
@@ -1099,6 +1135,7 @@ def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext
         nf = bad.cpu().numpy()
         if np.any(nf):
             raise NumericalBlowupError(f"non-finite state at t={t + dt}")
+    return fused is not None
 
 
 def _raise_pending(ctx):
@@ -1130,16 +1167,19 @@ def advance_hierarchy(hierarchy: PatchHierarchy, level: int, dt: float, ctx: Amr
         _raise_pending(ctx)
 
 
-def _advance(hierarchy, level, dt, ctx):
+def _advance(hierarchy, level, dt, ctx, restrict_into: bool = False) -> bool:
+    """One step of ``level`` and its subcycled finer levels; returns whether
+    the restriction of ``level`` into level-1 already ran (fused into the
+    step of the interval's last substep of the finest level)."""
     count = ctx.step_counts.get(level, 0)
     if level < hierarchy.max_levels and count > 0 and count % ctx.regrid_interval == 0:
         regrid(hierarchy, level + 1, ctx)
     patches = hierarchy.patches(level)
     if not patches:
-        return
+        return False
     t = patches[0].time
     pre = fill_level_ghosts(hierarchy, level, t, ctx, defer=True)
-    step_level(hierarchy, level, dt, ctx, prefill=pre)
+    fused = step_level(hierarchy, level, dt, ctx, prefill=pre, restrict_into=restrict_into)
     t_new = t + dt
     st = patches[0]._store
     st.set_level_times(t_new, t)
@@ -1149,9 +1189,12 @@ def _advance(hierarchy, level, dt, ctx):
     if level < hierarchy.max_levels and hierarchy.patches(level + 1):
         fill_level_ghosts(hierarchy, level, t_new, ctx)
         ratio = hierarchy.ratio_to_finer(level)
-        for _ in range(ratio):
-            _advance(hierarchy, level + 1, dt / ratio, ctx)
-        restrict_fine_to_coarse(hierarchy, level)
+        done = False
+        for k in range(ratio):
+            done = _advance(hierarchy, level + 1, dt / ratio, ctx, restrict_into=k == ratio - 1)
+        if not done:
+            restrict_fine_to_coarse(hierarchy, level)
+    return fused
 
 
 class SweepGraph:

@@ -83,6 +83,14 @@ int adj_step_level(const AdjStepArgs* a) {
         if (a->prefill.plan.nc > 0 && !(a->prefill.q_coarse_old && a->prefill.q_coarse_new && a->prefill.plan.c_base))
             return adj::bad("null prefill coarse state");
     }
+    if (a->fine_restrict.ratio != 0) {
+        const AdjStepRestrict& r = a->fine_restrict;
+        if (!(a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed && a->form == ADJ_FORM_WAVE &&
+              !a->reversed && !(a->flags & ADJ_STEP_TWO_ROWS) && a->prefill.plan.n == 0))
+            return adj::bad("fused restriction needs the FAST 2D static-CFL forward wave step without prefill");
+        if (!(r.ratio == 2 || r.ratio == 4)) return adj::bad("fused restriction ratio must be 2 or 4");
+        if (!(r.q_coarse && r.cell && r.base)) return adj::bad("null fused restriction tables");
+    }
     cudaStream_t st = (cudaStream_t)a->stream;
     int rc = ADJ_OK;
     const bool static_cfl = a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed;

@@ -365,7 +365,7 @@ constexpr int RING1 = 3 * NGRP;
 // lives in a 3-slot ring indexed by (column mod 3); column<K> is the body of
 // the march for a column in slot K, so the 3-way unrolled loop rotates roles
 // by renaming instead of moving registers.
-template <int SYS, int FORM, bool REV, int LIM, bool CFL>
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false>
 struct Strip {
     static constexpr bool SWE = SYS == ADJ_SYS_SWE2D;
     static constexpr bool FWD_WAVE = FORM == ADJ_FORM_WAVE && !REV;
@@ -391,6 +391,13 @@ struct Strip {
     double cup[3], mup[3];         // row j+1 materials of column
     double smx, smy;
     unsigned bad;
+    // fused restriction (RST): block sums of the new values over R rows x R columns
+    double ra0, ra1, ra2;
+    double* rq;                    // coarse state
+    const int32_t* rcell;
+    int64_t rcs;
+    int rr, rx0, rbase, rnyb, rby;  // ratio, strip x origin, patch block base, blocks per row, block row
+    bool rlead;                     // first row of an output block
 
     static constexpr int NARR = SWE ? 4 : 5;
 
@@ -531,6 +538,24 @@ struct Strip {
             const unsigned ex = 0x7ff00000u;
             bad |= (((unsigned)__double2hiint(n0) & ex) == ex) | (((unsigned)__double2hiint(n1) & ex) == ex) |
                    (((unsigned)__double2hiint(n2) & ex) == ex);
+            if (RST) { ra0 += n0; ra1 += n1; ra2 += n2; }
+        }
+        if (RST && s >= i0 + 2 && s <= s_last && ((s - 2) & (rr - 1)) == rr - 1) {   // warp-uniform
+            // sum the block's R rows (lanes), then its leader lane writes the mean
+            double v0 = ra0 + sh_dn(ra0), v1 = ra1 + sh_dn(ra1), v2 = ra2 + sh_dn(ra2);
+            if (rr == 4) {
+                v0 += __shfl_down_sync(FULL, v0, 2);
+                v1 += __shfl_down_sync(FULL, v1, 2);
+                v2 += __shfl_down_sync(FULL, v2, 2);
+            }
+            if (rlead) {
+                const int dst = __ldg(rcell + rbase + ((rx0 + s - 2) / rr) * rnyb + rby);
+                if (dst >= 0) {
+                    const double inv = rr == 4 ? 0.0625 : 0.25;   // np.mean: sum / r^2 (a power of two)
+                    rq[dst] = v0 * inv; rq[rcs + dst] = v1 * inv; rq[2 * rcs + dst] = v2 * inv;
+                }
+            }
+            ra0 = ra1 = ra2 = 0.0;
         }
     }
 
@@ -557,6 +582,17 @@ struct Strip {
         hx = 0.5 * dtdx; hy = 0.5 * dtdy;
         colbase = g + T.i0;
         i0 = 0; ni = T.ni;
+        if (RST) {
+            const AdjStepRestrict& R = a.fine_restrict;
+            ra0 = ra1 = ra2 = 0.0;
+            rq = R.q_coarse; rcell = R.cell; rcs = R.coarse_comp_stride; rr = R.ratio;
+            rx0 = T.i0;
+            rbase = __ldg(R.base + T.patch);
+            rnyb = p.ny / rr;
+            const int jr = T.j0 + l - 2;           // interior row of this lane
+            rby = jr >= 0 ? jr / rr : 0;
+            rlead = out_lane && jr % rr == 0;
+        }
     }
 
     ADJ_D void run() {
@@ -602,7 +638,7 @@ struct Strip {
     }
 };
 
-template <int SYS, int FORM, bool REV, int LIM, bool CFL>
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false>
 #ifdef K1_MAXREG
 __global__ void __maxnreg__(K1_MAXREG) k1_fast(AdjStepArgs a) {
 #else
@@ -610,7 +646,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
 #endif
     const int lane = threadIdx.x & 31;
     __shared__ int s_tile[K1_WARPS];
-    constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL>::NARR;
+    constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL, RST>::NARR;
     extern __shared__ __align__(16) double s_ring1[];   // [K1_WARPS][RING1 * NARR * 32]
     const int warp = threadIdx.x >> 5;
     pdl_wait();
@@ -644,7 +680,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
         }
         const AdjTile T = a.tiles[tix];
         const AdjPatch p = a.patches[T.patch];
-        Strip<SYS, FORM, REV, LIM, CFL> S;
+        Strip<SYS, FORM, REV, LIM, CFL, RST> S;
         S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
         S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32);
         S.run();
@@ -931,14 +967,15 @@ static void launch_two_rows(const AdjStepArgs& a, cudaStream_t st) {
     launch_pdl(k1_fast2<SYS, FORM, REV, LIM>, dim3(blocks), dim3(128), smem, st, a);
 }
 
-template <int SYS, int FORM, bool REV, int LIM, bool CFL>
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false>
 static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     static int blocks_per_sm = 0, sms = 0;
-    constexpr int smem = K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL>::NARR * 32 * (int)sizeof(double);
+    constexpr int smem = K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL, RST>::NARR * 32 * (int)sizeof(double);
     if (blocks_per_sm == 0) {
-        cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL>, 32 * K1_WARPS,
-                                                      smem);
+        cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL, RST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL, RST>,
+                                                      32 * K1_WARPS, smem);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -947,11 +984,17 @@ static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     int blocks = blocks_per_sm * sms;
     const int need = ((a.job_offsets ? a.njob : a.ntile) + K1_WARPS - 1) / K1_WARPS;
     if (blocks > need) blocks = need;
-    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL>, dim3(blocks), dim3(32 * K1_WARPS), smem, st, a);
+    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL, RST>, dim3(blocks), dim3(32 * K1_WARPS), smem, st, a);
 }
 
 template <int SYS, int FORM, bool REV, int LIM>
 static void launch_kernel(const AdjStepArgs& a, cudaStream_t st) {
+    if constexpr (FORM == ADJ_FORM_WAVE && !REV) {   // forward levels: optional fused restriction
+        if (a.fine_restrict.ratio > 0 && a.static_speed) {
+            launch_cfl<SYS, FORM, REV, LIM, false, true>(a, st);
+            return;
+        }
+    }
     if ((a.flags & ADJ_STEP_TWO_ROWS) && a.static_speed && !a.job_offsets) launch_two_rows<SYS, FORM, REV, LIM>(a, st);
     else if (a.static_speed) launch_cfl<SYS, FORM, REV, LIM, false>(a, st);
     else if (!a.job_offsets) launch_cfl<SYS, FORM, REV, LIM, true>(a, st);

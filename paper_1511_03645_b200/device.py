@@ -873,7 +873,7 @@ def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=Non
 
 
 def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index, stream=None,
-                accumulate=False, prefill=None):
+                accumulate=False, prefill=None, fine_restrict=None):
     """K1 on every patch: reads buf[cur], writes buf[out_buf_index].
     Returns (speed_max (npatch, 2) tensor, nonfinite (npatch,) tensor).
     ``accumulate`` (static-CFL fast path only): no per-launch memsets; the
@@ -932,6 +932,13 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     a.stream = _lib.stream_ptr(stream)
     if prefill is not None:
         a.prefill = prefill
+    if fine_restrict is not None:     # (FusedRestrict, coarse store): restriction fused into this step
+        fr, cst = fine_restrict
+        a.fine_restrict.q_coarse = _ptr(cst.buf[cst.cur])
+        a.fine_restrict.cell = _ptr(fr.cell)
+        a.fine_restrict.base = _ptr(fr.base)
+        a.fine_restrict.coarse_comp_stride = cst.plane
+        a.fine_restrict.ratio = fr.ratio
     _lib.check(_lib.lib().adj_step_level(_lib.C.byref(a)), "adj_step_level")
     return smax[: 2 * npatch].view(npatch, 2), bad[:npatch]
 
@@ -981,6 +988,52 @@ class RestrictPlan:
     def usable(coarse_store, fine_store) -> bool:
         lim = 2 ** 31 - 1
         return coarse_store.plane < lim and fine_store.plane < lim
+
+
+class FusedRestrict:
+    """Restriction fused into the fine level's step (AdjStepRestrict): per
+    fine r x r block (patch-major, then x block, then y block) the offset of
+    its covered coarse cell in the coarse plane, -1 where not covered.
+    Built once per regrid from restrict_cells."""
+
+    def __init__(self, coarse_store, fine_store, rects_np, ratio):
+        torch = _torch()
+        d, s_, _ = restrict_cells(coarse_store, fine_store, rects_np, ratio)
+        t = fine_store.table_np
+        g = fine_store.g
+        nbx, nby = t["nx"].astype(np.int64) // ratio, t["ny"].astype(np.int64) // ratio
+        base = np.concatenate([[0], np.cumsum(nbx * nby)[:-1]]).astype(np.int64)
+        cell = np.full(max(int((nbx * nby).sum()), 1), -1, dtype=np.int32)
+        if len(d):
+            offs = t["offset"].astype(np.int64)
+            order = np.argsort(offs, kind="stable")
+            k = order[np.searchsorted(offs[order], s_.astype(np.int64), side="right") - 1]
+            xr, yr = np.divmod(s_.astype(np.int64) - offs[k], t["pitch"][k].astype(np.int64))
+            cell[base[k] + ((xr - g) // ratio) * nby[k] + (yr - g) // ratio] = d
+        self.ratio = ratio
+        self.cell = torch.from_numpy(cell).to("cuda")
+        self.base = torch.from_numpy(base.astype(np.int32)).to("cuda")
+
+    @staticmethod
+    def usable(coarse_store, fine_store, ratio) -> bool:
+        """FAST 2D fine level without dry cells whose strip tiles all align to the ratio."""
+        if ratio not in (2, 4) or fine_store.ndim != 2 or fine_store.any_dry() or fine_store.two_rows():
+            return False
+        if coarse_store.any_dry():      # shallow water restricts into wet coarse cells only
+            return False
+        if not RestrictPlan.usable(coarse_store, fine_store):
+            return False
+        key = ("fused_restrict_ok", ratio)
+        ok = fine_store._scratch.get(key)
+        if ok is None:
+            tiles, ntile, _, _ = fine_store.tiles(_lib.VARIANT_FAST)
+            rows = np.frombuffer(tiles.cpu().numpy().tobytes(), dtype=_lib.TILE_DTYPE)[:ntile]
+            t = fine_store.table_np
+            ok = bool(np.all(rows["i0"] % ratio == 0) and np.all(rows["j0"] % ratio == 0)
+                      and np.all(rows["ni"] % ratio == 0) and np.all(rows["nj"] % ratio == 0)
+                      and np.all(t["nx"] % ratio == 0) and np.all(t["ny"] % ratio == 0))
+            fine_store._scratch[key] = ok
+        return ok
 
 
 def restrict_rects(coarse_store, fine_store, rects_np, ratio, swe, stream=None):
