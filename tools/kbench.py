@@ -52,10 +52,19 @@ if not a.no_flag:
         device.launch_flag(*args)
         torch.cuda.synchronize()
         reps = 10
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, stream=side):
+                for _ in range(reps):
+                    _, counts, _, _ = device.launch_flag(*args)
+        torch.cuda.current_stream().wait_stream(side)
+        gph.replay()
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(reps):
-            _, counts, _, _ = device.launch_flag(*args)
+        gph.replay()
         e1.record()
         torch.cuda.synchronize()
         res[f"k3_{label}_ms"] = round(e0.elapsed_time(e1) / reps, 4)

@@ -41,6 +41,6 @@ print("k1 ms:", [round(v, 4) for v in ms], "median", round(sorted(ms)[len(ms) //
 if a.flag or a.flag1:
     ring = bench.adjoint_ring(41)
     device.launch_flag(st, ring, (1024, 1024), (0.0, 0.0), bench.L / 1024, bench.L / 1024, (0.0, 0.0),
-                       bench.L / a.n, bench.L / a.n, [20] if a.flag1 else [19, 20], 1e-4)
+                       bench.L / a.n, bench.L / a.n, [20] if a.flag1 else list(range(20, 41)), 1e-4)
     torch.cuda.synchronize()
 print("ok")
