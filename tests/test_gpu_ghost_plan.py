@@ -97,17 +97,20 @@ def test_planned_restrict_equals_rect_restrict(name):
 def test_fused_fill_equals_separate_fill(name):
     """The planned fill run inside the step launch (prefill + grid barrier)
     gives bitwise the states of the separate gather launch (FAST variant,
-    several coarse steps incl. regrids)."""
+    several coarse steps incl. regrids).  The fused restriction is off in
+    both runs (a prefilled step never fuses it; its block sums would differ
+    in the last bit)."""
     from paper_1511_03645_b200 import _lib, amr
     from tests.test_gpu_amr import run
     outs = []
     for fused in (False, True):
-        old = amr.USE_FUSED_FILL
+        old, old_r = amr.USE_FUSED_FILL, amr.USE_FUSED_RESTRICT
         amr.USE_FUSED_FILL = fused
+        amr.USE_FUSED_RESTRICT = False
         try:
             outs.append(run(name, _lib.VARIANT_FAST))
         finally:
-            amr.USE_FUSED_FILL = old
+            amr.USE_FUSED_FILL, amr.USE_FUSED_RESTRICT = old, old_r
     for step, (a, b) in enumerate(zip(*outs)):
         assert a["nlev"] == b["nlev"] and a["flagged"] == b["flagged"]
         for lev in range(1, a["nlev"] + 1):
