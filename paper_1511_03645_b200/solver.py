@@ -9,6 +9,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _lib, device
@@ -139,34 +141,34 @@ def _finish_material(patch, mat_cls, arrays, others, boundary, level_shape):
 
 
 def sample_patches_material(patches, equation: EquationSet, boundary: BoundarySpec, level_shape: tuple[int, ...]):
-    """sample_patch_material for many new patches of one level.  When they
-    share a shape the material model is called once on the stacked
-    cell-centre arrays; each patch's values are then those of its own call
-    (verified exactly against a per-patch call on the first patch; any
-    difference or error falls back to one call per patch)."""
+    """sample_patch_material for many new patches of one level.  The material
+    model is called once on the concatenated (flattened) ghost-inclusive
+    cell-centre coordinates of all patches; each patch's values are then
+    those of its own call (verified exactly against a per-patch call on the
+    first patch; any difference or error falls back to one call per patch)."""
     P = len(patches)
-    if P < 4 or len({p.spec.shape for p in patches}) != 1 or any(p._store is not None for p in patches):
+    if P < 4 or any(p._store is not None for p in patches) or os.environ.get("ADJAMR_BATCH_MATERIAL") == "0":
         for p in patches:
             sample_patch_material(p, equation, boundary, level_shape)
         return
     nd = patches[0].spec.ndim
     cs = [p.spec.cell_centers(include_ghost=True) for p in patches]
+    shapes = [tuple(len(c) for c in cc) for cc in cs]
+    sizes = [int(np.prod(sh)) for sh in shapes]
     try:
         if nd == 1:
-            mat = equation.sample_material(np.stack([c[0] for c in cs]))
+            mat = equation.sample_material(np.concatenate([c[0] for c in cs]))
             mat0 = equation.sample_material(cs[0][0])
         else:
-            NX, NY = len(cs[0][0]), len(cs[0][1])
-            X = np.repeat(np.stack([c[0] for c in cs])[:, :, None], NY, axis=2)
-            Y = np.repeat(np.stack([c[1] for c in cs])[:, None, :], NX, axis=1)
-            mat = equation.sample_material(X, Y)
-            xx, yy = np.meshgrid(cs[0][0], cs[0][1], indexing="ij")
-            mat0 = equation.sample_material(xx, yy)
+            grids = [np.meshgrid(c[0], c[1], indexing="ij") for c in cs]
+            mat = equation.sample_material(np.concatenate([g[0].ravel() for g in grids]),
+                                           np.concatenate([g[1].ravel() for g in grids]))
+            mat0 = equation.sample_material(grids[0][0], grids[0][1])
         names = _field_names(type(mat))
         arr_names = [n for n in names if isinstance(getattr(mat0, n), np.ndarray)]
         ok = type(mat0) is type(mat) and all(
-            isinstance(getattr(mat, n), np.ndarray) and getattr(mat, n).shape == (P, *getattr(mat0, n).shape)
-            and np.array_equal(getattr(mat, n)[0], getattr(mat0, n)) for n in arr_names)
+            isinstance(getattr(mat, n), np.ndarray) and getattr(mat, n).shape == (sum(sizes),)
+            and np.array_equal(getattr(mat, n)[:sizes[0]].reshape(shapes[0]), getattr(mat0, n)) for n in arr_names)
         ok = ok and all(getattr(mat, n) == getattr(mat0, n) for n in names if n not in arr_names)
     except Exception:
         ok = False
@@ -176,9 +178,10 @@ def sample_patches_material(patches, equation: EquationSet, boundary: BoundarySp
         return
     others = {n: getattr(mat, n) for n in names if n not in arr_names}
     fields = {n: getattr(mat, n) for n in arr_names}
+    off = np.concatenate([[0], np.cumsum(sizes)])
     for k, p in enumerate(patches):
-        _finish_material(p, type(mat), {n: np.array(f[k], copy=True) for n, f in fields.items()}, others, boundary,
-                         level_shape)
+        _finish_material(p, type(mat), {n: np.array(f[off[k]:off[k + 1]].reshape(shapes[k]), copy=True)
+                                        for n, f in fields.items()}, others, boundary, level_shape)
 
 
 # ---------------------------------------------------------------------------

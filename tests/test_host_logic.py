@@ -170,6 +170,17 @@ def test_batched_material_sampling_equals_per_patch():
            E.SweLinear2D(E.SweMaterialModel(lambda x, y: -50.0 + 80.0 * np.sin(3 * np.asarray(x)) * np.cos(2 * np.asarray(y)),
                                             0.0, 9.81)))
     boxes = [((0, 32 * k), (31, 32 * k + 31)) for k in range(4)] + [((96, 32 * k), (127, 32 * k + 31)) for k in range(4)]
+    # regrid clusters come in mixed shapes: one flattened call covers them all
+    mixed = [((0, 0), (15, 47)), ((16, 0), (63, 7)), ((64, 64), (127, 127)), ((40, 100), (41, 127)), ((0, 120), (3, 127))]
+    for eq in eqs:
+        a = [Patch(h.make_spec(2, lo, hi), 3) for lo, hi in mixed]
+        b = [Patch(h.make_spec(2, lo, hi), 3) for lo, hi in mixed]
+        solver.sample_patches_material(a, eq, bc, (128, 128))
+        for p in b:
+            solver.sample_patch_material(p, eq, bc, (128, 128))
+        for pa, pb in zip(a, b):
+            for x, y in zip(pa.aux.planes(), pb.aux.planes()):
+                assert np.array_equal(x, y)
     for eq in eqs:
         a = [Patch(h.make_spec(2, lo, hi), 3) for lo, hi in boxes]
         b = [Patch(h.make_spec(2, lo, hi), 3) for lo, hi in boxes]
