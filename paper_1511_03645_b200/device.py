@@ -485,17 +485,19 @@ def ring_copy(store: LevelStore, src, dst, stream=None):
     """Copy every patch's ghost ring from buffer src to buffer dst."""
     if SHADOW:
         return
-    rects = []
-    g = store.g
-    for k, (off, NX, NY, pitch) in enumerate(store.boxes):
-        if store.ndim == 2:
-            parts = [(0, 0, g, NY), (NX - g, 0, g, NY), (g, 0, NX - 2 * g, g), (g, NY - g, NX - 2 * g, g)]
-        else:
-            parts = [(0, 0, g, 1), (NX - g, 0, g, 1)]
-        for (i0, j0, ni, nj) in parts:
-            rects.append((_lib.RECT_COPY, k, k, i0, j0, ni, nj, i0, j0, 0))
-    arr = np.array(rects, dtype=_lib.RECT_DTYPE)
-    copy_rects(store, store, arr, src, dst, stream)
+    tab = store._scratch.get("ring_rects")      # the store's patch set is fixed: build the table once
+    if tab is None:
+        rects = []
+        g = store.g
+        for k, (off, NX, NY, pitch) in enumerate(store.boxes):
+            if store.ndim == 2:
+                parts = [(0, 0, g, NY), (NX - g, 0, g, NY), (g, 0, NX - 2 * g, g), (g, NY - g, NX - 2 * g, g)]
+            else:
+                parts = [(0, 0, g, 1), (NX - g, 0, g, 1)]
+            for (i0, j0, ni, nj) in parts:
+                rects.append((_lib.RECT_COPY, k, k, i0, j0, ni, nj, i0, j0, 0))
+        tab = store._scratch["ring_rects"] = RectTable(np.array(rects, dtype=_lib.RECT_DTYPE))
+    copy_rects(store, store, tab, src, dst, stream)
 
 
 class RectTable:

@@ -72,6 +72,14 @@ class DistTransport:
                 r.wait()
         return lo_recv, hi_recv
 
+    def exchange_into(self, lo_send, hi_send, lo_recv, hi_recv):
+        """exchange() into preallocated receive buffers (the graphed step's)."""
+        lo, hi = self.exchange(lo_send, hi_send)
+        if lo is not None:
+            lo_recv.copy_(lo)
+        if hi is not None:
+            hi_recv.copy_(hi)
+
 
 def exchange_x_halos(q, m: int, plane: int, offset: int, pitch: int, nx: int, g: int, transport,
                      has_lo: bool, has_hi: bool) -> None:
@@ -196,13 +204,61 @@ def _check(st, dtdx, dtdy, ndim):
     return cfl
 
 
+def _graphed_pair(patch, equation, boundary, level_shape, dt, limiter, variant, key):
+    """Capture two consecutive steps of the slab as four CUDA graphs: per
+    step, pre = physical fill + ghost fold + packing of the boundary rows
+    into persistent send buffers, post = unpacking of the persistent receive
+    buffers into the ghost rows + K1.  The exchange itself runs between them
+    (not captured).  The buffer roles are 2-periodic, as in advance_uniform."""
+    import torch
+    from . import device
+    st, offset, pitch = _layout(patch)
+    g, m, nx = st.g, st.m, patch.spec.shape[0]
+    has_lo, has_hi = _edges(patch, level_shape)
+    bufs = [torch.empty((m, g * pitch), dtype=torch.float64, device="cuda") for _ in range(4)]
+    send_lo, send_hi, recv_lo, recv_hi = bufs
+    roles = (st.cur, st.old, st.ghost_src)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graphs = []
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            pre, post = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(pre, stream=side):
+                device.fill_physical(st, boundary, equation, level_shape)
+                st.fold_ghosts()
+                q = st.buf[st.cur]
+                if has_lo:
+                    send_lo.copy_(halo_rows(q, m, st.plane, offset, pitch, g, 2 * g))
+                if has_hi:
+                    send_hi.copy_(halo_rows(q, m, st.plane, offset, pitch, nx, nx + g))
+            with torch.cuda.graph(post, stream=side):
+                q = st.buf[st.cur]
+                if has_lo:
+                    halo_rows(q, m, st.plane, offset, pitch, 0, g).copy_(recv_lo)
+                if has_hi:
+                    halo_rows(q, m, st.plane, offset, pitch, nx + g, nx + 2 * g).copy_(recv_hi)
+                _launch(st, dt, equation, limiter, variant, None)
+            graphs.append((pre, post))
+    torch.cuda.current_stream().wait_stream(side)
+    if (st.cur, st.old, st.ghost_src) != roles:
+        raise RuntimeError("sharded step pair is not 2-periodic")
+    entry = (graphs, bufs, has_lo, has_hi)
+    st._scratch[key + (roles,)] = entry
+    return entry
+
+
 def advance_sharded(patch, equation, boundary, level_shape, dt: float, nsteps: int, transport,
-                    limiter: str = "MC", variant: int | None = None, stream=None, group=None) -> float:
+                    limiter: str = "MC", variant: int | None = None, stream=None, group=None,
+                    graph: bool = True) -> float:
     """nsteps of rank's slab (``solver.advance_uniform`` with the halo
     exchange).  2D levels without dry cells (either K1 variant): the Courant
     number is the static material bound, known on the host; the non-finite
     flag is accumulated on the device and all-reduced once at the end so
-    every rank raises together.  Returns this slab's Courant number."""
+    every rank raises together.  ``graph``: pairs of steps replay CUDA graphs
+    around the (uncaptured) exchange, so per step the host issues two graph
+    launches and the exchange.  Returns this slab's Courant number."""
     import torch.distributed as dist
     from .solver import DEFAULT_VARIANT, NumericalBlowupError
     variant = DEFAULT_VARIANT if variant is None else variant
@@ -211,8 +267,41 @@ def advance_sharded(patch, equation, boundary, level_shape, dt: float, nsteps: i
     _usable(st, variant)
     spec = patch.spec
     cfl = _check(st, dt / spec.dx, dt / spec.dy, 2)
-    for _ in range(nsteps):
+    graph = graph and stream is None and hasattr(transport, "exchange_into")
+    key = ("shard_graph", dt, limiter, variant, tuple(level_shape), boundary, id(equation))
+    done = 0
+
+    def cached():
+        return st._scratch.get(key + ((st.cur, st.old, st.ghost_src),))
+
+    def eager():
         _step_one(patch, equation, boundary, level_shape, dt, limiter, variant, transport, stream)
+
+    entry = cached() if graph else None
+    if graph and entry is None and nsteps >= 3 and any(isinstance(k, tuple) and k[:7] == key for k in st._scratch):
+        eager()                              # the other parity of a captured pair: realign
+        done += 1
+        entry = cached()
+    if graph and entry is None and nsteps - done >= 4:
+        for i in range(st.NBUF):
+            st._ensure_buf(i)
+        eager(); eager()                     # warm-up: first-touch allocations happen outside capture
+        done += 2
+        entry = _graphed_pair(patch, equation, boundary, level_shape, dt, limiter, variant, key)
+    if entry is not None:
+        graphs, (send_lo, send_hi, recv_lo, recv_hi), has_lo, has_hi = entry
+        while nsteps - done >= 2:
+            for pre, post in graphs:
+                pre.replay()
+                if has_lo or has_hi:
+                    transport.exchange_into(send_lo if has_lo else None, send_hi if has_hi else None,
+                                            recv_lo, recv_hi)
+                post.replay()
+                patch.time += dt
+            done += 2
+    while done < nsteps:
+        eager()
+        done += 1
     patch._loc = "device"
     bad = _pending_bad(st)
     if isinstance(transport, DistTransport) and dist.is_initialized() and dist.get_world_size() > 1:

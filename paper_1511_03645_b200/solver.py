@@ -455,15 +455,39 @@ def advance_uniform(patch: Patch, equation: EquationSet, boundary: BoundarySpec,
 
         done = 0
         key = ("uniform_graph", dt, limiter, tuple(level_shape), boundary, id(equation))
+        key1 = ("uniform_graph1",) + key[1:]
 
         def cached():
             return st._scratch.get(key + ((st.cur, st.old, st.ghost_src),)) if graph else None
 
-        g = cached()
-        if graph and g is None and nsteps >= 3 and any(isinstance(kk, tuple) and kk[:6] == key for kk in st._scratch):
-            one_step()                      # other parity of a captured pair: realign
-            done += 1
+        def capture_single():
+            """Capture (without running) one step from the current buffer roles;
+            the host roles advance as if it ran."""
+            roles = (st.cur, st.old, st.ghost_src)
+            cg1 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg1):
+                one_step()
+            st._scratch[key1 + (roles,)] = (cg1, (st.cur, st.old, st.ghost_src))
+
+        def single_step():
+            """One step from the single-step graph of the current buffer roles
+            (both parities are captured next to the pair)."""
+            roles = (st.cur, st.old, st.ghost_src)
+            e = st._scratch.get(key1 + (roles,))
+            if e is None:
+                torch.cuda.synchronize()
+                capture_single()
+                e = st._scratch[key1 + (roles,)]
+            else:
+                st.cur, st.old, st.ghost_src = e[1]
+            e[0].replay()
             patch.time += dt
+
+        captured = graph and any(isinstance(kk, tuple) and kk[:6] == key for kk in st._scratch)
+        g = cached()
+        if graph and g is None and captured and nsteps >= 1:
+            single_step()                   # other parity of a captured pair: realign from a graph
+            done += 1
             g = cached()
         if graph and (g is not None or nsteps - done >= 4):
             if g is None:
@@ -482,6 +506,10 @@ def advance_uniform(patch: Patch, equation: EquationSet, boundary: BoundarySpec,
                     raise RuntimeError("uniform step pair is not 2-periodic")
                 g = (cg, roles)
                 st._scratch[key + (roles,)] = g
+                capture_single()                # single steps of both parities (odd counts, realignment)
+                capture_single()
+                if (st.cur, st.old, st.ghost_src) != roles:
+                    raise RuntimeError("uniform single steps are not 2-periodic")
                 # the host state already reflects the captured pair; run it once
                 cg.replay()
                 done += 2
@@ -493,9 +521,12 @@ def advance_uniform(patch: Patch, equation: EquationSet, boundary: BoundarySpec,
                 patch.time += dt
                 patch.time += dt
         while done < nsteps:
-            one_step()
+            if g is not None:
+                single_step()
+            else:
+                one_step()
+                patch.time += dt
             done += 1
-            patch.time += dt
         patch._loc = "device"
         if st.nonfinite_acc is not None and bool(st.nonfinite_acc.any().item()):
             st.nonfinite_acc.zero_()
