@@ -578,15 +578,16 @@ def main():
 def build_c3(n=2048):
     """C3: 2048^2 two-layer acoustics on [0,1]^2 (K=4, rho=1 where y < 0.2x,
     else K=1, rho=1.5), 8 Gaussians (width 0.05, centres/amplitudes U[0.5,1],
-    seed 0).  Periodic x has no reference oracle: outflow in x,
-    walls in y."""
+    seed 0).  Periodic x (BoundarySpec "periodic": an extension checked
+    against the oracle's restatement, the reference has no periodic
+    condition), walls in y."""
     from paper_1511_03645_b200 import equations as E
     from paper_1511_03645_b200 import solver
     from paper_1511_03645_b200.geometry import Patch, PatchHierarchy
     lower = lambda x, y: np.asarray(y) < 0.2 * np.asarray(x)                      # noqa: E731
     eq = E.Acoustics2D(E.AcousticsMaterialModel(lambda x, y: np.where(lower(x, y), 4.0, 1.0),
                                                 lambda x, y: np.where(lower(x, y), 1.0, 1.5)))
-    bc = solver.BoundarySpec("outflow", "outflow", "wall", "wall")
+    bc = solver.BoundarySpec("periodic", "periodic", "wall", "wall")
     h = PatchHierarchy(xlim=(0.0, 1.0), ylim=(0.0, 1.0), base_shape=(n, n), ratios=[])
     p = Patch(h.make_spec(1, (0, 0), (n - 1, n - 1)), 3)
     solver.sample_patch_material(p, eq, bc, (n, n))
@@ -654,8 +655,8 @@ def bench_c3(steps, variant):
             "k1_ms": k1ms, "k1_achieved_GBps": 64 * n * n / (k1ms * 1e-3) / 1e9, "bytes_per_cell_update": 64,
             "flagging": {"value": n * n / (fms * 1e-3), "unit": "flagged cells/s", "snapshots": len(idx),
                          "kernel_ms": fms, "flagged": int(counts[0].item()), "tolerance": 0.05},
-            "workload": "C3: 2048^2 two-layer acoustics (y<0.2x), 8 Gaussians seed 0, outflow x (periodic "
-                        "has no oracle, SURVEY D3) / wall y, CFL 0.9, MC; flagging: 50 snapshots (seed 1), "
+            "workload": "C3: 2048^2 two-layer acoustics (y<0.2x), 8 Gaussians seed 0, periodic x (extension, "
+                        "oracle-checked; SURVEY D3) / wall y, CFL 0.9, MC; flagging: 50 snapshots (seed 1), "
                         "full-span window at step 100"}
 
 

@@ -69,6 +69,8 @@ extern "C" {
 /* boundary kinds per side (solver.BoundarySpec, solver.py:35-56) */
 #define ADJ_BC_WALL    0
 #define ADJ_BC_OUTFLOW 1
+#define ADJ_BC_PERIODIC 2   /* extension (BASELINE C3): ghosts wrap to the opposite interior; both
+                               sides of the axis periodic and every patch spanning the axis */
 
 /* One patch of a level store (device-resident table). */
 typedef struct AdjPatch {

@@ -325,8 +325,11 @@ def fill_physical(q, ghost, edges, bc, normal_comp):
         for side, high in ((lo, False), (hi, True)):
             if not edges.get(side, False):
                 continue
-            src_idx = (np.arange(n - g - 1, n - 2 * g - 1, -1) if high else np.arange(2 * g - 1, g - 1, -1)) \
-                if bc[side] == "wall" else np.full(g, n - g - 1 if high else g)
+            if bc[side] == "periodic":   # extension (no reference counterpart): wrap to the opposite interior
+                src_idx = np.arange(g, 2 * g) if high else np.arange(n - 2 * g, n - g)
+            else:
+                src_idx = (np.arange(n - g - 1, n - 2 * g - 1, -1) if high else np.arange(2 * g - 1, g - 1, -1)) \
+                    if bc[side] == "wall" else np.full(g, n - g - 1 if high else g)
             dst_idx = np.arange(n - g, n) if high else np.arange(0, g)
             vals = np.take(q, src_idx, axis=ax)
             if bc[side] == "wall":

@@ -21,7 +21,8 @@ FORM_WAVE, FORM_FWAVE = 0, 1
 LIMITERS = {"none": 0, "minmod": 1, "MC": 2, "superbee": 3}
 VARIANT_EXACT, VARIANT_FAST = 0, 1
 EDGE_XLO, EDGE_XHI, EDGE_YLO, EDGE_YHI = 1, 2, 4, 8
-BC_WALL, BC_OUTFLOW = 0, 1
+BC_WALL, BC_OUTFLOW, BC_PERIODIC = 0, 1, 2
+BC_CODES = {"wall": BC_WALL, "outflow": BC_OUTFLOW, "periodic": BC_PERIODIC}
 RECT_COPY, RECT_COARSE = 0, 1
 STEP_KEEP_NONFINITE, STEP_NO_SPEED_OUT, STEP_TWO_ROWS, STEP_COUNTER_ZERO = 1, 2, 4, 8
 

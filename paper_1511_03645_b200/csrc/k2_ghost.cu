@@ -24,11 +24,13 @@ ADJ_D int phys_src(int ii, int n, int g, bool lo_edge, bool hi_edge, int bc_lo, 
     if (ii < g && lo_edge) {
         *hit = true;
         if (bc_lo == ADJ_BC_WALL) { *neg = true; return 2 * g - 1 - ii; }
+        if (bc_lo == ADJ_BC_PERIODIC) return ii + n - 2 * g;   // the patch spans the axis
         return g;
     }
     if (ii >= n - g && hi_edge) {
         *hit = true;
         if (bc_hi == ADJ_BC_WALL) { *neg = true; return 2 * n - 2 * g - 1 - ii; }
+        if (bc_hi == ADJ_BC_PERIODIC) return ii - (n - 2 * g);
         return n - g - 1;
     }
     return ii;

@@ -691,8 +691,19 @@ def coarse_rects(fine_store, coarse_store, rects_np, q_old, q_new, hierarchy, ra
 
 
 def _bc_codes(boundary):
-    return tuple(_lib.BC_WALL if sd == "wall" else _lib.BC_OUTFLOW
-                 for sd in (boundary.left, boundary.right, boundary.bottom, boundary.top))
+    return tuple(_lib.BC_CODES[sd] for sd in (boundary.left, boundary.right, boundary.bottom, boundary.top))
+
+
+def check_periodic(store, boundary, level_shape):
+    """Periodic sides (an extension; the reference has wall and outflow) wrap
+    a patch's ghosts to its own opposite interior, so every patch of the
+    level must span each periodic axis."""
+    for axis in range(store.ndim):
+        if boundary.side(axis, False) != "periodic":
+            continue
+        for p in store.patches:
+            if p.spec.lo[axis] != 0 or p.spec.hi[axis] != level_shape[axis] - 1:
+                raise ValueError("periodic boundaries need every patch to span the periodic axis")
 
 
 def physical_cell_count(store: LevelStore, level_shape) -> int:
@@ -719,6 +730,8 @@ class GhostPlan:
 
     def __init__(self, store: LevelStore, rects: RectTable, coarse_store, boundary, equation, level_shape):
         torch = _torch()
+        if "periodic" in (boundary.left, boundary.right, boundary.bottom, boundary.top):
+            check_periodic(store, boundary, level_shape)
         r = rects.np if rects.n else np.zeros(0, dtype=_lib.RECT_DTYPE)
         kinds = r["kind"]
         is_c = kinds == _lib.RECT_COARSE
@@ -853,6 +866,8 @@ def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=Non
         full = full and bool(np.all(keep))
         if nedge == 0:
             return
+    if "periodic" in (boundary.left, boundary.right, boundary.bottom, boundary.top):
+        check_periodic(store, boundary, level_shape)
     store.prepare_write(full_ghosts=full, stream=stream)
     if SHADOW:
         return
@@ -866,7 +881,7 @@ def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=Non
     a.m = store.m
     sides = (boundary.left, boundary.right, boundary.bottom, boundary.top)
     for k, sd in enumerate(sides):
-        a.bc[k] = _lib.BC_WALL if sd == "wall" else _lib.BC_OUTFLOW
+        a.bc[k] = _lib.BC_CODES[sd]
     a.normal_comp[0] = equation.normal_component(0)
     a.normal_comp[1] = equation.normal_component(1) if store.ndim == 2 else -1
     a.max_ghost_cells = store.max_ghost_cells

@@ -35,7 +35,10 @@ class SchedulingError(RuntimeError):
 
 @dataclass(frozen=True)
 class BoundarySpec:
-    """Physical boundary condition per side: 'wall' or 'outflow' (solver.py:35-56)."""
+    """Physical boundary condition per side: 'wall' or 'outflow' (solver.py:35-56).
+    Extension: 'periodic' on both sides of an axis (BASELINE C3's periodic x;
+    the reference has no periodic condition), for levels whose patches span
+    that axis."""
 
     left: str = "wall"
     right: str = "wall"
@@ -44,8 +47,11 @@ class BoundarySpec:
 
     def __post_init__(self):
         for side in (self.left, self.right, self.bottom, self.top):
-            if side not in ("wall", "outflow"):
+            if side not in ("wall", "outflow", "periodic"):
                 raise ValueError(f"unknown boundary condition {side!r}")
+        if (self.left == "periodic") != (self.right == "periodic") or \
+                (self.bottom == "periodic") != (self.top == "periodic"):
+            raise ValueError("periodic boundaries come in pairs (both sides of an axis)")
 
     def side(self, axis: int, high: bool) -> str:
         if axis == 0:
@@ -70,16 +76,18 @@ class StepResult:
 # materials (host: arbitrary Python callables), solver.py:149-205
 
 
-def _fix_aux_ghosts(arr: np.ndarray, axis: int, high: bool, g: int, wall: bool):
+def _fix_aux_ghosts(arr: np.ndarray, axis: int, high: bool, g: int, wall, periodic: bool = False):
     n = arr.shape[axis]
     idx = [slice(None)] * arr.ndim
     src = [slice(None)] * arr.ndim
     if high:
         idx[axis] = slice(n - g, n)
-        src[axis] = slice(n - g - 1, n - 2 * g - 1, -1) if wall else slice(n - g - 1, n - g)
+        src[axis] = (slice(g, 2 * g) if periodic else
+                     slice(n - g - 1, n - 2 * g - 1, -1) if wall else slice(n - g - 1, n - g))
     else:
         idx[axis] = slice(0, g)
-        src[axis] = slice(2 * g - 1, g - 1, -1) if wall else slice(g, g + 1)
+        src[axis] = (slice(n - 2 * g, n - g) if periodic else
+                     slice(2 * g - 1, g - 1, -1) if wall else slice(g, g + 1))
     arr[tuple(idx)] = arr[tuple(src)]
 
 
@@ -113,8 +121,9 @@ def sample_patch_material(patch: Patch, equation: EquationSet, boundary: Boundar
             at_edge = spec.hi[axis] == level_shape[axis] - 1 if high else spec.lo[axis] == 0
             if at_edge:
                 wall = boundary.side(axis, high) == "wall"
+                per = boundary.side(axis, high) == "periodic"
                 for arr in arrays.values():
-                    _fix_aux_ghosts(arr, axis, high, g, wall)
+                    _fix_aux_ghosts(arr, axis, high, g, wall, per)
     others = {n: getattr(mat, n) for n in names if n not in arrays}
     patch.aux = type(mat)(**arrays, **others)
     if patch._store is not None:
@@ -135,8 +144,9 @@ def _finish_material(patch, mat_cls, arrays, others, boundary, level_shape):
             at_edge = spec.hi[axis] == level_shape[axis] - 1 if high else spec.lo[axis] == 0
             if at_edge:
                 wall = boundary.side(axis, high) == "wall"
+                per = boundary.side(axis, high) == "periodic"
                 for arr in arrays.values():
-                    _fix_aux_ghosts(arr, axis, high, g, wall)
+                    _fix_aux_ghosts(arr, axis, high, g, wall, per)
     patch.aux = mat_cls(**arrays, **others)
 
 
