@@ -654,6 +654,7 @@ def bench_c3(steps, variant):
     return {"value": n * n / (ms * 1e-3), "unit": "cell-updates/s", "ms_per_step": ms,
             "k1_ms": k1ms, "k1_achieved_GBps": 64 * n * n / (k1ms * 1e-3) / 1e9, "bytes_per_cell_update": 64,
             "flagging": {"value": n * n / (fms * 1e-3), "unit": "flagged cells/s", "snapshots": len(idx),
+                         "cell_snapshots_per_s": n * n * len(idx) / (fms * 1e-3),
                          "kernel_ms": fms, "flagged": int(counts[0].item()), "tolerance": 0.05},
             "workload": "C3: 2048^2 two-layer acoustics (y<0.2x), 8 Gaussians seed 0, periodic x (extension, "
                         "oracle-checked; SURVEY D3) / wall y, CFL 0.9, MC; flagging: 50 snapshots (seed 1), "
@@ -709,6 +710,7 @@ def bench_flagging(p, st, dt, stream):
         peak, _ = peaks()
         fp64 = 40 if variant == _lib.VARIANT_EXACT else 16      # FP64 instructions per cell-snapshot
         res[label] = {"value": N * N / (kms * 1e-3), "unit": "flagged cells/s", "snapshots": len(idx),
+                      "cell_snapshots_per_s": N * N * len(idx) / (kms * 1e-3),
                       "kernel_ms": kms, "achieved_GBps": nbytes / (kms * 1e-3) / 1e9,
                       "hbm_frac": nbytes / (kms * 1e-3) / 1e9 / peak,
                       "variant": "exact" if variant == _lib.VARIANT_EXACT else "fast",
