@@ -655,6 +655,8 @@ def bench_c3(steps, variant):
             "k1_ms": k1ms, "k1_achieved_GBps": 64 * n * n / (k1ms * 1e-3) / 1e9, "bytes_per_cell_update": 64,
             "flagging": {"value": n * n / (fms * 1e-3), "unit": "flagged cells/s", "snapshots": len(idx),
                          "cell_snapshots_per_s": n * n * len(idx) / (fms * 1e-3),
+                         "achieved_GBps": (24 * n * n * (1 + len(idx)) + n * n / 8) / (fms * 1e-3) / 1e9,
+                         "hbm_frac": (24 * n * n * (1 + len(idx)) + n * n / 8) / (fms * 1e-3) / 1e9 / peaks()[0],
                          "kernel_ms": fms, "flagged": int(counts[0].item()), "tolerance": 0.05},
             "workload": "C3: 2048^2 two-layer acoustics (y<0.2x), 8 Gaussians seed 0, periodic x (extension, "
                         "oracle-checked; SURVEY D3) / wall y, CFL 0.9, MC; flagging: 50 snapshots (seed 1), "

@@ -309,6 +309,9 @@ int adj_restrict(const AdjRestrictArgs* a);
                               shares its adjoint stencil column (ratio >= 4 on aligned grids) */
 #define ADJ_FLAG_QUADS 4   /* with ADJ_FLAG_PAIRS: every even-aligned row pair shares its adjoint
                               stencil row too, and every patch has an even number of rows */
+#define ADJ_FLAG_DIRECT 8  /* with ADJ_FLAG_ROWS: every interpolation weight is exactly 0 or 1
+                              (forward cell centres on adjoint cell centres, e.g. equal grids):
+                              the bilinear stencil reduces to one adjoint value per cell */
 typedef struct AdjFlagArgs {
     const double* q;             /* forward level store                        */
     const double* aux;           /* forward aux (swe: depth plane 1)          */

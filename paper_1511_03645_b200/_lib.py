@@ -128,6 +128,7 @@ ABI_VERSION = 4
 FLAG_ROWS = 1        # AdjFlagArgs.layout: ADJ_FLAG_ROWS
 FLAG_PAIRS = 2       # AdjFlagArgs.layout: ADJ_FLAG_PAIRS
 FLAG_QUADS = 4       # AdjFlagArgs.layout: ADJ_FLAG_QUADS
+FLAG_DIRECT = 8      # AdjFlagArgs.layout: ADJ_FLAG_DIRECT
 
 class AdjFunctionalArgs(C.Structure):
     _fields_ = [("q", P), ("patches", P), ("ring", P), ("finer", P), ("covered", P), ("partial", P), ("status", P),

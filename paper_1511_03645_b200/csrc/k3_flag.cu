@@ -1041,6 +1041,109 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, FASTW ? K3_QUAD_MINB_FAST :
     if (lane == 0 && cnt) atomicAdd(&a.counts[pidx], cnt);
 }
 
+// ---------------------------------------------------------------------------
+// Mode-0 windows when every weight is exactly 0 or 1 (ADJ_FLAG_DIRECT, e.g.
+// the C3 forward and adjoint grids coincide): the reference's bilinear
+// expression C00 ux uy + C10 wx uy + C01 ux wy + C11 wx wy reduces to the one
+// corner whose weights are 1 (the others contribute signed zeros), so each
+// cell-snapshot is one adjoint value per component -- bitwise equal for
+// finite adjoint fields.  Lane l owns columns j + 32kk (coalesced adjoint
+// loads); the next snapshot's values load while this one's dot products run.
+template <int NCD>
+__global__ void __launch_bounds__(32 * K3_ROW_WARPS, 3) k3_direct(AdjFlagArgs a, int run) {
+    __shared__ const char* s_base[K3_MAXN];
+    const int nidx = a.nidx;
+    {
+        const int64_t snap_b = (int64_t)a.nxa * a.nya * 3 * 8;
+        for (int n = threadIdx.x; n < nidx; n += blockDim.x)
+            s_base[n] = reinterpret_cast<const char*>(a.ring) + (int64_t)a.snap_index[n] * snap_b;
+    }
+    __syncthreads();
+    const int pidx = blockIdx.z;
+    const AdjPatch p = a.patches[pidx];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned seg = blockIdx.y * K3_ROW_WARPS + warp;
+    const unsigned nseg = (unsigned)p.ny / (32u * NCD);
+    const unsigned r0 = blockIdx.x * (unsigned)run;
+    if (seg >= nseg || r0 >= (unsigned)p.nx) return;               // warp-uniform; no barrier below
+    const unsigned r1 = min(r0 + (unsigned)run, (unsigned)p.nx);
+    const unsigned ny = (unsigned)p.ny, j = seg * (32u * NCD) + lane;
+    const int g = a.ghost;
+    const int64_t cs = a.comp_stride;
+    const int64_t nya = a.nya;
+    const int64_t plane_b = (int64_t)a.nxa * nya * 8;
+    const int64_t rowoff = a.axis_off[2 * pidx], coloff = a.axis_off[2 * pidx + 1];
+    unsigned coff[NCD];   // byte offset of this lane's adjoint column (j0 + the unit weight)
+    int ja[NCD];
+#pragma unroll
+    for (int kk = 0; kk < NCD; ++kk) {
+        const int jt = (int)(j + 32 * kk);
+        coff[kk] = (unsigned)((__ldg(a.axis_i + coloff + jt) + (__ldg(a.axis_w + coloff + jt) > 0.5 ? 1 : 0)) * 8);
+        ja[kk] = a.axis_dry ? __ldg(a.axis_dry + coloff + jt) : 0;
+    }
+    unsigned long long cnt = 0;
+    for (unsigned i = r0; i < r1; ++i) {
+        const int64_t rowb = (int64_t)(__ldg(a.axis_i + rowoff + i) + (__ldg(a.axis_w + rowoff + i) > 0.5 ? 1 : 0)) *
+                             nya * 8;
+        const double* qr = a.q + p.offset + (int64_t)(i + g) * p.pitch + g + j;
+        double q[NCD][3];
+#pragma unroll
+        for (int kk = 0; kk < NCD; ++kk)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) q[kk][c] = __ldcs(qr + c * cs + 32 * kk);   // streamed once
+        double V0[NCD][3], V1[NCD][3];
+        auto load = [&](double (&V)[NCD][3], int n) {
+            const char* b = s_base[n] + rowb;
+#pragma unroll
+            for (int kk = 0; kk < NCD; ++kk)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) V[kk][c] = __ldg(reinterpret_cast<const double*>(b + c * plane_b + coff[kk]));
+        };
+        double best[NCD];
+#pragma unroll
+        for (int kk = 0; kk < NCD; ++kk) best[kk] = 0.0;
+        auto accumulate = [&](const double (&V)[NCD][3]) {
+#pragma unroll
+            for (int kk = 0; kk < NCD; ++kk) {
+                double d = 0.0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) d = c == 0 ? V[kk][c] * q[kk][c] : d + V[kk][c] * q[kk][c];
+                best[kk] = fmax(best[kk], fabs(d));
+            }
+        };
+        load(V0, 0);
+        for (int n = 0; n < nidx; n += 2) {
+            if (n + 1 < nidx) load(V1, n + 1);
+            accumulate(V0);
+            if (n + 1 < nidx) {
+                if (n + 2 < nidx) load(V0, n + 2);
+                accumulate(V1);
+            }
+        }
+        if (a.swe) {   // forward dry cells
+            const double* cp = a.aux + a.aux_stride + p.offset + (int64_t)(i + g) * p.pitch + (j + g);
+#pragma unroll
+            for (int kk = 0; kk < NCD; ++kk)
+                if (!(__ldg(cp + 32 * kk) > 0.0)) best[kk] = 0.0;
+        }
+        if (a.adj_wet != nullptr && a.axis_dry) {
+            const int ia = __ldg(a.axis_dry + rowoff + i);
+#pragma unroll
+            for (int kk = 0; kk < NCD; ++kk)
+                if (!a.adj_wet[(int64_t)ia * nya + ja[kk]]) best[kk] = 0.0;
+        }
+        const unsigned base = i * ny + seg * (32u * NCD);
+#pragma unroll
+        for (int kk = 0; kk < NCD; ++kk) {
+            if (a.best != nullptr) a.best[a.best_offset[pidx] + base + 32u * kk + lane] = best[kk];
+            const unsigned word = __ballot_sync(0xffffffffu, best[kk] > a.tolerance);
+            if (lane == 0) a.flag_bits[p.flag_word + ((base >> 5) + kk)] = word;
+            cnt += __popc(word);
+        }
+    }
+    if (lane == 0 && cnt) atomicAdd(&a.counts[pidx], cnt);
+}
+
 // ADJAMR_K3_PAIRS=0 selects the one-cell-per-lane table kernel (A/B measurements)
 static bool k3_pairs() {
     static int on = -1;
@@ -1049,6 +1152,33 @@ static bool k3_pairs() {
         on = (e && e[0] == '0') ? 0 : 1;
     }
     return on == 1;
+}
+
+// ADJAMR_K3_DIRECT=0 disables the direct (unit-weight) kernel (A/B measurements)
+static bool k3_direct_on() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("ADJAMR_K3_DIRECT");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+// rows per warp of k3_direct: the grid about one wave of resident CTAs
+static int k3_direct_run(const AdjFlagArgs& a) {
+    static int res = 0;
+    if (res == 0) {
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_direct<4>, 32 * K3_ROW_WARPS, 0);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        res = (per_sm < 1 ? 1 : per_sm) * sms;
+    }
+    const int64_t segs = ((int64_t)a.max_cols / 128 + K3_ROW_WARPS - 1) / K3_ROW_WARPS;
+    int64_t runs = res / (segs * a.npatch > 0 ? segs * a.npatch : 1);
+    if (runs < 1) runs = 1;
+    const int64_t run = (a.max_rows + runs - 1) / runs;
+    return (int)(run < 1 ? 1 : run);
 }
 
 // ADJAMR_K3_QUAD=0 disables the quad kernel for multi-snapshot windows (A/B measurements)
@@ -1152,7 +1282,13 @@ int flag_adjoint(const AdjFlagArgs& a) {
         } else if (a.ndim == 2 && a.m == 3) {
             // pairs pay off once a window has several snapshots (measured: 1.37 vs 1.69 ms at
             // 21 snapshots on C4; 0.23 vs 0.22 ms at one)
-            if (!m1 && a.nidx >= (k3_quad1() ? 1 : 2) && (a.layout & ADJ_FLAG_ROWS) && (a.layout & ADJ_FLAG_QUADS) &&
+            if (!m1 && a.nidx >= 2 && (a.layout & ADJ_FLAG_ROWS) && (a.layout & ADJ_FLAG_DIRECT) && k3_direct_on() &&
+                (int64_t)a.nxa * a.nya * 3 * 8 < (int64_t(1) << 32)) {
+                const int run = k3_direct_run(a);
+                const dim3 gr((unsigned)((a.max_rows + run - 1) / run),
+                              (unsigned)((a.max_cols / 128 + K3_ROW_WARPS - 1) / K3_ROW_WARPS), (unsigned)a.npatch);
+                k3_direct<4><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a, run);
+            } else if (!m1 && a.nidx >= (k3_quad1() ? 1 : 2) && (a.layout & ADJ_FLAG_ROWS) && (a.layout & ADJ_FLAG_QUADS) &&
                 k3_quad_on() &&
                 (int64_t)a.nxa * a.nya * 3 * 8 < (int64_t(1) << 32)) {
                 const int run = k3_quad_run(a);

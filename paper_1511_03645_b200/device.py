@@ -1215,7 +1215,8 @@ def flag_axis_tables(store: LevelStore, ring_shape, a_origin, a_dx, a_dy, level_
             torch.from_numpy(I).to("cuda"),
             torch.from_numpy(Dr).to("cuda"),
             torch.from_numpy(np.array(offs, dtype=np.int64)).to("cuda"),
-            nd == 2 and pairs_ok, nd == 2 and pairs_ok and rows_ok)
+            nd == 2 and pairs_ok, nd == 2 and pairs_ok and rows_ok,
+            nd == 2 and bool(np.all((W == 0.0) | (W == 1.0))))    # every centre on an adjoint centre
     store._scratch[key] = tabs
     return tabs
 
@@ -1268,8 +1269,8 @@ def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level
     a.best = _ptr(best)
     a.best_offset = _ptr(best_off)
     a.status = _ptr(status)
-    tw, ti, tdry, toff, pairs_ok, quads_ok = flag_axis_tables(store, ring_shape, a_origin, a_dx, a_dy,
-                                                              level_origin, level_dx, level_dy)
+    tw, ti, tdry, toff, pairs_ok, quads_ok, direct_ok = flag_axis_tables(store, ring_shape, a_origin, a_dx, a_dy,
+                                                                         level_origin, level_dx, level_dy)
     a.axis_w, a.axis_i, a.axis_dry, a.axis_off = _ptr(tw), _ptr(ti), _ptr(tdry), _ptr(toff)
     a.comp_stride = store.plane
     a.aux_stride = store.plane
@@ -1286,7 +1287,8 @@ def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level
     # row layout: whole 128-cell row segments per warp, interior adjoint corners
     if (store.ndim == 2 and ring_shape[0] >= 2 and ring_shape[1] >= 2
             and bool((store.table_np["ny"] % K3_ROW_CELLS == 0).all())):
-        a.layout = (_lib.FLAG_ROWS | (_lib.FLAG_PAIRS if pairs_ok else 0) | (_lib.FLAG_QUADS if quads_ok else 0))
+        a.layout = (_lib.FLAG_ROWS | (_lib.FLAG_PAIRS if pairs_ok else 0) | (_lib.FLAG_QUADS if quads_ok else 0)
+                    | (_lib.FLAG_DIRECT if direct_ok else 0))
         a.max_rows = int(store.table_np["nx"].max())
         a.max_cols = int(store.table_np["ny"].max())
     a.origin_x = level_origin[0]

@@ -115,6 +115,7 @@ def test_pair_layout_detection(nya, expect):
                                    patches[0].spec.dx, patches[0].spec.dy)
     assert tabs[4] is expect
     assert tabs[5] is False      # 48 adjoint rows over 64 forward rows: row pairs straddle centres
+    assert tabs[6] is False
 
 
 @pytest.mark.parametrize("layout,nya", [("rows", 100), ("rows", 128), ("ragged", 100)])
@@ -187,4 +188,35 @@ def test_quad_kernel_multi_snapshot(variant, dry):
             assert np.max(np.abs(b - ref)) <= 1e-12 * np.max(np.abs(ref))
             far = np.abs(ref - tol) > 1e-12 * tol
             assert np.array_equal(f[far], (ref > tol)[far])
+        assert c == int(f.sum())
+
+
+@pytest.mark.parametrize("dry", [False, True])
+def test_direct_kernel_equal_grids(dry):
+    """Adjoint grid equal to the forward grid (64 x 512 under the 64 x 512
+    level, as in C3): every interpolation weight is exactly 0 or 1, so
+    windows of >= 2 snapshots run the direct kernel (k3_direct) -- bitwise
+    equal to the reference arithmetic."""
+    from paper_1511_03645_b200 import adjoint, device, solver
+    nxa, nya = 64, 512
+    _, patches = _level(ROWS, seed=11)
+    vals, wet, store = _store_n(12, nxa, nya, dry)
+    t, window = 0.3, adjoint.TimeWindow(0.0, 0.75)
+    tol = 0.7
+    flags, counts, best = adjoint.flag_level(patches, t, store, window, tol, want_best=True)
+    st = solver.store_of(patches[0])
+    tabs = device.flag_axis_tables(st, (nxa, nya), (0.0, 0.0), 1.0 / nxa, 1.0 / nya, (0.0, 0.0),
+                                   patches[0].spec.dx, patches[0].spec.dy)
+    assert tabs[6] is True
+    idx = adjoint.query_window_times(t, window, _FakeStore(window))
+    assert len(idx) >= 2
+    for p, f, c, b in zip(patches, flags, counts, best):
+        lo, shape, dx, dy = p.spec.lo, p.spec.shape, p.spec.dx, p.spec.dy
+        x = (np.arange(lo[0], lo[0] + shape[0]) + 0.5) * dx
+        y = (np.arange(lo[1], lo[1] + shape[1]) + 0.5) * dy
+        xc, yc = np.broadcast_to(x[:, None], shape), np.broadcast_to(y[None, :], shape)
+        ref = O.inner_product(p.state[:, 2:-2, 2:-2], xc, yc, vals, idx, (0.0, 0.0), 1.0 / nxa, 1.0 / nya,
+                              p.aux.wet[2:-2, 2:-2], wet)
+        assert np.array_equal(b, ref)
+        assert np.array_equal(f, ref > tol)
         assert c == int(f.sum())
