@@ -1282,7 +1282,7 @@ int flag_adjoint(const AdjFlagArgs& a) {
         } else if (a.ndim == 2 && a.m == 3) {
             // pairs pay off once a window has several snapshots (measured: 1.37 vs 1.69 ms at
             // 21 snapshots on C4; 0.23 vs 0.22 ms at one)
-            if (!m1 && a.nidx >= 2 && (a.layout & ADJ_FLAG_ROWS) && (a.layout & ADJ_FLAG_DIRECT) && k3_direct_on() &&
+            if (!m1 && (a.layout & ADJ_FLAG_ROWS) && (a.layout & ADJ_FLAG_DIRECT) && k3_direct_on() &&
                 (int64_t)a.nxa * a.nya * 3 * 8 < (int64_t(1) << 32)) {
                 const int run = k3_direct_run(a);
                 const dim3 gr((unsigned)((a.max_rows + run - 1) / run),

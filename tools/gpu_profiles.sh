@@ -15,6 +15,8 @@ ncu --set full --clock-control none --import-source on -k regex:k1_fast -s 2 -c 
 python tools/prof_k1.py --launches 1 --flag1 > $O/prof_k3.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k3_rowp -c 1 -o $O/k3_c4_single -f python tools/prof_k1.py --launches 1 --flag1 > $O/ncu_k3.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k3_quad -c 1 -o $O/k3_c4_span -f python tools/prof_k1.py --launches 1 --flag > $O/ncu_k3q.log 2>&1
+python tools/prof_c3.py 1 flag > $O/prof_c3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k3_direct -c 1 -o $O/k3_c3_direct -f python tools/prof_c3.py 1 flag > $O/ncu_k3d.log 2>&1
 python tools/c5_one_step.py 3 > $O/c5_one.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k1_fast -s 4 -c 1 -o $O/k1_c5 -f python tools/c5_one_step.py 2 > $O/ncu_k1c5.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k2_gather -s 20 -c 1 -o $O/gather_c5 -f python tools/c5_one_step.py 3 > $O/ncu_g.log 2>&1
