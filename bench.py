@@ -530,7 +530,7 @@ def main():
     achieved = BYTES_PER_CELL_SWE * N * N / (k1 * 1e-3) / 1e9
 
     # ---- K3 adjoint flagging on the same state (the adjoint grid covers rank 0's square)
-    flag = bench_flagging(p, st, dt, stream) if rank == 0 else None
+    flag = bench_flagging(p, st, dt, stream, with_cpu=world == 1 and not args.no_cpu_baseline) if rank == 0 else None
 
     # ---- e2e through the public API with host buffers
     e2e = bench_e2e(p, eq, bc, shape, dt, variant, min(args.steps, 5), world)
@@ -663,7 +663,25 @@ def bench_c3(steps, variant):
                         "full-span window at step 100"}
 
 
-def bench_flagging(p, st, dt, stream):
+def flag_cpu_baseline(st, p, ring, idx, nb=1024):
+    """The oracle's inner_product_field (numpy restatement of the reference,
+    1 core) on a bounded sample: an nb x nb block of the C4 state against the
+    window's snapshots."""
+    from oracle import adjamr_oracle as O
+    a0 = 1500
+    q = st.view(p._slot)[:, 2 + a0:2 + a0 + nb, 2 + a0:2 + a0 + nb].cpu().numpy()
+    fields = ring[list(idx)].cpu().numpy()
+    xs = (np.arange(a0, a0 + nb) + 0.5) * (L / N)
+    xc, yc = np.broadcast_to(xs[:, None], (nb, nb)), np.broadcast_to(xs[None, :], (nb, nb))
+    t0 = time.perf_counter()
+    O.inner_product(q, xc, yc, fields, list(range(len(idx))), (0.0, 0.0), L / 1024, L / 1024)
+    el = time.perf_counter() - t0
+    return {"value": nb * nb / el, "unit": "flagged cells/s", "cores": 1, "kind": "port",
+            "sample": f"oracle inner_product on a {nb}x{nb} block of the C4 state, {len(idx)} snapshots "
+                      f"({el:.2f} s)"}
+
+
+def bench_flagging(p, st, dt, stream, with_cpu=False):
     import torch
     from paper_1511_03645_b200 import _lib, device
     nsnap = 41
@@ -711,7 +729,9 @@ def bench_flagging(p, st, dt, stream):
         del best
         peak, _ = peaks()
         fp64 = 40 if variant == _lib.VARIANT_EXACT else 16      # FP64 instructions per cell-snapshot
+        cpu = flag_cpu_baseline(st, p, ring, idx) if with_cpu else None
         res[label] = {"value": N * N / (kms * 1e-3), "unit": "flagged cells/s", "snapshots": len(idx),
+                      "cpu_baseline": cpu,
                       "cell_snapshots_per_s": N * N * len(idx) / (kms * 1e-3),
                       "kernel_ms": kms, "achieved_GBps": nbytes / (kms * 1e-3) / 1e9,
                       "hbm_frac": nbytes / (kms * 1e-3) / 1e9 / peak,
