@@ -1,0 +1,72 @@
+"""advance_sharded end to end with real ranks: two processes on one GPU over
+a gloo group (host-staged exchange; a functional check of the N > 1 path,
+not a measurement), graph-replayed steps with odd call lengths.  Every
+rank's interior equals the unsharded advance_uniform run (EXACT bitwise,
+FAST within 1e-12)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+NX, NY, STEPS = 97, 131, (5, 4, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, variant, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1511_03645_b200 import _lib
+    from paper_1511_03645_b200.sharded import DistTransport, advance_sharded
+    from tests.test_gpu_sharded import _setup
+    var = _lib.VARIANT_EXACT if variant == "exact" else _lib.VARIANT_FAST
+    h, whole, shards, eq, bc, dt = _setup("ac", NX, NY, ("wall", "outflow", "outflow", "wall"), world)
+    p = shards[rank]
+    tr = DistTransport(rank, world)
+    for n in STEPS:
+        advance_sharded(p, eq, bc, (NX, NY), dt, n, tr, "MC", var)
+    results[rank] = (p.spec.lo[0], p.spec.hi[0] + 1, np.array(p.state)[:, 2:-2, 2:-2])
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("variant", ["exact", "fast"])
+def test_two_ranks_equal_unsharded(variant):
+    from paper_1511_03645_b200 import _lib, solver
+    from tests.helpers import norm_rel
+    from tests.test_gpu_sharded import _setup
+    world = 2
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        res = mgr.dict()
+        port = _free_port()
+        procs = [ctx.Process(target=_worker, args=(r, world, port, variant, res)) for r in range(world)]
+        for pr in procs:
+            pr.start()
+        for pr in procs:
+            pr.join(timeout=600)
+            assert pr.exitcode == 0
+        out = dict(res)
+    var = _lib.VARIANT_EXACT if variant == "exact" else _lib.VARIANT_FAST
+    h, whole, shards, eq, bc, dt = _setup("ac", NX, NY, ("wall", "outflow", "outflow", "wall"), 1)
+    solver.advance_uniform(whole, eq, bc, (NX, NY), dt, sum(STEPS), "MC", var, graph=False)
+    want = np.array(whole.state)[:, 2:-2, 2:-2]
+    for r in range(world):
+        x0, x1, got = out[r]
+        if variant == "exact":
+            assert np.array_equal(got, want[:, x0:x1])
+        else:
+            assert norm_rel(got, want[:, x0:x1]) <= 1e-12
