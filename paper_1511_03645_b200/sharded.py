@@ -204,17 +204,74 @@ def _check(st, dtdx, dtdy, ndim):
     return cfl
 
 
-def _graphed_pair(patch, equation, boundary, level_shape, dt, limiter, variant, key):
-    """Capture two consecutive steps of the slab as four CUDA graphs: per
-    step, pre = physical fill + ghost fold + packing of the boundary rows
-    into persistent send buffers, post = unpacking of the persistent receive
-    buffers into the ghost rows + K1.  The exchange itself runs between them
-    (not captured).  The buffer roles are 2-periodic, as in advance_uniform."""
-    import torch
+def _split_tiles(st, nx, g):
+    """FAST strip tables of the slab split into strips whose footprint
+    (x +- g) stays inside the slab's interior rows (interior) and the rest
+    (boundary, which read the exchanged ghost rows).  None if either is empty."""
+    import numpy as np
+    from . import _lib
+    key = ("shard_tiles", nx, g)
+    hit = st._scratch.get(key)
+    if hit is not None:
+        return hit
+    tiles, ntile, jobs, njob = st.tiles(_lib.VARIANT_FAST)
+    rows = np.frombuffer(tiles.cpu().numpy().tobytes(), dtype=_lib.TILE_DTYPE)[:ntile].copy()
+    offs = jobs.cpu().numpy() if jobs is not None else np.arange(ntile + 1, dtype=np.int32)
+    touch = (rows["i0"] < g) | (rows["i0"] + rows["ni"] + g > nx)
+    parts = []
+    for want in (False, True):
+        sel_rows, sel_offs = [], [0]
+        for j in range(len(offs) - 1):
+            seg = rows[offs[j]:offs[j + 1]]
+            if bool(np.any(touch[offs[j]:offs[j + 1]])) == want:
+                sel_rows.extend(seg)
+                sel_offs.append(len(sel_rows))
+        if not sel_rows:
+            st._scratch[key] = None
+            return None
+        arr = np.array(sel_rows, dtype=_lib.TILE_DTYPE)
+        parts.append((device_table(arr), len(arr), _torch_i32(sel_offs), len(sel_offs) - 1))
+    st._scratch[key] = tuple(parts)
+    return st._scratch[key]
+
+
+def device_table(arr):
     from . import device
+    return device._dev_table(arr)
+
+
+def _torch_i32(vals):
+    import numpy as np
+    import torch
+    return torch.from_numpy(np.array(vals, dtype=np.int32)).to("cuda")
+
+
+def _launch_tiles(st, dt, equation, limiter, variant, out, tab):
+    """K1 of the slab over one tile table (interior or boundary strips)."""
+    from . import device
+    saved = st._tiles[variant]
+    st._tiles[variant] = tab
+    try:
+        device.launch_step(st, dt, equation, limiter, variant, out, None, accumulate=True)
+    finally:
+        st._tiles[variant] = saved
+
+
+def _graphed_pair(patch, equation, boundary, level_shape, dt, limiter, variant, key):
+    """Capture two consecutive steps of the slab as CUDA graphs around the
+    (uncaptured) exchange.  Per step: pre = physical fill + ghost fold +
+    packing of the boundary rows into persistent send buffers; FAST with an
+    internal boundary: mid = K1 over the strips that do not read the ghost
+    rows (it runs while the exchange is in flight on a side stream), post =
+    unpacking into the ghost rows + K1 over the remaining strips; otherwise
+    post = unpacking + K1 over the whole slab.  The buffer roles are
+    2-periodic, as in advance_uniform."""
+    import torch
+    from . import _lib, device
     st, offset, pitch = _layout(patch)
     g, m, nx = st.g, st.m, patch.spec.shape[0]
     has_lo, has_hi = _edges(patch, level_shape)
+    split = _split_tiles(st, nx, g) if (has_lo or has_hi) and variant == _lib.VARIANT_FAST else None
     bufs = [torch.empty((m, g * pitch), dtype=torch.float64, device="cuda") for _ in range(4)]
     send_lo, send_hi, recv_lo, recv_hi = bufs
     roles = (st.cur, st.old, st.ghost_src)
@@ -224,7 +281,7 @@ def _graphed_pair(patch, equation, boundary, level_shape, dt, limiter, variant, 
     graphs = []
     with torch.cuda.stream(side):
         for _ in range(2):
-            pre, post = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            pre, mid, post = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
             with torch.cuda.graph(pre, stream=side):
                 device.fill_physical(st, boundary, equation, level_shape)
                 st.fold_ghosts()
@@ -233,14 +290,24 @@ def _graphed_pair(patch, equation, boundary, level_shape, dt, limiter, variant, 
                     send_lo.copy_(halo_rows(q, m, st.plane, offset, pitch, g, 2 * g))
                 if has_hi:
                     send_hi.copy_(halo_rows(q, m, st.plane, offset, pitch, nx, nx + g))
+            out = st._free(*([st.cur] + ([st.old] if st.old is not None else [])))
+            if split is not None:
+                with torch.cuda.graph(mid, stream=side):
+                    _launch_tiles(st, dt, equation, limiter, variant, out, split[0])
             with torch.cuda.graph(post, stream=side):
                 q = st.buf[st.cur]
                 if has_lo:
                     halo_rows(q, m, st.plane, offset, pitch, 0, g).copy_(recv_lo)
                 if has_hi:
                     halo_rows(q, m, st.plane, offset, pitch, nx + g, nx + 2 * g).copy_(recv_hi)
-                _launch(st, dt, equation, limiter, variant, None)
-            graphs.append((pre, post))
+                if split is not None:
+                    _launch_tiles(st, dt, equation, limiter, variant, out, split[1])
+                else:
+                    _launch(st, dt, equation, limiter, variant, None)
+            if split is not None:
+                st.ghost_src = st.cur
+                st.cur = out
+            graphs.append((pre, mid if split is not None else None, post))
     torch.cuda.current_stream().wait_stream(side)
     if (st.cur, st.old, st.ghost_src) != roles:
         raise RuntimeError("sharded step pair is not 2-periodic")
@@ -289,13 +356,27 @@ def advance_sharded(patch, equation, boundary, level_shape, dt: float, nsteps: i
         done += 2
         entry = _graphed_pair(patch, equation, boundary, level_shape, dt, limiter, variant, key)
     if entry is not None:
+        import torch
         graphs, (send_lo, send_hi, recv_lo, recv_hi), has_lo, has_hi = entry
+        main = torch.cuda.current_stream()
+        comm = st.__dict__.get("_shard_comm")
+        if comm is None:
+            comm = st._shard_comm = (torch.cuda.Stream(), torch.cuda.Event(), torch.cuda.Event())
+        cstream, packed, received = comm
         while nsteps - done >= 2:
-            for pre, post in graphs:
+            for pre, mid, post in graphs:
                 pre.replay()
                 if has_lo or has_hi:
-                    transport.exchange_into(send_lo if has_lo else None, send_hi if has_hi else None,
-                                            recv_lo, recv_hi)
+                    # the exchange runs on a side stream while the interior strips step
+                    packed.record(main)
+                    cstream.wait_event(packed)
+                    with torch.cuda.stream(cstream):
+                        transport.exchange_into(send_lo if has_lo else None, send_hi if has_hi else None,
+                                                recv_lo, recv_hi)
+                        received.record(cstream)
+                    if mid is not None:
+                        mid.replay()
+                    main.wait_event(received)
                 post.replay()
                 patch.time += dt
             done += 2
