@@ -563,8 +563,9 @@ def main():
         "c5_full_workflow": c5_full,
         "e2e": e2e,
         # per step: k2_physical + k1_fast (graph replay; no memset nodes, fold is a no-op);
-        # sharded (N > 1): + the ghost-ring fold (k2_ring) before the exchange
-        "gpu_launches": args.steps * (2 if world == 1 else 3),
+        # sharded (N > 1): k2_physical, the ghost-ring fold, K1 over the interior strips
+        # (during the exchange) and K1 over the boundary strips
+        "gpu_launches": args.steps * (2 if world == 1 else 4),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
