@@ -97,3 +97,61 @@ def test_fast_and_exact_flags_differ_only_at_the_tolerance(tol):
           f"{listed[:20].tolist()} max |best-tol|/tol {float(rel.max()) if len(listed) else 0.0}")
     assert cf > 0 and ce > 0
     assert bool(near[differ].all()), "a flag differs away from the tolerance"
+
+
+def _acoustics_level(n, sides, seed=5):
+    """Homogeneous acoustics (K=4, rho=1) on an n x n level with a seeded
+    random state (the constant-coefficient system the properties below need)."""
+    from paper_1511_03645_b200 import equations as E
+    from paper_1511_03645_b200 import solver
+    from paper_1511_03645_b200.geometry import Patch, PatchHierarchy
+    eq = E.Acoustics2D(E.AcousticsMaterialModel(lambda x, y: np.full_like(np.asarray(x, float), 4.0),
+                                                lambda x, y: np.ones_like(np.asarray(x, float))))
+    bc = solver.BoundarySpec(*sides)
+    h = PatchHierarchy(xlim=(0.0, 1.0), ylim=(0.0, 1.0), base_shape=(n, n), ratios=[])
+    p = Patch(h.make_spec(1, (0, 0), (n - 1, n - 1)), 3)
+    solver.sample_patch_material(p, eq, bc, (n, n))
+    rng = np.random.default_rng(seed)
+    p.interior()[...] = rng.standard_normal((3, n, n))
+    h.levels = [[p]]
+    return h, p, eq, bc, solver.select_dt(h, eq, 0.9)
+
+
+@pytest.mark.parametrize("variant", ["fast", "exact"])
+def test_conservation_periodic_full_size(variant):
+    """Constant coefficients and periodic sides on a 2048^2 level: the
+    wave-propagation update is conservative, so every component's sum is
+    invariant to roundoff over 6 steps (size-independent property)."""
+    import torch
+    from paper_1511_03645_b200 import _lib, solver
+    n = 2048
+    h, p, eq, bc, dt = _acoustics_level(n, ("periodic", "periodic", "periodic", "periodic"))
+    var = _lib.VARIANT_FAST if variant == "fast" else _lib.VARIANT_EXACT
+    q0 = torch.from_numpy(np.array(p.interior())).double()
+    solver.advance_uniform(p, eq, bc, (n, n), dt, 6, "MC", var)
+    q1 = p._store.view(p._slot)[:, 2:-2, 2:-2].cpu()
+    for c in range(3):
+        drift = abs(float(q1[c].sum() - q0[c].sum()))
+        assert drift <= 1e-12 * float(q0[c].abs().sum()), (c, drift)
+
+
+@pytest.mark.parametrize("variant", ["fast", "exact"])
+def test_linearity_without_limiter_full_size(variant):
+    """Without a limiter the scheme is linear in q: step(a q1 + b q2) =
+    a step(q1) + b step(q2) to 1e-12 norm-relative on a 2048^2 level
+    (test_solver.py:162-180 states it on small patches)."""
+    from paper_1511_03645_b200 import _lib, solver
+    from tests.helpers import norm_rel
+    n = 2048
+    var = _lib.VARIANT_FAST if variant == "fast" else _lib.VARIANT_EXACT
+    sides = ("wall", "outflow", "outflow", "wall")
+    outs = []
+    for seed in (5, 6):
+        h, p, eq, bc, dt = _acoustics_level(n, sides, seed)
+        solver.advance_uniform(p, eq, bc, (n, n), dt, 3, "none", var)
+        outs.append(np.array(p.interior()))
+    h, p, eq, bc, dt = _acoustics_level(n, sides, 5)
+    h2, p2, _, _, _ = _acoustics_level(n, sides, 6)
+    p.interior()[...] = 2.0 * np.array(p.interior()) - 0.5 * np.array(p2.interior())
+    solver.advance_uniform(p, eq, bc, (n, n), dt, 3, "none", var)
+    assert norm_rel(np.array(p.interior()), 2.0 * outs[0] - 0.5 * outs[1]) <= 1e-12
