@@ -14,6 +14,11 @@ exists in numpy), so the oracle is bitwise identical to the reference; the
 tests pin that against golden vectors produced by the reference itself
 (tests/golden/make_golden.py).  Importable only from tests/, bench.py's
 cpu_baseline / --impl reference legs and __graft_entry__.smoke().
+
+Exceptions (parity unpinned by the reference): the "periodic" side of
+fill_physical is an extension for BASELINE C3 (the reference has wall and
+outflow only) and inner_product_interp restates the north_star's
+time-interpolated window from adjoint.py:98-110 + 227-249.
 """
 from __future__ import annotations
 
