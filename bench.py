@@ -328,6 +328,7 @@ def k1_alone_ms(st, dt, eq, variant, launches=10):
     from paper_1511_03645_b200 import device
     st.fold_ghosts()
     out = st._free(*[b for b in (st.cur, st.ghost_src, st.old) if b is not None])
+    device.launch_step(st, dt, eq, "MC", variant, out, accumulate=True)   # eager once: tables, scratch
     torch.cuda.synchronize()
     side = torch.cuda.Stream()
     side.wait_stream(torch.cuda.current_stream())
