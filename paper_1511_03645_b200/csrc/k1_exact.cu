@@ -265,27 +265,30 @@ struct Step {
 
     static ADJ_D bool wet(const PatchView& P, int i, int j) { return P.A(1, i, j) > 0.0; }
 
-    // ftil at x-face (i,j) after transverse terms T3/T4 and SWE face mask (solver.py:470-500)
-    static __device__ K1X_TIL_INL void ftil(const PatchView& P, int i, int j, double dtdx, double dtdy,
-                                             double g, int lim, double* F) {
+    // ftil at x-face (i,j) after transverse terms T3/T4 and SWE face mask (solver.py:470-500).
+    // XF(i, j, r) / YF(i, j, r) give the x-face (i | i+1, row j) / y-face (j | j+1,
+    // column i) solve: computed on the spot, or read from a tile's shared memory.
+    template <class XF, class YF>
+    static __device__ K1X_TIL_INL void ftil_t(const PatchView& P, XF&& xf, YF&& yf, int i, int j, double dtdx,
+                                              double dtdy, double g, int lim, double* F) {
         Rp c, u, d;
-        face(P, 0, i, j, i + 1, j, g, c);
-        face(P, 0, i - 1, j, i, j, g, u);
-        face(P, 0, i + 1, j, i + 2, j, g, d);
+        xf(i, j, c);
+        xf(i - 1, j, u);
+        xf(i + 1, j, d);
         corr(c, u, d, dtdx, lim, F);
         const double h = 0.5 * dtdy;
         double bm[3], bp[3];
         Rp y;
-        face(P, 1, i + 1, j, i + 1, j + 1, g, y);          // amdq_y(i+1, j) -> bm
+        yf(i + 1, j, y);                                   // amdq_y(i+1, j) -> bm
         trans(P, 1, y.am, i, j, i + 2, j, g, bm, bp);
         for (int q = 0; q < 3; ++q) F[q] = F[q] - h * bm[q];
-        face(P, 1, i, j, i, j + 1, g, y);                  // amdq_y(i, j) -> bp
+        yf(i, j, y);                                       // amdq_y(i, j) -> bp
         trans(P, 1, y.am, i - 1, j, i + 1, j, g, bm, bp);
         for (int q = 0; q < 3; ++q) F[q] = F[q] - h * bp[q];
-        face(P, 1, i + 1, j - 1, i + 1, j, g, y);          // apdq_y(i+1, j-1) -> bm
+        yf(i + 1, j - 1, y);                               // apdq_y(i+1, j-1) -> bm
         trans(P, 1, y.ap, i, j, i + 2, j, g, bm, bp);
         for (int q = 0; q < 3; ++q) F[q] = F[q] - h * bm[q];
-        face(P, 1, i, j - 1, i, j, g, y);                  // apdq_y(i, j-1) -> bp
+        yf(i, j - 1, y);                                   // apdq_y(i, j-1) -> bp
         trans(P, 1, y.ap, i - 1, j, i + 1, j, g, bm, bp);
         for (int q = 0; q < 3; ++q) F[q] = F[q] - h * bp[q];
         if (SWE && !(wet(P, i, j) && wet(P, i + 1, j)))
@@ -293,30 +296,43 @@ struct Step {
     }
 
     // gtil at y-face (i,j) after transverse terms T1/T2 and SWE face mask
-    static __device__ K1X_TIL_INL void gtil(const PatchView& P, int i, int j, double dtdx, double dtdy,
-                                             double g, int lim, double* G) {
+    template <class XF, class YF>
+    static __device__ K1X_TIL_INL void gtil_t(const PatchView& P, XF&& xf, YF&& yf, int i, int j, double dtdx,
+                                              double dtdy, double g, int lim, double* G) {
         Rp c, u, d;
-        face(P, 1, i, j, i, j + 1, g, c);
-        face(P, 1, i, j - 1, i, j, g, u);
-        face(P, 1, i, j + 1, i, j + 2, g, d);
+        yf(i, j, c);
+        yf(i, j - 1, u);
+        yf(i, j + 1, d);
         corr(c, u, d, dtdy, lim, G);
         const double h = 0.5 * dtdx;
         double bm[3], bp[3];
         Rp x;
-        face(P, 0, i, j + 1, i + 1, j + 1, g, x);          // amdq_x(i, j+1) -> bm
+        xf(i, j + 1, x);                                   // amdq_x(i, j+1) -> bm
         trans(P, 0, x.am, i, j, i, j + 2, g, bm, bp);
         for (int q = 0; q < 3; ++q) G[q] = G[q] - h * bm[q];
-        face(P, 0, i, j, i + 1, j, g, x);                  // amdq_x(i, j) -> bp
+        xf(i, j, x);                                       // amdq_x(i, j) -> bp
         trans(P, 0, x.am, i, j - 1, i, j + 1, g, bm, bp);
         for (int q = 0; q < 3; ++q) G[q] = G[q] - h * bp[q];
-        face(P, 0, i - 1, j + 1, i, j + 1, g, x);          // apdq_x(i-1, j+1) -> bm
+        xf(i - 1, j + 1, x);                               // apdq_x(i-1, j+1) -> bm
         trans(P, 0, x.ap, i, j, i, j + 2, g, bm, bp);
         for (int q = 0; q < 3; ++q) G[q] = G[q] - h * bm[q];
-        face(P, 0, i - 1, j, i, j, g, x);                  // apdq_x(i-1, j) -> bp
+        xf(i - 1, j, x);                                   // apdq_x(i-1, j) -> bp
         trans(P, 0, x.ap, i, j - 1, i, j + 1, g, bm, bp);
         for (int q = 0; q < 3; ++q) G[q] = G[q] - h * bp[q];
         if (SWE && !(wet(P, i, j) && wet(P, i, j + 1)))
             for (int q = 0; q < 3; ++q) G[q] = 0.0;
+    }
+
+    static __device__ K1X_TIL_INL void ftil(const PatchView& P, int i, int j, double dtdx, double dtdy, double g,
+                                            int lim, double* F) {
+        ftil_t(P, [&](int a, int b, Rp& r) { face(P, 0, a, b, a + 1, b, g, r); },
+               [&](int a, int b, Rp& r) { face(P, 1, a, b, a, b + 1, g, r); }, i, j, dtdx, dtdy, g, lim, F);
+    }
+
+    static __device__ K1X_TIL_INL void gtil(const PatchView& P, int i, int j, double dtdx, double dtdy, double g,
+                                            int lim, double* G) {
+        gtil_t(P, [&](int a, int b, Rp& r) { face(P, 0, a, b, a + 1, b, g, r); },
+               [&](int a, int b, Rp& r) { face(P, 1, a, b, a, b + 1, g, r); }, i, j, dtdx, dtdy, g, lim, G);
     }
 };
 
@@ -406,8 +422,114 @@ __global__ void __launch_bounds__(256) k1_exact(AdjStepArgs a) {
     }
 }
 
+// 2D, tiled: a CTA owns a 16x16 AdjTile.  Every interface solve its stencil
+// needs is computed once into shared memory (phase 0), then every ftil /
+// gtil of the tile's faces (phase 1), then the cell updates (phase 2) -- the
+// per-cell kernel above recomputes ~32 interface solves and 4 ftil/gtil per
+// cell.  Same functions, same operands, same accumulation order: bitwise
+// equal to k1_exact.
+constexpr int XT = 16;
+constexpr int XS_N = (XT + 3) * (XT + 2);     // x-faces: i in [bi0-2, bi0+ni], j in [bj0-1, bj0+nj]
+constexpr int YS_N = (XT + 2) * (XT + 3);     // y-faces: i in [bi0-1, bi0+ni], j in [bj0-2, bj0+nj]
+constexpr int TILED_SMEM = (XS_N + YS_N) * (int)sizeof(Rp) + 2 * (XT + 1) * XT * 3 * (int)sizeof(double);
+
+template <int SYS, int FORM, bool REV>
+__global__ void __launch_bounds__(256) k1_exact_tiled(AdjStepArgs a) {
+    using S = Step<SYS, FORM, REV>;
+    extern __shared__ __align__(16) unsigned char smem_t[];
+    Rp* XS = reinterpret_cast<Rp*>(smem_t);
+    Rp* YS = XS + XS_N;
+    double* FS = reinterpret_cast<double*>(YS + YS_N);   // ftil, face i = bi0-1+a, row bj0+b: [(a*XT+b)*3]
+    double* GS = FS + (XT + 1) * XT * 3;                  // gtil, column bi0+a, face j = bj0-1+b: [(a*(XT+1)+b)*3]
+    const AdjTile t = a.tiles[blockIdx.x];
+    const AdjPatch p = a.patches[t.patch];
+    const int g = a.ghost;
+    const int ni = t.ni, nj = t.nj, bi0 = g + t.i0, bj0 = g + t.j0;
+    const int nxj = nj + 2, nyj = nj + 3;
+    PatchView P{a.q_in + p.offset, a.aux + p.offset, a.comp_stride, a.aux_stride, p.pitch};
+    const double dtdx = a.dtdx, dtdy = a.dtdy, gr = a.gravity;
+    for (int k = threadIdx.x; k < (ni + 3) * nxj; k += blockDim.x) {
+        const int i = bi0 - 2 + k / nxj, j = bj0 - 1 + k % nxj;
+        S::face(P, 0, i, j, i + 1, j, gr, XS[k]);
+    }
+    for (int k = threadIdx.x; k < (ni + 2) * nyj; k += blockDim.x) {
+        const int i = bi0 - 1 + k / nyj, j = bj0 - 2 + k % nyj;
+        S::face(P, 1, i, j, i, j + 1, gr, YS[k]);
+    }
+    __syncthreads();
+    auto xf = [&](int i, int j, Rp& r) { r = XS[(i - (bi0 - 2)) * nxj + (j - (bj0 - 1))]; };
+    auto yf = [&](int i, int j, Rp& r) { r = YS[(i - (bi0 - 1)) * nyj + (j - (bj0 - 2))]; };
+    for (int k = threadIdx.x; k < (ni + 1) * nj; k += blockDim.x) {
+        const int ai = k / nj, bj = k % nj;
+        S::ftil_t(P, xf, yf, bi0 - 1 + ai, bj0 + bj, dtdx, dtdy, gr, a.limiter, FS + (ai * XT + bj) * 3);
+    }
+    for (int k = threadIdx.x; k < ni * (nj + 1); k += blockDim.x) {
+        const int ai = k / (nj + 1), bj = k % (nj + 1);
+        S::gtil_t(P, xf, yf, bi0 + ai, bj0 - 1 + bj, dtdx, dtdy, gr, a.limiter, GS + (ai * (XT + 1) + bj) * 3);
+    }
+    __syncthreads();
+    const int di = threadIdx.x >> 4, dj = threadIdx.x & 15;
+    double smx = 0.0, smy = 0.0;
+    bool bad = false;
+    if (di < ni && dj < nj) {
+        const int i = bi0 + di, j = bj0 + dj;
+        double dq[3] = {0.0, 0.0, 0.0};
+        Rp f;
+        xf(i - 1, j, f);
+        for (int c = 0; c < 3; ++c) dq[c] = dq[c] - dtdx * f.ap[c];
+        for (int k = 0; k < 3; ++k) smx = fmax(smx, fabs(f.s[k]));
+        xf(i, j, f);
+        for (int c = 0; c < 3; ++c) dq[c] = dq[c] - dtdx * f.am[c];
+        if (i == g + p.nx - 1) for (int k = 0; k < 3; ++k) smx = fmax(smx, fabs(f.s[k]));
+        yf(i, j - 1, f);
+        for (int c = 0; c < 3; ++c) dq[c] = dq[c] - dtdy * f.ap[c];
+        for (int k = 0; k < 3; ++k) smy = fmax(smy, fabs(f.s[k]));
+        yf(i, j, f);
+        for (int c = 0; c < 3; ++c) dq[c] = dq[c] - dtdy * f.am[c];
+        if (j == g + p.ny - 1) for (int k = 0; k < 3; ++k) smy = fmax(smy, fabs(f.s[k]));
+        const double* Fr = FS + ((di + 1) * XT + dj) * 3;
+        const double* Fl = FS + (di * XT + dj) * 3;
+        for (int c = 0; c < 3; ++c) dq[c] = dq[c] - dtdx * (Fr[c] - Fl[c]);
+        const double* Gr = GS + (di * (XT + 1) + dj + 1) * 3;
+        const double* Gl = GS + (di * (XT + 1) + dj) * 3;
+        for (int c = 0; c < 3; ++c) dq[c] = dq[c] - dtdy * (Gr[c] - Gl[c]);
+        if (S::SWE) {
+            double w = S::wet(P, i, j) ? 1.0 : 0.0;
+            for (int c = 0; c < 3; ++c) dq[c] = dq[c] * w;
+        }
+        const int64_t o = p.offset + (int64_t)i * p.pitch + j;
+        for (int c = 0; c < 3; ++c) {
+            const double qn = P.Q(c, i, j) + dq[c];
+            a.q_out[c * a.comp_stride + o] = qn;
+            bad |= !isfinite(qn);
+        }
+    }
+    smx = warp_max(smx);
+    smy = warp_max(smy);
+    unsigned anybad = __ballot_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0) {
+        if (smx > 0.0) atomic_max_nonneg(&a.speed_max[2 * t.patch], smx);
+        if (smy > 0.0) atomic_max_nonneg(&a.speed_max[2 * t.patch + 1], smy);
+        if (anybad) a.nonfinite[t.patch] = 1;
+    }
+}
+
+#ifndef K1X_TILED
+#define K1X_TILED 1
+#endif
+
 template <int SYS, int FORM, bool REV>
 static void launch(const AdjStepArgs& a, cudaStream_t st) {
+    if (K1X_TILED && a.ndim == 2 && SYS != ADJ_SYS_AC1D) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k1_exact_tiled<SYS, FORM, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 TILED_SMEM);
+            attr = true;
+        }
+        k1_exact_tiled<SYS, FORM, REV><<<a.ntile, 256, TILED_SMEM, st>>>(a);
+        return;
+    }
     k1_exact<SYS, FORM, REV><<<a.ntile, 256, 0, st>>>(a);
 }
 
