@@ -183,7 +183,8 @@ typedef struct AdjStepArgs {
     const AdjPatch* patches;   /* device */
     const AdjTile* tiles;      /* device */
     double* speed_max;         /* device, 2*npatch (x, y), zeroed by the call */
-    int32_t* nonfinite;        /* device, npatch, zeroed by the call          */
+    int32_t* nonfinite;        /* device, npatch, zeroed by the call; 1: non-finite result,
+                                  2: an EXACT tile larger than adj_step_tile_shape (not stepped) */
     int32_t* work_counter;     /* device, 2 ints (tile queue head, exit count), zeroed by the call
                                   unless ADJ_STEP_COUNTER_ZERO */
     const double* static_speed;/* optional device (x, y) per patch: material speed bound over the

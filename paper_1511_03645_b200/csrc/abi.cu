@@ -73,6 +73,8 @@ int adj_step_level(const AdjStepArgs* a) {
     if (a->ndim == 2 && a->system == ADJ_SYS_AC1D) return adj::bad("2D requires a 2D system");
     if (a->limiter < ADJ_LIM_NONE || a->limiter > ADJ_LIM_SUPERBEE) return adj::bad("limiter");
     if (!(a->dt > 0.0)) return adj::bad("dt must be positive");
+    if (a->job_offsets && !(a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed))
+        return adj::bad("packed jobs (job_offsets) need the FAST 2D step with static_speed");
     if (a->prefill.plan.n > 0) {
         if (!(a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed && (a->flags & ADJ_STEP_COUNTER_ZERO) &&
               !(a->flags & ADJ_STEP_TWO_ROWS)))

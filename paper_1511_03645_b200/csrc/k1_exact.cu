@@ -341,6 +341,10 @@ __global__ void __launch_bounds__(256) k1_exact(AdjStepArgs a) {
     using S = Step<SYS, FORM, REV>;
     constexpr int M = S::M;
     const AdjTile t = a.tiles[blockIdx.x];
+    if (a.ndim == 2 ? (t.ni > 16 || t.nj > 16) : t.ni > 256) {   // not the adj_step_tile_shape the
+        if (threadIdx.x == 0) a.nonfinite[t.patch] = 2;          // CTA covers: reported, nothing written
+        return;
+    }
     const AdjPatch p = a.patches[t.patch];
     const int g = a.ghost;
     int di, dj;
@@ -442,6 +446,10 @@ __global__ void __launch_bounds__(256) k1_exact_tiled(AdjStepArgs a) {
     double* FS = reinterpret_cast<double*>(YS + YS_N);   // ftil, face i = bi0-1+a, row bj0+b: [(a*XT+b)*3]
     double* GS = FS + (XT + 1) * XT * 3;                  // gtil, column bi0+a, face j = bj0-1+b: [(a*(XT+1)+b)*3]
     const AdjTile t = a.tiles[blockIdx.x];
+    if (t.ni > XT || t.nj > XT) {   // the shared-memory face tables hold at most XT x XT cells
+        if (threadIdx.x == 0) a.nonfinite[t.patch] = 2;
+        return;
+    }
     const AdjPatch p = a.patches[t.patch];
     const int g = a.ghost;
     const int ni = t.ni, nj = t.nj, bi0 = g + t.i0, bj0 = g + t.j0;
@@ -519,39 +527,44 @@ __global__ void __launch_bounds__(256) k1_exact_tiled(AdjStepArgs a) {
 #endif
 
 template <int SYS, int FORM, bool REV>
-static void launch(const AdjStepArgs& a, cudaStream_t st) {
+static int launch(const AdjStepArgs& a, cudaStream_t st) {
     if (K1X_TILED && a.ndim == 2 && SYS != ADJ_SYS_AC1D) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k1_exact_tiled<SYS, FORM, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 TILED_SMEM);
-            attr = true;
+        // opt-in shared memory is a per-device function attribute: set once per device
+        static unsigned long long attr_set = 0ull;
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return check_launch("k1_exact_tiled");
+        if (!(attr_set & (1ull << dev))) {
+            if (cudaFuncSetAttribute(k1_exact_tiled<SYS, FORM, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     TILED_SMEM) != cudaSuccess)
+                return check_launch("k1_exact_tiled (shared memory attribute)");
+            attr_set |= 1ull << dev;
         }
         k1_exact_tiled<SYS, FORM, REV><<<a.ntile, 256, TILED_SMEM, st>>>(a);
-        return;
+        return ADJ_OK;
     }
     k1_exact<SYS, FORM, REV><<<a.ntile, 256, 0, st>>>(a);
+    return ADJ_OK;
 }
 
 template <int SYS>
-static void dispatch_form(const AdjStepArgs& a, cudaStream_t st) {
-    if (a.form == ADJ_FORM_WAVE) {
-        if (a.reversed) launch<SYS, ADJ_FORM_WAVE, true>(a, st); else launch<SYS, ADJ_FORM_WAVE, false>(a, st);
-    } else {
-        if (a.reversed) launch<SYS, ADJ_FORM_FWAVE, true>(a, st); else launch<SYS, ADJ_FORM_FWAVE, false>(a, st);
-    }
+static int dispatch_form(const AdjStepArgs& a, cudaStream_t st) {
+    if (a.form == ADJ_FORM_WAVE)
+        return a.reversed ? launch<SYS, ADJ_FORM_WAVE, true>(a, st) : launch<SYS, ADJ_FORM_WAVE, false>(a, st);
+    return a.reversed ? launch<SYS, ADJ_FORM_FWAVE, true>(a, st) : launch<SYS, ADJ_FORM_FWAVE, false>(a, st);
 }
 
 }  // namespace exact
 
 int step_exact(const AdjStepArgs& a, cudaStream_t st) {
     if (a.ntile <= 0) return ADJ_OK;
+    int rc;
     switch (a.system) {
-        case ADJ_SYS_AC1D: exact::dispatch_form<ADJ_SYS_AC1D>(a, st); break;
-        case ADJ_SYS_AC2D: exact::dispatch_form<ADJ_SYS_AC2D>(a, st); break;
-        case ADJ_SYS_SWE2D: exact::dispatch_form<ADJ_SYS_SWE2D>(a, st); break;
+        case ADJ_SYS_AC1D: rc = exact::dispatch_form<ADJ_SYS_AC1D>(a, st); break;
+        case ADJ_SYS_AC2D: rc = exact::dispatch_form<ADJ_SYS_AC2D>(a, st); break;
+        case ADJ_SYS_SWE2D: rc = exact::dispatch_form<ADJ_SYS_SWE2D>(a, st); break;
         default: return ADJ_ERR_BAD_ARG;
     }
+    if (rc != ADJ_OK) return rc;
     return check_launch("k1_exact");
 }
 

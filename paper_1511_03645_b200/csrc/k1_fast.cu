@@ -1030,6 +1030,7 @@ int step_exact(const AdjStepArgs& a, cudaStream_t st);
 int step_fast(const AdjStepArgs& a, cudaStream_t st) {
     if (a.ntile <= 0) return ADJ_OK;
     if (a.ndim == 1) return step_exact(a, st);   // 1D runs the exact kernel (tile shape 256x1)
+    if (a.job_offsets && !a.static_speed) return ADJ_ERR_BAD_ARG;   // packed jobs need the static CFL bound
     if (a.system == ADJ_SYS_AC2D) fast::launch_sys<ADJ_SYS_AC2D>(a, st);
     else if (a.system == ADJ_SYS_SWE2D) fast::launch_sys<ADJ_SYS_SWE2D>(a, st);
     else return ADJ_ERR_BAD_ARG;

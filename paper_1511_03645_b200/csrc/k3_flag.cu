@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, 3) k3_direct(AdjFlagArgs a,
                 best[kk] = fmax(best[kk], fabs(d));
             }
         };
-        load(V0, 0);
+        if (nidx > 0) load(V0, 0);   // empty window (t past the last snapshot): best stays 0
         for (int n = 0; n < nidx; n += 2) {
             if (n + 1 < nidx) load(V1, n + 1);
             accumulate(V0);
@@ -1282,7 +1282,7 @@ int flag_adjoint(const AdjFlagArgs& a) {
         } else if (a.ndim == 2 && a.m == 3) {
             // pairs pay off once a window has several snapshots (measured: 1.37 vs 1.69 ms at
             // 21 snapshots on C4; 0.23 vs 0.22 ms at one)
-            if (!m1 && (a.layout & ADJ_FLAG_ROWS) && (a.layout & ADJ_FLAG_DIRECT) && k3_direct_on() &&
+            if (!m1 && a.nidx >= 1 && (a.layout & ADJ_FLAG_ROWS) && (a.layout & ADJ_FLAG_DIRECT) && k3_direct_on() &&
                 (int64_t)a.nxa * a.nya * 3 * 8 < (int64_t(1) << 32)) {
                 const int run = k3_direct_run(a);
                 const dim3 gr((unsigned)((a.max_rows + run - 1) / run),

@@ -210,6 +210,8 @@ def _split_tiles(st, nx, g):
     (boundary, which read the exchanged ghost rows).  None if either is empty."""
     import numpy as np
     from . import _lib
+    if st.two_rows():
+        return None   # 64-row strips (ADJAMR_K1_ROWS=2) have no job table; the split would repack them
     key = ("shard_tiles", nx, g)
     hit = st._scratch.get(key)
     if hit is not None:

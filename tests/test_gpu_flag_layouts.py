@@ -191,7 +191,7 @@ def test_quad_kernel_multi_snapshot(variant, dry):
         assert c == int(f.sum())
 
 
-@pytest.mark.parametrize("case", ["span", "snapshot"])
+@pytest.mark.parametrize("case", ["span", "snapshot", "empty"])
 @pytest.mark.parametrize("dry", [False, True])
 def test_direct_kernel_equal_grids(dry, case):
     """Adjoint grid equal to the forward grid (64 x 512 under the 64 x 512
@@ -202,15 +202,19 @@ def test_direct_kernel_equal_grids(dry, case):
     nxa, nya = 64, 512
     _, patches = _level(ROWS, seed=11)
     vals, wet, store = _store_n(12, nxa, nya, dry)
-    t, window = (0.3, adjoint.TimeWindow(0.0, 0.75)) if case == "span" else (0.6, adjoint.TimeWindow(0.6, 0.6))
-    tol = 0.7
+    t, window = {"span": (0.3, adjoint.TimeWindow(0.0, 0.75)), "snapshot": (0.6, adjoint.TimeWindow(0.6, 0.6)),
+                 "empty": (1.5, adjoint.TimeWindow(0.0, 1.0))}[case]   # empty: t past the last snapshot
+    tol = 0.7 if case != "empty" else 0.0
     flags, counts, best = adjoint.flag_level(patches, t, store, window, tol, want_best=True)
     st = solver.store_of(patches[0])
     tabs = device.flag_axis_tables(st, (nxa, nya), (0.0, 0.0), 1.0 / nxa, 1.0 / nya, (0.0, 0.0),
                                    patches[0].spec.dx, patches[0].spec.dy)
     assert tabs[6] is True
     idx = adjoint.query_window_times(t, window, _FakeStore(window))
-    assert len(idx) >= 2 if case == "span" else len(idx) == 1
+    assert len(idx) == {"span": len(idx) if len(idx) >= 2 else -1, "snapshot": 1, "empty": 0}[case]
+    if case == "empty":   # the reference's inner product is zero everywhere (adjoint.py:227-249)
+        assert not any(np.any(b) for b in best) and not any(f.any() for f in flags) and not any(counts)
+        return
     for p, f, c, b in zip(patches, flags, counts, best):
         lo, shape, dx, dy = p.spec.lo, p.spec.shape, p.spec.dx, p.spec.dy
         x = (np.arange(lo[0], lo[0] + shape[0]) + 0.5) * dx

@@ -2,7 +2,9 @@
 a gloo group (host-staged exchange; a functional check of the N > 1 path,
 not a measurement), graph-replayed steps with odd call lengths.  Every
 rank's interior equals the unsharded advance_uniform run (EXACT bitwise,
-FAST within 1e-12)."""
+FAST within 1e-12).  The wide case (300-row slabs) has strips whose x
+footprint stays inside the slab, so the FAST step runs overlapped: interior
+strips while the exchange is in flight, boundary strips after the unpack."""
 import os
 import socket
 
@@ -12,7 +14,7 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-NX, NY, STEPS = 97, 131, (5, 4, 2)
+NY, STEPS = 131, (5, 4, 2)
 
 
 def _free_port():
@@ -23,7 +25,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, variant, results):
+def _worker(rank, world, port, variant, NX, results):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch
@@ -39,12 +41,16 @@ def _worker(rank, world, port, variant, results):
     tr = DistTransport(rank, world)
     for n in STEPS:
         advance_sharded(p, eq, bc, (NX, NY), dt, n, tr, "MC", var)
-    results[rank] = (p.spec.lo[0], p.spec.hi[0] + 1, np.array(p.state)[:, 2:-2, 2:-2])
+    from paper_1511_03645_b200 import solver
+    from paper_1511_03645_b200.sharded import _split_tiles
+    st = solver.store_of(p)
+    split = _split_tiles(st, p.spec.shape[0], st.g) if var == _lib.VARIANT_FAST else None
+    results[rank] = (p.spec.lo[0], p.spec.hi[0] + 1, np.array(p.state)[:, 2:-2, 2:-2], split is not None)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("variant", ["exact", "fast"])
-def test_two_ranks_equal_unsharded(variant):
+@pytest.mark.parametrize("variant,NX", [("exact", 97), ("fast", 97), ("exact", 600), ("fast", 600)])
+def test_two_ranks_equal_unsharded(variant, NX):
     from paper_1511_03645_b200 import _lib, solver
     from tests.helpers import norm_rel
     from tests.test_gpu_sharded import _setup
@@ -53,7 +59,7 @@ def test_two_ranks_equal_unsharded(variant):
     with ctx.Manager() as mgr:
         res = mgr.dict()
         port = _free_port()
-        procs = [ctx.Process(target=_worker, args=(r, world, port, variant, res)) for r in range(world)]
+        procs = [ctx.Process(target=_worker, args=(r, world, port, variant, NX, res)) for r in range(world)]
         for pr in procs:
             pr.start()
         for pr in procs:
@@ -65,7 +71,9 @@ def test_two_ranks_equal_unsharded(variant):
     solver.advance_uniform(whole, eq, bc, (NX, NY), dt, sum(STEPS), "MC", var, graph=False)
     want = np.array(whole.state)[:, 2:-2, 2:-2]
     for r in range(world):
-        x0, x1, got = out[r]
+        x0, x1, got, overlapped = out[r]
+        # 48-row slabs: every strip touches a slab edge (no overlap); 300-row slabs overlap
+        assert overlapped == (variant == "fast" and NX == 600)
         if variant == "exact":
             assert np.array_equal(got, want[:, x0:x1])
         else:

@@ -85,3 +85,40 @@ def test_fast_kernel_rows_per_lane(case, rows, monkeypatch):
     d = STEP[case]
     q, cfl = _run(d, _lib.VARIANT_FAST)
     assert norm_rel(q, d["q_out"]) <= 1e-12
+
+
+@pytest.mark.parametrize("ni,nj", [(20, 16), (16, 17)])
+def test_exact_oversized_tile_reported(ni, nj):
+    """An ABI caller passing an EXACT tile larger than adj_step_tile_shape
+    (16 x 16) gets nonfinite[patch] = 2 and an untouched output instead of a
+    shared-memory overflow (the tiled kernel's face tables hold 16 x 16)."""
+    import torch
+    from paper_1511_03645_b200 import _lib, device, solver
+    d = STEP[sorted(STEP)[0]]
+    eq = make_equation(d["name"], gravity=d["gravity"] or 9.81)
+    _, p = patch_from_arrays(d["q_in"], d["aux"], eq.is_swe, d["dx"], d["dy"], gravity=d["gravity"] or 9.81)
+    st = solver.store_of(p)
+    st.sync_in()
+    out = st._free(st.cur)
+    before = st.buf[out].clone()
+    bad_tile = np.array([(0, 0, 0, ni, nj, 0)], dtype=_lib.TILE_DTYPE)
+    st._tiles[_lib.VARIANT_EXACT] = (device._dev_table(bad_tile), 1, None, 1)
+    _, nf = device.launch_step(st, d["dt"], eq, d["limiter"], _lib.VARIANT_EXACT, out)
+    torch.cuda.synchronize()
+    assert int(nf[0].item()) == 2
+    assert torch.equal(st.buf[out], before)
+    del st._tiles[_lib.VARIANT_EXACT]
+
+
+def test_packed_jobs_need_static_speed():
+    """FAST with a job table but no static CFL bound is rejected (ADJ_ERR_BAD_ARG)
+    instead of launching nothing."""
+    from paper_1511_03645_b200 import _lib
+    a = _lib.AdjStepArgs()
+    a.ntile, a.njob, a.ndim, a.variant, a.system = 1, 1, 2, _lib.VARIANT_FAST, 1
+    a.ghost, a.dt, a.limiter = 2, 1.0, _lib.LIMITERS["MC"]
+    # any non-null pointers: the call is rejected before a launch reads them
+    a.q_in, a.q_out, a.aux, a.patches, a.tiles, a.speed_max, a.nonfinite, a.work_counter = range(8, 72, 8)
+    a.job_offsets = 80
+    a.static_speed = 0
+    assert _lib.lib().adj_step_level(_lib.C.byref(a)) == 5
