@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define ADJ_ABI_VERSION 4
+#define ADJ_ABI_VERSION 5
 
 /* status codes (mapped to the reference's exception classes by the host) */
 #define ADJ_OK                 0
@@ -168,6 +168,37 @@ typedef struct AdjStepRestrict {
     int32_t ratio, pad;          /* ratio 2 or 4; 0: no fused restriction                          */
 } AdjStepRestrict;
 
+/* Level ghost fill fused into the step, per warp job (FAST 2D static-CFL
+ * path): the level's planned fill (AdjGhostPlan entries, same values) is
+ * regrouped by the step's warp jobs; before a job marches, its lanes fill the
+ * ghost cells its strips read (entries [entry_off[job], entry_off[job+1]))
+ * into q_in.  Entries of two jobs that overlap write identical values.  No
+ * grid barrier: every source (same-level interiors, the coarse level) was
+ * written by earlier launches.  COARSE entries carry their stencil inline.
+ * cache_mode 1 also stores the entry's space-interpolated coarse values at
+ * t0 and t1 (interpolate_patch on state_old / state, geometry.py:302-327) in
+ * cache[c * n + e] (c < m: old, m + c: new); cache_mode 2 reads them instead
+ * of the coarse level: the later substeps of one coarse interval reuse them,
+ * which also keeps them off coarse cells a fused restriction rewrites. */
+typedef struct AdjJobFill {
+    const int32_t* entry_off;    /* [njob + 1] first entry of each warp job                      */
+    const int32_t* dst;          /* [n] ghost cell offset in the level plane                      */
+    const int32_t* src;          /* [n] COPY / physical: source offset in the level plane         */
+    const uint32_t* meta;        /* [n] bit 0: COARSE; bit 1+c: negate component c                */
+    const int32_t* c_base;       /* [n] COARSE: offset of (i0, j0) in the coarse level plane      */
+    const int32_t* c_step;       /* [n] COARSE: (i1-i0)*pitch | (j1-j0) << 30                     */
+    const double* c_wx;          /* [n] COARSE: x weight                                          */
+    const double* c_wy;          /* [n] COARSE: y weight                                          */
+    double* cache;               /* [2 m n] coarse values at t0 and t1, or NULL                   */
+    const double* q_coarse_old;  /* coarse state at t0 / t1                                       */
+    const double* q_coarse_new;
+    int64_t coarse_comp_stride;
+    int32_t n, cache_mode;       /* entries; 0: interpolate, 1: interpolate + store, 2: read cache */
+    int32_t time_mode, pad;      /* 0: old only, 1: blend, 2: new only (as AdjGhostPlanFillArgs)  */
+    double w_time;
+    const double* w_time_dev;    /* optional device weight (< 0: old only)                        */
+} AdjJobFill;
+
 /* K1: wave-propagation step of every patch of a level.
  * Replaces step_patch / step_patch_1d / step_patch_2d (solver.py:415-522), the
  * Riemann and transverse solvers (equations.py:98-349), TimeReversed
@@ -206,6 +237,8 @@ typedef struct AdjStepArgs {
                                   work_counter then holds 3 zeroed ints */
     AdjStepRestrict fine_restrict; /* optional (ratio > 0): restriction into the coarse level fused
                                   into this step (FAST 2D, static_speed, forward wave form) */
+    AdjJobFill job_fill;       /* optional (job_fill.n > 0): the level's ghost fill per warp job
+                                  (FAST 2D, static_speed, job_offsets, ADJ_STEP_COUNTER_ZERO, no prefill) */
 } AdjStepArgs;
 /* AdjStepArgs.flags */
 #define ADJ_STEP_KEEP_NONFINITE 1   /* do not zero nonfinite: accumulate over launches */

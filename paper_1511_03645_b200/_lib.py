@@ -74,6 +74,13 @@ class AdjStepRestrict(C.Structure):
                 ("pad", I32)]
 
 
+class AdjJobFill(C.Structure):
+    _fields_ = [("entry_off", P), ("dst", P), ("src", P), ("meta", P), ("c_base", P), ("c_step", P),
+                ("c_wx", P), ("c_wy", P), ("cache", P), ("q_coarse_old", P), ("q_coarse_new", P),
+                ("coarse_comp_stride", I64), ("n", I32), ("cache_mode", I32), ("time_mode", I32), ("pad", I32),
+                ("w_time", D), ("w_time_dev", P)]
+
+
 class AdjStepArgs(C.Structure):
     _fields_ = [("q_in", P), ("q_out", P), ("aux", P), ("patches", P), ("tiles", P),
                 ("speed_max", P), ("nonfinite", P), ("work_counter", P), ("static_speed", P), ("job_offsets", P),
@@ -82,7 +89,7 @@ class AdjStepArgs(C.Structure):
                 ("system", I32), ("form", I32), ("reversed", I32), ("limiter", I32),
                 ("variant", I32), ("flags", I32),
                 ("dt", D), ("dtdx", D), ("dtdy", D), ("gravity", D), ("stream", P), ("prefill", AdjGhostPlanFillArgs),
-                ("fine_restrict", AdjStepRestrict)]
+                ("fine_restrict", AdjStepRestrict), ("job_fill", AdjJobFill)]
 
 
 class AdjPhysArgs(C.Structure):
@@ -124,7 +131,7 @@ class AdjFlagArgs(C.Structure):
                 ("tolerance", D), ("stream", P)]
 
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 FLAG_ROWS = 1        # AdjFlagArgs.layout: ADJ_FLAG_ROWS
 FLAG_PAIRS = 2       # AdjFlagArgs.layout: ADJ_FLAG_PAIRS
 FLAG_QUADS = 4       # AdjFlagArgs.layout: ADJ_FLAG_QUADS

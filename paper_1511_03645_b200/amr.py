@@ -11,6 +11,7 @@ bookkeeping stay on the host, as north_star prescribes.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -706,6 +707,13 @@ USE_FUSED_RESTRICT = True
 # Off: measured slower on C5 (0.94-0.96 vs 0.75 ms per coarse step) -- the persistent step grid
 # has ~57K threads for ~400K gather entries, the standalone gather ~300K
 USE_FUSED_FILL = False
+# fast static-CFL levels of small patches: the level's fill runs per warp job inside the step
+# launch (device.JobFill; no grid barrier, no separate gather launch); coarse-interpolated ghost
+# values of a coarse interval are computed in its first substep and reused from a cache after.
+# Opt-in (ADJAMR_JOB_FILL=1): measured on C5 0.93 vs 0.76 ms per coarse step -- a cached-substep
+# launch costs what the separate gather + step did (51.9 vs 51.3 us on L3), a first substep
+# (coarse values at both times) far more (93.5 vs 54.8 us): every warp fills before it marches
+USE_JOB_FILL = os.environ.get("ADJAMR_JOB_FILL", "0") == "1"
 
 
 def _static_fast(st, ctx) -> bool:
@@ -740,6 +748,15 @@ class LevelPlan:
         self.full = bool(np.all(covered + phys >= ring))
         self.restrict_to = None      # (coarse store, RectTable) for restriction into level-1
         self._gather = {}            # (boundary, normals, level shape) -> device.GhostPlan
+
+    def job_fill(self, gp):
+        """The planned fill regrouped per warp job (built once per plan), or None."""
+        jf = self.__dict__.setdefault("_job_fill", {})
+        hit = jf.get(id(gp))
+        if hit is None or hit[0] is not gp:
+            hit = (gp, device.JobFill(self.st, gp) if device.JobFill.usable(self.st) else None)
+            jf[id(gp)] = hit
+        return hit[1]
 
     def gather(self, hierarchy, level, ctx):
         """The level's whole fill as one planned gather (built once, on first use)."""
@@ -790,12 +807,15 @@ def _store_time_mode(cst, t):
     return None
 
 
-def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrContext, defer: bool = False):
+def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrContext, defer: bool = False,
+                      substep: int = 0):
     """Coarse interpolation, then same-level copies, then physical boundaries
     (amr.py:479-491), each a batched device launch over the whole level.
     ``defer``: on the fast static-CFL path return the planned fill as step
-    prefill arguments instead of launching it (the next launch_step on this
-    level runs it; nothing may touch the level in between)."""
+    arguments instead of launching it (the next launch_step on this level
+    runs it; nothing may touch the level in between): ("job", AdjJobFill)
+    for a per-warp-job fill, else AdjGhostPlanFillArgs (USE_FUSED_FILL).
+    ``substep``: index of this step inside the coarse level's interval."""
     patches = hierarchy.patches(level)
     if not patches:
         return
@@ -815,6 +835,17 @@ def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrC
         # level-synchronised times: coarse, copy and physical phases in one gather
         gp = pl.gather(hierarchy, level, ctx)
         if gp is not None:
+            if defer and USE_JOB_FILL and gp.n and _static_fast(st, ctx):
+                jf = pl.job_fill(gp)
+                if jf is not None:
+                    st.ghost_src = st.cur
+                    if coarse_in and jf.c_base is not None:
+                        # coarse values of this interval: computed in its first substep, then cached
+                        key = (id(cst), device._ptr(old_buf), device._ptr(cst.buf[cst.cur]), cst.level_time, cst.level_time_old)
+                        cmode = 2 if (substep > 0 and jf.cache_key == key) else 1
+                        jf.cache_key = key
+                        return ("job", jf.args(old_buf, cst.buf[cst.cur], cst, mw[1], mw[0], cmode))
+                    return ("job", jf.args())
             if defer and USE_FUSED_FILL and gp.n and _static_fast(st, ctx):
                 args = (gp.fill_args(st, old_buf, cst.buf[cst.cur], cst, mw[1], mw[0]) if coarse_in
                         else gp.fill_args(st))
@@ -1105,6 +1136,9 @@ def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext
     static = ctx.variant == _lib.VARIANT_FAST and st.ndim == 2 and not st.any_dry()
     if prefill is not None and not static:
         raise RuntimeError("a deferred ghost fill needs the fast static-CFL step")
+    job_fill = None
+    if isinstance(prefill, tuple):              # ("job", AdjJobFill)
+        job_fill, prefill = prefill[1], None
     spec = patches[0].spec
     dtdx = dt / spec.dx
     dtdy = dt / spec.dy if spec.ndim == 2 else 0.0
@@ -1112,11 +1146,14 @@ def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext
     if static:
         sm0 = st.static_speed_np()
         cfl_static = np.maximum(sm0[:, 0] * dtdx, sm0[:, 1] * dtdy)
-    fused = _fused_restrict(hierarchy, level, pl, ctx, cfl_static) if restrict_into and prefill is None else None
+    # the fused restriction rewrites coarse interior cells: only with a fill that does not read the
+    # coarse level in this launch (cached coarse values, or no coarse entries)
+    may_fuse = prefill is None and (job_fill is None or job_fill.cache_mode == 2 or not job_fill.c_base)
+    fused = _fused_restrict(hierarchy, level, pl, ctx, cfl_static) if restrict_into and may_fuse else None
     if fused is not None:
         ctx.__dict__["fused_restrictions"] = ctx.__dict__.get("fused_restrictions", 0) + 1
     smax, bad = device.launch_step(st, dt, ctx.equation, ctx.limiter, ctx.variant, out, accumulate=static,
-                                   prefill=prefill, fine_restrict=fused)
+                                   prefill=prefill, fine_restrict=fused, job_fill=job_fill)
     sm = st.static_speed_np() if static else smax.cpu().numpy()
     cfl = sm[:, 0] * dtdx if spec.ndim == 1 else np.maximum(sm[:, 0] * dtdx, sm[:, 1] * dtdy)
     st.ghost_src = st.cur
@@ -1167,7 +1204,7 @@ def advance_hierarchy(hierarchy: PatchHierarchy, level: int, dt: float, ctx: Amr
         _raise_pending(ctx)
 
 
-def _advance(hierarchy, level, dt, ctx, restrict_into: bool = False) -> bool:
+def _advance(hierarchy, level, dt, ctx, restrict_into: bool = False, substep: int = 0) -> bool:
     """One step of ``level`` and its subcycled finer levels; returns whether
     the restriction of ``level`` into level-1 already ran (fused into the
     step of the interval's last substep of the finest level)."""
@@ -1178,7 +1215,7 @@ def _advance(hierarchy, level, dt, ctx, restrict_into: bool = False) -> bool:
     if not patches:
         return False
     t = patches[0].time
-    pre = fill_level_ghosts(hierarchy, level, t, ctx, defer=True)
+    pre = fill_level_ghosts(hierarchy, level, t, ctx, defer=True, substep=substep)
     fused = step_level(hierarchy, level, dt, ctx, prefill=pre, restrict_into=restrict_into)
     t_new = t + dt
     st = patches[0]._store
@@ -1191,7 +1228,7 @@ def _advance(hierarchy, level, dt, ctx, restrict_into: bool = False) -> bool:
         ratio = hierarchy.ratio_to_finer(level)
         done = False
         for k in range(ratio):
-            done = _advance(hierarchy, level + 1, dt / ratio, ctx, restrict_into=k == ratio - 1)
+            done = _advance(hierarchy, level + 1, dt / ratio, ctx, restrict_into=k == ratio - 1, substep=k)
         if not done:
             restrict_fine_to_coarse(hierarchy, level)
     return fused

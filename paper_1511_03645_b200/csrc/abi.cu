@@ -93,6 +93,18 @@ int adj_step_level(const AdjStepArgs* a) {
         if (!(r.ratio == 2 || r.ratio == 4)) return adj::bad("fused restriction ratio must be 2 or 4");
         if (!(r.q_coarse && r.cell && r.base)) return adj::bad("null fused restriction tables");
     }
+    if (a->job_fill.n > 0) {
+        const AdjJobFill& f = a->job_fill;
+        if (!(a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed && a->job_offsets &&
+              (a->flags & ADJ_STEP_COUNTER_ZERO) && !(a->flags & ADJ_STEP_TWO_ROWS) && a->prefill.plan.n == 0))
+            return adj::bad("job fill needs the FAST 2D static-CFL step with job_offsets, "
+                            "ADJ_STEP_COUNTER_ZERO and no prefill");
+        if (!(f.entry_off && f.dst && f.src && f.meta)) return adj::bad("null job fill tables");
+        if (f.cache_mode < 0 || f.cache_mode > 2 || (f.cache_mode && !f.cache))
+            return adj::bad("job fill cache_mode needs a cache");
+        if (f.cache_mode != 2 && f.c_base && !(f.q_coarse_old && f.q_coarse_new && f.c_step && f.c_wx && f.c_wy))
+            return adj::bad("null job fill coarse state");
+    }
     cudaStream_t st = (cudaStream_t)a->stream;
     int rc = ADJ_OK;
     const bool static_cfl = a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed;

@@ -150,6 +150,89 @@ ADJ_D void prefill_gather(const AdjGhostPlanFillArgs& a) {
     }
 }
 
+// ---- job fill: the level's planned ghost fill, regrouped per warp job
+// (AdjJobFill).  The lanes fill the ghost cells this job's strips read, then
+// the march reads them back through the shared ring.  Same entries and
+// arithmetic as k2_gather; reads bypass L1 (ld.global.cg) so no line cached
+// here can hold a ghost cell another warp is about to rewrite.
+ADJ_D void job_fill(const AdjJobFill& f, double* q, int64_t cs, int job, int lane) {
+    const int e0 = __ldg(f.entry_off + job), e1 = __ldg(f.entry_off + job + 1);
+    if (e0 >= e1) return;
+    double wt = f.w_time;
+    int tmode = f.time_mode;
+    if (f.w_time_dev) {           // graph replays: negative weight = old state only
+        wt = __ldcg(f.w_time_dev);
+        tmode = wt < 0.0 ? 0 : 1;
+    }
+    const int64_t ccs = f.coarse_comp_stride, n = f.n;
+    const int mode = f.cache_mode;
+    const bool coarse = f.c_base != nullptr;
+    constexpr int U = 2;
+    for (int t0 = e0 + lane; t0 < e1; t0 += 32 * U) {
+        int dst[U], src[U], cb[U], step[U];
+        unsigned meta[U];
+        double wx[U], wy[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + 32 * u;
+            const bool ok = t < e1;
+            const int tt = ok ? t : e0;
+            dst[u] = ok ? __ldg(f.dst + tt) : -1;
+            src[u] = __ldg(f.src + tt);
+            meta[u] = ok ? __ldg(f.meta + tt) : 0u;
+            const bool lc = coarse && mode != 2;
+            cb[u] = lc ? __ldg(f.c_base + tt) : 0;
+            step[u] = lc ? __ldg(f.c_step + tt) : 0;
+            wx[u] = lc ? __ldg(f.c_wx + tt) : 0.0;
+            wy[u] = lc ? __ldg(f.c_wy + tt) : 0.0;
+        }
+        double v[U][3];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + 32 * u;
+            if (meta[u] & 1u) {
+                double vo[3], vn[3];
+                if (mode == 2) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        vo[c] = tmode != 2 ? __ldcg(f.cache + c * n + t) : 0.0;
+                        vn[c] = tmode != 0 ? __ldcg(f.cache + (3 + c) * n + t) : 0.0;
+                    }
+                } else {
+                    const int di = step[u] & 0x3fffffff, dj = (int)((unsigned)step[u] >> 30);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        vo[c] = (tmode != 2 || mode == 1) ? ip2(f.q_coarse_old + c * ccs + cb[u], di, dj, wx[u], wy[u]) : 0.0;
+                        vn[c] = (tmode != 0 || mode == 1) ? ip2(f.q_coarse_new + c * ccs + cb[u], di, dj, wx[u], wy[u]) : 0.0;
+                    }
+                    if (mode == 1) {
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            f.cache[c * n + t] = vo[c];
+                            f.cache[(3 + c) * n + t] = vn[c];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    v[u][c] = tmode == 0 ? vo[c]
+                            : (tmode == 2 ? vn[c] : __dadd_rn(__dmul_rn(__dsub_rn(1.0, wt), vo[c]), __dmul_rn(wt, vn[c])));
+            } else {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) v[u][c] = dst[u] >= 0 ? __ldcg(q + c * cs + src[u]) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (dst[u] < 0) continue;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                q[c * cs + dst[u]] = (meta[u] >> (1 + c)) & 1u ? __dmul_rn(v[u][c], -1.0) : v[u][c];
+        }
+    }
+    __threadfence_block();
+}
+
 // Software grid barrier: the persistent grid is sized to be co-resident.
 ADJ_D void grid_barrier(int* counter, int nblocks) {
     __syncthreads();
@@ -681,6 +764,10 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
                 const int next0 = a.tiles[t + 1].pad;
                 if (lane < next0) { tix = t; lane0 = a.tiles[t].pad; break; }
             }
+        }
+        if (!CFL && a.job_fill.n > 0) {   // this job's ghost cells, then every lane sees them
+            job_fill(a.job_fill, const_cast<double*>(a.q_in), a.comp_stride, job, lane);
+            __syncwarp();
         }
         const AdjTile T = a.tiles[tix];
         const AdjPatch p = a.patches[T.patch];

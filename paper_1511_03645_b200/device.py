@@ -847,6 +847,114 @@ class GhostPlan:
         _lib.check(_lib.lib().adj_fill_ghost_plan(_lib.C.byref(a)), "adj_fill_ghost_plan")
 
 
+class JobFill:
+    """A level's planned ghost fill (GhostPlan) regrouped by the FAST step's
+    warp jobs (AdjJobFill): every job gets the plan entries whose ghost cell
+    lies in the window its strips read (rows j0-2 .. j0+nj+1, columns
+    i0-2 .. i0+ni+1 of the tile, ghost-inclusive), COARSE entries with their
+    stencil inline.  The step launch then fills and marches in one kernel
+    (no separate gather launch).  Built once per plan, on the host, from the
+    device plan; only for levels of small patches (at most MAX_TILES strip
+    tiles per patch)."""
+
+    MAX_TILES = 16
+
+    @staticmethod
+    def usable(store: LevelStore) -> bool:
+        if store.ndim != 2 or store.two_rows():
+            return False
+        tiles, ntile, jobs, njob = store.tiles(_lib.VARIANT_FAST)
+        if jobs is None or ntile == 0:
+            return False
+        rows = store.__dict__.get("_tile_rows")
+        if rows is None:
+            rows = np.frombuffer(tiles.cpu().numpy().tobytes(), dtype=_lib.TILE_DTYPE)[:ntile].copy()
+            store._tile_rows = rows
+        return int(np.bincount(rows["patch"], minlength=len(store.patches)).max()) <= JobFill.MAX_TILES
+
+    def __init__(self, store: LevelStore, gp: "GhostPlan"):
+        torch = _torch()
+        tiles, ntile, jobs, njob = store.tiles(_lib.VARIANT_FAST)
+        rows = store._tile_rows
+        offs_job = jobs.cpu().numpy().astype(np.int64)
+        n, nc = gp.n, gp.nc
+        dst = gp.dst[:n].cpu().numpy().astype(np.int64)
+        src = gp.src[:n].cpu().numpy()
+        meta = gp.meta[:n].cpu().numpy().view(np.uint32)
+        isc = (meta & 1) != 0
+        # owning patch and ghost-inclusive local cell of every entry
+        toff = store.table_np["offset"].astype(np.int64)
+        tpitch = store.table_np["pitch"].astype(np.int64)
+        k = np.searchsorted(toff, dst, side="right") - 1
+        rem = dst - toff[k]
+        ii, jj = rem // tpitch[k], rem % tpitch[k]
+        # candidate tiles of the entry's patch
+        order = np.argsort(rows["patch"], kind="stable")
+        cnt = np.bincount(rows["patch"], minlength=len(store.patches))
+        first = np.zeros(len(cnt) + 1, dtype=np.int64)
+        np.cumsum(cnt, out=first[1:])
+        g = store.g
+        ent, tix = [], []
+        for t in range(int(cnt.max()) if len(cnt) else 0):
+            sel = np.flatnonzero(cnt[k] > t)
+            tt = order[first[k[sel]] + t]
+            r = rows[tt]
+            i0, j0 = g + r["i0"].astype(np.int64), g + r["j0"].astype(np.int64)
+            inside = ((ii[sel] >= i0 - 2) & (ii[sel] < i0 + r["ni"] + 2) &
+                      (jj[sel] >= j0 - 2) & (jj[sel] < j0 + r["nj"] + 2))
+            ent.append(sel[inside])
+            tix.append(tt[inside])
+        ent = np.concatenate(ent) if ent else np.zeros(0, np.int64)
+        tix = np.concatenate(tix) if tix else np.zeros(0, np.int64)
+        job = np.searchsorted(offs_job, tix, side="right") - 1
+        o = np.lexsort((ent, job))
+        ent, job = ent[o], job[o]
+        self.n = m = len(ent)
+        self.nc = int(isc[ent].sum()) if m else 0
+        entry_off = np.searchsorted(job, np.arange(njob + 1)).astype(np.int32)
+        i32, f64 = torch.int32, torch.float64
+        up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)
+        self.entry_off = up(entry_off, i32)
+        self.dst = up(dst[ent].astype(np.int32), i32)
+        self.src = up(src[ent].astype(np.int32), i32)
+        self.meta = up(meta[ent].view(np.int32), i32)
+        self.c_base = self.c_step = self.c_wx = self.c_wy = self.cache = None
+        if nc and self.nc:
+            # own coarse stencil (rect COARSE entries e < nc) or the mirrored entry's (physical)
+            e = ent
+            ci = np.where(e < nc, e, src[e])
+            ci = np.where(isc[e], ci, 0)
+            self.c_base = up(gp.c_base[:nc].cpu().numpy()[ci], i32)
+            self.c_step = up(gp.c_step[:nc].cpu().numpy()[ci], i32)
+            self.c_wx = up(gp.c_wx[:nc].cpu().numpy()[ci], f64)
+            self.c_wy = up(gp.c_wy[:nc].cpu().numpy()[ci], f64)
+            self.cache = torch.zeros(6 * max(m, 1), dtype=f64, device="cuda")
+        self.cache_key = None     # the coarse interval whose values the cache holds
+
+    def args(self, q_old=None, q_new=None, coarse_store=None, w_time=0.0, mode=0, cache_mode=0):
+        """The AdjJobFill struct of one step launch (takes the captured-sweep
+        weight slot like GhostPlan.fill_args)."""
+        wptr = 0
+        if PARAMS is not None and self.c_base is not None:
+            if mode == 2:
+                raise RuntimeError("coarse patches without saved state cannot be graph-replayed")
+            wptr = PARAMS.take(w_time if mode == 1 else -1.0)
+        f = _lib.AdjJobFill()
+        f.entry_off, f.dst, f.src, f.meta = (_ptr(self.entry_off), _ptr(self.dst), _ptr(self.src), _ptr(self.meta))
+        if self.c_base is not None:
+            f.c_base, f.c_step, f.c_wx, f.c_wy = (_ptr(self.c_base), _ptr(self.c_step), _ptr(self.c_wx),
+                                                  _ptr(self.c_wy))
+            f.cache = _ptr(self.cache)
+            f.cache_mode = cache_mode
+            f.q_coarse_old, f.q_coarse_new = _ptr(q_old), _ptr(q_new)
+            f.coarse_comp_stride = coarse_store.plane
+        f.n = self.n
+        f.time_mode = mode
+        f.w_time = w_time
+        f.w_time_dev = wptr
+        return f
+
+
 def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=None, slots=None):
     """K2 physical phase on every patch of the store (solver.py:125-146);
     ``slots`` restricts it to a subset of patches."""
@@ -890,7 +998,7 @@ def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=Non
 
 
 def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index, stream=None,
-                accumulate=False, prefill=None, fine_restrict=None):
+                accumulate=False, prefill=None, fine_restrict=None, job_fill=None):
     """K1 on every patch: reads buf[cur], writes buf[out_buf_index].
     Returns (speed_max (npatch, 2) tensor, nonfinite (npatch,) tensor).
     ``accumulate`` (static-CFL fast path only): no per-launch memsets; the
@@ -949,6 +1057,8 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     a.stream = _lib.stream_ptr(stream)
     if prefill is not None:
         a.prefill = prefill
+    if job_fill is not None:          # AdjJobFill: the level's ghost fill per warp job
+        a.job_fill = job_fill
     if fine_restrict is not None:     # (FusedRestrict, coarse store): restriction fused into this step
         fr, cst = fine_restrict
         a.fine_restrict.q_coarse = _ptr(cst.buf[cst.cur])

@@ -58,7 +58,7 @@ def _struct_fields(name):
     fields = []
     typewords = {"const", "unsigned", "long", "double", "int32_t", "int64_t", "uint32_t", "uint8_t", "void", "char",
                  "AdjPatch", "AdjTile", "AdjRect", "AdjGhostPlan", "AdjGauge", "AdjGhostPlanFillArgs",
-                 "AdjStepRestrict"}
+                 "AdjStepRestrict", "AdjJobFill"}
     for decl in body.split(";"):
         toks = decl.replace("*", " ").replace(",", " , ").split()
         if not toks:
@@ -71,7 +71,7 @@ def _struct_fields(name):
     return fields
 
 
-@pytest.mark.parametrize("name", ["AdjStepArgs", "AdjStepRestrict", "AdjPhysArgs", "AdjGhostArgs", "AdjRestrictArgs", "AdjFlagArgs",
+@pytest.mark.parametrize("name", ["AdjStepArgs", "AdjStepRestrict", "AdjJobFill", "AdjPhysArgs", "AdjGhostArgs", "AdjRestrictArgs", "AdjFlagArgs",
                                   "AdjGhostPlan", "AdjGhostPlanBuildArgs", "AdjGhostPlanFillArgs",
                                   "AdjFlagMaskArgs", "AdjFunctionalArgs", "AdjGaugeArgs"])
 def test_ctypes_structs_mirror_header(name):
