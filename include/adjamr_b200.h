@@ -377,6 +377,16 @@ typedef struct AdjFlagArgs {
     double origin_x, origin_y, dx, dy;             /* forward level geometry   */
     double a_origin_x, a_origin_y, a_dx, a_dy;     /* adjoint grid geometry    */
     double tolerance;
+    double* envelope;            /* optional scratch of 6*nxa*nya doubles.  With best == NULL and
+                                    tolerance > 1e-280 the call first writes the window's envelope
+                                    max_k |snapshot_k| per adjoint node and component (planes 3..5)
+                                    and its max over each bilinear stencil (planes 0..2); a cell
+                                    whose bound sum_c |q_c| E_c (1 + 1e-12) is <= tolerance cannot
+                                    be flagged (|qhat_c| <= E_c for the bilinear and time-linear
+                                    weights) and skips its window.  Flags and counts are unchanged
+                                    (quad-layout windows of >= 2 snapshots).                      */
+    int32_t* work;               /* with envelope: scratch of 2 + 4 * (blocks of 2 rows x 64 columns)
+                                    ints, the list of blocks that may exceed the tolerance          */
     void* stream;
 } AdjFlagArgs;
 int adj_flag_adjoint(const AdjFlagArgs* a);

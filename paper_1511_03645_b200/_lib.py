@@ -128,7 +128,7 @@ class AdjFlagArgs(C.Structure):
                 ("layout", I32), ("max_rows", I32), ("max_cols", I32), ("variant", I32),
                 ("origin_x", D), ("origin_y", D), ("dx", D), ("dy", D),
                 ("a_origin_x", D), ("a_origin_y", D), ("a_dx", D), ("a_dy", D),
-                ("tolerance", D), ("stream", P)]
+                ("tolerance", D), ("envelope", P), ("work", P), ("stream", P)]
 
 
 ABI_VERSION = 5

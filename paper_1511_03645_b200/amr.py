@@ -899,24 +899,32 @@ def make_patch(hierarchy: PatchHierarchy, level: int, lo, hi, ctx: AmrContext, t
 
 
 def _restrict_rects(coarse, fine, r):
+    """Overlap of every fine patch's coarsened box with every coarse patch,
+    fine patch major then coarse patch ascending (the order of a per-patch
+    candidate scan), vectorised over blocks of fine patches."""
     c_lo, c_hi = _boxes(coarse)
-    rects = []
-    for fk, fp in enumerate(fine):
-        flo = tuple(l // r for l in fp.spec.lo)
-        fhi = tuple(h // r for h in fp.spec.hi)
-        for c in _candidates(c_lo, c_hi, flo, fhi):
-            ib = _intersect(flo, fhi, tuple(c_lo[c]), tuple(c_hi[c]))
-            if ib is None:
-                continue
-            lo, hi = ib
-            ext = [h - l + 1 for l, h in zip(lo, hi)]
-            di = [lo[a] - c_lo[c][a] for a in range(len(lo))]
-            si = [lo[a] * r - fp.spec.lo[a] for a in range(len(lo))]
-            if len(lo) == 1:
-                rects.append((0, int(c), fk, di[0], 0, ext[0], 1, si[0], 0, 0))
-            else:
-                rects.append((0, int(c), fk, di[0], di[1], ext[0], ext[1], si[0], si[1], 0))
-    return np.array(rects, dtype=_lib.RECT_DTYPE)
+    f_lo, f_hi = _boxes(fine)
+    nd = c_lo.shape[1]
+    out = []
+    blk = max(1, (1 << 20) // max(1, len(coarse)))
+    for b0 in range(0, len(fine), blk):
+        flo, fhi = f_lo[b0:b0 + blk] // r, f_hi[b0:b0 + blk] // r
+        lo = np.maximum(flo[:, None, :], c_lo[None])
+        hi = np.minimum(fhi[:, None, :], c_hi[None])
+        fk, c = np.nonzero(np.all(lo <= hi, axis=2))
+        if not len(fk):
+            continue
+        lo, hi = lo[fk, c], hi[fk, c]
+        rc = np.zeros(len(fk), dtype=_lib.RECT_DTYPE)
+        rc["dst_patch"], rc["src_patch"] = c, fk + b0
+        di, si, ext = lo - c_lo[c], lo * r - f_lo[fk + b0], hi - lo + 1
+        rc["di0"], rc["ni"], rc["si0"] = di[:, 0], ext[:, 0], si[:, 0]
+        if nd == 2:
+            rc["dj0"], rc["nj"], rc["sj0"] = di[:, 1], ext[:, 1], si[:, 1]
+        else:
+            rc["nj"] = 1
+        out.append(rc)
+    return np.concatenate(out) if out else np.zeros(0, dtype=_lib.RECT_DTYPE)
 
 
 def restrict_fine_to_coarse(hierarchy: PatchHierarchy, level: int):

@@ -844,6 +844,52 @@ __global__ void __launch_bounds__(256, 3) k3_pair(AdjFlagArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Window envelope (AdjFlagArgs.envelope): env[c][node] = max over the window's
+// snapshots of |ring[k][c][node]| (NaN propagates, so a non-finite field is
+// never pruned).  Mode 1 entries cover both snapshots of their blend.
+__global__ void k3_envelope(AdjFlagArgs a) {
+    const int64_t plane = (int64_t)a.nxa * a.nya, snap = 3 * plane;
+    const int nidx = a.nidx;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < plane; v += (int64_t)gridDim.x * blockDim.x) {
+        double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+        auto take = [&](int k) {
+            const double* f = a.ring + (int64_t)k * snap + v;
+            const double x0 = fabs(__ldcs(f)), x1 = fabs(__ldcs(f + plane)), x2 = fabs(__ldcs(f + 2 * plane));
+            m0 = (x0 > m0 || x0 != x0) ? x0 : m0;
+            m1 = (x1 > m1 || x1 != x1) ? x1 : m1;
+            m2 = (x2 > m2 || x2 != x2) ? x2 : m2;
+        };
+        for (int n = 0; n < nidx; ++n) {
+            const int k = __ldg(a.snap_index + n);
+            if (a.mode == 1 && k >= 0) { take(k); take(k + 1); }
+            else take(k >= 0 ? k : -k - 1);
+        }
+        a.envelope[3 * plane + v] = m0;      // node envelope in planes 3..5
+        a.envelope[4 * plane + v] = m1;
+        a.envelope[5 * plane + v] = m2;
+    }
+}
+
+ADJ_D double nanmax(double x, double m) { return (x > m || x != x) ? x : m; }
+
+// Stencil envelope: planes 0..2 at (i, j) = max of the node envelope over the
+// bilinear stencil (i..i+1, j..j+1), i < nxa-1, j < nya-1 (the clamped
+// stencil of interpolate_uniform always has this form).
+__global__ void k3_envelope2(AdjFlagArgs a) {
+    const int64_t nya = a.nya, plane = (int64_t)a.nxa * nya;
+    const double* n = a.envelope + 3 * plane;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < plane; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = v / nya, j = v - i * nya;
+        if (i + 1 >= a.nxa || j + 1 >= nya) continue;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double* e = n + c * plane + v;
+            a.envelope[c * plane + v] = nanmax(nanmax(e[0], e[1]), nanmax(e[nya], e[nya + 1]));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Windows of >= 2 snapshots on the row layout with quads (ADJ_FLAG_QUADS:
 // even-aligned row pairs and column pairs share their adjoint stencil, e.g.
 // ratio 4 on aligned grids, C4).  Lane l owns the 2x2 cells (rows i, i+1;
@@ -864,25 +910,13 @@ __global__ void __launch_bounds__(256, 3) k3_pair(AdjFlagArgs a) {
 #endif
 
 template <bool FASTW>
-__global__ void __launch_bounds__(32 * K3_ROW_WARPS, FASTW ? K3_QUAD_MINB_FAST : K3_QUAD_MINB)
-    k3_quad(AdjFlagArgs a, int run) {
-    __shared__ const char* s_base[K3_MAXN];     // snapshot base addresses
-    __shared__ double2 s_q[K3_ROW_WARPS][RDEPTH][6][32];
+ADJ_D void quad_rows(const AdjFlagArgs& a, const char* const* s_base, double2 (*s_qw)[6][32], int pidx,
+                     unsigned seg, unsigned r0, unsigned rend, int lane) {
     const int nidx = a.nidx;
-    {
-        const int64_t snap_b = (int64_t)a.nxa * a.nya * 3 * 8;
-        for (int n = threadIdx.x; n < nidx; n += blockDim.x)
-            s_base[n] = reinterpret_cast<const char*>(a.ring) + (int64_t)a.snap_index[n] * snap_b;
-    }
-    __syncthreads();
-    const int pidx = blockIdx.z;
     const AdjPatch p = a.patches[pidx];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned seg = blockIdx.y * K3_ROW_WARPS + warp;
     const unsigned nseg = (unsigned)p.ny / 64u;
-    const unsigned r0 = blockIdx.x * (unsigned)run;               // run is even
     if (seg >= nseg || r0 >= (unsigned)p.nx) return;               // warp-uniform; no barrier below
-    const unsigned r1 = min(r0 + (unsigned)run, (unsigned)p.nx);   // nx is even
+    const unsigned r1 = min(rend, (unsigned)p.nx);                 // nx is even
     const unsigned ny = (unsigned)p.ny, j = seg * 64u + 2u * lane;
     const int g = a.ghost;
     const int64_t cs = a.comp_stride;
@@ -896,7 +930,7 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, FASTW ? K3_QUAD_MINB_FAST :
         for (int r = 0; r < 2; ++r)
 #pragma unroll
             for (int cc = 0; cc < 3; ++cc) {
-                const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_q[warp][buf][r * 3 + cc][lane]);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_qw[buf][r * 3 + cc][lane]);
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
                              "l"(qcol + (int64_t)(i + r) * p.pitch + cc * cs) : "memory");
             }
@@ -962,7 +996,7 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, FASTW ? K3_QUAD_MINB_FAST :
         for (int r = 0; r < 2; ++r)
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const double2 v = s_q[warp][buf][r * 3 + c][lane];
+                const double2 v = s_qw[buf][r * 3 + c][lane];
                 q[r][0][c] = v.x; q[r][1][c] = v.y;
             }
         __syncwarp();
@@ -1039,6 +1073,116 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, FASTW ? K3_QUAD_MINB_FAST :
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     if (lane == 0 && cnt) atomicAdd(&a.counts[pidx], cnt);
+}
+
+template <bool FASTW>
+__global__ void __launch_bounds__(32 * K3_ROW_WARPS, FASTW ? K3_QUAD_MINB_FAST : K3_QUAD_MINB)
+    k3_quad(AdjFlagArgs a, int run) {
+    __shared__ const char* s_base[K3_MAXN];     // snapshot base addresses
+    __shared__ double2 s_q[K3_ROW_WARPS][RDEPTH][6][32];
+    {
+        const int64_t snap_b = (int64_t)a.nxa * a.nya * 3 * 8;
+        for (int n = threadIdx.x; n < a.nidx; n += blockDim.x)
+            s_base[n] = reinterpret_cast<const char*>(a.ring) + (int64_t)a.snap_index[n] * snap_b;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned r0 = blockIdx.x * (unsigned)run;               // run is even
+    quad_rows<FASTW>(a, s_base, s_q[warp], blockIdx.z, blockIdx.y * K3_ROW_WARPS + warp, r0, r0 + (unsigned)run,
+                     lane);
+}
+
+// Bound pass of a pruned window: one warp per 64-column segment and a run of
+// row pairs of the quad layout (the blocks k3_quad's warps own).  Per block the
+// cells' bounds sum_c |q_c| E_c from the stencil envelope (planes 0..2 of
+// AdjFlagArgs.envelope); a block none of whose cells can exceed the tolerance
+// gets zero flag words, the others go to the work list for k3_quad_list.
+// Loads of the next row pair are issued before this one's bound is formed.
+__global__ void __launch_bounds__(256) k3_bound(AdjFlagArgs a, int run) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int pidx = blockIdx.z;
+    const AdjPatch p = a.patches[pidx];
+    const unsigned nseg = (unsigned)p.ny / 64u;
+    const unsigned seg = (unsigned)warp % (nseg ? nseg : 1u), chunk = (unsigned)warp / (nseg ? nseg : 1u);
+    const unsigned r0 = chunk * (unsigned)run;
+    if (nseg == 0 || r0 >= (unsigned)p.nx) return;
+    const unsigned r1 = min(r0 + (unsigned)run, (unsigned)p.nx);
+    const unsigned ny = (unsigned)p.ny, j = seg * 64u + 2u * lane;
+    const int64_t nya = a.nya, plane = (int64_t)a.nxa * nya, cs = a.comp_stride;
+    const int64_t rowoff = a.axis_off[2 * pidx], coloff = a.axis_off[2 * pidx + 1];
+    const double* env = a.envelope + __ldg(a.axis_i + coloff + j);
+    const double* qc = a.q + p.offset + (int64_t)a.ghost * p.pitch + a.ghost + j;
+    const double tol = a.tolerance;
+    double2 Q[2][3];
+    double E[3];
+    auto load = [&](unsigned i) {
+        const int64_t eo = (int64_t)__ldg(a.axis_i + rowoff + i) * nya;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            E[c] = __ldg(env + c * plane + eo);
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+                Q[r][c] = __ldcs(reinterpret_cast<const double2*>(qc + (int64_t)(i + r) * p.pitch + c * cs));
+        }
+    };
+    load(r0);
+    for (unsigned i = r0; i < r1; i += 2) {
+        double2 q[2][3];
+        double e[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { e[c] = E[c]; q[0][c] = Q[0][c]; q[1][c] = Q[1][c]; }
+        if (i + 2 < r1) load(i + 2);
+        bool need = false;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            // |d| <= (1 + 12u) sum_c |q_c| E_c for every snapshot of the window (bilinear and
+            // time-linear weights in [0, 1]); the 1e-12 margin covers that and this sum's rounding
+            const double b0 = fma(fabs(q[r][2].x), e[2], fma(fabs(q[r][1].x), e[1], fabs(q[r][0].x) * e[0]));
+            const double b1 = fma(fabs(q[r][2].y), e[2], fma(fabs(q[r][1].y), e[1], fabs(q[r][0].y) * e[0]));
+            need |= !(b0 * (1.0 + 1e-12) <= tol) || !(b1 * (1.0 + 1e-12) <= tol);
+        }
+        if (__any_sync(0xffffffffu, need)) {
+            if (lane == 0) {
+                const int k = atomicAdd(a.work, 1);
+                reinterpret_cast<int4*>(a.work)[1 + k] = make_int4(pidx, (int)seg, (int)i, 0);
+            }
+        } else if (lane < 4) {
+            const unsigned r = lane >> 1, h = lane & 1u;
+            a.flag_bits[p.flag_word + (((i + r) * ny + seg * 64u) >> 5) + h] = 0u;
+        }
+    }
+}
+
+// Pruned windows (AdjFlagArgs.envelope): k3_bound streamed every row pair of
+// the quad layout once and wrote zero flag words where no cell of the warp's
+// 2 x 64 block can reach the tolerance; the remaining blocks, listed in
+// work[2 ..] as (patch, segment, row pair), are evaluated here by persistent
+// warps pulling from the list (the unpruned blocks cluster where the wave and
+// the adjoint overlap, so a static split would leave most warps idle).
+template <bool FASTW>
+__global__ void __launch_bounds__(32 * K3_ROW_WARPS, FASTW ? K3_QUAD_MINB_FAST : K3_QUAD_MINB)
+    k3_quad_list(AdjFlagArgs a) {
+    __shared__ const char* s_base[K3_MAXN];
+    __shared__ double2 s_q[K3_ROW_WARPS][RDEPTH][6][32];
+    __shared__ int s_item[K3_ROW_WARPS];
+    {
+        const int64_t snap_b = (int64_t)a.nxa * a.nya * 3 * 8;
+        for (int n = threadIdx.x; n < a.nidx; n += blockDim.x)
+            s_base[n] = reinterpret_cast<const char*>(a.ring) + (int64_t)a.snap_index[n] * snap_b;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int count = __ldcg(a.work);
+    for (;;) {
+        if (lane == 0) s_item[warp] = atomicAdd(a.work + 1, 1);
+        __syncwarp();
+        const int it = s_item[warp];
+        __syncwarp();
+        if (it >= count) break;
+        const int4 w = __ldcg(reinterpret_cast<const int4*>(a.work) + 1 + it);
+        quad_rows<FASTW>(a, s_base, s_q[warp], w.x, (unsigned)w.y, (unsigned)w.z, (unsigned)w.z + 2u, lane);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1294,8 +1438,34 @@ int flag_adjoint(const AdjFlagArgs& a) {
                 const int run = k3_quad_run(a);
                 const dim3 gr((unsigned)((a.max_rows + run - 1) / run),
                               (unsigned)((a.max_cols / 64 + K3_ROW_WARPS - 1) / K3_ROW_WARPS), (unsigned)a.npatch);
-                if (a.variant == ADJ_VARIANT_FAST) k3_quad<true><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a, run);
-                else k3_quad<false><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a, run);
+                if (a.envelope && a.work && !a.best && a.tolerance > 1e-280) {
+                    // pruned window: envelope, bound pass + work list, listed blocks only
+                    const int64_t nodes = (int64_t)a.nxa * a.nya;
+                    const int eb = (int)((nodes + 255) / 256 < 148 * 16 ? (nodes + 255) / 256 : 148 * 16);
+                    int rc = record_cuda(cudaMemsetAsync(a.work, 0, 2 * sizeof(int32_t), st), "memset work");
+                    if (rc) return rc;
+                    k3_envelope<<<eb, 256, 0, st>>>(a);
+                    k3_envelope2<<<eb, 256, 0, st>>>(a);
+                    constexpr int BRUN = 16;   // rows per bound warp (8 row pairs)
+                    const int64_t warps = (int64_t)(a.max_cols / 64) * ((a.max_rows + BRUN - 1) / BRUN);
+                    k3_bound<<<dim3((unsigned)((warps + 7) / 8), 1, (unsigned)a.npatch), 256, 0, st>>>(a, BRUN);
+                    static int list_ctas[2] = {0, 0};
+                    const bool fw = a.variant == ADJ_VARIANT_FAST;
+                    if (!list_ctas[fw]) {
+                        int per_sm = 0, dev = 0, sms = 0;
+                        if (fw) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_quad_list<true>, 32 * K3_ROW_WARPS, 0);
+                        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_quad_list<false>, 32 * K3_ROW_WARPS, 0);
+                        cudaGetDevice(&dev);
+                        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                        list_ctas[fw] = (per_sm < 1 ? 1 : per_sm) * sms;
+                    }
+                    if (fw) k3_quad_list<true><<<list_ctas[1], 32 * K3_ROW_WARPS, 0, st>>>(a);
+                    else k3_quad_list<false><<<list_ctas[0], 32 * K3_ROW_WARPS, 0, st>>>(a);
+                } else if (a.variant == ADJ_VARIANT_FAST) {
+                    k3_quad<true><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a, run);
+                } else {
+                    k3_quad<false><<<gr, 32 * K3_ROW_WARPS, 0, st>>>(a, run);
+                }
             } else if (k3_pairs() && a.nidx >= 2) {
                 const bool fw = a.variant == ADJ_VARIANT_FAST;
                 if (m1 && fw) k3_pair<true, true><<<grid, threads, 0, st>>>(a);

@@ -19,6 +19,8 @@ CFL violation (solver.py:461) free: the new buffer is simply discarded.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -150,8 +152,9 @@ class LevelStore:
         self._phys_args = {}
         self.nonfinite_acc = None
         # material planes of every patch assembled on the host, one upload
-        host_aux = np.zeros(self.naux * self.plane, dtype=np.float64)
+        host_aux = None
         if len({(b[1], b[2], b[3]) for b in self.boxes}) == 1:
+            host_aux = np.zeros(self.naux * self.plane, dtype=np.float64)
             # one box shape (e.g. uniform 32^2 patches): one scatter for all patches
             _, NX0, NY0, P0 = self.boxes[0]
             stacked = np.stack([np.stack([np.asarray(pl, dtype=float).reshape(NX0, NY0) for pl in p.aux.planes()])
@@ -159,14 +162,26 @@ class LevelStore:
             cell = (np.arange(NX0)[:, None] * P0 + np.arange(NY0)[None, :]).reshape(-1)
             dst = (np.arange(self.naux)[None, :, None] * self.plane + offs[:, None, None] + cell[None, None, :])
             host_aux[dst.reshape(-1)] = stacked.reshape(-1)
+        if host_aux is not None:
+            self.aux.copy_(torch.from_numpy(host_aux))
         else:
-            for k, p in enumerate(patches):
-                off_k, NX, NY, pitch = self.boxes[k]
-                v = np.lib.stride_tricks.as_strided(host_aux[off_k:], (self.naux, NX, NY),
-                                                    (8 * self.plane, 8 * pitch, 8), writeable=True)
-                for a, pl in enumerate(p.aux.planes()):
-                    v[a] = np.asarray(pl, dtype=float).reshape(NX, NY)
-        self.aux.copy_(torch.from_numpy(host_aux))
+            # mixed box shapes: the planes of all patches concatenated on the host (one upload),
+            # scattered into the boxes on the device (element e = ii * NY + jj of patch k goes to
+            # offs[k] + ii * pitch[k] + jj)
+            src = np.empty((self.naux, int((NXa * NYa).sum())), dtype=np.float64)
+            planes = [p.aux.planes() for p in patches]
+            for a in range(self.naux):
+                np.concatenate([np.asarray(pl[a], dtype=float).reshape(-1) for pl in planes], out=src[a])
+            dev = lambda v: torch.from_numpy(np.ascontiguousarray(v, dtype=np.int64)).to("cuda")
+            nx_d, ny_d, off_d, pit_d = dev(NXa), dev(NYa), dev(offs), dev(pitch_a)
+            nrow, ncell = int(NXa.sum()), src.shape[1]
+            rep = lambda v, r, n: torch.repeat_interleave(v, r, output_size=n)   # no size sync
+            ri = torch.arange(nrow, device="cuda") - rep(torch.cumsum(nx_d, 0) - nx_d, nx_d, nrow)
+            rbase = rep(off_d, nx_d, nrow) + ri * rep(pit_d, nx_d, nrow)
+            rlen = rep(ny_d, nx_d, nrow)
+            j = torch.arange(ncell, device="cuda") - rep(torch.cumsum(rlen, 0) - rlen, rlen, ncell)
+            dst = rep(rbase, rlen, ncell) + j
+            self.aux.view(self.naux, self.plane)[:, dst] = torch.from_numpy(src).to("cuda")
         for k, p in enumerate(patches):
             self._attach(p, k, upload=False)
 
@@ -1334,6 +1349,11 @@ def flag_axis_tables(store: LevelStore, ring_shape, a_origin, a_dx, a_dy, level_
 K3_ROW_CELLS = 128   # cells per warp of the K3 row-layout kernel (32 lanes x NC)
 
 
+# K3 window pruning by the window's |snapshot| envelope (AdjFlagArgs.envelope; flags-only calls
+# on multi-snapshot windows; flags and counts unchanged).  ADJAMR_FLAG_PRUNE=0 switches it off.
+USE_FLAG_PRUNING = os.environ.get("ADJAMR_FLAG_PRUNE", "1") != "0"
+
+
 def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level_origin, level_dx, level_dy,
                 snap_index, tolerance, adj_wet=None, interp_w=None, want_best=False, stream=None,
                 variant=None):
@@ -1409,6 +1429,19 @@ def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level
     a.a_dx, a.a_dy = a_dx, a_dy
     a.tolerance = tolerance
     a.variant = _lib.VARIANT_EXACT if variant is None else variant
+    if not want_best and USE_FLAG_PRUNING and len(snap_index) >= 2:
+        # window envelope scratch: cells whose bound cannot reach the tolerance skip the window
+        env = store.__dict__.get("_flag_envelope")
+        need = 6 * int(np.prod(ring_shape))       # stencil envelope, then node envelope
+        if env is None or env.numel() < need:
+            env = store._flag_envelope = torch.empty(need, dtype=torch.float64, device="cuda")
+        a.envelope = _ptr(env)
+        t = store.table_np
+        nblk = int(((t["nx"].astype(np.int64) // 2) * (t["ny"].astype(np.int64) // 64)).sum())
+        work = store.__dict__.get("_flag_work")
+        if work is None or work.numel() < 2 + 4 * nblk:
+            work = store._flag_work = torch.empty(2 + 4 * max(nblk, 1) + 2, dtype=torch.int32, device="cuda")
+        a.work = _ptr(work)
     a.stream = _lib.stream_ptr(stream)
     _lib.check(_lib.lib().adj_flag_adjoint(_lib.C.byref(a)), "adj_flag_adjoint")
     best_list = None

@@ -150,30 +150,55 @@ def _finish_material(patch, mat_cls, arrays, others, boundary, level_shape):
     patch.aux = mat_cls(**arrays, **others)
 
 
+def _centres_flat(specs):
+    """Ghost-inclusive cell centres of many patches of one level, flattened
+    patch after patch in meshgrid 'ij' order: the values cell_centers()
+    gives (origin + (index + 0.5) * width, the same operations), built
+    without a per-patch meshgrid.  Returns (coordinate arrays, shapes)."""
+    nd, g = specs[0].ndim, specs[0].ghost_width
+    lo = np.array([s.lo for s in specs], dtype=np.int64).reshape(len(specs), nd) - g
+    n = np.array([s.shape for s in specs], dtype=np.int64).reshape(len(specs), nd) + 2 * g
+    o, w = specs[0].origin, specs[0].widths
+    nx = n[:, 0]
+    ri = np.arange(int(nx.sum()), dtype=np.int64) - np.repeat(np.cumsum(nx) - nx, nx)   # row within patch
+    xrow = o[0] + ((np.repeat(lo[:, 0], nx) + ri) + 0.5) * w[0]
+    shapes = [tuple(r) for r in n.tolist()]
+    if nd == 1:
+        return (xrow,), shapes
+    rlen = np.repeat(n[:, 1], nx)                                                        # cells per row
+    j = np.arange(int(rlen.sum()), dtype=np.int64) - np.repeat(np.cumsum(rlen) - rlen, rlen)
+    y = o[1] + ((np.repeat(np.repeat(lo[:, 1], nx), rlen) + j) + 0.5) * w[1]
+    return (np.repeat(xrow, rlen), y), shapes
+
+
 def sample_patches_material(patches, equation: EquationSet, boundary: BoundarySpec, level_shape: tuple[int, ...]):
     """sample_patch_material for many new patches of one level.  The material
     model is called once on the concatenated (flattened) ghost-inclusive
     cell-centre coordinates of all patches; each patch's values are then
     those of its own call (verified exactly against a per-patch call on the
-    first patch; any difference or error falls back to one call per patch)."""
+    first patch; any difference or error falls back to one call per patch).
+    Each patch's material arrays are views into the one sampled array per
+    field (disjoint slices; the physical-boundary ghost fixes write only
+    their own patch's slice)."""
     P = len(patches)
     if P < 4 or any(p._store is not None for p in patches) or os.environ.get("ADJAMR_BATCH_MATERIAL") == "0":
         for p in patches:
             sample_patch_material(p, equation, boundary, level_shape)
         return
-    nd = patches[0].spec.ndim
-    cs = [p.spec.cell_centers(include_ghost=True) for p in patches]
-    shapes = [tuple(len(c) for c in cc) for cc in cs]
-    sizes = [int(np.prod(sh)) for sh in shapes]
+    specs = [p.spec for p in patches]
+    nd = specs[0].ndim
+    s0 = specs[0]
+    same_geom = all(s.origin == s0.origin and s.dx == s0.dx and s.dy == s0.dy and s.ghost_width == s0.ghost_width
+                    for s in specs)
     try:
-        if nd == 1:
-            mat = equation.sample_material(np.concatenate([c[0] for c in cs]))
-            mat0 = equation.sample_material(cs[0][0])
-        else:
-            grids = [np.meshgrid(c[0], c[1], indexing="ij") for c in cs]
-            mat = equation.sample_material(np.concatenate([g[0].ravel() for g in grids]),
-                                           np.concatenate([g[1].ravel() for g in grids]))
-            mat0 = equation.sample_material(grids[0][0], grids[0][1])
+        if not same_geom:
+            raise ValueError("patches of different geometry")
+        coords, shapes = _centres_flat(specs)
+        sizes = [int(np.prod(sh)) for sh in shapes]
+        mat = equation.sample_material(*coords)
+        cs0 = s0.cell_centers(include_ghost=True)
+        mat0 = (equation.sample_material(cs0[0]) if nd == 1 else
+                equation.sample_material(*np.meshgrid(cs0[0], cs0[1], indexing="ij")))
         names = _field_names(type(mat))
         arr_names = [n for n in names if isinstance(getattr(mat0, n), np.ndarray)]
         ok = type(mat0) is type(mat) and all(
@@ -187,11 +212,12 @@ def sample_patches_material(patches, equation: EquationSet, boundary: BoundarySp
             sample_patch_material(p, equation, boundary, level_shape)
         return
     others = {n: getattr(mat, n) for n in names if n not in arr_names}
-    fields = {n: getattr(mat, n) for n in arr_names}
-    off = np.concatenate([[0], np.cumsum(sizes)])
+    fields = {n: np.array(getattr(mat, n), copy=True) for n in arr_names}   # owned, writable
+    off = np.concatenate([[0], np.cumsum(sizes)]).tolist()
+    mat_cls = type(mat)
     for k, p in enumerate(patches):
-        _finish_material(p, type(mat), {n: np.array(f[off[k]:off[k + 1]].reshape(shapes[k]), copy=True)
-                                        for n, f in fields.items()}, others, boundary, level_shape)
+        _finish_material(p, mat_cls, {n: f[off[k]:off[k + 1]].reshape(shapes[k]) for n, f in fields.items()},
+                         others, boundary, level_shape)
 
 
 # ---------------------------------------------------------------------------

@@ -225,3 +225,56 @@ def test_direct_kernel_equal_grids(dry, case):
         assert np.array_equal(b, ref)
         assert np.array_equal(f, ref > tol)
         assert c == int(f.sum())
+
+
+@pytest.mark.parametrize("variant", ["exact", "fast"])
+@pytest.mark.parametrize("dry", [False, True])
+@pytest.mark.parametrize("scale", [1e-3, 1.0])
+def test_quad_window_pruning_keeps_flags(variant, dry, scale):
+    """Flags-only calls on multi-snapshot windows prune cells whose envelope
+    bound sum_c |q_c| max|qhat_c| cannot reach the tolerance
+    (AdjFlagArgs.envelope).  Forward state: a localized bump (most cells far
+    below the tolerance, some cells near it) -- flags and raw counts equal
+    the reference's windowed max > tol (EXACT: the reference arithmetic;
+    FAST: away from the tolerance) and the unpruned run's, bit for bit."""
+    from paper_1511_03645_b200 import _lib, adjoint, device
+    nxa, nya = 16, 128
+    shapes = [((0, 0), (20, 256)), ((20, 256), (18, 128)), ((40, 0), (8, 384))]
+    _, patches = _level(shapes, seed=8)
+    for p in patches:      # a bump centred in the level: far cells are tiny
+        cs = p.spec.cell_centers(include_ghost=True)
+        X, Y = np.meshgrid(cs[0], cs[1], indexing="ij")
+        env = scale * np.exp(-((X - 0.4) ** 2 + (Y - 0.5) ** 2) / 0.02)
+        p.state = p.state * env[None]
+    vals, wet, store = _store_n(9, nxa, nya, dry)
+    t, window = 0.3, adjoint.TimeWindow(0.0, 0.75)
+    var = _lib.VARIANT_EXACT if variant == "exact" else _lib.VARIANT_FAST
+    idx = adjoint.query_window_times(t, window, _FakeStore(window))
+    assert len(idx) >= 2
+    refs = []
+    for p in patches:
+        lo, shape, dx, dy = p.spec.lo, p.spec.shape, p.spec.dx, p.spec.dy
+        x = (np.arange(lo[0], lo[0] + shape[0]) + 0.5) * dx
+        y = (np.arange(lo[1], lo[1] + shape[1]) + 0.5) * dy
+        xc, yc = np.broadcast_to(x[:, None], shape), np.broadcast_to(y[None, :], shape)
+        refs.append(O.inner_product(p.state[:, 2:-2, 2:-2], xc, yc, vals, idx, (0.0, 0.0), 1.0 / nxa, 1.0 / nya,
+                                    p.aux.wet[2:-2, 2:-2], wet))
+    tol = float(np.quantile(np.concatenate([r.ravel() for r in refs]), 0.97))   # ~3% flagged
+    assert tol > 0
+    old = device.USE_FLAG_PRUNING
+    try:
+        device.USE_FLAG_PRUNING = True
+        fp, cp, _ = adjoint.flag_level(patches, t, store, window, tol, variant=var)
+        device.USE_FLAG_PRUNING = False
+        fu, cu, _ = adjoint.flag_level(patches, t, store, window, tol, variant=var)
+    finally:
+        device.USE_FLAG_PRUNING = old
+    assert cp == cu
+    for a, b, ref in zip(fp, fu, refs):
+        assert np.array_equal(a, b)
+        if variant == "exact":
+            assert np.array_equal(a, ref > tol)
+        else:
+            far = np.abs(ref - tol) > 1e-12 * tol
+            assert np.array_equal(a[far], (ref > tol)[far])
+    assert sum(cp) > 0
