@@ -239,6 +239,8 @@ typedef struct AdjStepArgs {
                                   into this step (FAST 2D, static_speed, forward wave form) */
     AdjJobFill job_fill;       /* optional (job_fill.n > 0): the level's ghost fill per warp job
                                   (FAST 2D, static_speed, job_offsets, ADJ_STEP_COUNTER_ZERO, no prefill) */
+    int32_t phys_bc[4];        /* ADJ_STEP_PHYS_IN: x-lo, x-hi, y-lo, y-hi ADJ_BC_* of the domain sides  */
+    int32_t phys_normal[2];    /* component negated at an x / a y wall                                     */
 } AdjStepArgs;
 /* AdjStepArgs.flags */
 #define ADJ_STEP_KEEP_NONFINITE 1   /* do not zero nonfinite: accumulate over launches */
@@ -247,6 +249,12 @@ typedef struct AdjStepArgs {
                                        two rows per lane; no job_offsets */
 #define ADJ_STEP_COUNTER_ZERO   8   /* FAST 2D: work_counter holds 2 ints that are zero on entry; the
                                        kernel leaves them zero (no memset node per launch) */
+#define ADJ_STEP_PHYS_IN       16   /* FAST 2D static CFL, one patch spanning the level: the launch
+                                       first performs fill_ghost_physical (solver.py:125-146) on q_in --
+                                       each warp job writes the physical ghost cells its strip reads,
+                                       sources from q_in's interior (side rules from phys_bc; corners x
+                                       then y; nx, ny >= 2) -- so no separate fill launch precedes the
+                                       step */
 int adj_step_level(const AdjStepArgs* a);
 
 /* Tile shape (ni, nj) the given variant expects in AdjStepArgs.tiles. */

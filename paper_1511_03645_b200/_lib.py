@@ -24,7 +24,7 @@ EDGE_XLO, EDGE_XHI, EDGE_YLO, EDGE_YHI = 1, 2, 4, 8
 BC_WALL, BC_OUTFLOW, BC_PERIODIC = 0, 1, 2
 BC_CODES = {"wall": BC_WALL, "outflow": BC_OUTFLOW, "periodic": BC_PERIODIC}
 RECT_COPY, RECT_COARSE = 0, 1
-STEP_KEEP_NONFINITE, STEP_NO_SPEED_OUT, STEP_TWO_ROWS, STEP_COUNTER_ZERO = 1, 2, 4, 8
+STEP_KEEP_NONFINITE, STEP_NO_SPEED_OUT, STEP_TWO_ROWS, STEP_COUNTER_ZERO, STEP_PHYS_IN = 1, 2, 4, 8, 16
 
 
 class NativeUnavailableError(RuntimeError):
@@ -89,7 +89,8 @@ class AdjStepArgs(C.Structure):
                 ("system", I32), ("form", I32), ("reversed", I32), ("limiter", I32),
                 ("variant", I32), ("flags", I32),
                 ("dt", D), ("dtdx", D), ("dtdy", D), ("gravity", D), ("stream", P), ("prefill", AdjGhostPlanFillArgs),
-                ("fine_restrict", AdjStepRestrict), ("job_fill", AdjJobFill)]
+                ("fine_restrict", AdjStepRestrict), ("job_fill", AdjJobFill),
+                ("phys_bc", I32 * 4), ("phys_normal", I32 * 2)]
 
 
 class AdjPhysArgs(C.Structure):

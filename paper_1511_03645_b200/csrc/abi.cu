@@ -93,6 +93,16 @@ int adj_step_level(const AdjStepArgs* a) {
         if (!(r.ratio == 2 || r.ratio == 4)) return adj::bad("fused restriction ratio must be 2 or 4");
         if (!(r.q_coarse && r.cell && r.base)) return adj::bad("null fused restriction tables");
     }
+    if (a->flags & ADJ_STEP_PHYS_IN) {
+        if (!(a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed && a->npatch == 1 && a->ghost == 2 &&
+              !(a->flags & ADJ_STEP_TWO_ROWS) && a->prefill.plan.n == 0 && a->job_fill.n == 0))
+            return adj::bad("ADJ_STEP_PHYS_IN needs the FAST 2D static-CFL step of one patch, ghost width 2");
+        for (int k = 0; k < 4; ++k)
+            if (a->phys_bc[k] < ADJ_BC_WALL || a->phys_bc[k] > ADJ_BC_PERIODIC) return adj::bad("phys_bc");
+        if ((a->phys_bc[0] == ADJ_BC_PERIODIC) != (a->phys_bc[1] == ADJ_BC_PERIODIC) ||
+            (a->phys_bc[2] == ADJ_BC_PERIODIC) != (a->phys_bc[3] == ADJ_BC_PERIODIC))
+            return adj::bad("periodic sides come in pairs");
+    }
     if (a->job_fill.n > 0) {
         const AdjJobFill& f = a->job_fill;
         if (!(a->variant == ADJ_VARIANT_FAST && a->ndim == 2 && a->static_speed && a->job_offsets &&

@@ -725,7 +725,82 @@ struct Strip {
     }
 };
 
-template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false>
+// ---- ADJ_STEP_PHYS_IN: fill_ghost_physical of q_in inside the step launch.
+// One patch spanning the level, ghost width 2.  A ghost-inclusive index ii
+// on an axis of n interior cells maps to its interior source and a wall sign
+// (solver.py:84-122; periodic wraps); a corner takes the x rule then the y
+// rule, as the x-slab-then-y-slab fill leaves it.
+ADJ_D int phys_src(int ii, int n, int bclo, int bchi, bool& neg) {
+    const int i = ii - 2;
+    if (i < 0) {
+        const int k = -i;
+        neg = bclo == ADJ_BC_WALL;
+        return bclo == ADJ_BC_OUTFLOW ? 0 : (bclo == ADJ_BC_WALL ? k - 1 : n - k);
+    }
+    if (i >= n) {
+        const int k = i - n + 1;
+        neg = bchi == ADJ_BC_WALL;
+        return bchi == ADJ_BC_OUTFLOW ? n - 1 : (bchi == ADJ_BC_WALL ? n - k : k - 1);
+    }
+    neg = false;
+    return i;
+}
+
+// The ghost cells of strip T's read window (ghost-inclusive rows T.j0 ..
+// T.j0 + nj + 3, columns T.i0 .. T.i0 + ni + 3), spread over the warp's lanes.
+// Sources are interior cells (not written by this launch); a ghost cell in two
+// windows gets the same value from both jobs.  Strips away from the domain
+// sides have no ghost cells in their window and return at once.
+ADJ_D void phys_prefill(const AdjStepArgs& a, const AdjTile& T, const AdjPatch& p, int lane) {
+    const int nx = p.nx, ny = p.ny;
+    const int r0 = T.j0, r1 = min(T.j0 + T.nj + 4, ny + 4);
+    const int c0 = T.i0, c1 = min(T.i0 + T.ni + 4, nx + 4);
+    const int glo = max(0, min(2, r1) - r0), ghi = max(0, r1 - max(r0, ny + 2));
+    const int clo = max(0, min(2, c1) - c0), chi = max(0, c1 - max(c0, nx + 2));
+    const int gr = glo + ghi, gc = clo + chi, Wc = c1 - c0, Wr = r1 - r0;
+    const int G = gr * Wc + gc * (Wr - gr);
+    if (G == 0) return;
+    double* q = const_cast<double*>(a.q_in) + p.offset;
+    const int64_t cs = a.comp_stride;
+    const int nnx = a.phys_normal[0], nny = a.phys_normal[1];
+    constexpr int U = 4;                           // cells per lane with their loads in flight together
+    for (int e0 = lane; e0 < G; e0 += 32 * U) {
+        int64_t dst[U];
+        unsigned neg[U];
+        double v[U][3];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + 32 * u;
+            int ii, jj;
+            if (e < gr * Wc) {                     // ghost rows (y sides), every window column
+                const int rr = e / Wc;
+                jj = rr < glo ? r0 + rr : max(r0, ny + 2) + (rr - glo);
+                ii = c0 + e % Wc;
+            } else {                               // ghost columns (x sides), the other rows
+                const int e2 = e - gr * Wc, k = e2 % max(gc, 1);
+                jj = max(r0, 2) + e2 / max(gc, 1);
+                ii = k < clo ? c0 + k : max(c0, nx + 2) + (k - clo);
+            }
+            bool xn, yn;
+            const int si = phys_src(ii, nx, a.phys_bc[0], a.phys_bc[1], xn);
+            const int sj = phys_src(jj, ny, a.phys_bc[2], a.phys_bc[3], yn);
+            const bool ok = e < G;
+            const int64_t src = ok ? (int64_t)(si + 2) * p.pitch + (sj + 2) : 0;
+            dst[u] = ok ? (int64_t)ii * p.pitch + jj : -1;
+            neg[u] = (xn ? 1u << nnx : 0u) ^ (yn ? 1u << nny : 0u);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[u][c] = __ldcg(q + c * cs + src);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (dst[u] < 0) continue;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) q[c * cs + dst[u]] = (neg[u] >> c) & 1u ? -v[u][c] : v[u][c];
+        }
+    }
+}
+
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false>
 #ifdef K1_MAXREG
 __global__ void __maxnreg__(K1_MAXREG) k1_fast(AdjStepArgs a) {
 #else
@@ -767,6 +842,15 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
         }
         if (!CFL && a.job_fill.n > 0) {   // this job's ghost cells, then every lane sees them
             job_fill(a.job_fill, const_cast<double*>(a.q_in), a.comp_stride, job, lane);
+            __syncwarp();
+        }
+        if (PFILL) {   // the physical ghosts of every strip of this job, then the march reads them
+            const int t0 = a.job_offsets ? a.job_offsets[job] : job, t1 = a.job_offsets ? a.job_offsets[job + 1] : job + 1;
+            for (int t = t0; t < t1; ++t) {
+                const AdjTile Tt = a.tiles[t];
+                phys_prefill(a, Tt, a.patches[Tt.patch], lane);
+            }
+            __threadfence_block();
             __syncwarp();
         }
         const AdjTile T = a.tiles[tix];
@@ -1058,14 +1142,14 @@ static void launch_two_rows(const AdjStepArgs& a, cudaStream_t st) {
     launch_pdl(k1_fast2<SYS, FORM, REV, LIM>, dim3(blocks), dim3(128), smem, st, a);
 }
 
-template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false>
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false>
 static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     static int blocks_per_sm = 0, sms = 0;
     constexpr int smem = K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL, RST>::NARR * 32 * (int)sizeof(double);
     if (blocks_per_sm == 0) {
-        cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL, RST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL, RST>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL>,
                                                       32 * K1_WARPS, smem);
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1075,7 +1159,7 @@ static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     int blocks = blocks_per_sm * sms;
     const int need = ((a.job_offsets ? a.njob : a.ntile) + K1_WARPS - 1) / K1_WARPS;
     if (blocks > need) blocks = need;
-    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL, RST>, dim3(blocks), dim3(32 * K1_WARPS), smem, st, a);
+    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL>, dim3(blocks), dim3(32 * K1_WARPS), smem, st, a);
 }
 
 template <int SYS, int FORM, bool REV, int LIM>
@@ -1085,6 +1169,10 @@ static void launch_kernel(const AdjStepArgs& a, cudaStream_t st) {
             launch_cfl<SYS, FORM, REV, LIM, false, true>(a, st);
             return;
         }
+    }
+    if ((a.flags & ADJ_STEP_PHYS_IN) && a.static_speed) {
+        launch_cfl<SYS, FORM, REV, LIM, false, false, true>(a, st);
+        return;
     }
     if ((a.flags & ADJ_STEP_TWO_ROWS) && a.static_speed && !a.job_offsets) launch_two_rows<SYS, FORM, REV, LIM>(a, st);
     else if (a.static_speed) launch_cfl<SYS, FORM, REV, LIM, false>(a, st);

@@ -472,6 +472,32 @@ class LevelStore:
                 self._tiles[variant] = (_dev_table(arr), len(rows), None, len(rows))
         return self._tiles[variant]
 
+    def tiles_edge_first(self, level_shape):
+        """The FAST job table with the jobs whose strips read physical ghost
+        cells first (ADJ_STEP_PHYS_IN: those jobs fill them before they march,
+        so they start early and the other warps' marches absorb the extra)."""
+        key = ("tiles_edge_first", tuple(level_shape))
+        hit = self._scratch.get(key)
+        if hit is not None:
+            return hit
+        tiles, ntile, jobs, njob = self.tiles(_lib.VARIANT_FAST)
+        rows = np.frombuffer(tiles.cpu().numpy().tobytes(), dtype=_lib.TILE_DTYPE)[:ntile].copy()
+        offs = jobs.cpu().numpy().astype(np.int64) if jobs is not None else np.arange(ntile + 1, dtype=np.int64)
+        nx = self.table_np["nx"][rows["patch"]]
+        ny = self.table_np["ny"][rows["patch"]]
+        edge = (rows["i0"] < 2) | (rows["i0"] + rows["ni"] + 2 > nx) | (rows["j0"] < 2) | (rows["j0"] + rows["nj"] + 2 > ny)
+        job_edge = np.array([bool(edge[offs[j]:offs[j + 1]].any()) for j in range(len(offs) - 1)])
+        order = np.concatenate([np.flatnonzero(job_edge), np.flatnonzero(~job_edge)])
+        new_rows, new_offs = [], [0]
+        for j in order:
+            new_rows.extend(rows[offs[j]:offs[j + 1]])
+            new_offs.append(len(new_rows))
+        arr = np.array(new_rows, dtype=_lib.TILE_DTYPE)
+        hit = (_dev_table(arr), len(arr), _torch().from_numpy(np.array(new_offs, dtype=np.int32)).to("cuda"),
+               len(new_offs) - 1)
+        self._scratch[key] = hit
+        return hit
+
     def scratch(self, name, n, dtype):
         torch = _torch()
         t = self._scratch.get(name)
@@ -1033,7 +1059,7 @@ def fill_physical(store: LevelStore, boundary, equation, level_shape, stream=Non
 
 
 def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index, stream=None,
-                accumulate=False, prefill=None, fine_restrict=None, job_fill=None):
+                accumulate=False, prefill=None, fine_restrict=None, job_fill=None, phys_in=None):
     """K1 on every patch: reads buf[cur], writes buf[out_buf_index].
     Returns (speed_max (npatch, 2) tensor, nonfinite (npatch,) tensor).
     ``accumulate`` (static-CFL fast path only): no per-launch memsets; the
@@ -1046,6 +1072,8 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
     if variant == _lib.VARIANT_FAST and store.any_dry():
         variant = _lib.VARIANT_EXACT   # the fast strip kernel has no wet/dry logic
     tiles, ntile, jobs, njob = store.tiles(variant)
+    if phys_in is not None:          # jobs that fill physical ghosts go first
+        tiles, ntile, jobs, njob = store.tiles_edge_first(phys_in[2])
     smax = store.scratch("smax", 2 * npatch, torch.float64)
     accumulate = accumulate and variant == _lib.VARIANT_FAST and store.ndim == 2
     if accumulate:
@@ -1094,6 +1122,13 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
         a.prefill = prefill
     if job_fill is not None:          # AdjJobFill: the level's ghost fill per warp job
         a.job_fill = job_fill
+    if phys_in is not None:           # (boundary, equation, level shape): fill_ghost_physical of q_in inside the launch
+        bd, eq = phys_in[0], phys_in[1]
+        a.flags |= _lib.STEP_PHYS_IN
+        for k, sd in enumerate((bd.left, bd.right, bd.bottom, bd.top)):
+            a.phys_bc[k] = _lib.BC_CODES[sd]
+        a.phys_normal[0] = eq.normal_component(0)
+        a.phys_normal[1] = eq.normal_component(1)
     if fine_restrict is not None:     # (FusedRestrict, coarse store): restriction fused into this step
         fr, cst = fine_restrict
         a.fine_restrict.q_coarse = _ptr(cst.buf[cst.cur])

@@ -459,6 +459,11 @@ def integrate_patch(patch: Patch, equation: EquationSet, boundary: BoundarySpec,
         flush()
 
 
+# advance_uniform: the physical ghost fill runs inside the step launch (ADJ_STEP_PHYS_IN) for a
+# patch spanning its level; ADJAMR_PHYS_IN=0 launches fill_ghost_physical separately
+USE_PHYS_IN = os.environ.get("ADJAMR_PHYS_IN", "1") != "0"
+
+
 def advance_uniform(patch: Patch, equation: EquationSet, boundary: BoundarySpec,
                     level_shape: tuple[int, ...], dt: float, nsteps: int, limiter: str = "MC",
                     variant: int | None = None, stream=None, graph: bool = True) -> float:
@@ -481,11 +486,22 @@ def advance_uniform(patch: Patch, equation: EquationSet, boundary: BoundarySpec,
         if cfl > 1.0 + 1e-12:
             raise CflViolationError(f"Courant number {cfl:.4f} > 1")
 
+        # a patch spanning its level has only physical ghosts: the step launch fills them itself
+        # (ADJ_STEP_PHYS_IN; each warp job the ones its strip reads), no fill launch in between
+        pin = (USE_PHYS_IN and len(st.patches) == 1 and st.g == 2 and spec.ndim == 2 and min(spec.shape) >= 2
+               and st.all_edges_physical(level_shape) and not st.two_rows())
+        if pin and "periodic" in (boundary.left, boundary.right, boundary.bottom, boundary.top):
+            device.check_periodic(st, boundary, level_shape)
+
         def one_step():
-            device.fill_physical(st, boundary, equation, level_shape, stream)
+            if pin:
+                st.prepare_write(full_ghosts=True, stream=stream)   # the launch writes every ghost cell
+            else:
+                device.fill_physical(st, boundary, equation, level_shape, stream)
             st.fold_ghosts(stream)
             out = st._free(*([st.cur] + ([st.old] if st.old is not None else [])))
-            device.launch_step(st, dt, equation, limiter, variant, out, stream, accumulate=True)
+            device.launch_step(st, dt, equation, limiter, variant, out, stream, accumulate=True,
+                               phys_in=(boundary, equation, tuple(level_shape)) if pin else None)
             st.ghost_src = st.cur
             st.cur = out
 
