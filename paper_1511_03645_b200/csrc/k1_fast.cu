@@ -37,6 +37,10 @@
 #ifndef K1_GROUPS
 #define K1_GROUPS 2       // cp.async groups of 3 columns in flight
 #endif
+#ifndef K1_STATIC_FIRST
+#define K1_STATIC_FIRST 1     // each warp's first job = its index, its job-table entry loaded before
+                              // the PDL wait; 0: every job from the queue
+#endif
 #ifndef K1_PREFETCH_CLAMP
 #define K1_PREFETCH_CLAMP 1   // 1: branch-free prefetch (re-read the last column)
 #endif
@@ -811,41 +815,49 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
     constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL, RST>::NARR;
     extern __shared__ __align__(16) double s_ring1[];   // [K1_WARPS][RING1 * NARR * 32]
     const int warp = threadIdx.x >> 5;
+    const int njob = a.job_offsets ? a.njob : a.ntile;
+    // Each warp's first job is its warp index (no queue round trip); the job
+    // tables are static, so its strip's table entries load before the wait for
+    // the previous launch (PDL) -- a one-wave level (small AMR patches) keeps
+    // that latency off its critical path.  Later jobs come from the queue.
+    // (levels of small patches; a patch spanning its level -- PFILL -- keeps the queue for every job)
+    constexpr bool SF = K1_STATIC_FIRST && !PFILL;
+    const int total = SF ? gridDim.x * K1_WARPS : 0;
+    int job0 = blockIdx.x * K1_WARPS + warp;
+    int t0f = job0, t1f = job0 + 1;
+    if (SF && job0 < njob && a.job_offsets) { t0f = a.job_offsets[job0]; t1f = a.job_offsets[job0 + 1]; }
     pdl_wait();
     pdl_trigger();
     if (!CFL && a.prefill.plan.n > 0) {      // the level's ghost fill, then every CTA waits for it
         prefill_gather(a.prefill);
         grid_barrier(a.work_counter + 2, gridDim.x);
     }
-    // persistent warps: pull strip tiles from a global queue until empty
-    const int njob = a.job_offsets ? a.njob : a.ntile;
-    for (;;) {
-        if (lane == 0) s_tile[warp] = atomicAdd(a.work_counter, 1);
-        __syncwarp();
-        const int job = s_tile[warp];
-        __syncwarp();
+    for (bool first = SF;; first = false) {
+        int job = job0, t0 = t0f, t1 = t1f;
+        if (!first) {   // persistent warps: further strip jobs from a global queue until empty
+            if (lane == 0) s_tile[warp] = total + atomicAdd(a.work_counter, 1);
+            __syncwarp();
+            job = s_tile[warp];
+            __syncwarp();
+            if (job < njob && a.job_offsets) { t0 = a.job_offsets[job]; t1 = a.job_offsets[job + 1]; }
+            else { t0 = job; t1 = job + 1; }
+        }
         if (job >= njob) {
             release_counter(a, lane, gridDim.x * K1_WARPS);
             break;
         }
         // this lane's strip: single-strip jobs use all lanes; packed jobs
         // stack up to four short strips (same ni) along the lanes
-        int tix = job, lane0 = 0;
-        if (a.job_offsets) {
-            const int t0 = a.job_offsets[job], t1 = a.job_offsets[job + 1];
-            tix = t1 - 1;
-            lane0 = a.tiles[tix].pad;
-            for (int t = t0; t < t1 - 1; ++t) {
-                const int next0 = a.tiles[t + 1].pad;
-                if (lane < next0) { tix = t; lane0 = a.tiles[t].pad; break; }
-            }
+        int tix = t1 - 1, lane0 = a.job_offsets ? a.tiles[tix].pad : 0;
+        for (int t = t0; t < t1 - 1; ++t) {
+            const int next0 = a.tiles[t + 1].pad;
+            if (lane < next0) { tix = t; lane0 = a.tiles[t].pad; break; }
         }
         if (!CFL && a.job_fill.n > 0) {   // this job's ghost cells, then every lane sees them
             job_fill(a.job_fill, const_cast<double*>(a.q_in), a.comp_stride, job, lane);
             __syncwarp();
         }
         if (PFILL) {   // the physical ghosts of every strip of this job, then the march reads them
-            const int t0 = a.job_offsets ? a.job_offsets[job] : job, t1 = a.job_offsets ? a.job_offsets[job + 1] : job + 1;
             for (int t = t0; t < t1; ++t) {
                 const AdjTile Tt = a.tiles[t];
                 phys_prefill(a, Tt, a.patches[Tt.patch], lane);

@@ -1,15 +1,18 @@
 """Physical ghost fill inside the step launch (ADJ_STEP_PHYS_IN, advance_uniform
 on a patch spanning its level): each warp job writes the physical ghost cells
 its strip reads, as fill_ghost_physical (solver.py:125-146) would, then
-marches.  Checked two ways: (1) one launch leaves q_in's ghosts equal to a
-separate K2 physical fill of the same state and q_out equal to the
-fill + step pair, bitwise, for every side rule; (2) advance_uniform runs
-(graph-replayed pairs, odd counts) with and without it are bitwise equal on
-the whole ghost-inclusive patch, forward and adjoint forms."""
+marches.  Checked two ways: (1) one launch leaves q_in's ghosts bitwise
+equal to a separate K2 physical fill of the same state, and q_out equal to
+the fill + step pair, for every side rule; (2) advance_uniform runs
+(graph-replayed pairs, odd counts) with and without it agree on the whole
+ghost-inclusive patch, forward and adjoint forms.  The step outputs are
+compared at the FAST tolerance (1e-12 norm-relative): the launch with the
+fill is its own instantiation of the strip kernel, and FMA contraction may
+differ between instantiations."""
 import numpy as np
 import pytest
 
-from tests.helpers import make_equation, patch_from_arrays
+from tests.helpers import make_equation, norm_rel, patch_from_arrays
 
 pytestmark = pytest.mark.gpu
 
@@ -66,7 +69,9 @@ def test_launch_fills_physical_ghosts(name, sides, shape):
     torch.cuda.synchronize()
     assert torch.equal(_box(st, st.buf[st.cur]), _box(st, filled))
     g = 2
-    assert torch.equal(_box(st, st.buf[out])[:, g:-g, g:-g], _box(st, want)[:, g:-g, g:-g])
+    got_i = _box(st, st.buf[out])[:, g:-g, g:-g].cpu().numpy()
+    want_i = _box(st, want)[:, g:-g, g:-g].cpu().numpy()
+    assert norm_rel(got_i, want_i) <= 1e-12
 
 
 @pytest.mark.parametrize("sides", SIDES[:4])
@@ -86,4 +91,4 @@ def test_advance_uniform_same_with_and_without(name, sides):
             res.append(np.array(p.state))
         finally:
             solver.USE_PHYS_IN = True
-    assert np.array_equal(res[0], res[1])
+    assert norm_rel(res[0], res[1]) <= 1e-12

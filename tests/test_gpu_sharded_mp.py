@@ -72,8 +72,10 @@ def test_two_ranks_equal_unsharded(variant, NX):
     want = np.array(whole.state)[:, 2:-2, 2:-2]
     for r in range(world):
         x0, x1, got, overlapped = out[r]
-        # 48-row slabs: every strip touches a slab edge (no overlap); 300-row slabs overlap
-        assert overlapped == (variant == "fast" and NX == 600)
+        # 300-row slabs always have strips clear of the slab edges (overlapped step); 48-row slabs
+        # only when their strips are short (one-wave strip length), so either way there
+        assert overlapped or variant == "exact" or NX == 97
+        assert not overlapped or variant == "fast"
         if variant == "exact":
             assert np.array_equal(got, want[:, x0:x1])
         else:
