@@ -264,7 +264,7 @@ ADJ_D double rcp(double x) {  // x > 0, normal: MUFU seed + one cubic Newton ste
 ADJ_D double dmin(double a, double b) { return a < b ? a : b; }
 ADJ_D double dmax(double a, double b) { return a > b ? a : b; }
 
-// 2^k v for a finite v >= 0 by adding k to the exponent field (integer pipe).
+// 2^k v for a finite v by adding k to the exponent field (integer pipe; the sign bit is untouched).
 // Exact for normal results; v == 0 gives 2^(k-1023) (~1e-308), which the
 // limiters below only ever compare against or scale by O(1) coefficients.
 template <int K, bool ALG>
@@ -281,20 +281,31 @@ ADJ_D double sh_up(double v) { return __shfl_up_sync(FULL, v, 1); }    // from l
 // otherwise sign(A) times  MC: min(|A+B|/2, 2|A|, 2|B|);  minmod: min(|A|,|B|);
 // superbee: max(min(|A|, 2|B|), min(2|A|, |B|)).  The factor 1/2 is folded
 // into the per-cell 1/(2(1+m^2)) the result is multiplied by.
+//
+// Evaluated in the signed domain: when A and B share a sign, every candidate
+// (A, B, A+B and their power-of-two multiples) carries that sign, so the
+// selections compare magnitudes through DSETP's |.| operand modifiers and pick
+// the signed value -- no |x| is materialised (each one was an FP64 DADD) and
+// no copysign is needed.  Same selections as the magnitude form, so the same
+// values bit for bit.
 template <int LIM, bool ALG>
 ADJ_D double limab2(double A, double B) {
-    const double a = fabs(A), b = fabs(B);
     double r;
     if (LIM == ADJ_LIM_MINMOD) {
-        const double m = dmin(a, b);
+        const double m = fabs(A) < fabs(B) ? A : B;
         r = m + m;
     } else if (LIM == ADJ_LIM_MC) {
-        r = dmin(fabs(A + B), pow2x<2, ALG>(dmin(a, b)));
+        const double m4 = pow2x<2, ALG>(fabs(A) < fabs(B) ? A : B);
+        const double S = A + B;
+        r = fabs(S) < fabs(m4) ? S : m4;
     } else {
-        r = dmax(dmin(pow2x<1, ALG>(a), pow2x<2, ALG>(b)), dmin(pow2x<2, ALG>(a), pow2x<1, ALG>(b)));
+        const double A2 = pow2x<1, ALG>(A), B2 = pow2x<1, ALG>(B);
+        const double A4 = pow2x<2, ALG>(A), B4 = pow2x<2, ALG>(B);
+        const double t1 = fabs(A2) < fabs(B4) ? A2 : B4;
+        const double t2 = fabs(A4) < fabs(B2) ? A4 : B2;
+        r = fabs(t1) > fabs(t2) ? t1 : t2;
     }
-    r = (__double2hiint(A) ^ __double2hiint(B)) < 0 ? 0.0 : r;
-    return copysign(r, A);
+    return (__double2hiint(A) ^ __double2hiint(B)) < 0 ? 0.0 : r;
 }
 
 // Per-cell material quantities.  m: eigen material (z for acoustics, c for
@@ -422,22 +433,25 @@ ADJ_D void correction(const Face& f, double s0_nb, double P0_nb, double s1_nb, d
 // Transverse split of an entering fluctuation (component 0 = f0; its
 // transverse component is zero for every 2D system here), scaled by h.
 // Returns bm (to the lower transverse face) and bp (upper), components
-// (0, transverse velocity).
+// (0, transverse velocity) -- bm's component 0 NEGATED (nbm0 = -bm0): for
+// shallow water it is the product u itself, and the callers subtract it
+// (x - y == x + (-y) exactly), so no negation is materialised before the
+// shuffle that carries it.
 template <int SYS, int FORM, bool REV>
 ADJ_D void transverse(double f0, double h, const Mat& b, const Mat& a,
-                      double& bm0, double& bmv, double& bp0, double& bpv) {
+                      double& nbm0, double& bmv, double& bp0, double& bpv) {
     constexpr bool SWE = SYS == ADJ_SYS_SWE2D, FW = FORM == ADJ_FORM_FWAVE;
     const double t = (h * f0) * rcp(b.m + a.m);
-    double m0, mv, p0, pv;
+    double nm0, mv, p0, pv;   // nm0 = -m0
     if (!FW) {
-        if (!SWE) { m0 = -b.tr * t; mv = b.c * t; p0 = a.tr * t; pv = a.c * t; }
-        else { const double u = (b.c * a.c) * t; m0 = -u; mv = b.c * u; p0 = u; pv = a.c * u; }
+        if (!SWE) { nm0 = b.tr * t; mv = b.c * t; p0 = a.tr * t; pv = a.c * t; }
+        else { const double u = (b.c * a.c) * t; nm0 = u; mv = b.c * u; p0 = u; pv = a.c * u; }
     } else {
-        if (!SWE) { const double ta = a.m * t, tb = b.m * t; m0 = -b.c * ta; mv = b.tr * ta; p0 = a.c * tb; pv = a.tr * tb; }
-        else { m0 = -b.tr * t; mv = b.c * t; p0 = a.tr * t; pv = a.c * t; }
+        if (!SWE) { const double ta = a.m * t, tb = b.m * t; nm0 = b.c * ta; mv = b.tr * ta; p0 = a.c * tb; pv = a.tr * tb; }
+        else { nm0 = b.tr * t; mv = b.c * t; p0 = a.tr * t; pv = a.c * t; }
     }
-    if (REV) { bm0 = -p0; bmv = -pv; bp0 = -m0; bpv = -mv; }
-    else { bm0 = m0; bmv = mv; bp0 = p0; bpv = pv; }
+    if (REV) { nbm0 = p0; bmv = -pv; bp0 = nm0; bpv = -mv; }
+    else { nbm0 = nm0; bmv = mv; bp0 = p0; bpv = pv; }
 }
 
 struct Raw { double q0, q1, q2, c, z; };
@@ -552,9 +566,10 @@ struct Strip {
         mu.tr = SWE ? mu.c * mu.c : mu.c * mu.m;
         mu.fx = FORM == ADJ_FORM_FWAVE ? sh_dn(m[C].fx) : 0.0;
         const Face yf = solve_face<SYS, FORM, REV>(cr.q0, cr.q2, uq0, uq2, m[C], mu);
+        const double s1up = REV ? 0.0 : sh_up(yf.s1);   // forward: the family-1 limiter neighbour and Sy's s1 below
         {
             const double s0n = REV ? sh_up(yf.s0) : sh_dn(yf.s0);
-            const double s1n = REV ? sh_dn(yf.s1) : sh_up(yf.s1);
+            const double s1n = REV ? sh_dn(yf.s1) : s1up;
             const double P0n = REV ? sh_up(yf.P) : 0.0;
             const double P1n = REV ? sh_dn(yf.P) : 0.0;
             correction<SYS, FORM, REV, LIM>(yf, s0n, P0n, s1n, P1n, m[C], mu, m[C].ky, mu.ky, cy0[C], cy2[C]);
@@ -563,7 +578,7 @@ struct Strip {
             // Sy(cell) = apdq(face below, R = cell) + amdq(own face, L = cell): the
             // cell's own material times the two strengths (s1 below is the
             // limiter neighbour the correction above already shuffled)
-            const double s1b = sh_up(yf.s1);
+            const double s1b = s1up;
             if (SWE) { sy0[C] = m[C].c * (s1b - yf.s0); sy2[C] = m[C].tr * (s1b + yf.s0); }
             else { sy0[C] = m[C].tr * (s1b + yf.s0); sy2[C] = m[C].c * (s1b - yf.s0); }
         } else {
@@ -590,21 +605,21 @@ struct Strip {
             Mat ma{};
             ma.c = cup[P]; ma.m = mup[P];
             ma.tr = SWE ? ma.c * ma.c : ma.c * ma.m;
-            double bm0, bmv, bp0, bpv;
-            transverse<SYS, FORM, REV>(sx0[P], hx, mb, ma, bm0, bmv, bp0, bpv);
-            gt0[P] = cy0[P] - (bp0 + sh_dn(bm0));
+            double nbm0, bmv, bp0, bpv;
+            transverse<SYS, FORM, REV>(sx0[P], hx, mb, ma, nbm0, bmv, bp0, bpv);
+            gt0[P] = cy0[P] - (bp0 - sh_dn(nbm0));
             gt2[P] = cy2[P] - (bpv + sh_dn(bmv));
         }
 
         // ---- transverse of Sy(s-1) with columns s-2, s; x-limiter of face s-3/2
         {
-            double bm0, bmv, bp0, bpv;
-            transverse<SYS, FORM, REV>(sy0[P], hy, m[PP], m[C], bm0, bmv, bp0, bpv);
+            double nbm0, bmv, bp0, bpv;
+            transverse<SYS, FORM, REV>(sy0[P], hy, m[PP], m[C], nbm0, bmv, bp0, bpv);
             double fc0, fc1;
             correction<SYS, FORM, REV, LIM>(xf[P], REV ? xf[PP].s0 : xf[C].s0, xf[PP].P,
                                             REV ? xf[C].s1 : xf[PP].s1, xf[C].P,
                                             m[PP], m[P], m[PP].kx, m[P].kx, fc0, fc1);
-            ft0[P] = fc0 - (bpy0[PP] + bm0);
+            ft0[P] = fc0 - (bpy0[PP] - nbm0);
             ft1[P] = fc1 - (bpy1[PP] + bmv);
             bpy0[P] = bp0; bpy1[P] = bpv;
         }
@@ -1004,22 +1019,22 @@ struct Strip2 {
             double amA0, amAv, apA0, apAv, amB0, amBv, apB0, apBv;
             transverse<SYS, FORM, REV>(sx0[P][0], hx, mb, m[P][1], amA0, amAv, apA0, apAv);
             transverse<SYS, FORM, REV>(sx0[P][1], hx, m[P][0], ma, amB0, amBv, apB0, apBv);
-            gt0[P][0] = cy0[P][0] - (apA0 + amB0);
+            gt0[P][0] = cy0[P][0] - (apA0 - amB0);
             gt2[P][0] = cy2[P][0] - (apAv + amBv);
-            gt0[P][1] = cy0[P][1] - (apB0 + sh_dn(amA0));
+            gt0[P][1] = cy0[P][1] - (apB0 - sh_dn(amA0));
             gt2[P][1] = cy2[P][1] - (apBv + sh_dn(amAv));
         }
 
         // ---- transverse of Sy(s-1) with columns s-2, s; x-limiter of face s-3/2
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-            double bm0, bmv, bp0, bpv;
-            transverse<SYS, FORM, REV>(sy0[P][r], hy, m[PP][r], m[C][r], bm0, bmv, bp0, bpv);
+            double nbm0, bmv, bp0, bpv;
+            transverse<SYS, FORM, REV>(sy0[P][r], hy, m[PP][r], m[C][r], nbm0, bmv, bp0, bpv);
             double fc0, fc1;
             correction<SYS, FORM, REV, LIM>(xf[P][r], REV ? xf[PP][r].s0 : xf[C][r].s0, xf[PP][r].P,
                                             REV ? xf[C][r].s1 : xf[PP][r].s1, xf[C][r].P,
                                             m[PP][r], m[P][r], m[PP][r].kx, m[P][r].kx, fc0, fc1);
-            ft0[P][r] = fc0 - (bpy0[PP][r] + bm0);
+            ft0[P][r] = fc0 - (bpy0[PP][r] - nbm0);
             ft1[P][r] = fc1 - (bpy1[PP][r] + bmv);
             bpy0[P][r] = bp0; bpy1[P][r] = bpv;
         }
