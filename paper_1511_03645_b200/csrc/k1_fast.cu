@@ -254,11 +254,18 @@ ADJ_D void grid_barrier(int* counter, int nblocks) {
     __syncthreads();
 }
 
+#ifndef K1_RCP_CUBIC
+#define K1_RCP_CUBIC 1   // 0: one quadratic Newton step (relative error ~e^2)
+#endif
 ADJ_D double rcp(double x) {  // x > 0, normal: MUFU seed + one cubic Newton step
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     const double e = fma(-x, r, 1.0);
+#if K1_RCP_CUBIC
     return fma(r, fma(e, e, e), r);   // r (1 + e + e^2): relative error ~e^3
+#else
+    return fma(r, e, r);
+#endif
 }
 
 ADJ_D double dmin(double a, double b) { return a < b ? a : b; }
@@ -317,8 +324,8 @@ struct Mat {
     double c, m, k1, k1i, kx, ky, tr, fx;   // k1 = 1+m^2, k1i = 1/(2 k1); kx, ky include k1i when limited
 };
 
-template <int SYS, int FORM, int LIM>
-ADJ_D Mat make_mat(double c, double z, double dtdx, double dtdy) {
+template <int SYS, int FORM, int LIM, bool SQ = false>
+ADJ_D Mat make_mat(double c, double z, double dtdx, double dtdy) {   // SQ: dtdx == dtdy, so ky == kx
     constexpr bool SWE = SYS == ADJ_SYS_SWE2D, FW = FORM == ADJ_FORM_FWAVE;
     Mat t;
     t.c = c;
@@ -332,19 +339,19 @@ ADJ_D Mat make_mat(double c, double z, double dtdx, double dtdy) {
         const double ck = FW ? r : c * r;
         t.k1i = 0.5 * r;
         t.kx = ck * fma(-0.25 * dtdx, c, 0.25);
-        t.ky = ck * fma(-0.25 * dtdy, c, 0.25);
+        t.ky = SQ ? t.kx : ck * fma(-0.25 * dtdy, c, 0.25);
     } else {
         t.kx = FW ? fma(-0.5 * dtdx, c, 0.5) : c * fma(-0.5 * dtdx, c, 0.5);
-        t.ky = FW ? fma(-0.5 * dtdy, c, 0.5) : c * fma(-0.5 * dtdy, c, 0.5);
+        t.ky = SQ ? t.kx : (FW ? fma(-0.5 * dtdy, c, 0.5) : c * fma(-0.5 * dtdy, c, 0.5));
     }
     } else {
-    const double hx = 0.5 * fma(-dtdx, c, 1.0), hy = 0.5 * fma(-dtdy, c, 1.0);
+    const double hx = 0.5 * fma(-dtdx, c, 1.0), hy = SQ ? hx : 0.5 * fma(-dtdy, c, 1.0);
     t.kx = FW ? hx : c * hx;
-    t.ky = FW ? hy : c * hy;
+    t.ky = SQ ? t.kx : (FW ? hy : c * hy);
     if (LIM != ADJ_LIM_NONE) {   // the limited strength is only ever used scaled by k / (2 (1 + m^2))
         t.k1i = rcp(t.k1 + t.k1);
         t.kx *= t.k1i;
-        t.ky *= t.k1i;
+        t.ky = SQ ? t.kx : t.ky * t.k1i;
     }
     }
     t.tr = SWE ? c * c : c * z;
@@ -470,7 +477,7 @@ constexpr int RING1 = 3 * NGRP;
 // lives in a 3-slot ring indexed by (column mod 3); column<K> is the body of
 // the march for a column in slot K, so the 3-way unrolled loop rotates roles
 // by renaming instead of moving registers.
-template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false>
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool SQ = false>
 struct Strip {
     static constexpr bool SWE = SYS == ADJ_SYS_SWE2D;
     static constexpr bool FWD_WAVE = FORM == ADJ_FORM_WAVE && !REV;
@@ -540,7 +547,7 @@ struct Strip {
     template <int K>
     ADJ_D void column(int s, const Raw& cr, const double* up, const double* dn) {
         constexpr int C = K, P = (K + 2) % 3, PP = (K + 1) % 3;
-        m[C] = make_mat<SYS, FORM, LIM>(cr.c, cr.z, dtdx, dtdy);
+        m[C] = make_mat<SYS, FORM, LIM, SQ>(cr.c, cr.z, dtdx, dtdy);
         // CFL: max |speed| of the faces is the max material speed of the cells
         // they touch (fast path = no dry cells): x-faces of this strip touch
         // columns [i0-1, i0+ni] of the output rows, y-faces rows j0-1..j0+nj
@@ -819,7 +826,7 @@ ADJ_D void phys_prefill(const AdjStepArgs& a, const AdjTile& T, const AdjPatch& 
     }
 }
 
-template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false>
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false, bool SQ = false>
 #ifdef K1_MAXREG
 __global__ void __maxnreg__(K1_MAXREG) k1_fast(AdjStepArgs a) {
 #else
@@ -827,7 +834,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
 #endif
     const int lane = threadIdx.x & 31;
     __shared__ int s_tile[K1_WARPS];
-    constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL, RST>::NARR;
+    constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL, RST, SQ>::NARR;
     extern __shared__ __align__(16) double s_ring1[];   // [K1_WARPS][RING1 * NARR * 32]
     const int warp = threadIdx.x >> 5;
     const int njob = a.job_offsets ? a.njob : a.ntile;
@@ -882,7 +889,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
         }
         const AdjTile T = a.tiles[tix];
         const AdjPatch p = a.patches[T.patch];
-        Strip<SYS, FORM, REV, LIM, CFL, RST> S;
+        Strip<SYS, FORM, REV, LIM, CFL, RST, SQ> S;
         S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
         S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32);
         S.run();
@@ -1169,14 +1176,14 @@ static void launch_two_rows(const AdjStepArgs& a, cudaStream_t st) {
     launch_pdl(k1_fast2<SYS, FORM, REV, LIM>, dim3(blocks), dim3(128), smem, st, a);
 }
 
-template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false>
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false, bool SQ = false>
 static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     static int blocks_per_sm = 0, sms = 0;
-    constexpr int smem = K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL, RST>::NARR * 32 * (int)sizeof(double);
+    constexpr int smem = K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL, RST, SQ>::NARR * 32 * (int)sizeof(double);
     if (blocks_per_sm == 0) {
-        cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ>,
                                                       32 * K1_WARPS, smem);
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1186,24 +1193,40 @@ static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     int blocks = blocks_per_sm * sms;
     const int need = ((a.job_offsets ? a.njob : a.ntile) + K1_WARPS - 1) / K1_WARPS;
     if (blocks > need) blocks = need;
-    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL>, dim3(blocks), dim3(32 * K1_WARPS), smem, st, a);
+    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ>, dim3(blocks), dim3(32 * K1_WARPS), smem, st, a);
+}
+
+// Square cells (dt/dx == dt/dy, every BASELINE configuration) share the x and
+// y correction magnitudes: a separate instantiation (SQ) of the static-CFL
+// kernels for the MC limiter drops their recomputation.
+template <int SYS, int FORM, bool REV, int LIM, bool SQ>
+static void launch_static(const AdjStepArgs& a, cudaStream_t st) {
+    if constexpr (FORM == ADJ_FORM_WAVE && !REV) {   // forward levels: optional fused restriction
+        if (a.fine_restrict.ratio > 0) {
+            launch_cfl<SYS, FORM, REV, LIM, false, true, false, SQ>(a, st);
+            return;
+        }
+    }
+    if (a.flags & ADJ_STEP_PHYS_IN) launch_cfl<SYS, FORM, REV, LIM, false, false, true, SQ>(a, st);
+    else launch_cfl<SYS, FORM, REV, LIM, false, false, false, SQ>(a, st);
 }
 
 template <int SYS, int FORM, bool REV, int LIM>
 static void launch_kernel(const AdjStepArgs& a, cudaStream_t st) {
-    if constexpr (FORM == ADJ_FORM_WAVE && !REV) {   // forward levels: optional fused restriction
-        if (a.fine_restrict.ratio > 0 && a.static_speed) {
-            launch_cfl<SYS, FORM, REV, LIM, false, true>(a, st);
-            return;
+    if ((a.flags & ADJ_STEP_TWO_ROWS) && a.static_speed && !a.job_offsets && !(a.flags & ADJ_STEP_PHYS_IN) &&
+        !(FORM == ADJ_FORM_WAVE && !REV && a.fine_restrict.ratio > 0)) {
+        launch_two_rows<SYS, FORM, REV, LIM>(a, st);
+    } else if (a.static_speed) {
+        if constexpr (LIM == ADJ_LIM_MC) {
+            if (a.dtdx == a.dtdy) {
+                launch_static<SYS, FORM, REV, LIM, true>(a, st);
+                return;
+            }
         }
+        launch_static<SYS, FORM, REV, LIM, false>(a, st);
+    } else if (!a.job_offsets) {
+        launch_cfl<SYS, FORM, REV, LIM, true>(a, st);
     }
-    if ((a.flags & ADJ_STEP_PHYS_IN) && a.static_speed) {
-        launch_cfl<SYS, FORM, REV, LIM, false, false, true>(a, st);
-        return;
-    }
-    if ((a.flags & ADJ_STEP_TWO_ROWS) && a.static_speed && !a.job_offsets) launch_two_rows<SYS, FORM, REV, LIM>(a, st);
-    else if (a.static_speed) launch_cfl<SYS, FORM, REV, LIM, false>(a, st);
-    else if (!a.job_offsets) launch_cfl<SYS, FORM, REV, LIM, true>(a, st);
 }
 
 template <int SYS, int FORM, bool REV>

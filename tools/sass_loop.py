@@ -25,5 +25,6 @@ base = collections.Counter()
 for k, v in ops.items():
     base[k.split(".")[0] if not k.startswith("IMAD.MOV") else "IMAD.MOV"] += v
 fp64 = sum(base[k] for k in ("DADD", "DMUL", "DFMA", "DSETP"))
-print(f"loop {hex(lo)}-{hex(hi)}: {len(loop) / 3:.1f} instr/column, FP64 {fp64 / 3:.1f}/column")
+loc = sum(v for k, v in ops.items() if k.startswith(("LDL", "STL")))
+print(f"loop {hex(lo)}-{hex(hi)}: {len(loop) / 3:.1f} instr/column, FP64 {fp64 / 3:.1f}/column, local ld/st {loc}")
 print(", ".join(f"{k} {v / 3:.1f}" for k, v in base.most_common(16)))
