@@ -110,9 +110,11 @@ def build_c4(n=N, rank=0, world=1):
     return h, p, eq, bc, dt
 
 
+C5_COARSE_STEPS = 50   # BASELINE C5: "across 50 coarse steps"
 C5_STEPS_NOTE = ("C5: 3-level acoustics hierarchy (K=4, rho=1), base 1024^2 in 1024 patches of 32^2, "
                  "ratios 2, 4; 32^2 fine patches from seed 3 covering ~40% / nested; 1 step = one coarse "
-                 "step of advance_hierarchy (ghost fill + step + restriction on 11 level-steps)")
+                 "step of advance_hierarchy (ghost fill + step + restriction on 11 level-steps); 50 coarse "
+                 "steps timed (CUDA-graph pairs, host bookkeeping by the verified lite shadow)")
 
 
 def c5_layout(seed=3, cover=0.40):
@@ -542,7 +544,7 @@ def main():
     # ---- e2e through the public API with host buffers
     e2e = bench_e2e(p, eq, bc, shape, dt, variant, min(args.steps, 5), world)
     single = not args.no_c5 and world == 1     # C5 / C3 are single-GPU configurations
-    c5 = bench_c5(min(args.steps, 10), 3, variant) if single else None
+    c5 = bench_c5(C5_COARSE_STEPS, 3, variant) if single else None
     c3 = bench_c3(min(args.steps, 20), variant) if single else None
     c5_full = bench_c5_full(args.c5_full, variant) if args.c5_full and single else None
 

@@ -1283,6 +1283,104 @@ class SweepGraph:
         if self._roles() != before:
             raise RuntimeError("level sweep is not 2-periodic; cannot replay")
         self.graph.replay()                     # the device catches up with the captured steps
+        # lite shadow: the host bookkeeping of a pair (level times, counters,
+        # time-weight slots) without the orchestration; trusted only after it
+        # reproduced a full shadow pair exactly (_shadow_pair)
+        self.lite_ok = None
+        self._levels = [lev for lev in range(1, hierarchy.num_levels() + 1) if hierarchy.patches(lev)]
+        self._stores = {lev: _plan(hierarchy, lev).st for lev in self._levels}
+        self._coarse_in = {lev: lev >= 2 and bool(_plan(hierarchy, lev).coarse_all.n) for lev in self._levels}
+        self._fused_per_pair = None
+
+    def _book(self):
+        ctx = self.ctx
+        return ({lev: (st.time_synced, st.level_time, st.level_time_old) for lev, st in self._stores.items()},
+                dict(ctx.step_counts), dict(ctx.cell_steps), ctx.__dict__.get("fused_restrictions", 0))
+
+    def _restore(self, book):
+        times, counts, cells, fused = book
+        for lev, (synced, t, t_old) in times.items():
+            self._stores[lev].set_level_times(t, t_old)
+        self.ctx.step_counts.clear(); self.ctx.step_counts.update(counts)
+        self.ctx.cell_steps.clear(); self.ctx.cell_steps.update(cells)
+        self.ctx.__dict__["fused_restrictions"] = fused
+
+    def _lite_pair(self) -> list:
+        """Two coarse steps of the _advance recursion on the host bookkeeping
+        only: the same float operations on the level times (t + dt, dt / r,
+        _store_time_mode), the same counter updates; returns the slot values
+        in take() order."""
+        h, ctx, st_of = self.h, self.ctx, self._stores
+        vals = []
+
+        def fill(lev, t):
+            if self._coarse_in.get(lev):
+                mode, w = _store_time_mode(st_of[lev - 1], t)
+                vals.append(w if mode == 1 else -1.0)
+
+        def adv(lev, dt):
+            count = ctx.step_counts.get(lev, 0)
+            st = st_of[lev]
+            t = st.level_time
+            fill(lev, t)
+            st.set_level_times(t, t)
+            ctx.count_step(lev, st.total_cells)
+            t_new = t + dt
+            st.set_level_times(t_new, t)
+            ctx.step_counts[lev] = count + 1
+            if lev < h.max_levels and (lev + 1) in st_of:
+                fill(lev, t_new)
+                ratio = h.ratio_to_finer(lev)
+                for _ in range(ratio):
+                    adv(lev + 1, dt / ratio)
+
+        for _ in range(2):
+            adv(1, self.dt)
+        ctx.__dict__["fused_restrictions"] = ctx.__dict__.get("fused_restrictions", 0) + self._fused_per_pair
+        for st in st_of.values():
+            ctx.__dict__.setdefault("_bad_stores", {})[id(st)] = st
+        return vals
+
+    def _full_shadow(self):
+        device.SHADOW = True
+        device.PARAMS = self.params
+        self.params.rewind()
+        self.ctx._defer_checks = True
+        try:
+            for _ in range(2):
+                advance_hierarchy(self.h, 1, self.dt, self.ctx)
+        finally:
+            device.SHADOW = False
+            device.PARAMS = None
+            self.ctx._defer_checks = False
+
+    def _shadow_pair(self):
+        """Host bookkeeping of the next replayed pair.  The first pair runs
+        both the lite shadow and the full one (from the same bookkeeping) and
+        keeps the lite one only if times, counters and slot values agree
+        exactly; otherwise every pair runs the full shadow."""
+        if self.lite_ok:
+            self.params.vals = self._lite_pair()
+            return
+        if self.lite_ok is None and self.ctx.on_level_advanced is None and not USE_JOB_FILL:
+            before = self._book()
+            f0 = before[3]
+            self._fused_per_pair = 0
+            try:
+                lite_vals = self._lite_pair()
+                lite_book = self._book()
+            except Exception:       # noqa: BLE001 -- any mismatch disables the lite path
+                lite_vals, lite_book = None, None
+            self._restore(before)
+            self._full_shadow()
+            full_book = self._book()
+            self._fused_per_pair = full_book[3] - f0
+            if lite_book is not None:
+                lite_book = lite_book[:3] + (lite_book[3] + self._fused_per_pair,)
+            self.lite_ok = lite_vals is not None and lite_vals == self.params.vals and lite_book == full_book
+            return
+        self.lite_ok = False
+        self._full_shadow()
 
     def _roles(self):
         out = []
@@ -1309,17 +1407,7 @@ class SweepGraph:
         if self._regrid_due(coarse_steps):
             raise ValueError("a regrid falls inside the replayed steps")
         for _ in range(coarse_steps // 2):
-            device.SHADOW = True
-            device.PARAMS = self.params
-            self.params.rewind()
-            self.ctx._defer_checks = True
-            try:
-                for _ in range(2):
-                    advance_hierarchy(self.h, 1, self.dt, self.ctx)
-            finally:
-                device.SHADOW = False
-                device.PARAMS = None
-                self.ctx._defer_checks = False
+            self._shadow_pair()
             self.params.upload()
             self.graph.replay()
         self.ctx._bad_pending = True

@@ -47,3 +47,23 @@ def test_sweep_graph_matches_eager():
         for pa, pb in zip(ha.patches(lev), hb.patches(lev)):
             assert pa.time == pb.time
             assert np.array_equal(pa.interior(), pb.interior())
+
+
+def test_sweep_graph_lite_shadow_matches_eager():
+    """After its first pair (full shadow + lite shadow, compared), replays use
+    the lite host bookkeeping; many pairs later the states, times and
+    counters still equal the eager sweep bitwise."""
+    from paper_1511_03645_b200 import _lib, amr
+    ha, ca, dt = small_hierarchy(_lib.VARIANT_FAST)
+    hb, cb, _ = small_hierarchy(_lib.VARIANT_FAST)
+    for _ in range(4 + 14):
+        amr.advance_hierarchy(ha, 1, dt, ca)
+    g = amr.SweepGraph(hb, dt, cb)
+    g.advance(2)
+    assert g.lite_ok is True
+    g.advance(12)
+    assert ca.cell_steps == cb.cell_steps and ca.step_counts == cb.step_counts
+    for lev in (1, 2, 3):
+        for pa, pb in zip(ha.patches(lev), hb.patches(lev)):
+            assert pa.time == pb.time and pa.time_old == pb.time_old
+            assert np.array_equal(pa.interior(), pb.interior())

@@ -17,6 +17,7 @@ ap.add_argument("--n", type=int, default=4096)
 ap.add_argument("--variant", default="fast")
 ap.add_argument("--flag", action="store_true")
 ap.add_argument("--flag1", action="store_true", help="single-snapshot window")
+ap.add_argument("--phys-in", action="store_true", help="the bench's launch (fills its input's physical ghosts)")
 a = ap.parse_args()
 bench.N = a.n
 h, p, eq, bc, dt = bench.build_c4(a.n)
@@ -30,7 +31,7 @@ for _ in range(a.launches):
     out = st._free(st.cur, -1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    device.launch_step(st, dt, eq, "MC", var, out)
+    device.launch_step(st, dt, eq, "MC", var, out, phys_in=(bc, eq, (a.n, a.n)) if a.phys_in else None)
     e1.record()
     st.ghost_src = st.cur
     st.cur = out
