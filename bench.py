@@ -84,7 +84,14 @@ def c4_fields(n=N, g=2, device="cuda", x_off=0):
     return B
 
 
-def build_c4(n=N, rank=0, world=1):
+def build_c4(n=N, rank=0, world=1, land=0.0):
+    """land > 0 (extension, not a BASELINE configuration): the bathymetry is
+    raised by ``land`` metres, so the shelf beyond x' ~ 0.75 is dry land (a
+    coastline through the level; the FAST kernel's wet/dry instantiation)."""
+    return _build_c4(n, rank, world, land)
+
+
+def _build_c4(n=N, rank=0, world=1, land=0.0):
     """The C4 level; world > 1: rank's n-row x-slab of the (world*n) x n
     level on [0, world*L] x [0, L] (weak scaling, sharded.py), dt from the
     global select_dt."""
@@ -92,7 +99,7 @@ def build_c4(n=N, rank=0, world=1):
     from paper_1511_03645_b200 import equations as E
     from paper_1511_03645_b200 import sharded, solver
     from paper_1511_03645_b200.geometry import Patch, PatchHierarchy
-    B = c4_fields(n, x_off=rank * n)
+    B = c4_fields(n, x_off=rank * n) + land
     depth = (0.0 - B)
     c = torch.sqrt(GRAV * torch.clamp(depth, min=0.0))
     mat = E.SweMaterial(bathymetry=B.cpu().numpy(), depth=depth.cpu().numpy(), wet=(depth > 0).cpu().numpy(),
@@ -547,6 +554,7 @@ def main():
     c5 = bench_c5(C5_COARSE_STEPS, 3, variant) if single else None
     c3 = bench_c3(min(args.steps, 20), variant) if single else None
     c5_full = bench_c5_full(args.c5_full, variant) if args.c5_full and single else None
+    coast = bench_c4_coast(min(args.steps, 20), variant) if single else None
 
     line = {
         "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
@@ -572,6 +580,7 @@ def main():
         "c5_batched_patches": c5,
         "c3_heterogeneous_acoustics": c3,
         "c5_full_workflow": c5_full,
+        "c4_coastline": coast,
         "e2e": e2e,
         # per step: k2_physical + k1_fast (graph replay; no memset nodes, fold is a no-op);
         # sharded (N > 1): k2_physical, the ghost-ring fold, K1 over the interior strips
@@ -585,6 +594,40 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_c4_coast(steps, variant):
+    """Extension (not a BASELINE configuration): C4 with the bathymetry
+    raised 1500 m, so a coastline crosses the level (dry land beyond it;
+    walls on every side).  FAST steps with the strip kernel's wet/dry
+    instantiation; the EXACT kernel is timed beside it."""
+    import torch
+    from paper_1511_03645_b200 import _lib, solver
+    out = {}
+    for name, var, k in (("fast", variant, steps), ("exact", _lib.VARIANT_EXACT, 3)):
+        h, p, eq, bc, dt = build_c4(N, land=1500.0)
+        bc = solver.BoundarySpec("wall", "wall", "wall", "wall")
+        st = solver.store_of(p)
+        solver.advance_uniform(p, eq, bc, (N, N), dt, 4, "MC", var)    # captures the step-pair graph
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        solver.advance_uniform(p, eq, bc, (N, N), dt, k, "MC", var)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        out[name] = {"ms_per_step": ms, "value": N * N / (ms * 1e-3), "steps": k}
+        if name == "fast":
+            k1 = k1_alone_ms(st, dt, eq, var, 10, phys_in=(bc, eq, (N, N)))
+            out["dry_fraction"] = float((~p.aux.wet[2:-2, 2:-2]).mean())
+            out["k1_ms"] = k1
+            out["k1_hbm_frac"] = BYTES_PER_CELL_SWE * N * N / (k1 * 1e-3) / 1e9 / peaks()[0]
+        del h, p, st
+        torch.cuda.empty_cache()
+    out["unit"] = "cell-updates/s"
+    out["workload"] = ("extension: C4 bathymetry + 1500 m (coastline, dry land), walls; FAST = strip kernel with "
+                       "wet/dry effective states (ADJ_STEP_WET_DRY), EXACT = reference-order kernel")
+    return out
 
 
 def build_c3(n=2048):

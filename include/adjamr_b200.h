@@ -255,6 +255,14 @@ typedef struct AdjStepArgs {
                                        sources from q_in's interior (side rules from phys_bc; corners x
                                        then y; nx, ny >= 2) -- so no separate fill launch precedes the
                                        step */
+#define ADJ_STEP_WET_DRY       32   /* FAST, shallow water (SweLinear2D, forward wave form) with dry
+                                       cells, static CFL bound: wet <=> aux c > 0; a dry side of a face
+                                       takes the wet side's state (normal momentum negated) and material,
+                                       both-dry faces carry no waves, corrections only on wet-wet faces,
+                                       transverse materials of dry cells at unit depth, dry cells keep
+                                       their state (_swe_effective_states / _swe_transverse_material /
+                                       dq *= wet, solver.py:357-387, 500-505); without this flag a FAST
+                                       step assumes every cell wet */
 int adj_step_level(const AdjStepArgs* a);
 
 /* Tile shape (ni, nj) the given variant expects in AdjStepArgs.tiles. */

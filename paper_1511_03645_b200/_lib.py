@@ -25,6 +25,7 @@ BC_WALL, BC_OUTFLOW, BC_PERIODIC = 0, 1, 2
 BC_CODES = {"wall": BC_WALL, "outflow": BC_OUTFLOW, "periodic": BC_PERIODIC}
 RECT_COPY, RECT_COARSE = 0, 1
 STEP_KEEP_NONFINITE, STEP_NO_SPEED_OUT, STEP_TWO_ROWS, STEP_COUNTER_ZERO, STEP_PHYS_IN = 1, 2, 4, 8, 16
+STEP_WET_DRY = 32
 
 
 class NativeUnavailableError(RuntimeError):

@@ -1141,7 +1141,7 @@ def step_level(hierarchy: PatchHierarchy, level: int, dt: float, ctx: AmrContext
     st.save_old_all()
     st.set_level_times(t, t)
     out = st._free(st.cur)
-    static = ctx.variant == _lib.VARIANT_FAST and st.ndim == 2 and not st.any_dry()
+    static = device.fast_static(st, ctx.equation, ctx.variant)
     if prefill is not None and not static:
         raise RuntimeError("a deferred ghost fill needs the fast static-CFL step")
     job_fill = None
@@ -1262,8 +1262,8 @@ class SweepGraph:
             advance_hierarchy(hierarchy, 1, dt, ctx)
         for lev in range(1, hierarchy.num_levels() + 1):
             st = _plan(hierarchy, lev).st
-            if st.any_dry():
-                raise ValueError("SweepGraph needs a level without dry cells")
+            if not device.fast_static(st, ctx.equation, ctx.variant):
+                raise ValueError("SweepGraph needs the static-CFL fast path on every level")
             for i in range(st.NBUF):
                 st._ensure_buf(i)
         torch.cuda.synchronize()

@@ -411,6 +411,26 @@ ADJ_D Face solve_face(double qL0, double qLn, double qR0, double qRn, const Mat&
     return f;
 }
 
+// Shallow water, forward wave form, with dry cells (_swe_effective_states,
+// solver.py:357-380): a dry side takes the wet side's state with the normal
+// momentum negated and the wet side's material; a both-dry face has no waves
+// (zero strengths).  wet <=> c > 0 (SweMaterial.create: c = sqrt(g max(depth, 0))).
+ADJ_D Face solve_face_swe_wd(double qL0, double qLn, double qR0, double qRn, double cL, double cR,
+                             bool wl, bool wr) {
+    const double a0 = wl ? qL0 : qR0, an = wl ? qLn : -qRn;
+    const double b0 = wr ? qR0 : qL0, bn = wr ? qRn : -qLn;
+    const bool dd = !wl && !wr;
+    const double cl = wl ? cL : (wr ? cR : 1.0), cr = wr ? cR : (wl ? cL : 1.0);   // dd: finite dummies
+    Face f;
+    const double inv = rcp(cl + cr);
+    const double d0 = b0 - a0, dn = bn - an;
+    f.s0 = dd ? 0.0 : (cr * d0 - dn) * inv;
+    f.s1 = dd ? 0.0 : (cl * d0 + dn) * inv;
+    f.P = fma(cl, cr, 1.0);
+    f.am0 = f.am1 = f.ap0 = f.ap1 = 0.0;   // the forward wave form sums fluctuations from strengths
+    return f;
+}
+
 // Limited correction flux (component 0, normal component) of face f.
 //   non-reversed: family 0 upwind = next face, family 1 upwind = previous face
 //   reversed:     family 0 upwind = previous face, family 1 upwind = next face
@@ -477,7 +497,7 @@ constexpr int RING1 = 3 * NGRP;
 // lives in a 3-slot ring indexed by (column mod 3); column<K> is the body of
 // the march for a column in slot K, so the 3-way unrolled loop rotates roles
 // by renaming instead of moving registers.
-template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool SQ = false>
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool SQ = false, bool WD = false>
 struct Strip {
     static constexpr bool SWE = SYS == ADJ_SYS_SWE2D;
     static constexpr bool FWD_WAVE = FORM == ADJ_FORM_WAVE && !REV;
@@ -500,7 +520,12 @@ struct Strip {
     double bpy0[3], bpy1[3];       // bp of transverse(Sy(column))
     double ft0[3], ft1[3];         // ftil at the x-face left of column
     double sx0[3], sx1[3];         // Sx(column)
-    double cup[3], mup[3];         // row j+1 materials of column
+    double cup[3], mup[3];         // row j+1 materials of column (WD: transverse materials)
+    // WD (shallow water with dry cells, forward wave form): per-column wet
+    // flags of this row, wet-wet flag of the y-face above, transverse
+    // material (dry cells at unit depth: sqrt(g), _swe_transverse_material)
+    bool wet[3], wwy[3];
+    double tcv[3], sqrtg;
     double smx, smy;
     unsigned bad;
     // fused restriction (RST): block sums of the new values over R rows x R columns
@@ -548,6 +573,10 @@ struct Strip {
     ADJ_D void column(int s, const Raw& cr, const double* up, const double* dn) {
         constexpr int C = K, P = (K + 2) % 3, PP = (K + 1) % 3;
         m[C] = make_mat<SYS, FORM, LIM, SQ>(cr.c, cr.z, dtdx, dtdy);
+        if (WD) {
+            wet[C] = __double2hiint(cr.c) > 0;   // c >= 0: c > 0 <=> its high word is positive
+            tcv[C] = wet[C] ? cr.c : sqrtg;
+        }
         // CFL: max |speed| of the faces is the max material speed of the cells
         // they touch (fast path = no dry cells): x-faces of this strip touch
         // columns [i0-1, i0+ni] of the output rows, y-faces rows j0-1..j0+nj
@@ -559,7 +588,8 @@ struct Strip {
         q0[C] = cr.q0; q1[C] = cr.q1; q2[C] = cr.q2;
 
         // ---- x-face s-1/2 between columns s-1 and s
-        xf[C] = solve_face<SYS, FORM, REV>(q0[P], q1[P], cr.q0, cr.q1, m[P], m[C]);
+        if (WD) xf[C] = solve_face_swe_wd(q0[P], q1[P], cr.q0, cr.q1, m[P].c, m[C].c, wet[P], wet[C]);
+        else xf[C] = solve_face<SYS, FORM, REV>(q0[P], q1[P], cr.q0, cr.q1, m[P], m[C]);
 
         // ---- y-face between rows j and j+1 at column s
         const double uq0 = K1_LDSNB ? up[0] : sh_dn(cr.q0);
@@ -572,7 +602,10 @@ struct Strip {
         mu.kx = 0.0;
         mu.tr = SWE ? mu.c * mu.c : mu.c * mu.m;
         mu.fx = FORM == ADJ_FORM_FWAVE ? sh_dn(m[C].fx) : 0.0;
-        const Face yf = solve_face<SYS, FORM, REV>(cr.q0, cr.q2, uq0, uq2, m[C], mu);
+        const bool wu = WD ? __double2hiint(mu.c) > 0 : true;
+        const Face yf = WD ? solve_face_swe_wd(cr.q0, cr.q2, uq0, uq2, m[C].c, mu.c, wet[C], wu)
+                           : solve_face<SYS, FORM, REV>(cr.q0, cr.q2, uq0, uq2, m[C], mu);
+        if (WD) wwy[C] = wet[C] && wu;
         const double s1up = REV ? 0.0 : sh_up(yf.s1);   // forward: the family-1 limiter neighbour and Sy's s1 below
         {
             const double s0n = REV ? sh_up(yf.s0) : sh_dn(yf.s0);
@@ -592,8 +625,8 @@ struct Strip {
             sy0[C] = yf.am0 + sh_up(yf.ap0);
             sy2[C] = yf.am1 + sh_up(yf.ap1);
         }
-        cup[C] = mu.c;
-        mup[C] = mu.m;
+        cup[C] = WD ? sh_dn(tcv[C]) : mu.c;
+        mup[C] = WD ? cup[C] : mu.m;
 
         // ---- Sx(s-1) and its transverse split with rows j-1, j+1 of column s-1
         if (FWD_WAVE) {   // Sx(s-1) from the strengths of its two x-faces and its own material
@@ -606,7 +639,7 @@ struct Strip {
         }
         {
             Mat mb{};
-            mb.c = K1_LDSNB ? dn[96] : sh_up(m[P].c);
+            mb.c = WD ? sh_up(tcv[P]) : (K1_LDSNB ? dn[96] : sh_up(m[P].c));
             mb.m = SWE ? mb.c : (K1_LDSNB ? dn[128] : sh_up(m[P].m));
             mb.tr = SWE ? mb.c * mb.c : mb.c * mb.m;
             Mat ma{};
@@ -616,18 +649,27 @@ struct Strip {
             transverse<SYS, FORM, REV>(sx0[P], hx, mb, ma, nbm0, bmv, bp0, bpv);
             gt0[P] = cy0[P] - (bp0 - sh_dn(nbm0));
             gt2[P] = cy2[P] - (bpv + sh_dn(bmv));
+            if (WD && !wwy[P]) gt0[P] = gt2[P] = 0.0;   // gtil[:, ~wwy] = 0 (solver.py:500-502)
         }
 
         // ---- transverse of Sy(s-1) with columns s-2, s; x-limiter of face s-3/2
         {
             double nbm0, bmv, bp0, bpv;
-            transverse<SYS, FORM, REV>(sy0[P], hy, m[PP], m[C], nbm0, bmv, bp0, bpv);
+            if (WD) {
+                Mat tb{}, ta{};
+                tb.c = tb.m = tcv[PP];
+                ta.c = ta.m = tcv[C];
+                transverse<SYS, FORM, REV>(sy0[P], hy, tb, ta, nbm0, bmv, bp0, bpv);
+            } else {
+                transverse<SYS, FORM, REV>(sy0[P], hy, m[PP], m[C], nbm0, bmv, bp0, bpv);
+            }
             double fc0, fc1;
             correction<SYS, FORM, REV, LIM>(xf[P], REV ? xf[PP].s0 : xf[C].s0, xf[PP].P,
                                             REV ? xf[C].s1 : xf[PP].s1, xf[C].P,
                                             m[PP], m[P], m[PP].kx, m[P].kx, fc0, fc1);
             ft0[P] = fc0 - (bpy0[PP] - nbm0);
             ft1[P] = fc1 - (bpy1[PP] + bmv);
+            if (WD && !(wet[PP] && wet[P])) ft0[P] = ft1[P] = 0.0;   // ftil[:, ~wwx] = 0
             bpy0[P] = bp0; bpy1[P] = bpv;
         }
 
@@ -645,6 +687,7 @@ struct Strip {
                 const double d2 = -dtdy * ((sy2[PP] + gt2[PP]) - gb2);
                 n0 = q0[PP] + d0; n1 = q1[PP] + d1; n2 = q2[PP] + d2;
             }
+            if (WD && !wet[PP]) { n0 = q0[PP]; n1 = q1[PP]; n2 = q2[PP]; }   // dq *= wet
             const int64_t o = (int64_t)(colbase + s - 2) * pitch;
             qout[o] = n0; qout[cs + o] = n1; qout[2 * cs + o] = n2;
             // non-finite <=> exponent bits all set (integer pipe)
@@ -693,6 +736,7 @@ struct Strip {
         pitch = p.pitch;
         dtdx = a.dtdx; dtdy = a.dtdy;
         hx = 0.5 * dtdx; hy = 0.5 * dtdy;
+        sqrtg = WD ? sqrt(a.gravity) : 0.0;
         colbase = g + T.i0;
         i0 = 0; ni = T.ni;
         if (RST) {
@@ -722,6 +766,7 @@ struct Strip {
             q0[k] = q1[k] = q2[k] = 0.0;
             sy0[k] = sy2[k] = gt0[k] = gt2[k] = cy0[k] = cy2[k] = 0.0;
             bpy0[k] = bpy1[k] = ft0[k] = ft1[k] = sx0[k] = sx1[k] = cup[k] = mup[k] = 0.0;
+            if (WD) { wet[k] = wwy[k] = false; tcv[k] = 0.0; }
         }
         // columns beyond s_last (at most two, rounding the march to whole
         // rotations) compute on stale registers and write nothing
@@ -826,7 +871,8 @@ ADJ_D void phys_prefill(const AdjStepArgs& a, const AdjTile& T, const AdjPatch& 
     }
 }
 
-template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false, bool SQ = false>
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false, bool SQ = false,
+          bool WD = false>
 #ifdef K1_MAXREG
 __global__ void __maxnreg__(K1_MAXREG) k1_fast(AdjStepArgs a) {
 #else
@@ -834,7 +880,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
 #endif
     const int lane = threadIdx.x & 31;
     __shared__ int s_tile[K1_WARPS];
-    constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL, RST, SQ>::NARR;
+    constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD>::NARR;
     extern __shared__ __align__(16) double s_ring1[];   // [K1_WARPS][RING1 * NARR * 32]
     const int warp = threadIdx.x >> 5;
     const int njob = a.job_offsets ? a.njob : a.ntile;
@@ -889,7 +935,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
         }
         const AdjTile T = a.tiles[tix];
         const AdjPatch p = a.patches[T.patch];
-        Strip<SYS, FORM, REV, LIM, CFL, RST, SQ> S;
+        Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD> S;
         S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
         S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32);
         S.run();
@@ -1176,14 +1222,15 @@ static void launch_two_rows(const AdjStepArgs& a, cudaStream_t st) {
     launch_pdl(k1_fast2<SYS, FORM, REV, LIM>, dim3(blocks), dim3(128), smem, st, a);
 }
 
-template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false, bool SQ = false>
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false, bool SQ = false,
+          bool WD = false>
 static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     static int blocks_per_sm = 0, sms = 0;
-    constexpr int smem = K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL, RST, SQ>::NARR * 32 * (int)sizeof(double);
+    constexpr int smem = K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD>::NARR * 32 * (int)sizeof(double);
     if (blocks_per_sm == 0) {
-        cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ, WD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ, WD>,
                                                       32 * K1_WARPS, smem);
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1193,7 +1240,7 @@ static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     int blocks = blocks_per_sm * sms;
     const int need = ((a.job_offsets ? a.njob : a.ntile) + K1_WARPS - 1) / K1_WARPS;
     if (blocks > need) blocks = need;
-    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ>, dim3(blocks), dim3(32 * K1_WARPS), smem, st, a);
+    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ, WD>, dim3(blocks), dim3(32 * K1_WARPS), smem, st, a);
 }
 
 // Square cells (dt/dx == dt/dy, every BASELINE configuration) share the x and
@@ -1211,8 +1258,31 @@ static void launch_static(const AdjStepArgs& a, cudaStream_t st) {
     else launch_cfl<SYS, FORM, REV, LIM, false, false, false, SQ>(a, st);
 }
 
+// Shallow water with dry cells (ADJ_STEP_WET_DRY): forward wave form, static
+// CFL bound, no fused restriction (shallow water restricts wet-weighted);
+// step_fast checks the arguments.
+template <int SYS, int FORM, bool REV, int LIM>
+static void launch_wet_dry(const AdjStepArgs& a, cudaStream_t st) {
+    if constexpr (SYS == ADJ_SYS_SWE2D && FORM == ADJ_FORM_WAVE && !REV) {
+        const bool pin = a.flags & ADJ_STEP_PHYS_IN;
+        if constexpr (LIM == ADJ_LIM_MC) {
+            if (a.dtdx == a.dtdy) {
+                if (pin) launch_cfl<SYS, FORM, REV, LIM, false, false, true, true, true>(a, st);
+                else launch_cfl<SYS, FORM, REV, LIM, false, false, false, true, true>(a, st);
+                return;
+            }
+        }
+        if (pin) launch_cfl<SYS, FORM, REV, LIM, false, false, true, false, true>(a, st);
+        else launch_cfl<SYS, FORM, REV, LIM, false, false, false, false, true>(a, st);
+    }
+}
+
 template <int SYS, int FORM, bool REV, int LIM>
 static void launch_kernel(const AdjStepArgs& a, cudaStream_t st) {
+    if (a.flags & ADJ_STEP_WET_DRY) {
+        launch_wet_dry<SYS, FORM, REV, LIM>(a, st);
+        return;
+    }
     if ((a.flags & ADJ_STEP_TWO_ROWS) && a.static_speed && !a.job_offsets && !(a.flags & ADJ_STEP_PHYS_IN) &&
         !(FORM == ADJ_FORM_WAVE && !REV && a.fine_restrict.ratio > 0)) {
         launch_two_rows<SYS, FORM, REV, LIM>(a, st);
@@ -1256,6 +1326,9 @@ int step_fast(const AdjStepArgs& a, cudaStream_t st) {
     if (a.ntile <= 0) return ADJ_OK;
     if (a.ndim == 1) return step_exact(a, st);   // 1D runs the exact kernel (tile shape 256x1)
     if (a.job_offsets && !a.static_speed) return ADJ_ERR_BAD_ARG;   // packed jobs need the static CFL bound
+    if ((a.flags & ADJ_STEP_WET_DRY) && !(a.system == ADJ_SYS_SWE2D && a.form == ADJ_FORM_WAVE && !a.reversed &&
+                                          a.static_speed && a.fine_restrict.ratio <= 0))
+        return ADJ_ERR_BAD_ARG;   // dry cells: forward shallow water, static CFL bound, no fused restriction
     if (a.system == ADJ_SYS_AC2D) fast::launch_sys<ADJ_SYS_AC2D>(a, st);
     else if (a.system == ADJ_SYS_SWE2D) fast::launch_sys<ADJ_SYS_SWE2D>(a, st);
     else return ADJ_ERR_BAD_ARG;

@@ -538,6 +538,23 @@ class LevelStore:
         return self._dry
 
 
+def fast_dry_ok(store: LevelStore, equation) -> bool:
+    """Whether the FAST strip kernel steps this level although it has dry
+    cells: forward shallow water (wave form, not time-reversed), 2D, one row
+    per lane (ADJ_STEP_WET_DRY)."""
+    return (store.swe and store.ndim == 2 and not store.two_rows() and
+            tuple(equation.kernel_spec()) == (_lib.SYS_SWE2D, _lib.FORM_WAVE, 0))
+
+
+def fast_static(store: LevelStore, equation, variant) -> bool:
+    """The FAST static-CFL path applies: 2D, and no dry cell or the wet/dry
+    strip kernel (the static per-patch bound equals the reference's face
+    maximum there too: a wet/dry face moves at the wet side's speed, a
+    both-dry face not at all, and dry cells have c = 0)."""
+    return (variant == _lib.VARIANT_FAST and store.ndim == 2 and
+            (not store.any_dry() or fast_dry_ok(store, equation)))
+
+
 # ---------------------------------------------------------------------------
 # launch wrappers
 
@@ -1069,8 +1086,14 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
         raise ValueError(f"unknown limiter {limiter!r}")
     torch = _torch()
     npatch = len(store.patches)
+    wet_dry = False
     if variant == _lib.VARIANT_FAST and store.any_dry():
-        variant = _lib.VARIANT_EXACT   # the fast strip kernel has no wet/dry logic
+        # dry cells: the strip kernel's wet/dry instantiation (forward shallow water, no fused
+        # restriction or in-launch fill); anything else steps with the EXACT kernel
+        if fast_dry_ok(store, equation) and fine_restrict is None and prefill is None and job_fill is None:
+            wet_dry = True
+        else:
+            variant = _lib.VARIANT_EXACT
     tiles, ntile, jobs, njob = store.tiles(variant)
     if phys_in is not None:          # jobs that fill physical ghosts go first
         tiles, ntile, jobs, njob = store.tiles_edge_first(phys_in[2])
@@ -1113,6 +1136,8 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
         a.flags |= _lib.STEP_COUNTER_ZERO
         if store.two_rows():
             a.flags |= _lib.STEP_TWO_ROWS
+        if wet_dry:
+            a.flags |= _lib.STEP_WET_DRY
     a.dt = dt
     a.dtdx = dt / spec0.dx
     a.dtdy = dt / spec0.dy if store.ndim == 2 else 0.0

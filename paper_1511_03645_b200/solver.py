@@ -321,8 +321,8 @@ def step_patch_host(patch: Patch, host_state, dt: float, equation: EquationSet, 
     if limiter not in LIMITERS:
         raise ValueError(f"unknown limiter {limiter!r}")
     st = store_of(patch)
-    if len(st.patches) != 1 or st.ndim != 2 or st.any_dry():
-        raise ValueError("step_patch_host needs a single 2D patch store without dry cells")
+    if len(st.patches) != 1 or not device.fast_static(st, equation, _lib.VARIANT_FAST):
+        raise ValueError("step_patch_host needs a single 2D patch store on the static-CFL fast path")
     spec = patch.spec
     dtdx, dtdy = dt / spec.dx, dt / spec.dy
     cfl = float(_cfl(st.static_speed_np(), dtdx, dtdy, 2)[0])
@@ -338,7 +338,7 @@ def step_patch_host(patch: Patch, host_state, dt: float, equation: EquationSet, 
 
 def _launch_single(st, slot, dt, equation, limiter, variant, out):
     """Step one patch of a multi-patch store (work tables restricted to it)."""
-    if variant == _lib.VARIANT_FAST and st.any_dry():
+    if variant == _lib.VARIANT_FAST and st.any_dry() and not device.fast_dry_ok(st, equation):
         variant = _lib.VARIANT_EXACT
     key = ("single", variant, slot)
     if key not in st._tiles:
@@ -480,7 +480,7 @@ def advance_uniform(patch: Patch, equation: EquationSet, boundary: BoundarySpec,
     spec = patch.spec
     dtdx = dt / spec.dx
     dtdy = dt / spec.dy if spec.ndim == 2 else 0.0
-    static = variant == _lib.VARIANT_FAST and st.ndim == 2 and not st.any_dry()
+    static = device.fast_static(st, equation, variant)
     if static:
         cfl = float(_cfl(st.static_speed_np(), dtdx, dtdy, spec.ndim)[0])
         if cfl > 1.0 + 1e-12:
