@@ -522,12 +522,65 @@ __global__ void __launch_bounds__(256) k4_cells(AdjRestrictArgs a) {
     }
 }
 
+// Planned restriction, 2D acoustics-type state (no wet weighting), fixed
+// ratio R in both axes: every fine value of a coarse cell (all components)
+// is loaded before the first store, so the loads of one cell form a single
+// round trip (the generic loop above re-loads after each component's store,
+// which the compiler must assume may alias).  Same summation order as
+// block_sum (row sums, then their running total; the flat numpy order for a
+// one-cell-wide overlap box goes through block_sum), so bitwise equal.
+template <int M, int R>
+__global__ void __launch_bounds__(256) k4_cells_r(AdjRestrictArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    const double cnt = (double)(R * R);
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.ncell) return;
+    const int cdst = a.cell_dst[t], fsrc = a.cell_src[t], meta = a.cell_meta[t];
+    const int fpitch = meta >> 1;
+    double out[M];
+    if (meta & 1) {
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+            out[c] = block_sum(a.q_fine + c * a.fine_comp_stride + fsrc, nullptr, fpitch, 0, 0, R, R, true) / cnt;
+    } else {
+        double v[M][R][R];
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+#pragma unroll
+            for (int p = 0; p < R; ++p)
+#pragma unroll
+                for (int q = 0; q < R; ++q)
+                    v[c][p][q] = __ldg(a.q_fine + c * a.fine_comp_stride + fsrc + (int64_t)p * fpitch + q);
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+            double tot = 0.0;
+#pragma unroll
+            for (int p = 0; p < R; ++p) {
+                double s = v[c][p][0];
+#pragma unroll
+                for (int q = 1; q < R; ++q) s = s + v[c][p][q];
+                tot = p == 0 ? s : tot + s;
+            }
+            out[c] = tot / cnt;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < M; ++c) a.q_coarse[c * a.coarse_comp_stride + cdst] = out[c];
+}
+
 int restrict_level(const AdjRestrictArgs& a) {
     if (a.cell_dst) {
         if (a.ncell <= 0) return ADJ_OK;
+        const cudaStream_t st = (cudaStream_t)a.stream;
+        if (a.ndim == 2 && !a.swe && a.m == 3 && (a.ratio == 2 || a.ratio == 4)) {
+            const dim3 g((a.ncell + 255) / 256), b(256);
+            if (a.ratio == 2) launch_pdl(k4_cells_r<3, 2>, g, b, 0, st, a);
+            else launch_pdl(k4_cells_r<3, 4>, g, b, 0, st, a);
+            return check_launch("k4_cells_r");
+        }
         int blocks = (a.ncell + 255) / 256;
         if (blocks > 148 * 8) blocks = 148 * 8;
-        const cudaStream_t st = (cudaStream_t)a.stream;
         const dim3 g(blocks), b(256);
         if (a.m == 3 && !a.swe) launch_pdl(k4_cells<3, false>, g, b, 0, st, a);
         else if (a.m == 3) launch_pdl(k4_cells<3, true>, g, b, 0, st, a);
