@@ -254,6 +254,13 @@ ADJ_D void grid_barrier(int* counter, int nblocks) {
     __syncthreads();
 }
 
+#ifndef K1_S1SUM
+#define K1_S1SUM 1   // 1: wave form, s1 = (jump) - s0 (the two strengths sum to the jump of the
+                     // eigen-coordinate; one FMA + one multiply fewer per face)
+#endif
+#ifndef K1_SHFL_K1
+#define K1_SHFL_K1 0   // 1: the upper cell's 1 + m^2 by shuffle instead of recomputed
+#endif
 #ifndef K1_RCP_CUBIC
 #define K1_RCP_CUBIC 1   // 0: one quadratic Newton step (relative error ~e^2)
 #endif
@@ -376,13 +383,13 @@ ADJ_D Face solve_face(double qL0, double qLn, double qR0, double qRn, const Mat&
         const double d0 = qR0 - qL0, dn = qRn - qLn;
         if (!SWE) {       // acoustics_rp_normal_2d
             f.s0 = (R.m * dn - d0) * inv;
-            f.s1 = (L.m * dn + d0) * inv;
+            f.s1 = K1_S1SUM ? dn - f.s0 : (L.m * dn + d0) * inv;
             // amdq = -cL W1 = s0 (cL zL, -cL) ; apdq = cR W2 = s1 (cR zR, cR)
             f.am0 = f.s0 * L.tr; f.am1 = -f.s0 * L.c;
             f.ap0 = f.s1 * R.tr; f.ap1 = f.s1 * R.c;
         } else {          // swe_linear_rp
             f.s0 = (R.c * d0 - dn) * inv;
-            f.s1 = (L.c * d0 + dn) * inv;
+            f.s1 = K1_S1SUM ? d0 - f.s0 : (L.c * d0 + dn) * inv;
             f.am0 = -f.s0 * L.c; f.am1 = f.s0 * L.tr;
             f.ap0 = f.s1 * R.c;  f.ap1 = f.s1 * R.tr;
         }
@@ -425,7 +432,7 @@ ADJ_D Face solve_face_swe_wd(double qL0, double qLn, double qR0, double qRn, dou
     const double inv = rcp(cl + cr);
     const double d0 = b0 - a0, dn = bn - an;
     f.s0 = dd ? 0.0 : (cr * d0 - dn) * inv;
-    f.s1 = dd ? 0.0 : (cl * d0 + dn) * inv;
+    f.s1 = dd ? 0.0 : (K1_S1SUM ? d0 - f.s0 : (cl * d0 + dn) * inv);
     f.P = fma(cl, cr, 1.0);
     f.am0 = f.am1 = f.ap0 = f.ap1 = 0.0;   // the forward wave form sums fluctuations from strengths
     return f;
@@ -597,7 +604,7 @@ struct Strip {
         Mat mu{};
         mu.c = K1_LDSNB ? up[96] : sh_dn(m[C].c);
         mu.m = SWE ? mu.c : (K1_LDSNB ? up[128] : sh_dn(m[C].m));
-        mu.k1 = fma(mu.m, mu.m, 1.0);
+        mu.k1 = K1_SHFL_K1 ? sh_dn(m[C].k1) : fma(mu.m, mu.m, 1.0);
         mu.ky = sh_dn(m[C].ky);
         mu.kx = 0.0;
         mu.tr = SWE ? mu.c * mu.c : mu.c * mu.m;
