@@ -9,7 +9,12 @@ rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
-lines = [l for l in out.splitlines() if l.startswith('"0x') or l.startswith('"Address"')]
+lines = []
+for l in out.splitlines():          # first kernel of the report only
+    if l.startswith('"Address"') and lines:
+        break
+    if l.startswith('"0x') or l.startswith('"Address"'):
+        lines.append(l)
 rows = list(csv.reader(io.StringIO("\n".join(lines))))
 hdr, rows = rows[0], rows[1:]
 ci = {h: i for i, h in enumerate(hdr)}
