@@ -368,8 +368,8 @@ def k1_alone_ms(st, dt, eq, variant, launches=10, phys_in=None):
 
 def k1_traffic():
     """DRAM bytes (read + write) per K1 launch on C4 from the committed ncu
-    --set full capture (profiles/r01_k1_traffic.json), or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_k1_traffic.json")
+    --set full capture (profiles/r02b_k1_traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02b_k1_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)

@@ -17,10 +17,13 @@ ap.add_argument("--n", type=int, default=4096)
 ap.add_argument("--variant", default="fast")
 ap.add_argument("--flag", action="store_true")
 ap.add_argument("--flag1", action="store_true", help="single-snapshot window")
+ap.add_argument("--coast", action="store_true", help="C4 + 1500 m: coastline, wet/dry kernel")
 ap.add_argument("--phys-in", action="store_true", help="the bench's launch (fills its input's physical ghosts)")
 a = ap.parse_args()
 bench.N = a.n
-h, p, eq, bc, dt = bench.build_c4(a.n)
+h, p, eq, bc, dt = bench.build_c4(a.n, land=1500.0 if a.coast else 0.0)
+if a.coast:
+    bc = solver.BoundarySpec("wall", "wall", "wall", "wall")
 st = solver.store_of(p)
 st.sync_in()
 var = _lib.VARIANT_FAST if a.variant == "fast" else _lib.VARIANT_EXACT
