@@ -1556,7 +1556,7 @@ def _fast_tile_shape():
     return ni_t.value, nj_t.value
 
 
-def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, limiter, slabs=8):
+def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, limiter, slabs=8, wait=True):
     """fill_ghost_physical + the fast step of the single patch of ``store``
     on a state held in host memory ``host`` (m, NX, NY), updated in place.
 
@@ -1565,7 +1565,15 @@ def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, li
     virtual patch over the real one (its rows with a g-row halo; x edge bits
     only on the first / last slab), so K1 and the fill run unchanged; the
     halo rows come from the neighbouring chunk, which is copied first.
-    Leaves the new state (interior and filled ghosts) in the store's ``cur``."""
+    Leaves the new state (interior and filled ghosts) in the store's ``cur``.
+
+    ``wait=False``: return with the device-to-host copies in flight (the
+    device state is complete for later launches on the current stream; the
+    host state is complete after ``stream_finish``).  A following call then
+    starts its host-to-device copy of a slab as soon as the copies that
+    wrote (or read, on the device) the same rows finished, so consecutive
+    steps overlap their two PCIe directions.  Non-finite flags accumulate
+    until ``stream_finish``.  Returns None in that mode."""
     torch = _torch()
     p = store.patches[0]
     off, NX, NY, pitch = store.boxes[0]
@@ -1590,6 +1598,9 @@ def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, li
     start.record(main)
     for s in (s_in, s_cmp, s_out):
         s.wait_event(start)
+    # an unfinished previous call (wait=False): slab k's H2D writes the host rows the previous
+    # D2H of slabs k-1..k+1 wrote (and their device rows it read) -> wait for exactly those
+    prev = store.__dict__.pop("_stream_pending", None)
     dev_in = store.buf[inb].as_strided((m, NX, NY), (store.plane, pitch, 1), off)
     dev_out = store.buf[outb].as_strided((m, NX, NY), (store.plane, pitch, 1), off)
     # per-slab virtual patch tables and tiles (cached per geometry)
@@ -1620,10 +1631,21 @@ def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, li
     sides = _bc_codes(boundary)
     ev_in = [torch.cuda.Event() for _ in range(S)]
     ev_cmp = [torch.cuda.Event() for _ in range(S)]
-    with torch.cuda.stream(s_cmp):
-        scratch.zero_()
+    if prev is None or prev[0] != tuple(o):
+        if prev is not None:            # other geometry: wait for every pending copy
+            for ev in prev[1]:
+                s_in.wait_event(ev)
+            prev = None
+        with torch.cuda.stream(s_cmp):
+            if prev is None and not store.__dict__.get("_stream_acc"):
+                scratch.zero_()
+    ev_out = [torch.cuda.Event() for _ in range(S)]
     for k in range(S):
         with torch.cuda.stream(s_in):
+            if prev is not None:
+                for j in (k - 1, k, k + 1):
+                    if 0 <= j < S:
+                        s_in.wait_event(prev[1][j])
             for c in range(m):     # per component: contiguous rows on both sides
                 dev_in[c, r[k]:r[k + 1]].copy_(host[c, r[k]:r[k + 1]], non_blocking=True)
             ev_in[k].record(s_in)
@@ -1674,9 +1696,35 @@ def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, li
             s_out.wait_event(ev_cmp[k])
             for c in range(m):
                 host[c, d[k]:d[k + 1]].copy_(dev_out[c, d[k]:d[k + 1]], non_blocking=True)
+            ev_out[k].record(s_out)
+    store.ghost_src = outb
+    store.cur = outb
+    if not wait:
+        main.wait_stream(s_in)
+        main.wait_stream(s_cmp)
+        store._stream_pending = (tuple(o), ev_out)
+        store._stream_acc = True
+        return None
     for s in (s_in, s_cmp, s_out):
         main.wait_stream(s)
     s_out.synchronize()
-    store.ghost_src = outb
-    store.cur = outb
+    store._stream_acc = False
     return bool(scratch[0].item())
+
+
+def stream_finish(store: LevelStore) -> bool:
+    """Complete the pending device-to-host copies of ``stream_step(wait=False)``
+    calls; returns whether any of those steps produced a non-finite value."""
+    torch = _torch()
+    pend = store.__dict__.pop("_stream_pending", None)
+    if pend is None and not store.__dict__.get("_stream_acc"):
+        return False
+    s_in, s_cmp, s_out = store._streams
+    main = torch.cuda.current_stream()
+    for s in (s_in, s_cmp, s_out):
+        main.wait_stream(s)
+    s_out.synchronize()
+    store._stream_acc = False
+    bad = bool(store._stream_scratch[0].item())
+    store._stream_scratch.zero_()
+    return bad

@@ -307,15 +307,21 @@ def step_patch(patch: Patch, dt: float, equation: EquationSet, limiter: str = "M
 
 
 def step_patch_host(patch: Patch, host_state, dt: float, equation: EquationSet, boundary: BoundarySpec,
-                    level_shape: tuple[int, ...], limiter: str = "MC", slabs: int = 8) -> StepResult:
+                    level_shape: tuple[int, ...], limiter: str = "MC", slabs: int = 8,
+                    wait: bool = True) -> StepResult:
     """fill_ghost_physical + step_patch (solver.py:125-146, 515-522) on a state
     that lives in host memory, as the reference keeps it: ``host_state``
     (m, nx+2g, ny+2g) -- a torch CPU tensor, pinned for full overlap -- is
     read, advanced by dt and overwritten in place; the patch's device copy
     holds the same state afterwards.  Row slabs stream through the device
     with the host-to-device copy, the step and the device-to-host copy of
-    consecutive slabs overlapping.  Needs the fast 2D path (static CFL bound,
-    no dry cells); raises CflViolationError before any mutation."""
+    consecutive slabs overlapping.  Needs the fast 2D path (static CFL bound);
+    raises CflViolationError before any mutation.
+
+    ``wait=False``: return with the device-to-host copies in flight, like a
+    ``non_blocking`` torch copy.  The next call (same host buffer) overlaps its
+    host-to-device copies with them slab by slab; ``host_stream_finish``
+    completes them and raises NumericalBlowupError for any non-finite step."""
     if dt <= 0:
         raise ValueError("dt must be positive")
     if limiter not in LIMITERS:
@@ -328,12 +334,18 @@ def step_patch_host(patch: Patch, host_state, dt: float, equation: EquationSet, 
     cfl = float(_cfl(st.static_speed_np(), dtdx, dtdy, 2)[0])
     if cfl > 1.0 + 1e-12:
         raise CflViolationError(f"Courant number {cfl:.4f} > 1")
-    bad = device.stream_step(st, host_state, dt, equation, boundary, level_shape, limiter, slabs)
+    bad = device.stream_step(st, host_state, dt, equation, boundary, level_shape, limiter, slabs, wait=wait)
     patch._loc = "device"
     patch.time += dt
     if bad:
         raise NumericalBlowupError(f"non-finite state at t={patch.time}")
     return StepResult(lambda: patch.state, cfl)
+
+
+def host_stream_finish(patch: Patch):
+    """Completes the host state of ``step_patch_host(..., wait=False)`` calls."""
+    if device.stream_finish(store_of(patch)):
+        raise NumericalBlowupError(f"non-finite state at or before t={patch.time}")
 
 
 def _launch_single(st, slot, dt, equation, limiter, variant, out):

@@ -71,3 +71,32 @@ def test_streamed_step_raises_cfl_before_mutation():
     with pytest.raises(solver.CflViolationError):
         solver.step_patch_host(p, host, 3.0 * dt, eq, bc, (64, 48), "MC")
     assert torch.equal(host, before)
+
+
+@pytest.mark.parametrize("slabs", [1, 5, 16])
+def test_streamed_steps_without_wait_equal_waited_steps(slabs):
+    """step_patch_host(wait=False): consecutive steps overlap their copies slab
+    by slab; after host_stream_finish the host state equals the waited path's
+    bitwise, and a non-finite value is still reported."""
+    import torch
+    from paper_1511_03645_b200 import solver
+    sides = ("wall", "outflow", "outflow", "wall")
+    shape = (301, 263)
+    outs = []
+    for wait in (True, False):
+        h, p, eq, bc, dt = _patch("swe", *shape, sides)
+        host = torch.from_numpy(np.array(p.state, copy=True)).pin_memory()
+        for _ in range(5):
+            solver.step_patch_host(p, host, dt, eq, bc, shape, "MC", slabs=slabs, wait=wait)
+        solver.host_stream_finish(p)
+        outs.append(host.numpy().copy())
+        assert np.array_equal(np.array(p.state), outs[-1])
+    assert np.array_equal(outs[0], outs[1])
+    h, p, eq, bc, dt = _patch("ac", *shape, sides)
+    q = np.array(p.state, copy=True)
+    q[0, 40, 40] = np.nan
+    host = torch.from_numpy(q).pin_memory()
+    solver.step_patch_host(p, host, dt, eq, bc, shape, "MC", slabs=slabs, wait=False)
+    solver.step_patch_host(p, host, dt, eq, bc, shape, "MC", slabs=slabs, wait=False)
+    with pytest.raises(solver.NumericalBlowupError):
+        solver.host_stream_finish(p)

@@ -10,6 +10,8 @@ for _ in range(2):
 torch.cuda.synchronize()
 for lev in range(1, h.num_levels() + 1):
     pl = amr._plan(h, lev)
-    gp = getattr(pl, "gplan", None) or getattr(pl, "plan", None)
-    print(lev, len(h.patches(lev)), {k: getattr(v, "n", None) for k, v in vars(pl).items() if hasattr(v, "nc")},
-          {k: getattr(v, "nc", None) for k, v in vars(pl).items() if hasattr(v, "nc")})
+    for key, gp in pl._gather.items():
+        meta = gp.meta[:gp.n].cpu().numpy()
+        nphys_coarse = int(((meta & 1) != 0).sum()) - gp.nc
+        print(f"L{lev}: patches {len(h.patches(lev))} ghost entries {gp.n} coarse rect cells {gp.nc} "
+              f"physical mirroring coarse {nphys_coarse} copy+physical {gp.n - gp.nc - nphys_coarse}")
