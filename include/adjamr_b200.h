@@ -513,6 +513,13 @@ int adj_box_overlaps(int ndim, int kind, int ndst, const int32_t* dlo, const int
                      int nsrc, const int32_t* slo, const int32_t* shi, int gsrc, int ratio,
                      AdjRect* rects, int max_rects, int32_t* nrects);
 
+/* Stream-ordered strided copy (cudaMemcpy2DAsync, cudaMemcpyDefault): height
+ * rows of width bytes, row pitches in bytes.  step_patch_host moves a row slab
+ * of every component plane with one call per direction (the planes sit
+ * comp_stride apart on the device and nx*ny apart in the host state). */
+int adj_copy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                     void* stream);
+
 int adj_abi_version(void);
 
 #ifdef __cplusplus

@@ -166,6 +166,8 @@ class AdjFlagMaskArgs(C.Structure):
 
 EXPORTS = {
     "adj_abi_version": ([], C.c_int),
+    "adj_copy2d_async": ([C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p],
+                         C.c_int),
     "adj_last_error": ([], C.c_char_p),
     "adj_step_tile_shape": ([C.c_int, C.c_int, C.POINTER(I32), C.POINTER(I32)], C.c_int),
     "adj_step_level": ([C.POINTER(AdjStepArgs)], C.c_int),

@@ -215,6 +215,16 @@ int adj_functional(const AdjFunctionalArgs* a) {
     return adj::functional(*a);
 }
 
+int adj_copy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                     void* stream) {
+    if (!dst || !src) return adj::bad("null pointer");
+    if (width > dpitch || width > spitch) return adj::bad("width exceeds a pitch");
+    if (width == 0 || height == 0) return ADJ_OK;
+    const cudaError_t e = cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault,
+                                            (cudaStream_t)stream);
+    return adj::record_cuda(e, "cudaMemcpy2DAsync");
+}
+
 int adj_gauges(const AdjGaugeArgs* a) {
     if (!a || !a->q || (a->ngauge > 0 && (!a->gauges || !a->out))) return adj::bad("null pointer");
     return adj::gauges(*a);

@@ -1646,8 +1646,7 @@ def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, li
                 for j in (k - 1, k, k + 1):
                     if 0 <= j < S:
                         s_in.wait_event(prev[1][j])
-            for c in range(m):     # per component: contiguous rows on both sides
-                dev_in[c, r[k]:r[k + 1]].copy_(host[c, r[k]:r[k + 1]], non_blocking=True)
+            _copy_rows(dev_in, host, r[k], r[k + 1], s_in)
             ev_in[k].record(s_in)
         with torch.cuda.stream(s_cmp):
             s_cmp.wait_event(ev_in[k])
@@ -1694,8 +1693,7 @@ def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, li
             ev_cmp[k].record(s_cmp)
         with torch.cuda.stream(s_out):
             s_out.wait_event(ev_cmp[k])
-            for c in range(m):
-                host[c, d[k]:d[k + 1]].copy_(dev_out[c, d[k]:d[k + 1]], non_blocking=True)
+            _copy_rows(host, dev_out, d[k], d[k + 1], s_out)
             ev_out[k].record(s_out)
     store.ghost_src = outb
     store.cur = outb
@@ -1710,6 +1708,23 @@ def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, li
     s_out.synchronize()
     store._stream_acc = False
     return bool(scratch[0].item())
+
+
+def _copy_rows(dst, src, lo, hi, stream):
+    """Rows [lo, hi) of every component of (m, NX, NY) views whose rows are
+    contiguous (the component planes at any stride): one strided copy
+    (adj_copy2d_async) instead of one copy per component."""
+    if hi <= lo:
+        return
+    m, _, NY = src.shape
+    width = (hi - lo) * NY * 8
+    if not (dst.stride(1) == NY and src.stride(1) == NY and dst.stride(2) == 1 and src.stride(2) == 1):
+        for c in range(m):
+            dst[c, lo:hi].copy_(src[c, lo:hi], non_blocking=True)
+        return
+    _lib.check(_lib.lib().adj_copy2d_async(dst[0, lo].data_ptr(), dst.stride(0) * 8, src[0, lo].data_ptr(),
+                                           src.stride(0) * 8, width, m, _lib.stream_ptr(stream)),
+               "adj_copy2d_async")
 
 
 def stream_finish(store: LevelStore) -> bool:

@@ -307,7 +307,7 @@ def step_patch(patch: Patch, dt: float, equation: EquationSet, limiter: str = "M
 
 
 def step_patch_host(patch: Patch, host_state, dt: float, equation: EquationSet, boundary: BoundarySpec,
-                    level_shape: tuple[int, ...], limiter: str = "MC", slabs: int = 8,
+                    level_shape: tuple[int, ...], limiter: str = "MC", slabs: int | None = None,
                     wait: bool = True) -> StepResult:
     """fill_ghost_physical + step_patch (solver.py:125-146, 515-522) on a state
     that lives in host memory, as the reference keeps it: ``host_state``
@@ -334,6 +334,8 @@ def step_patch_host(patch: Patch, host_state, dt: float, equation: EquationSet, 
     cfl = float(_cfl(st.static_speed_np(), dtdx, dtdy, 2)[0])
     if cfl > 1.0 + 1e-12:
         raise CflViolationError(f"Courant number {cfl:.4f} > 1")
+    if slabs is None:      # measured on C4: 8 slabs best for a waited step, 4 for chained ones
+        slabs = 8 if wait else 4
     bad = device.stream_step(st, host_state, dt, equation, boundary, level_shape, limiter, slabs, wait=wait)
     patch._loc = "device"
     patch.time += dt
