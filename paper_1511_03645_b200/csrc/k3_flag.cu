@@ -522,13 +522,18 @@ ADJ_D unsigned spread16(unsigned x) {   // bit k -> bit 2k
 // streams in as 16-byte cp.async pieces read back with one LDS.128.  Each
 // cell's arithmetic is k3_row's (bitwise); the even/odd ballots are
 // interleaved into the standard flag words.
+#ifndef K3_ROWP_DEPTH
+#define K3_ROWP_DEPTH 3   // state rows in flight per warp of k3_rowp (round 2: 3 measured 0.090 vs 0.094 ms
+                          // with 2 on C4; 4 exceeds the static shared-memory limit)
+#endif
+constexpr int RPDEPTH = K3_ROWP_DEPTH;
 #ifndef K3_ROWP_MINB
 #define K3_ROWP_MINB 3
 #endif
 constexpr int NPR = 2;   // pairs per lane
 
 __global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROWP_MINB) k3_rowp(AdjFlagArgs a, int run) {
-    __shared__ double2 s_q[K3_ROW_WARPS][RDEPTH][NPR * 3][32];
+    __shared__ double2 s_q[K3_ROW_WARPS][RPDEPTH][NPR * 3][32];
     const int pidx = blockIdx.z;
     const AdjPatch p = a.patches[pidx];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -559,7 +564,7 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROWP_MINB) k3_rowp(AdjFl
             }
     };
 #pragma unroll
-    for (int d = 0; d < RDEPTH - 1; ++d) {
+    for (int d = 0; d < RPDEPTH - 1; ++d) {
         if (r0 + d < r1) prefetch(r0 + d, d);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
@@ -601,9 +606,9 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROWP_MINB) k3_rowp(AdjFl
     double wxn = r0 + 1 < r1 ? __ldg(a.axis_w + rowoff + r0 + 1) : 0.0;
     unsigned long long cnt = 0;
     int buf = 0;
-    for (unsigned i = r0; i < r1; ++i, buf = buf + 1 == RDEPTH ? 0 : buf + 1) {
+    for (unsigned i = r0; i < r1; ++i, buf = buf + 1 == RPDEPTH ? 0 : buf + 1) {
         const bool more = i + 1 < r1;
-        if (i + RDEPTH - 1 < r1) prefetch(i + RDEPTH - 1, buf == 0 ? RDEPTH - 1 : buf - 1);
+        if (i + RPDEPTH - 1 < r1) prefetch(i + RPDEPTH - 1, buf == 0 ? RPDEPTH - 1 : buf - 1);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         const double ux = 1.0 - wx;
         double qh[NPR][2][3];
@@ -619,7 +624,7 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, K3_ROWP_MINB) k3_rowp(AdjFl
         const bool more2 = i + 2 < r1;
         const int i0nn = more2 ? __ldg(a.axis_i + rowoff + i + 2) : 0;
         const double wxnn = more2 ? __ldg(a.axis_w + rowoff + i + 2) : 0.0;
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(RDEPTH - 1) : "memory");
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(RPDEPTH - 1) : "memory");
         __syncwarp();
         double best[NPR][2];
 #pragma unroll
