@@ -582,10 +582,11 @@ def main():
         "c5_full_workflow": c5_full,
         "c4_coastline": coast,
         "e2e": e2e,
-        # per step: k2_physical + k1_fast (graph replay; no memset nodes, fold is a no-op);
+        # per step (graph replay, no memset nodes, fold is a no-op): N = 1 one k1_fast launch that
+        # also fills its input's physical ghosts (solver.USE_PHYS_IN; else k2_physical + k1_fast);
         # sharded (N > 1): k2_physical, the ghost-ring fold, K1 over the interior strips
         # (during the exchange) and K1 over the boundary strips
-        "gpu_launches": args.steps * (2 if world == 1 else 4),
+        "gpu_launches": args.steps * ((1 if solver.USE_PHYS_IN else 2) if world == 1 else 4),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
