@@ -264,6 +264,14 @@ ADJ_D void grid_barrier(int* counter, int nblocks) {
 #ifndef K1_RCP_CUBIC
 #define K1_RCP_CUBIC 1   // 0: one quadratic Newton step (relative error ~e^2)
 #endif
+#ifndef K1_PRED_STORE
+#define K1_PRED_STORE 0   // 1: the update runs on every lane, only its stores are predicated by out_lane
+#endif
+ADJ_D void st_pred(double* p, double v, bool pred) {   // st.global.f64 under a predicate (no branch)
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}\n" ::"l"(p), "d"(v),
+                 "r"((int)pred) : "memory");
+}
+
 ADJ_D double rcp(double x) {  // x > 0, normal: MUFU seed + one cubic Newton step
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
@@ -682,7 +690,11 @@ struct Strip {
 
         // ---- update cell s-2
         const double gb0 = sh_up(gt0[PP]), gb2 = sh_up(gt2[PP]);
+#if K1_PRED_STORE
+        if (s >= i0 + 2 && s <= s_last) {   // warp-uniform; only the stores are per lane (predicated)
+#else
         if (s >= i0 + 2 && s <= s_last && out_lane) {
+#endif
             double n0, n1, n2;
             if (K1_ALG2 && (SWE || (K1_ALG2_AC & 2))) {
                 n0 = fma(-dtdy, (sy0[PP] + gt0[PP]) - gb0, fma(-dtdx, (sx0[PP] + ft0[P]) - ft0[PP], q0[PP]));
@@ -696,12 +708,19 @@ struct Strip {
             }
             if (WD && !wet[PP]) { n0 = q0[PP]; n1 = q1[PP]; n2 = q2[PP]; }   // dq *= wet
             const int64_t o = (int64_t)(colbase + s - 2) * pitch;
-            qout[o] = n0; qout[cs + o] = n1; qout[2 * cs + o] = n2;
             // non-finite <=> exponent bits all set (integer pipe)
             const unsigned ex = 0x7ff00000u;
-            bad |= (((unsigned)__double2hiint(n0) & ex) == ex) | (((unsigned)__double2hiint(n1) & ex) == ex) |
-                   (((unsigned)__double2hiint(n2) & ex) == ex);
+            const bool nf = (((unsigned)__double2hiint(n0) & ex) == ex) | (((unsigned)__double2hiint(n1) & ex) == ex) |
+                            (((unsigned)__double2hiint(n2) & ex) == ex);
+#if K1_PRED_STORE
+            st_pred(qout + o, n0, out_lane); st_pred(qout + cs + o, n1, out_lane); st_pred(qout + 2 * cs + o, n2, out_lane);
+            bad |= out_lane & nf;
+            if (RST) { ra0 += out_lane ? n0 : 0.0; ra1 += out_lane ? n1 : 0.0; ra2 += out_lane ? n2 : 0.0; }
+#else
+            qout[o] = n0; qout[cs + o] = n1; qout[2 * cs + o] = n2;
+            bad |= nf;
             if (RST) { ra0 += n0; ra1 += n1; ra2 += n2; }
+#endif
         }
         if (RST && s >= i0 + 2 && s <= s_last && ((s - 2) & (rr - 1)) == rr - 1) {   // warp-uniform
             // sum the block's R rows (lanes), then its leader lane writes the mean
