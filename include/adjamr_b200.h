@@ -255,8 +255,9 @@ typedef struct AdjStepArgs {
                                        sources from q_in's interior (side rules from phys_bc; corners x
                                        then y; nx, ny >= 2) -- so no separate fill launch precedes the
                                        step */
-#define ADJ_STEP_WET_DRY       32   /* FAST, shallow water (SweLinear2D, forward wave form) with dry
-                                       cells, static CFL bound: wet <=> aux c > 0; a dry side of a face
+#define ADJ_STEP_WET_DRY       32   /* FAST, shallow water with dry cells (SweLinear2D forward wave
+                                       form, or its adjoint as the time-reversed f-wave form), static
+                                       CFL bound: wet <=> aux c > 0; a dry side of a face
                                        takes the wet side's state (normal momentum negated) and material,
                                        both-dry faces carry no waves, corrections only on wet-wet faces,
                                        transverse materials of dry cells at unit depth, dry cells keep

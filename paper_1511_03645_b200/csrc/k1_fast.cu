@@ -426,23 +426,25 @@ ADJ_D Face solve_face(double qL0, double qLn, double qR0, double qRn, const Mat&
     return f;
 }
 
-// Shallow water, forward wave form, with dry cells (_swe_effective_states,
-// solver.py:357-380): a dry side takes the wet side's state with the normal
-// momentum negated and the wet side's material; a both-dry face has no waves
-// (zero strengths).  wet <=> c > 0 (SweMaterial.create: c = sqrt(g max(depth, 0))).
-ADJ_D Face solve_face_swe_wd(double qL0, double qLn, double qR0, double qRn, double cL, double cR,
-                             bool wl, bool wr) {
+// Shallow water with dry cells (_swe_effective_states, solver.py:357-380): a
+// dry side takes the wet side's state with the normal momentum negated and the
+// wet side's material; a both-dry face has no waves (zero strengths and
+// fluctuations).  wet <=> c > 0 (SweMaterial.create: c = sqrt(g max(depth, 0))).
+// The solve itself is the regular one on the effective states and materials
+// (forward wave form and the time-reversed f-wave adjoint).
+template <int SYS, int FORM, bool REV>
+ADJ_D Face solve_face_wd(double qL0, double qLn, double qR0, double qRn, double cL, double cR, bool wl, bool wr) {
     const double a0 = wl ? qL0 : qR0, an = wl ? qLn : -qRn;
     const double b0 = wr ? qR0 : qL0, bn = wr ? qRn : -qLn;
     const bool dd = !wl && !wr;
     const double cl = wl ? cL : (wr ? cR : 1.0), cr = wr ? cR : (wl ? cL : 1.0);   // dd: finite dummies
-    Face f;
-    const double inv = rcp(cl + cr);
-    const double d0 = b0 - a0, dn = bn - an;
-    f.s0 = dd ? 0.0 : (cr * d0 - dn) * inv;
-    f.s1 = dd ? 0.0 : (K1_S1SUM ? d0 - f.s0 : (cl * d0 + dn) * inv);
-    f.P = fma(cl, cr, 1.0);
-    f.am0 = f.am1 = f.ap0 = f.ap1 = 0.0;   // the forward wave form sums fluctuations from strengths
+    Mat Le{}, Re{};
+    Le.c = Le.m = cl;
+    Re.c = Re.m = cr;
+    Le.tr = Le.fx = cl * cl;   // shallow water: c^2 = g h (transverse helper and f-wave flux factor)
+    Re.tr = Re.fx = cr * cr;
+    Face f = solve_face<SYS, FORM, REV>(a0, an, b0, bn, Le, Re);
+    if (dd) { f.s0 = f.s1 = 0.0; f.am0 = f.am1 = f.ap0 = f.ap1 = 0.0; }
     return f;
 }
 
@@ -603,7 +605,7 @@ struct Strip {
         q0[C] = cr.q0; q1[C] = cr.q1; q2[C] = cr.q2;
 
         // ---- x-face s-1/2 between columns s-1 and s
-        if (WD) xf[C] = solve_face_swe_wd(q0[P], q1[P], cr.q0, cr.q1, m[P].c, m[C].c, wet[P], wet[C]);
+        if (WD) xf[C] = solve_face_wd<SYS, FORM, REV>(q0[P], q1[P], cr.q0, cr.q1, m[P].c, m[C].c, wet[P], wet[C]);
         else xf[C] = solve_face<SYS, FORM, REV>(q0[P], q1[P], cr.q0, cr.q1, m[P], m[C]);
 
         // ---- y-face between rows j and j+1 at column s
@@ -618,7 +620,7 @@ struct Strip {
         mu.tr = SWE ? mu.c * mu.c : mu.c * mu.m;
         mu.fx = FORM == ADJ_FORM_FWAVE ? sh_dn(m[C].fx) : 0.0;
         const bool wu = WD ? __double2hiint(mu.c) > 0 : true;
-        const Face yf = WD ? solve_face_swe_wd(cr.q0, cr.q2, uq0, uq2, m[C].c, mu.c, wet[C], wu)
+        const Face yf = WD ? solve_face_wd<SYS, FORM, REV>(cr.q0, cr.q2, uq0, uq2, m[C].c, mu.c, wet[C], wu)
                            : solve_face<SYS, FORM, REV>(cr.q0, cr.q2, uq0, uq2, m[C], mu);
         if (WD) wwy[C] = wet[C] && wu;
         const double s1up = REV ? 0.0 : sh_up(yf.s1);   // forward: the family-1 limiter neighbour and Sy's s1 below
@@ -674,6 +676,8 @@ struct Strip {
                 Mat tb{}, ta{};
                 tb.c = tb.m = tcv[PP];
                 ta.c = ta.m = tcv[C];
+                tb.tr = tb.c * tb.c;   // shallow water: c^2 (the f-wave transverse uses it)
+                ta.tr = ta.c * ta.c;
                 transverse<SYS, FORM, REV>(sy0[P], hy, tb, ta, nbm0, bmv, bp0, bpv);
             } else {
                 transverse<SYS, FORM, REV>(sy0[P], hy, m[PP], m[C], nbm0, bmv, bp0, bpv);
@@ -1284,12 +1288,12 @@ static void launch_static(const AdjStepArgs& a, cudaStream_t st) {
     else launch_cfl<SYS, FORM, REV, LIM, false, false, false, SQ>(a, st);
 }
 
-// Shallow water with dry cells (ADJ_STEP_WET_DRY): forward wave form, static
-// CFL bound, no fused restriction (shallow water restricts wet-weighted);
-// step_fast checks the arguments.
+// Shallow water with dry cells (ADJ_STEP_WET_DRY): forward wave form or the
+// time-reversed f-wave adjoint, static CFL bound, no fused restriction
+// (shallow water restricts wet-weighted); step_fast checks the arguments.
 template <int SYS, int FORM, bool REV, int LIM>
 static void launch_wet_dry(const AdjStepArgs& a, cudaStream_t st) {
-    if constexpr (SYS == ADJ_SYS_SWE2D && FORM == ADJ_FORM_WAVE && !REV) {
+    if constexpr (SYS == ADJ_SYS_SWE2D && ((FORM == ADJ_FORM_WAVE && !REV) || (FORM == ADJ_FORM_FWAVE && REV))) {
         const bool pin = a.flags & ADJ_STEP_PHYS_IN;
         if constexpr (LIM == ADJ_LIM_MC) {
             if (a.dtdx == a.dtdy) {
@@ -1352,9 +1356,11 @@ int step_fast(const AdjStepArgs& a, cudaStream_t st) {
     if (a.ntile <= 0) return ADJ_OK;
     if (a.ndim == 1) return step_exact(a, st);   // 1D runs the exact kernel (tile shape 256x1)
     if (a.job_offsets && !a.static_speed) return ADJ_ERR_BAD_ARG;   // packed jobs need the static CFL bound
-    if ((a.flags & ADJ_STEP_WET_DRY) && !(a.system == ADJ_SYS_SWE2D && a.form == ADJ_FORM_WAVE && !a.reversed &&
-                                          a.static_speed && a.fine_restrict.ratio <= 0))
-        return ADJ_ERR_BAD_ARG;   // dry cells: forward shallow water, static CFL bound, no fused restriction
+    if ((a.flags & ADJ_STEP_WET_DRY) &&
+        !(a.system == ADJ_SYS_SWE2D && a.static_speed && a.fine_restrict.ratio <= 0 &&
+          ((a.form == ADJ_FORM_WAVE && !a.reversed) || (a.form == ADJ_FORM_FWAVE && a.reversed))))
+        return ADJ_ERR_BAD_ARG;   // dry cells: shallow water forward (wave) or adjoint (time-reversed f-wave),
+                                  // static CFL bound, no fused restriction
     if (a.system == ADJ_SYS_AC2D) fast::launch_sys<ADJ_SYS_AC2D>(a, st);
     else if (a.system == ADJ_SYS_SWE2D) fast::launch_sys<ADJ_SYS_SWE2D>(a, st);
     else return ADJ_ERR_BAD_ARG;

@@ -540,10 +540,10 @@ class LevelStore:
 
 def fast_dry_ok(store: LevelStore, equation) -> bool:
     """Whether the FAST strip kernel steps this level although it has dry
-    cells: forward shallow water (wave form, not time-reversed), 2D, one row
-    per lane (ADJ_STEP_WET_DRY)."""
+    cells: shallow water, forward (wave form) or the time-reversed f-wave
+    adjoint, 2D, one row per lane (ADJ_STEP_WET_DRY)."""
     return (store.swe and store.ndim == 2 and not store.two_rows() and
-            tuple(equation.kernel_spec()) == (_lib.SYS_SWE2D, _lib.FORM_WAVE, 0))
+            tuple(equation.kernel_spec()) in ((_lib.SYS_SWE2D, _lib.FORM_WAVE, 0), (_lib.SYS_SWE2D, _lib.FORM_FWAVE, 1)))
 
 
 def fast_static(store: LevelStore, equation, variant) -> bool:

@@ -77,12 +77,35 @@ def test_fast_wet_dry_multistep_vs_exact():
     assert norm_rel(outs[1], outs[0]) <= 1e-12, norm_rel(outs[1], outs[0])
 
 
-def test_wet_dry_flag_rejected_for_other_forms():
-    """The C ABI refuses ADJ_STEP_WET_DRY outside forward shallow water."""
+@pytest.mark.parametrize("limiter", ["MC", "minmod"])
+@pytest.mark.parametrize("square", [True, False])
+@pytest.mark.parametrize("seed", [0, 3])
+def test_fast_wet_dry_adjoint_vs_oracle(limiter, square, seed):
+    """The time-reversed f-wave adjoint (solve_adjoint's step) on a level with
+    dry cells: the strip kernel's wet/dry instantiation against the oracle."""
     from paper_1511_03645_b200 import _lib, device, solver
-    q, aux = dry_case(2, 40, 36)
+    q, aux = dry_case(seed)
+    dx, dy = (1000.0, 1000.0) if square else (1000.0, 750.0)
+    dt = 0.45 * min(dx, dy) / float(np.max(aux[0]))
     eq = make_equation("swe_adj_rev", gravity=G)
+    _, p = patch_from_arrays(q, aux, True, dx, dy, gravity=G)
+    assert device.fast_dry_ok(solver.store_of(p), eq)
+    res = solver.step_patch(p, dt, eq, limiter, variant=_lib.VARIANT_FAST)
+    want, cfl = O.step_2d(q, aux, dt, dx, dy, O.SWE2D, True, True, limiter, G)
+    assert norm_rel(p.state, want) <= 1e-12, norm_rel(p.state, want)
+    assert abs(res.max_courant - cfl) <= 1e-14 * max(cfl, 1.0)
+
+
+def test_wet_dry_flag_rejected_for_other_forms():
+    """ADJ_STEP_WET_DRY covers forward shallow water and its time-reversed
+    f-wave adjoint; other forms on dry levels step with the EXACT kernel."""
+    from paper_1511_03645_b200 import device, solver
+    q, aux = dry_case(2, 40, 36)
     _, p = patch_from_arrays(q, aux, True, 1000.0, 1000.0, gravity=G)
     st = solver.store_of(p)
     st.sync_in()
-    assert not device.fast_dry_ok(st, eq)     # the adjoint form steps with the EXACT kernel
+    assert device.fast_dry_ok(st, make_equation("swe_adj_rev", gravity=G))
+    assert device.fast_dry_ok(st, make_equation("swe_dry", gravity=G))
+    from paper_1511_03645_b200 import equations as E
+    from tests.helpers import dummy_model
+    assert not device.fast_dry_ok(st, E.SweLinear2D(dummy_model("swe", G)).adjoint())   # f-wave, not reversed
