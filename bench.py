@@ -480,7 +480,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", default="fast", choices=["fast", "exact"])
     ap.add_argument("--no-c5", action="store_true")
-    ap.add_argument("--c5-full", type=int, default=12, help="coarse steps of the full C5 workflow (0: skip)")
+    ap.add_argument("--c5-full", type=int, default=C5_COARSE_STEPS,
+                    help="coarse steps of the full C5 workflow (0: skip; default: the 50 BASELINE C5 states)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
