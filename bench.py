@@ -858,7 +858,9 @@ def bench_e2e(p, eq, bc, shape, dt, variant, steps, world=1):
                         "exchange, step) -> D2H; max wall time over ranks"}
     if variant == _lib_variant_fast():
         # streamed: H2D / physical fill + step / D2H of consecutive row slabs overlap
-        solver.step_patch_host(p, host, dt, eq, bc, shape, "MC")       # warm-up (plans, streams)
+        for _ in range(2):                                               # warm-up (plans, streams, pages)
+            solver.step_patch_host(p, host, dt, eq, bc, shape, "MC", wait=False)
+        solver.host_stream_finish(p)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(steps):
