@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define ADJ_ABI_VERSION 5
+#define ADJ_ABI_VERSION 6
 
 /* status codes (mapped to the reference's exception classes by the host) */
 #define ADJ_OK                 0
@@ -241,6 +241,9 @@ typedef struct AdjStepArgs {
                                   (FAST 2D, static_speed, job_offsets, ADJ_STEP_COUNTER_ZERO, no prefill) */
     int32_t phys_bc[4];        /* ADJ_STEP_PHYS_IN: x-lo, x-hi, y-lo, y-hi ADJ_BC_* of the domain sides  */
     int32_t phys_normal[2];    /* component negated at an x / a y wall                                     */
+    const int8_t* job_class;   /* optional with ADJ_STEP_WET_DRY (device, njob or ntile): 0 every cell of
+                                  the job's strip windows wet (the all-wet march), 1 mixed (the wet/dry
+                                  march), 2 every output cell dry (outputs copied: dq *= wet)              */
 } AdjStepArgs;
 /* AdjStepArgs.flags */
 #define ADJ_STEP_KEEP_NONFINITE 1   /* do not zero nonfinite: accumulate over launches */

@@ -91,7 +91,7 @@ class AdjStepArgs(C.Structure):
                 ("variant", I32), ("flags", I32),
                 ("dt", D), ("dtdx", D), ("dtdy", D), ("gravity", D), ("stream", P), ("prefill", AdjGhostPlanFillArgs),
                 ("fine_restrict", AdjStepRestrict), ("job_fill", AdjJobFill),
-                ("phys_bc", I32 * 4), ("phys_normal", I32 * 2)]
+                ("phys_bc", I32 * 4), ("phys_normal", I32 * 2), ("job_class", P)]
 
 
 class AdjPhysArgs(C.Structure):
@@ -133,7 +133,7 @@ class AdjFlagArgs(C.Structure):
                 ("tolerance", D), ("envelope", P), ("work", P), ("stream", P)]
 
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 FLAG_ROWS = 1        # AdjFlagArgs.layout: ADJ_FLAG_ROWS
 FLAG_PAIRS = 2       # AdjFlagArgs.layout: ADJ_FLAG_PAIRS
 FLAG_QUADS = 4       # AdjFlagArgs.layout: ADJ_FLAG_QUADS

@@ -826,6 +826,28 @@ struct Strip {
     }
 };
 
+// A strip whose output cells are all dry: dq *= wet leaves them unchanged, so
+// the step copies them (every lane its row, column by column, coalesced).
+// Returns whether a copied value is non-finite (the reference's q + 0 dq).
+ADJ_D bool dry_copy(const AdjStepArgs& a, const AdjTile& T, const AdjPatch& p, int lane, int lane0) {
+    const int l = lane - lane0;
+    if (l < 2 || l >= 2 + T.nj) return false;
+    const int g = a.ghost;
+    const int64_t cs = a.comp_stride;
+    const int64_t base = p.offset + (int64_t)(g + T.i0) * p.pitch + (g + T.j0 + l - 2);
+    bool bad = false;
+    for (int i = 0; i < T.ni; ++i) {
+        const int64_t o = base + (int64_t)i * p.pitch;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double v = __ldg(a.q_in + c * cs + o);
+            a.q_out[c * cs + o] = v;
+            bad |= (((unsigned)__double2hiint(v) & 0x7ff00000u) == 0x7ff00000u);
+        }
+    }
+    return bad;
+}
+
 // ---- ADJ_STEP_PHYS_IN: fill_ghost_physical of q_in inside the step launch.
 // One patch spanning the level, ghost width 2.  A ghost-inclusive index ii
 // on an axis of n interior cells maps to its interior source and a wall sign
@@ -965,6 +987,21 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
         }
         const AdjTile T = a.tiles[tix];
         const AdjPatch p = a.patches[T.patch];
+        if (WD && a.job_class) {   // wet/dry level: all-wet jobs march without the selects, all-dry ones copy
+            const int cls = a.job_class[job];
+            if (cls == 0) {
+                Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, false> S;
+                S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
+                S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32);
+                S.run();
+                if (S.bad) a.nonfinite[T.patch] = 1;
+                continue;
+            }
+            if (cls == 2) {
+                if (dry_copy(a, T, p, lane, lane0)) a.nonfinite[T.patch] = 1;
+                continue;
+            }
+        }
         Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD> S;
         S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
         S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32);

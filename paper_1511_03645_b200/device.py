@@ -31,6 +31,9 @@ _SLACK = 64   # elements of slack after each plane set (strip loads may over-rea
 # times, counters) but no work is launched -- used to keep the host state in
 # step with CUDA-graph replays of the same sweep (amr.SweepGraph).
 SHADOW = False
+# wet/dry levels: per-job classes (all-wet jobs march without the wet/dry selects, all-dry jobs
+# copy); ADJAMR_JOB_CLASS=0 runs every job through the wet/dry march
+USE_JOB_CLASS = os.environ.get("ADJAMR_JOB_CLASS", "1") != "0"
 
 
 class ParamSlots:
@@ -527,6 +530,38 @@ class LevelStore:
     def static_speed_np(self):
         self.static_speed()
         return self._static_speed_np
+
+    def job_classes(self, tiles, ntile, jobs, njob):
+        """Per warp job of a FAST job table (ADJ_STEP_WET_DRY): 0 when every
+        cell its strips read is wet (the all-wet march), 2 when every output
+        cell is dry (copied), 1 otherwise; cached per table (materials are
+        static)."""
+        key = ("job_class", _ptr(tiles), ntile, _ptr(jobs) if jobs is not None else 0, njob)
+        hit = self._scratch.get(key)
+        if hit is not None:
+            return hit
+        rows = np.frombuffer(tiles.cpu().numpy().tobytes(), dtype=_lib.TILE_DTYPE)[:ntile]
+        offs = (jobs.cpu().numpy().astype(np.int64) if jobs is not None
+                else np.arange(ntile + 1, dtype=np.int64))
+        wet = [np.asarray(p.aux.c) > 0.0 for p in self.patches]
+        g = self.g
+        tcls = np.empty(ntile, dtype=np.int8)
+        for t, r in enumerate(rows):
+            w = wet[int(r["patch"])]
+            i0, j0, ni, nj = int(r["i0"]), int(r["j0"]), int(r["ni"]), int(r["nj"])
+            if w[i0:i0 + ni + 2 * g, j0:j0 + nj + 2 * g].all():
+                tcls[t] = 0
+            elif not w[i0 + g:i0 + g + ni, j0 + g:j0 + g + nj].any():
+                tcls[t] = 2
+            else:
+                tcls[t] = 1
+        jcls = np.ones(len(offs) - 1, dtype=np.int8)
+        for j in range(len(offs) - 1):
+            c = tcls[offs[j]:offs[j + 1]]
+            jcls[j] = 0 if (c == 0).all() else (2 if (c == 2).all() else 1)
+        dev = _torch().from_numpy(jcls).to("cuda")
+        self._scratch[key] = dev
+        return dev
 
     def any_dry(self) -> bool:
         """Whether any cell of the level is dry (cached; materials are static
@@ -1138,6 +1173,8 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
             a.flags |= _lib.STEP_TWO_ROWS
         if wet_dry:
             a.flags |= _lib.STEP_WET_DRY
+            if USE_JOB_CLASS:
+                a.job_class = _ptr(store.job_classes(tiles, ntile, jobs, njob))
     a.dt = dt
     a.dtdx = dt / spec0.dx
     a.dtdy = dt / spec0.dy if store.ndim == 2 else 0.0
@@ -1679,6 +1716,8 @@ def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, li
             b.limiter = _lib.LIMITERS[limiter]
             b.variant = _lib.VARIANT_FAST
             b.flags = _lib.STEP_KEEP_NONFINITE | _lib.STEP_NO_SPEED_OUT | _lib.STEP_COUNTER_ZERO
+            if store.any_dry():      # the wet/dry march for every job (no per-job classes on the slabs)
+                b.flags |= _lib.STEP_WET_DRY
             b.dt, b.dtdx, b.dtdy, b.gravity = dt, dt / spec.dx, dt / spec.dy, equation.gravity
             b.stream = _lib.stream_ptr(s_cmp)
             _lib.check(_lib.lib().adj_step_level(_lib.C.byref(b)), "adj_step_level")

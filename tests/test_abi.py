@@ -56,7 +56,7 @@ def _struct_fields(name):
     body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (name, name), text, re.S).group(1)
     body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
     fields = []
-    typewords = {"const", "unsigned", "long", "double", "int32_t", "int64_t", "uint32_t", "uint8_t", "void", "char",
+    typewords = {"const", "unsigned", "long", "double", "int32_t", "int64_t", "uint32_t", "uint8_t", "int8_t", "void", "char",
                  "AdjPatch", "AdjTile", "AdjRect", "AdjGhostPlan", "AdjGauge", "AdjGhostPlanFillArgs",
                  "AdjStepRestrict", "AdjJobFill"}
     for decl in body.split(";"):

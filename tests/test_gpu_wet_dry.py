@@ -109,3 +109,41 @@ def test_wet_dry_flag_rejected_for_other_forms():
     from paper_1511_03645_b200 import equations as E
     from tests.helpers import dummy_model
     assert not device.fast_dry_ok(st, E.SweLinear2D(dummy_model("swe", G)).adjoint())   # f-wave, not reversed
+
+
+def test_streamed_host_step_with_dry_cells():
+    """step_patch_host on a level with dry cells (row slabs through the wet/dry
+    march) equals the device step."""
+    import torch
+    from paper_1511_03645_b200 import _lib, solver
+    q, aux = dry_case(7, 150, 120)
+    dx = dy = 500.0
+    dt = 0.8 * dx / float(np.max(aux[0]))
+    eq = make_equation("swe_dry", gravity=G)
+    bc = solver.BoundarySpec("wall", "outflow", "wall", "wall")
+    _, p1 = patch_from_arrays(q, aux, True, dx, dy, gravity=G)
+    _, p2 = patch_from_arrays(q, aux, True, dx, dy, gravity=G)
+    host = torch.from_numpy(np.array(q, copy=True)).pin_memory()
+    for _ in range(3):
+        solver.fill_ghost_physical(p1, bc, eq, (150, 120))
+        solver.step_patch(p1, dt, eq, "MC", variant=_lib.VARIANT_FAST)
+        solver.step_patch_host(p2, host, dt, eq, bc, (150, 120), "MC", slabs=3)
+    assert np.array_equal(host.numpy(), np.array(p1.state))
+
+
+def test_job_classes_equal_wet_dry_march(monkeypatch):
+    """Per-job classes (all-wet jobs without the selects, all-dry jobs copied)
+    change no value against running every job through the wet/dry march."""
+    from paper_1511_03645_b200 import _lib, device, solver
+    outs = []
+    for use in (False, True):
+        monkeypatch.setattr(device, "USE_JOB_CLASS", use)
+        q, aux = dry_case(9, 300, 260)
+        dx = dy = 500.0
+        dt = 0.8 * dx / float(np.max(aux[0]))
+        eq = make_equation("swe_dry", gravity=G)
+        _, p = patch_from_arrays(q, aux, True, dx, dy, gravity=G)
+        bc = solver.BoundarySpec("wall", "wall", "wall", "wall")
+        solver.advance_uniform(p, eq, bc, (300, 260), dt, 6, "MC", _lib.VARIANT_FAST)
+        outs.append(np.array(p.state))
+    assert np.array_equal(outs[0], outs[1])
