@@ -249,7 +249,19 @@ class LevelStore:
             self.buf[i] = torch.zeros(self.m * self.plane, dtype=torch.float64, device="cuda")
         return self.buf[i]
 
-    def _free(self, *busy):
+    def settle_pending(self, stream=None):
+        """Order the given (current) stream after the device-to-host copies of
+        pending ``stream_step(wait=False)`` calls, which read this store's
+        buffers: any other write to the store must not overtake them."""
+        pend = self.__dict__.get("_stream_pending")
+        if pend is not None:
+            s = stream if stream is not None else _torch().cuda.current_stream()
+            for ev in pend[1]:
+                s.wait_event(ev)
+
+    def _free(self, *busy, settle=True):
+        if settle:
+            self.settle_pending()
         for i in range(self.NBUF):
             if i not in busy:
                 self._ensure_buf(i)
@@ -267,6 +279,7 @@ class LevelStore:
             self.cur = nb
 
     def fold_ghosts(self, stream=None):
+        self.settle_pending(stream)
         """Copy the current ghost ring into cur (see module docstring)."""
         if self.ghost_src == self.cur:
             return
@@ -278,6 +291,7 @@ class LevelStore:
     def prepare_write(self, full_ghosts: bool = False, stream=None):
         """Before an in-place write to cur: unalias, and fold the ghosts unless
         the write rewrites every ghost cell."""
+        self.settle_pending(stream)
         self._unalias()
         if full_ghosts:
             self.ghost_src = self.cur
@@ -287,6 +301,7 @@ class LevelStore:
     # ----------------------------------------------------------- coherence
     def sync_in(self, stream=None):
         """Upload every patch whose authoritative state is on the host."""
+        self.settle_pending(stream)
         if self.all_device:
             return
         pending = [p for p in self.patches if p._store is self and p._loc == "host"]
@@ -300,6 +315,7 @@ class LevelStore:
             p._loc = "device"
 
     def download(self, slot, out: np.ndarray):
+        self.settle_pending(None)
         torch = _torch()
         v = self.view(slot)
         if self.ghost_src != self.cur:
@@ -317,6 +333,7 @@ class LevelStore:
         return self.old is not None and bool(self.old_valid[slot])
 
     def download_old(self, slot, out: np.ndarray):
+        self.settle_pending(None)
         out[...] = self.view(slot, "old").cpu().numpy()
 
     def drop_old(self, slot):
@@ -1618,7 +1635,7 @@ def stream_step(store: LevelStore, host, dt, equation, boundary, level_shape, li
     store.edges_table(level_shape)
     edges = int(store.table_np["edges"][0])
     inb = store.cur
-    outb = store._free(store.cur, store.ghost_src, -1 if store.old is None else store.old)
+    outb = store._free(store.cur, store.ghost_src, -1 if store.old is None else store.old, settle=False)
     ti, tj = _fast_tile_shape()
     ti = store._strip_length(ti, tj)
     o = _slab_bounds(NX, g, slabs, ti)

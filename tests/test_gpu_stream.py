@@ -100,3 +100,24 @@ def test_streamed_steps_without_wait_equal_waited_steps(slabs):
     solver.step_patch_host(p, host, dt, eq, bc, shape, "MC", slabs=slabs, wait=False)
     with pytest.raises(solver.NumericalBlowupError):
         solver.host_stream_finish(p)
+
+
+def test_async_host_steps_then_device_steps_are_ordered():
+    """Device steps issued after step_patch_host(wait=False) wait for its
+    pending device-to-host copies (LevelStore.settle_pending): the host state
+    after host_stream_finish is the async step's result, not a later one."""
+    import torch
+    from paper_1511_03645_b200 import _lib, solver
+    sides = ("wall", "outflow", "outflow", "wall")
+    shape = (301, 263)
+    h, p, eq, bc, dt = _patch("ac", *shape, sides)
+    h2, p2, eq2, bc2, _ = _patch("ac", *shape, sides)
+    host = torch.from_numpy(np.array(p.state, copy=True)).pin_memory()
+    solver.step_patch_host(p, host, dt, eq, bc, shape, "MC", slabs=4, wait=False)
+    for _ in range(4):                       # device steps overwrite the store's buffers in rotation
+        solver.fill_ghost_physical(p, bc, eq, shape)
+        solver.step_patch(p, dt, eq, "MC", variant=_lib.VARIANT_FAST)
+    solver.host_stream_finish(p)
+    solver.fill_ghost_physical(p2, bc2, eq2, shape)
+    solver.step_patch(p2, dt, eq2, "MC", variant=_lib.VARIANT_FAST)
+    assert np.array_equal(host.numpy(), np.array(p2.state))
