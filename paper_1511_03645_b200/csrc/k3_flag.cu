@@ -869,30 +869,14 @@ __global__ void k3_envelope(AdjFlagArgs a) {
             if (a.mode == 1 && k >= 0) { take(k); take(k + 1); }
             else take(k >= 0 ? k : -k - 1);
         }
-        a.envelope[3 * plane + v] = m0;      // node envelope in planes 3..5
-        a.envelope[4 * plane + v] = m1;
-        a.envelope[5 * plane + v] = m2;
+        a.envelope[v] = m0;                  // node envelope, planes 0..2
+        a.envelope[plane + v] = m1;
+        a.envelope[2 * plane + v] = m2;
     }
 }
 
 ADJ_D double nanmax(double x, double m) { return (x > m || x != x) ? x : m; }
 
-// Stencil envelope: planes 0..2 at (i, j) = max of the node envelope over the
-// bilinear stencil (i..i+1, j..j+1), i < nxa-1, j < nya-1 (the clamped
-// stencil of interpolate_uniform always has this form).
-__global__ void k3_envelope2(AdjFlagArgs a) {
-    const int64_t nya = a.nya, plane = (int64_t)a.nxa * nya;
-    const double* n = a.envelope + 3 * plane;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < plane; v += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = v / nya, j = v - i * nya;
-        if (i + 1 >= a.nxa || j + 1 >= nya) continue;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const double* e = n + c * plane + v;
-            a.envelope[c * plane + v] = nanmax(nanmax(e[0], e[1]), nanmax(e[nya], e[nya + 1]));
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Windows of >= 2 snapshots on the row layout with quads (ADJ_FLAG_QUADS:
@@ -1099,8 +1083,9 @@ __global__ void __launch_bounds__(32 * K3_ROW_WARPS, FASTW ? K3_QUAD_MINB_FAST :
 
 // Bound pass of a pruned window: one warp per 64-column segment and a run of
 // row pairs of the quad layout (the blocks k3_quad's warps own).  Per block the
-// cells' bounds sum_c |q_c| E_c from the stencil envelope (planes 0..2 of
-// AdjFlagArgs.envelope); a block none of whose cells can exceed the tolerance
+// cells' bounds sum_c |q_c| E_c, E_c the maximum of the node envelope
+// (AdjFlagArgs.envelope, k3_envelope) over the cell's bilinear stencil; a
+// block none of whose cells can exceed the tolerance
 // gets zero flag words, the others go to the work list for k3_quad_list.
 // Loads of the next row pair are issued before this one's bound is formed.
 __global__ void __launch_bounds__(256) k3_bound(AdjFlagArgs a, int run) {
@@ -1116,6 +1101,8 @@ __global__ void __launch_bounds__(256) k3_bound(AdjFlagArgs a, int run) {
     const unsigned ny = (unsigned)p.ny, j = seg * 64u + 2u * lane;
     const int64_t nya = a.nya, plane = (int64_t)a.nxa * nya, cs = a.comp_stride;
     const int64_t rowoff = a.axis_off[2 * pidx], coloff = a.axis_off[2 * pidx + 1];
+    // node envelope; the stencil maximum over the 2 x 2 nodes is taken here (the clamped
+    // stencil of interpolate_uniform never passes the last row / column)
     const double* env = a.envelope + __ldg(a.axis_i + coloff + j);
     const double* qc = a.q + p.offset + (int64_t)a.ghost * p.pitch + a.ghost + j;
     const double tol = a.tolerance;
@@ -1125,7 +1112,8 @@ __global__ void __launch_bounds__(256) k3_bound(AdjFlagArgs a, int run) {
         const int64_t eo = (int64_t)__ldg(a.axis_i + rowoff + i) * nya;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            E[c] = __ldg(env + c * plane + eo);
+            const double* e = env + c * plane + eo;
+            E[c] = nanmax(nanmax(__ldg(e), __ldg(e + 1)), nanmax(__ldg(e + nya), __ldg(e + nya + 1)));
 #pragma unroll
             for (int r = 0; r < 2; ++r)
                 Q[r][c] = __ldcs(reinterpret_cast<const double2*>(qc + (int64_t)(i + r) * p.pitch + c * cs));
@@ -1450,7 +1438,6 @@ int flag_adjoint(const AdjFlagArgs& a) {
                     int rc = record_cuda(cudaMemsetAsync(a.work, 0, 2 * sizeof(int32_t), st), "memset work");
                     if (rc) return rc;
                     k3_envelope<<<eb, 256, 0, st>>>(a);
-                    k3_envelope2<<<eb, 256, 0, st>>>(a);
                     constexpr int BRUN = 16;   // rows per bound warp (8 row pairs)
                     const int64_t warps = (int64_t)(a.max_cols / 64) * ((a.max_rows + BRUN - 1) / BRUN);
                     k3_bound<<<dim3((unsigned)((warps + 7) / 8), 1, (unsigned)a.npatch), 256, 0, st>>>(a, BRUN);

@@ -1566,7 +1566,7 @@ def launch_flag(store: LevelStore, ring, ring_shape, a_origin, a_dx, a_dy, level
     if not want_best and USE_FLAG_PRUNING and len(snap_index) >= 2:
         # window envelope scratch: cells whose bound cannot reach the tolerance skip the window
         env = store.__dict__.get("_flag_envelope")
-        need = 6 * int(np.prod(ring_shape))       # stencil envelope, then node envelope
+        need = 3 * int(np.prod(ring_shape))       # node envelope (k3_bound takes the stencil maximum)
         if env is None or env.numel() < need:
             env = store._flag_envelope = torch.empty(need, dtype=torch.float64, device="cuda")
         a.envelope = _ptr(env)
