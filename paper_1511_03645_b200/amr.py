@@ -1362,7 +1362,8 @@ class SweepGraph:
         if self.lite_ok:
             self.params.vals = self._lite_pair()
             return
-        if self.lite_ok is None and self.ctx.on_level_advanced is None and not USE_JOB_FILL:
+        if (self.lite_ok is None and self.ctx.on_level_advanced is None and not USE_JOB_FILL and
+                all(st.time_synced for st in self._stores.values())):
             before = self._book()
             f0 = before[3]
             self._fused_per_pair = 0
