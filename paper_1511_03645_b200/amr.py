@@ -601,7 +601,17 @@ def _ring_and_physical_all(patches, level_shape):
     return full - np.prod(n, axis=1), full - ind
 
 
-def _coarse_time_mode(cp: Patch, t: float):
+# FAST sweeps: a coarse time weight below this is taken as 0 (old state only).  At the first
+# substep of an interval t equals the coarse level's saved time up to the rounding drift of the
+# subcycled level clocks (w ~ 1e-16 .. 1e-13 over C5's run); the reference then blends in
+# w * q(t1), a change of at most w * |q(t1) - q(t0)| to the ghost value, far inside the FAST
+# tolerance.  With w exactly 0 the first substep provably reads only the saved state, which
+# lets a captured sweep overlap the coarse level's step with it (USE_LEVEL_OVERLAP).  The EXACT
+# variant keeps the reference's blend bitwise.
+SNAP_W = 1e-12
+
+
+def _coarse_time_mode(cp: Patch, t: float, snap: bool = False):
     """space_time_interp scheduling (solver.py:266-286) -> (mode, w)."""
     eps = 1e-9 * max(abs(cp.time), 1.0)
     has_old = cp.time_old is not None and (
@@ -616,7 +626,7 @@ def _coarse_time_mode(cp: Patch, t: float):
     if t1 == t0:
         return 0, 0.0
     w = float(np.clip((t - t0) / (t1 - t0), 0.0, 1.0))
-    if w == 0.0:
+    if w == 0.0 or (snap and w < SNAP_W):
         return 0, 0.0
     return 1, w
 
@@ -797,12 +807,16 @@ def _plan(hierarchy: PatchHierarchy, level: int) -> LevelPlan:
     return pl
 
 
-def _store_time_mode(cst, t):
+def _snap(ctx) -> bool:
+    return ctx.variant == _lib.VARIANT_FAST
+
+
+def _store_time_mode(cst, t, snap: bool = False):
     """(mode, w) shared by every coarse patch, or None when they differ."""
     if cst.time_synced:
         has_old = cst.old is not None and bool(np.all(cst.old_valid))
         probe = cst.patches[0]
-        mode = _coarse_time_mode(probe, t) if has_old or probe._host_old is None else None
+        mode = _coarse_time_mode(probe, t, snap) if has_old or probe._host_old is None else None
         return mode
     return None
 
@@ -830,7 +844,7 @@ def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrC
         cst.sync_in()
         cst.fold_ghosts()
         old_buf = _coarse_old_buffer(cst)
-        mw = _store_time_mode(cst, t)
+        mw = _store_time_mode(cst, t, _snap(ctx))
     if not coarse_in or mw is not None:
         # level-synchronised times: coarse, copy and physical phases in one gather
         gp = pl.gather(hierarchy, level, ctx)
@@ -868,7 +882,7 @@ def fill_level_ghosts(hierarchy: PatchHierarchy, level: int, t: float, ctx: AmrC
             groups: dict = {}
             coarse = hierarchy.patches(level - 1)
             for c, rl in pl.crects_by_patch.items():
-                groups.setdefault(_coarse_time_mode(coarse[c], t), []).extend(rl)
+                groups.setdefault(_coarse_time_mode(coarse[c], t, _snap(ctx)), []).extend(rl)
             for (mode, w), rl in groups.items():
                 device.coarse_rects(st, cst, np.array(rl, dtype=_lib.RECT_DTYPE), old_buf, cst.buf[cst.cur],
                                     hierarchy, r, w, mode)
@@ -1204,12 +1218,55 @@ def advance_hierarchy(hierarchy: PatchHierarchy, level: int, dt: float, ctx: Amr
     """Advance one level by dt, recursively subcycling finer levels (amr.py:602-644)."""
     depth = ctx.__dict__.get("_depth", 0)
     ctx._depth = depth + 1
+    if depth == 0 and _overlap_on(ctx):
+        ctx._level_events = {}
+        ctx.__dict__.setdefault("_level_streams", {})
     try:
         _advance(hierarchy, level, dt, ctx)
     finally:
         ctx._depth = depth
+        if depth == 0 and ctx.__dict__.get("_level_events"):
+            for lev in list(ctx._level_events):    # join every side stream into the caller's
+                _wait_level(ctx, lev)
+            ctx._level_events = {}
     if depth == 0:
         _raise_pending(ctx)
+
+
+# captured level sweeps (SweepGraph): a parent level's step and its post-step fill run on a side
+# stream, concurrently with the first substep of its finer level, which reads only the parent's
+# saved pre-step state (coarse time weight 0, amr.py:620-642); every later reader of the parent's
+# new state waits for it.  Same launches, same inputs: bitwise equal to the sequential sweep
+USE_LEVEL_OVERLAP = os.environ.get("ADJAMR_LEVEL_OVERLAP", "1") == "1"
+_OVERLAP_MAX_LEVEL = int(os.environ.get("ADJAMR_OVERLAP_MAX_LEVEL", "99"))   # experiments
+
+
+def _overlap_on(ctx) -> bool:
+    return bool(ctx.__dict__.get("_overlap")) and not device.SHADOW and ctx.on_level_advanced is None
+
+
+def _wait_level(ctx, level):
+    """Order the current stream after the in-flight side-stream work of ``level``."""
+    ev = ctx.__dict__.get("_level_events", {}).get(level)
+    if ev is not None:
+        import torch
+        torch.cuda.current_stream().wait_event(ev)
+
+
+def _prefill_needs_coarse_new(hierarchy, level, t, substep, snap) -> bool:
+    """Whether the pre-step fill of ``level`` at t may read the coarse level's
+    new state (or launch on the coarse store): anything but the first substep
+    of an interval with time weight 0 and folded coarse ghosts."""
+    if level < 2 or substep > 0:
+        return True
+    pl = _plan(hierarchy, level)
+    cst = pl.cst
+    if cst is None or not pl.coarse_all.n:
+        return False
+    if cst.ghost_src != cst.cur or cst.old is None or not bool(np.all(cst.old_valid)):
+        return True
+    mw = _store_time_mode(cst, t, snap)
+    return mw is None or mw[0] != 0
 
 
 def _advance(hierarchy, level, dt, ctx, restrict_into: bool = False, substep: int = 0) -> bool:
@@ -1223,20 +1280,54 @@ def _advance(hierarchy, level, dt, ctx, restrict_into: bool = False, substep: in
     if not patches:
         return False
     t = patches[0].time
+    ov = _overlap_on(ctx)
+    if ov:
+        if _prefill_needs_coarse_new(hierarchy, level, t, substep, _snap(ctx)):
+            _wait_level(ctx, level - 1)
+        elif device.PARAMS is not None and level >= 2 and _plan(hierarchy, level).coarse_all.n:
+            # the replayed weight of this fill must stay 0 (SweepGraph checks it per pair)
+            ctx._skip_slots.append(len(device.PARAMS.vals))
     pre = fill_level_ghosts(hierarchy, level, t, ctx, defer=True, substep=substep)
-    fused = step_level(hierarchy, level, dt, ctx, prefill=pre, restrict_into=restrict_into)
-    t_new = t + dt
-    st = patches[0]._store
-    st.set_level_times(t_new, t)
-    if ctx.on_level_advanced is not None:
-        ctx.on_level_advanced(hierarchy, level, t_new)
-    ctx.step_counts[level] = count + 1
-    if level < hierarchy.max_levels and hierarchy.patches(level + 1):
-        fill_level_ghosts(hierarchy, level, t_new, ctx)
+    children = level < hierarchy.max_levels and bool(hierarchy.patches(level + 1))
+    side = None
+    if ov and children and level <= _OVERLAP_MAX_LEVEL:
+        import torch
+        side = ctx._level_streams.get(level)
+        if side is None:
+            side = ctx._level_streams[level] = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        side_ctx = torch.cuda.stream(side)
+        side_ctx.__enter__()
+    elif ov and restrict_into:
+        _wait_level(ctx, level - 1)            # a fused restriction writes the coarse new state
+    try:
+        fused = step_level(hierarchy, level, dt, ctx, prefill=pre, restrict_into=restrict_into)
+        t_new = t + dt
+        st = patches[0]._store
+        st.set_level_times(t_new, t)
+        if ctx.on_level_advanced is not None:
+            ctx.on_level_advanced(hierarchy, level, t_new)
+        ctx.step_counts[level] = count + 1
+        if children:
+            if side is not None:
+                _wait_level(ctx, level - 1)    # the post-step fill reads the coarse new state
+            fill_level_ghosts(hierarchy, level, t_new, ctx)
+            if side is not None:
+                import torch
+                ev = torch.cuda.Event()
+                ev.record(side)
+                ctx._level_events[level] = ev
+    finally:
+        if side is not None:
+            side_ctx.__exit__(None, None, None)
+    if children:
         ratio = hierarchy.ratio_to_finer(level)
         done = False
         for k in range(ratio):
             done = _advance(hierarchy, level + 1, dt / ratio, ctx, restrict_into=k == ratio - 1, substep=k)
+        if ov:
+            _wait_level(ctx, level)
+            _wait_level(ctx, level + 1)        # the restriction reads the finer level's last step
         if not done:
             restrict_fine_to_coarse(hierarchy, level)
     return fused
@@ -1251,7 +1342,12 @@ class SweepGraph:
     cell counters, buffer roles) is kept exact by re-running the orchestration
     in shadow mode (device.SHADOW: nothing is launched) before every replay.
     Only valid on the static-CFL fast path (fast variant, 2D, no dry cells)
-    and while no regrid is due; ``advance`` checks both."""
+    and while no regrid is due; ``advance`` checks both.
+
+    With USE_LEVEL_OVERLAP the capture puts each parent level's step and
+    post-step fill on a side stream: they run concurrently with the first
+    substep of the finer level (which reads the parent's saved state only),
+    and the graph's edges are exactly the sweep's data dependencies."""
 
     def __init__(self, hierarchy: PatchHierarchy, dt: float, ctx: AmrContext):
         import torch
@@ -1267,30 +1363,58 @@ class SweepGraph:
             for i in range(st.NBUF):
                 st._ensure_buf(i)
         torch.cuda.synchronize()
-        before = self._roles()
+        self._levels = [lev for lev in range(1, hierarchy.num_levels() + 1) if hierarchy.patches(lev)]
+        self._stores = {lev: _plan(hierarchy, lev).st for lev in self._levels}
         self.params = device.ParamSlots()
-        self.graph = torch.cuda.CUDAGraph()
-        ctx._defer_checks = True
-        device.PARAMS = self.params
-        try:
-            with torch.cuda.graph(self.graph):
-                for _ in range(2):
-                    advance_hierarchy(hierarchy, 1, dt, ctx)
-        finally:
-            ctx._defer_checks = False
-            device.PARAMS = None
-        self.params.upload()
-        if self._roles() != before:
-            raise RuntimeError("level sweep is not 2-periodic; cannot replay")
-        self.graph.replay()                     # the device catches up with the captured steps
+        # the overlapped capture (parent steps on side streams); when some first-substep fill of
+        # it skipped the wait for its coarse level, also a sequential one, replayed for a pair
+        # whose weight at such a fill is not 0
+        self.graph, self.skip_slots = self._capture(USE_LEVEL_OVERLAP)
+        self.graph_seq = None
+        if self.skip_slots:                     # captured, not run: the bookkeeping is restored
+            book = self._book()
+            self.graph_seq = self._capture(False, replay=False)[0]
+            self._restore(book)
+        self.seq_replays = 0
         # lite shadow: the host bookkeeping of a pair (level times, counters,
         # time-weight slots) without the orchestration; trusted only after it
         # reproduced a full shadow pair exactly (_shadow_pair)
         self.lite_ok = None
-        self._levels = [lev for lev in range(1, hierarchy.num_levels() + 1) if hierarchy.patches(lev)]
-        self._stores = {lev: _plan(hierarchy, lev).st for lev in self._levels}
         self._coarse_in = {lev: lev >= 2 and bool(_plan(hierarchy, lev).coarse_all.n) for lev in self._levels}
         self._fused_per_pair = None
+
+    def _capture(self, overlap, replay=True):
+        """Capture two coarse steps, then replay them once (the device catches
+        up with the captured steps' bookkeeping); returns (graph, slots whose
+        weight must be -1 for a replay)."""
+        import torch
+        h, ctx = self.h, self.ctx
+        before = self._roles()
+        graph = torch.cuda.CUDAGraph()
+        self.params.rewind()
+        ctx._defer_checks = True
+        ctx._overlap = overlap
+        ctx._skip_slots = []
+        ctx.__dict__.setdefault("_level_streams", {})
+        for lev in range(1, h.num_levels() + 1):   # side streams exist before the capture
+            ctx._level_streams.setdefault(lev, torch.cuda.Stream())
+        device.PARAMS = self.params
+        try:
+            with torch.cuda.graph(graph):
+                for _ in range(2):
+                    advance_hierarchy(h, 1, self.dt, ctx)
+        finally:
+            ctx._defer_checks = False
+            ctx._overlap = False
+            device.PARAMS = None
+        skip = list(ctx._skip_slots)
+        ctx._skip_slots = []
+        self.params.upload()
+        if self._roles() != before:
+            raise RuntimeError("level sweep is not 2-periodic; cannot replay")
+        if replay:
+            graph.replay()
+        return graph, skip
 
     def _book(self):
         ctx = self.ctx
@@ -1315,7 +1439,7 @@ class SweepGraph:
 
         def fill(lev, t):
             if self._coarse_in.get(lev):
-                mode, w = _store_time_mode(st_of[lev - 1], t)
+                mode, w = _store_time_mode(st_of[lev - 1], t, _snap(ctx))
                 vals.append(w if mode == 1 else -1.0)
 
         def adv(lev, dt):
@@ -1410,6 +1534,10 @@ class SweepGraph:
         for _ in range(coarse_steps // 2):
             self._shadow_pair()
             self.params.upload()
-            self.graph.replay()
+            g = self.graph
+            if self.graph_seq is not None and any(self.params.vals[i] != -1.0 for i in self.skip_slots):
+                g = self.graph_seq
+                self.seq_replays += 1
+            g.replay()
         self.ctx._bad_pending = True
         _raise_pending(self.ctx)

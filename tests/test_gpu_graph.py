@@ -67,3 +67,36 @@ def test_sweep_graph_lite_shadow_matches_eager():
         for pa, pb in zip(ha.patches(lev), hb.patches(lev)):
             assert pa.time == pb.time and pa.time_old == pb.time_old
             assert np.array_equal(pa.interior(), pb.interior())
+
+
+def test_sweep_graph_overlap_used():
+    """The captured sweep overlaps parent steps with the first substep of the
+    finer level (side streams); with the FAST weight snap every replayed
+    pair may use it."""
+    from paper_1511_03645_b200 import _lib, amr
+    if not amr.USE_LEVEL_OVERLAP:
+        pytest.skip("level overlap disabled (ADJAMR_LEVEL_OVERLAP=0)")
+    hb, cb, dt = small_hierarchy(_lib.VARIANT_FAST)
+    g = amr.SweepGraph(hb, dt, cb)
+    g.advance(8)
+    assert g.skip_slots and g.graph_seq is not None
+    assert g.seq_replays == 0
+
+
+def test_sweep_graph_sequential_fallback(monkeypatch):
+    """Without the weight snap, first-substep weights pick up the level
+    clocks' rounding drift; pairs with such a weight replay the sequential
+    capture, and the result still equals the eager sweep bitwise."""
+    from paper_1511_03645_b200 import _lib, amr
+    monkeypatch.setattr(amr, "SNAP_W", 0.0)
+    ha, ca, dt = small_hierarchy(_lib.VARIANT_FAST)
+    hb, cb, _ = small_hierarchy(_lib.VARIANT_FAST)
+    for _ in range(4 + 20):
+        amr.advance_hierarchy(ha, 1, dt, ca)
+    g = amr.SweepGraph(hb, dt, cb)
+    g.advance(20)
+    assert ca.cell_steps == cb.cell_steps and ca.step_counts == cb.step_counts
+    for lev in (1, 2, 3):
+        for pa, pb in zip(ha.patches(lev), hb.patches(lev)):
+            assert pa.time == pb.time and pa.time_old == pb.time_old
+            assert np.array_equal(pa.interior(), pb.interior())
