@@ -1242,7 +1242,10 @@ _OVERLAP_MAX_LEVEL = int(os.environ.get("ADJAMR_OVERLAP_MAX_LEVEL", "99"))   # e
 
 
 def _overlap_on(ctx) -> bool:
-    return bool(ctx.__dict__.get("_overlap")) and not device.SHADOW and ctx.on_level_advanced is None
+    # the in-launch fills (opt-in) read the coarse level's new state from the fine level's step
+    # launch, cached interval values included: they keep the sequential capture
+    return (bool(ctx.__dict__.get("_overlap")) and not device.SHADOW and ctx.on_level_advanced is None
+            and not USE_JOB_FILL and not USE_FUSED_FILL)
 
 
 def _wait_level(ctx, level):
