@@ -41,6 +41,9 @@
 #define K1_STATIC_FIRST 1     // each warp's first job = its index, its job-table entry loaded before
                               // the PDL wait; 0: every job from the queue
 #endif
+#ifndef K1_MARCH_UNROLL_SWE
+#define K1_MARCH_UNROLL_SWE 2   // march loop unroll factor (groups of three columns) on shallow water
+#endif
 #ifndef K1_PREFETCH_CLAMP
 #define K1_PREFETCH_CLAMP 1   // 1: branch-free prefetch (re-read the last column)
 #endif
@@ -518,6 +521,7 @@ template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool
 struct Strip {
     static constexpr bool SWE = SYS == ADJ_SYS_SWE2D;
     static constexpr bool FWD_WAVE = FORM == ADJ_FORM_WAVE && !REV;
+    static constexpr int MARCH_UNROLL = SWE && !WD ? K1_MARCH_UNROLL_SWE : 1;
     const double* __restrict__ qin;
     const double* __restrict__ aux;
     double* __restrict__ qout;
@@ -801,7 +805,9 @@ struct Strip {
         // columns beyond s_last (at most two, rounding the march to whole
         // rotations) compute on stale registers and write nothing
         int base = 0;
-#pragma unroll 1
+        // shallow water: six columns per loop body (fewer loop-carried register moves, 253 -> 244
+        // instructions per column; C4 K1 0.2127 -> 0.2110 ms); acoustics measured neutral-to-slower
+#pragma unroll(MARCH_UNROLL)
         for (int s = s_first; s <= s_last; s += 3) {
             // one wait per group of three columns, then the columns 3*GROUPS
             // ahead go to the group after the in-flight ones (with K1_LDSNB the

@@ -311,8 +311,11 @@ ADJ_D double interp_at(const double* p, int di, int dj, double wx, double wy) {
     return p[0] * (1.0 - wx) + p[di] * wx;
 }
 
+#ifndef K2_GATHER_MINB
+#define K2_GATHER_MINB 1   // resident CTAs per SM the gather's register budget targets (experiments)
+#endif
 template <int NDIM, int M, int U>
-__global__ void __launch_bounds__(256) k2_gather(AdjGhostPlanFillArgs a) {
+__global__ void __launch_bounds__(256, K2_GATHER_MINB) k2_gather(AdjGhostPlanFillArgs a) {
     pdl_wait();
     pdl_trigger();
     double wt = a.w_time;

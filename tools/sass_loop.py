@@ -1,4 +1,5 @@
-"""Instruction mix per column of K1's inner march loop (the longest backward branch body / 3)."""
+"""Instruction mix per column of K1's inner march loop (the backward-branch body with the
+cp.async prefetches; three columns per cp.async wait, so columns = 3 x its DEPBAR count)."""
 import collections, re, subprocess, sys
 lib, pat = sys.argv[1], sys.argv[2]
 out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
@@ -20,11 +21,13 @@ def body_of(l):
 cands = [l for l in loops if any("LDGSTS" in t for t in body_of(l)) and not any("WARPSYNC" in t for t in body_of(l))]
 lo, hi = min(cands, key=lambda l: l[1] - l[0])
 loop = [t for a, t in ins if lo <= a <= hi]
+ncol = 3 * max(1, sum(1 for t in loop if t.startswith("DEPBAR")))
 ops = collections.Counter(re.sub(r"^@!?U?P\w+\s+", "", t).split()[0] for t in loop)
 base = collections.Counter()
 for k, v in ops.items():
     base[k.split(".")[0] if not k.startswith("IMAD.MOV") else "IMAD.MOV"] += v
 fp64 = sum(base[k] for k in ("DADD", "DMUL", "DFMA", "DSETP"))
 loc = sum(v for k, v in ops.items() if k.startswith(("LDL", "STL")))
-print(f"loop {hex(lo)}-{hex(hi)}: {len(loop) / 3:.1f} instr/column, FP64 {fp64 / 3:.1f}/column, local ld/st {loc}")
-print(", ".join(f"{k} {v / 3:.1f}" for k, v in base.most_common(16)))
+print(f"loop {hex(lo)}-{hex(hi)} ({ncol} columns): {len(loop) / ncol:.1f} instr/column, FP64 {fp64 / ncol:.1f}/column, "
+      f"local ld/st {loc}")
+print(", ".join(f"{k} {v / ncol:.1f}" for k, v in base.most_common(16)))
