@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define ADJ_ABI_VERSION 6
+#define ADJ_ABI_VERSION 7
 
 /* status codes (mapped to the reference's exception classes by the host) */
 #define ADJ_OK                 0
@@ -244,6 +244,7 @@ typedef struct AdjStepArgs {
     const int8_t* job_class;   /* optional with ADJ_STEP_WET_DRY (device, njob or ntile): 0 every cell of
                                   the job's strip windows wet (the all-wet march), 1 mixed (the wet/dry
                                   march), 2 every output cell dry (outputs copied: dq *= wet)              */
+    double uniform_c, uniform_z;/* ADJ_STEP_UNIFORM_MAT: the aux planes' (c, z) of every cell, ghosts included */
 } AdjStepArgs;
 /* AdjStepArgs.flags */
 #define ADJ_STEP_KEEP_NONFINITE 1   /* do not zero nonfinite: accumulate over launches */
@@ -267,6 +268,12 @@ typedef struct AdjStepArgs {
                                        their state (_swe_effective_states / _swe_transverse_material /
                                        dq *= wet, solver.py:357-387, 500-505); without this flag a FAST
                                        step assumes every cell wet */
+#define ADJ_STEP_UNIFORM_MAT   64   /* hint, FAST 2D acoustics (forward wave form, static CFL bound): every
+                                       cell of aux (ghosts included) holds c = uniform_c, z = uniform_z, so
+                                       the material terms of the march (sample_patch_material's arrays,
+                                       solver.py:180-205, as the Riemann and transverse solvers use them) are
+                                       computed once per strip instead of per cell -- same operations on the
+                                       same values; other configurations ignore the flag and read aux */
 int adj_step_level(const AdjStepArgs* a);
 
 /* Tile shape (ni, nj) the given variant expects in AdjStepArgs.tiles. */

@@ -26,6 +26,7 @@ BC_CODES = {"wall": BC_WALL, "outflow": BC_OUTFLOW, "periodic": BC_PERIODIC}
 RECT_COPY, RECT_COARSE = 0, 1
 STEP_KEEP_NONFINITE, STEP_NO_SPEED_OUT, STEP_TWO_ROWS, STEP_COUNTER_ZERO, STEP_PHYS_IN = 1, 2, 4, 8, 16
 STEP_WET_DRY = 32
+STEP_UNIFORM_MAT = 64
 
 
 class NativeUnavailableError(RuntimeError):
@@ -91,7 +92,8 @@ class AdjStepArgs(C.Structure):
                 ("variant", I32), ("flags", I32),
                 ("dt", D), ("dtdx", D), ("dtdy", D), ("gravity", D), ("stream", P), ("prefill", AdjGhostPlanFillArgs),
                 ("fine_restrict", AdjStepRestrict), ("job_fill", AdjJobFill),
-                ("phys_bc", I32 * 4), ("phys_normal", I32 * 2), ("job_class", P)]
+                ("phys_bc", I32 * 4), ("phys_normal", I32 * 2), ("job_class", P),
+                ("uniform_c", D), ("uniform_z", D)]
 
 
 class AdjPhysArgs(C.Structure):
@@ -133,7 +135,7 @@ class AdjFlagArgs(C.Structure):
                 ("tolerance", D), ("envelope", P), ("work", P), ("stream", P)]
 
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 FLAG_ROWS = 1        # AdjFlagArgs.layout: ADJ_FLAG_ROWS
 FLAG_PAIRS = 2       # AdjFlagArgs.layout: ADJ_FLAG_PAIRS
 FLAG_QUADS = 4       # AdjFlagArgs.layout: ADJ_FLAG_QUADS

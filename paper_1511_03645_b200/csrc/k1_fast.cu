@@ -28,6 +28,9 @@
 #ifndef K1_MIN_BLOCKS
 #define K1_MIN_BLOCKS 3   // CTAs of 128 threads per SM the register budget targets
 #endif
+#ifndef K1_MIN_BLOCKS_HM
+#define K1_MIN_BLOCKS_HM 3   // the same for the homogeneous-material instantiation (140 registers)
+#endif
 #ifndef K1_WARPS
 #define K1_WARPS 4        // warps per CTA of the single-row kernel
 #endif
@@ -517,7 +520,13 @@ constexpr int RING1 = 3 * NGRP;
 // lives in a 3-slot ring indexed by (column mod 3); column<K> is the body of
 // the march for a column in slot K, so the 3-way unrolled loop rotates roles
 // by renaming instead of moving registers.
-template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool SQ = false, bool WD = false>
+// HM: homogeneous material (ADJ_STEP_UNIFORM_MAT) -- every cell of the level has the material
+// (uniform_c, uniform_z), so the per-cell material quantities, the face and transverse
+// reciprocals and 1 + mL mR are loop invariants of the march (computed once per strip by the same
+// functions on the same values: bitwise equal to the per-cell form), no material plane is
+// loaded and no material crosses lanes.
+template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool SQ = false, bool WD = false,
+          bool HM = false>
 struct Strip {
     static constexpr bool SWE = SYS == ADJ_SYS_SWE2D;
     static constexpr bool FWD_WAVE = FORM == ADJ_FORM_WAVE && !REV;
@@ -533,6 +542,7 @@ struct Strip {
     double* ring;                  // this warp's cp.async ring: [RING1][NARR][32]
     int lane, lup, ldn;            // lane, and the lanes of rows j+1, j-1 (clamped like the shuffles)
     Mat m[3];
+    Mat mh;                        // HM: the level's material
     double q0[3], q1[3], q2[3];
     Face xf[3];                    // xf[k]: x-face left of column k
     double sy0[3], sy2[3];         // Sy(column)
@@ -557,7 +567,7 @@ struct Strip {
     int rr, rx0, rbase, rnyb, rby;  // ratio, strip x origin, patch block base, blocks per row, block row
     bool rlead;                     // first row of an output block
 
-    static constexpr int NARR = SWE ? 4 : 5;
+    static constexpr int NARR = HM ? 3 : (SWE ? 4 : 5);
 
     // issue the cp.async copies of column s into ring slot `slot`
     ADJ_D void prefetch(int s, int slot) const {
@@ -583,8 +593,9 @@ struct Strip {
     ADJ_D Raw read(int slot) const {
         const double* r = ring + slot * NARR * 32 + lane;
         Raw v;
-        v.q0 = r[0]; v.q1 = r[32]; v.q2 = r[64]; v.c = r[96];
-        v.z = SWE ? 0.0 : r[128];
+        v.q0 = r[0]; v.q1 = r[32]; v.q2 = r[64];
+        if (HM) { v.c = mh.c; v.z = mh.m; }
+        else { v.c = r[96]; v.z = SWE ? 0.0 : r[128]; }
         return v;
     }
 
@@ -593,7 +604,7 @@ struct Strip {
     template <int K>
     ADJ_D void column(int s, const Raw& cr, const double* up, const double* dn) {
         constexpr int C = K, P = (K + 2) % 3, PP = (K + 1) % 3;
-        m[C] = make_mat<SYS, FORM, LIM, SQ>(cr.c, cr.z, dtdx, dtdy);
+        if (!HM) m[C] = make_mat<SYS, FORM, LIM, SQ>(cr.c, cr.z, dtdx, dtdy);   // HM: m[] = mh throughout
         if (WD) {
             wet[C] = __double2hiint(cr.c) > 0;   // c >= 0: c > 0 <=> its high word is positive
             tcv[C] = wet[C] ? cr.c : sqrtg;
@@ -616,13 +627,17 @@ struct Strip {
         const double uq0 = K1_LDSNB ? up[0] : sh_dn(cr.q0);
         const double uq2 = K1_LDSNB ? up[64] : sh_dn(cr.q2);
         Mat mu{};
-        mu.c = K1_LDSNB ? up[96] : sh_dn(m[C].c);
-        mu.m = SWE ? mu.c : (K1_LDSNB ? up[128] : sh_dn(m[C].m));
-        mu.k1 = K1_SHFL_K1 ? sh_dn(m[C].k1) : fma(mu.m, mu.m, 1.0);
-        mu.ky = sh_dn(m[C].ky);
-        mu.kx = 0.0;
-        mu.tr = SWE ? mu.c * mu.c : mu.c * mu.m;
-        mu.fx = FORM == ADJ_FORM_FWAVE ? sh_dn(m[C].fx) : 0.0;
+        if (HM) {
+            mu = mh;
+        } else {
+            mu.c = K1_LDSNB ? up[96] : sh_dn(m[C].c);
+            mu.m = SWE ? mu.c : (K1_LDSNB ? up[128] : sh_dn(m[C].m));
+            mu.k1 = K1_SHFL_K1 ? sh_dn(m[C].k1) : fma(mu.m, mu.m, 1.0);
+            mu.ky = sh_dn(m[C].ky);
+            mu.kx = 0.0;
+            mu.tr = SWE ? mu.c * mu.c : mu.c * mu.m;
+            mu.fx = FORM == ADJ_FORM_FWAVE ? sh_dn(m[C].fx) : 0.0;
+        }
         const bool wu = WD ? __double2hiint(mu.c) > 0 : true;
         const Face yf = WD ? solve_face_wd<SYS, FORM, REV>(cr.q0, cr.q2, uq0, uq2, m[C].c, mu.c, wet[C], wu)
                            : solve_face<SYS, FORM, REV>(cr.q0, cr.q2, uq0, uq2, m[C], mu);
@@ -659,13 +674,16 @@ struct Strip {
             sx1[P] = xf[P].ap1 + xf[C].am1;
         }
         {
-            Mat mb{};
-            mb.c = WD ? sh_up(tcv[P]) : (K1_LDSNB ? dn[96] : sh_up(m[P].c));
-            mb.m = SWE ? mb.c : (K1_LDSNB ? dn[128] : sh_up(m[P].m));
-            mb.tr = SWE ? mb.c * mb.c : mb.c * mb.m;
-            Mat ma{};
-            ma.c = cup[P]; ma.m = mup[P];
-            ma.tr = SWE ? ma.c * ma.c : ma.c * ma.m;
+            Mat mb{}, ma{};
+            if (HM) {
+                mb = mh; ma = mh;
+            } else {
+                mb.c = WD ? sh_up(tcv[P]) : (K1_LDSNB ? dn[96] : sh_up(m[P].c));
+                mb.m = SWE ? mb.c : (K1_LDSNB ? dn[128] : sh_up(m[P].m));
+                mb.tr = SWE ? mb.c * mb.c : mb.c * mb.m;
+                ma.c = cup[P]; ma.m = mup[P];
+                ma.tr = SWE ? ma.c * ma.c : ma.c * ma.m;
+            }
             double nbm0, bmv, bp0, bpv;
             transverse<SYS, FORM, REV>(sx0[P], hx, mb, ma, nbm0, bmv, bp0, bpv);
             gt0[P] = cy0[P] - (bp0 - sh_dn(nbm0));
@@ -771,6 +789,7 @@ struct Strip {
         dtdx = a.dtdx; dtdy = a.dtdy;
         hx = 0.5 * dtdx; hy = 0.5 * dtdy;
         sqrtg = WD ? sqrt(a.gravity) : 0.0;
+        if (HM) mh = make_mat<SYS, FORM, LIM, SQ>(a.uniform_c, a.uniform_z, dtdx, dtdy);
         colbase = g + T.i0;
         i0 = 0; ni = T.ni;
         if (RST) {
@@ -796,7 +815,7 @@ struct Strip {
         }
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            m[k] = Mat{}; xf[k] = Face{};
+            m[k] = HM ? mh : Mat{}; xf[k] = Face{};
             q0[k] = q1[k] = q2[k] = 0.0;
             sy0[k] = sy2[k] = gt0[k] = gt2[k] = cy0[k] = cy2[k] = 0.0;
             bpy0[k] = bpy1[k] = ft0[k] = ft1[k] = sx0[k] = sx1[k] = cup[k] = mup[k] = 0.0;
@@ -930,15 +949,15 @@ ADJ_D void phys_prefill(const AdjStepArgs& a, const AdjTile& T, const AdjPatch& 
 }
 
 template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false, bool SQ = false,
-          bool WD = false>
+          bool WD = false, bool HM = false>
 #ifdef K1_MAXREG
 __global__ void __maxnreg__(K1_MAXREG) k1_fast(AdjStepArgs a) {
 #else
-__global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepArgs a) {
+__global__ void __launch_bounds__(32 * K1_WARPS, HM ? K1_MIN_BLOCKS_HM : K1_MIN_BLOCKS) k1_fast(AdjStepArgs a) {
 #endif
     const int lane = threadIdx.x & 31;
     __shared__ int s_tile[K1_WARPS];
-    constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD>::NARR;
+    constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, HM>::NARR;
     extern __shared__ __align__(16) double s_ring1[];   // [K1_WARPS][RING1 * NARR * 32]
     const int warp = threadIdx.x >> 5;
     const int njob = a.job_offsets ? a.njob : a.ntile;
@@ -1008,7 +1027,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, K1_MIN_BLOCKS) k1_fast(AdjStepA
                 continue;
             }
         }
-        Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD> S;
+        Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, HM> S;
         S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
         S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32);
         S.run();
@@ -1296,15 +1315,16 @@ static void launch_two_rows(const AdjStepArgs& a, cudaStream_t st) {
 }
 
 template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool PFILL = false, bool SQ = false,
-          bool WD = false>
+          bool WD = false, bool HM = false>
 static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     static int blocks_per_sm = 0, sms = 0;
-    constexpr int smem = K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD>::NARR * 32 * (int)sizeof(double);
+    constexpr int smem =
+        K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, HM>::NARR * 32 * (int)sizeof(double);
     if (blocks_per_sm == 0) {
-        cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ, WD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ, WD>,
-                                                      32 * K1_WARPS, smem);
+        cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ, WD, HM>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &blocks_per_sm, k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ, WD, HM>, 32 * K1_WARPS, smem);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1313,7 +1333,7 @@ static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     int blocks = blocks_per_sm * sms;
     const int need = ((a.job_offsets ? a.njob : a.ntile) + K1_WARPS - 1) / K1_WARPS;
     if (blocks > need) blocks = need;
-    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ, WD>, dim3(blocks), dim3(32 * K1_WARPS), smem, st, a);
+    launch_pdl(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ, WD, HM>, dim3(blocks), dim3(32 * K1_WARPS), smem, st, a);
 }
 
 // Square cells (dt/dx == dt/dy, every BASELINE configuration) share the x and
@@ -1321,6 +1341,14 @@ static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
 // kernels for the MC limiter drops their recomputation.
 template <int SYS, int FORM, bool REV, int LIM, bool SQ>
 static void launch_static(const AdjStepArgs& a, cudaStream_t st) {
+    if constexpr (SYS == ADJ_SYS_AC2D && FORM == ADJ_FORM_WAVE && !REV) {   // homogeneous acoustics levels
+        if (a.flags & ADJ_STEP_UNIFORM_MAT) {
+            if (a.fine_restrict.ratio > 0) launch_cfl<SYS, FORM, REV, LIM, false, true, false, SQ, false, true>(a, st);
+            else if (a.flags & ADJ_STEP_PHYS_IN) launch_cfl<SYS, FORM, REV, LIM, false, false, true, SQ, false, true>(a, st);
+            else launch_cfl<SYS, FORM, REV, LIM, false, false, false, SQ, false, true>(a, st);
+            return;
+        }
+    }
     if constexpr (FORM == ADJ_FORM_WAVE && !REV) {   // forward levels: optional fused restriction
         if (a.fine_restrict.ratio > 0) {
             launch_cfl<SYS, FORM, REV, LIM, false, true, false, SQ>(a, st);

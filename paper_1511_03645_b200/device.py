@@ -89,6 +89,11 @@ def _ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
 
+# K1's homogeneous-material instantiation on levels whose aux planes are constant (False: always
+# read the planes; same results bitwise)
+USE_UNIFORM_MAT = os.environ.get("ADJAMR_UNIFORM_MAT", "1") == "1"
+
+
 class LevelStore:
     """All patches of one refinement level, resident in HBM."""
 
@@ -187,6 +192,26 @@ class LevelStore:
             self.aux.view(self.naux, self.plane)[:, dst] = torch.from_numpy(src).to("cuda")
         for k, p in enumerate(patches):
             self._attach(p, k, upload=False)
+        self.uniform_mat = self._uniform_material(patches)
+
+    @staticmethod
+    def _uniform_material(patches):
+        """(c, z) when every cell of every patch (ghosts included) has the same
+        acoustic material, else None: K1's homogeneous-material instantiation
+        (ADJ_STEP_UNIFORM_MAT) then computes the material terms once per strip."""
+        if not USE_UNIFORM_MAT or hasattr(patches[0].aux, "wet") or patches[0].spec.ndim != 2:
+            return None
+        c0 = z0 = None
+        for p in patches:
+            c, z = p.aux.planes()[:2]
+            c, z = np.asarray(c), np.asarray(z)
+            if c0 is None:
+                c0, z0 = float(c.flat[0]), float(z.flat[0])
+                if not (np.isfinite(c0) and np.isfinite(z0) and c0 > 0.0 and z0 > 0.0):
+                    return None
+            if c.min() != c0 or c.max() != c0 or z.min() != z0 or z.max() != z0:
+                return None
+        return c0, z0
 
     # ------------------------------------------------------------------ views
     def _view(self, t, slot, comps):
@@ -1188,6 +1213,9 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
         a.flags |= _lib.STEP_COUNTER_ZERO
         if store.two_rows():
             a.flags |= _lib.STEP_TWO_ROWS
+        if store.uniform_mat is not None and a.static_speed:
+            a.flags |= _lib.STEP_UNIFORM_MAT
+            a.uniform_c, a.uniform_z = store.uniform_mat
         if wet_dry:
             a.flags |= _lib.STEP_WET_DRY
             if USE_JOB_CLASS:

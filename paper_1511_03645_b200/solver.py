@@ -129,6 +129,7 @@ def sample_patch_material(patch: Patch, equation: EquationSet, boundary: Boundar
     if patch._store is not None:
         patch._store._dry = None
         patch._store._static_speed = None
+        patch._store.uniform_mat = device.LevelStore._uniform_material(patch._store.patches)
         av = patch._store.aux_view(patch._slot)
         import torch
         for k, pl in enumerate(patch.aux.planes()):
