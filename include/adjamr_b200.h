@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define ADJ_ABI_VERSION 7
+#define ADJ_ABI_VERSION 8
 
 /* status codes (mapped to the reference's exception classes by the host) */
 #define ADJ_OK                 0
@@ -245,6 +245,10 @@ typedef struct AdjStepArgs {
                                   the job's strip windows wet (the all-wet march), 1 mixed (the wet/dry
                                   march), 2 every output cell dry (outputs copied: dq *= wet)              */
     double uniform_c, uniform_z;/* ADJ_STEP_UNIFORM_MAT: the aux planes' (c, z) of every cell, ghosts included */
+    const double* job_uniform; /* optional with ADJ_STEP_UNIFORM_MAT (device, 2 per warp job or tile): the
+                                  (c, z) every cell read by the job's strips holds (rows j0-2 .. j0+nj+1,
+                                  columns i0-2 .. i0+ni+1 of each strip), or (0, 0) for a job that reads
+                                  several materials (it marches per cell); replaces uniform_c / uniform_z */
 } AdjStepArgs;
 /* AdjStepArgs.flags */
 #define ADJ_STEP_KEEP_NONFINITE 1   /* do not zero nonfinite: accumulate over launches */
@@ -273,7 +277,9 @@ typedef struct AdjStepArgs {
                                        the material terms of the march (sample_patch_material's arrays,
                                        solver.py:180-205, as the Riemann and transverse solvers use them) are
                                        computed once per strip instead of per cell -- same operations on the
-                                       same values; other configurations ignore the flag and read aux */
+                                       same values; with job_uniform the material is given per warp job
+                                       (piecewise-constant media: jobs away from the interfaces); other
+                                       configurations ignore the flag and read aux */
 int adj_step_level(const AdjStepArgs* a);
 
 /* Tile shape (ni, nj) the given variant expects in AdjStepArgs.tiles. */

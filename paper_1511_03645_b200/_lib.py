@@ -93,7 +93,7 @@ class AdjStepArgs(C.Structure):
                 ("dt", D), ("dtdx", D), ("dtdy", D), ("gravity", D), ("stream", P), ("prefill", AdjGhostPlanFillArgs),
                 ("fine_restrict", AdjStepRestrict), ("job_fill", AdjJobFill),
                 ("phys_bc", I32 * 4), ("phys_normal", I32 * 2), ("job_class", P),
-                ("uniform_c", D), ("uniform_z", D)]
+                ("uniform_c", D), ("uniform_z", D), ("job_uniform", P)]
 
 
 class AdjPhysArgs(C.Structure):
@@ -135,7 +135,7 @@ class AdjFlagArgs(C.Structure):
                 ("tolerance", D), ("envelope", P), ("work", P), ("stream", P)]
 
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 FLAG_ROWS = 1        # AdjFlagArgs.layout: ADJ_FLAG_ROWS
 FLAG_PAIRS = 2       # AdjFlagArgs.layout: ADJ_FLAG_PAIRS
 FLAG_QUADS = 4       # AdjFlagArgs.layout: ADJ_FLAG_QUADS

@@ -324,7 +324,7 @@ ADJ_D double limab2(double A, double B) {
         r = m + m;
     } else if (LIM == ADJ_LIM_MC) {
         const double m4 = pow2x<2, ALG>(fabs(A) < fabs(B) ? A : B);
-        const double S = A + B;
+        const double S = __dadd_rn(A, B);   // A, B are products: no contraction (see correction())
         r = fabs(S) < fabs(m4) ? S : m4;
     } else {
         const double A2 = pow2x<1, ALG>(A), B2 = pow2x<1, ALG>(B);
@@ -463,21 +463,28 @@ ADJ_D void correction(const Face& f, double s0_nb, double P0_nb, double s1_nb, d
     constexpr bool SWE = SYS == ADJ_SYS_SWE2D, FW = FORM == ADJ_FORM_FWAVE;
     constexpr bool MPOS0 = (!SWE && !FW) || (SWE && FW);  // material multiplies component 0
     double p0, p1;
+    // Products that feed both a sum and another use are written with explicit roundings, so that
+    // which of them fuses into the sum (FMA contraction) is not the compiler's choice per
+    // instantiation.  (Other contractions still differ between instantiations -- e.g. the
+    // transverse products the homogeneous march shares -- so instantiations agree to rounding,
+    // not bitwise.)
     if (LIM == ADJ_LIM_NONE) {
         p0 = f.s0; p1 = f.s1;
     } else {
-        const double A0 = f.s0 * L.k1;
-        const double A1 = f.s1 * R.k1;
-        const double B0 = s0_nb * (REV ? P0_nb : f.P);
-        const double B1 = s1_nb * (REV ? P1_nb : f.P);
+        const double A0 = __dmul_rn(f.s0, L.k1);
+        const double A1 = __dmul_rn(f.s1, R.k1);
+        const double B0 = __dmul_rn(s0_nb, REV ? P0_nb : f.P);
+        const double B1 = __dmul_rn(s1_nb, REV ? P1_nb : f.P);
         p0 = limab2<LIM, K1_ALG2 && (SWE || (K1_ALG2_AC & 4))>(A0, B0);   // 1/(2(1+m^2)) folded into kL, kR
         p1 = limab2<LIM, K1_ALG2 && (SWE || (K1_ALG2_AC & 4))>(A1, B1);
     }
     // coefficients: wave 0.5|s|(1-dtd|s|) for both; f-wave sign(s) 0.5(1-dtd|s|)
-    const double u0 = (FW ? -kL : kL) * p0;
-    const double u1 = kR * p1;
-    if (MPOS0) { F0 = (SWE ? R.c * u1 - L.c * u0 : R.m * u1 - L.m * u0); Fn = u0 + u1; }
-    else { F0 = u0 + u1; Fn = (SWE ? R.c * u1 - L.c * u0 : R.m * u1 - L.m * u0); }
+    const double u0 = __dmul_rn(FW ? -kL : kL, p0);
+    const double u1 = __dmul_rn(kR, p1);
+    const double mL = SWE ? L.c : L.m, mR = SWE ? R.c : R.m;
+    const double dif = fma(mR, u1, -__dmul_rn(mL, u0)), sum = __dadd_rn(u0, u1);
+    if (MPOS0) { F0 = dif; Fn = sum; }
+    else { F0 = sum; Fn = dif; }
 }
 
 // Transverse split of an entering fluctuation (component 0 = f0; its
@@ -769,7 +776,7 @@ struct Strip {
 
     // Lane setup for a strip T placed at lanes [lane0, lane0 + nj + 4).
     ADJ_D void setup(const AdjTile& T, const AdjPatch& p, const AdjStepArgs& a, int lane_, int lane0,
-                     double* ring_) {
+                     double* ring_, double hc = 0.0, double hz = 0.0) {
         lane = lane_;
         lup = lane < 31 ? lane + 1 : 31;
         ldn = lane > 0 ? lane - 1 : 0;
@@ -789,7 +796,7 @@ struct Strip {
         dtdx = a.dtdx; dtdy = a.dtdy;
         hx = 0.5 * dtdx; hy = 0.5 * dtdy;
         sqrtg = WD ? sqrt(a.gravity) : 0.0;
-        if (HM) mh = make_mat<SYS, FORM, LIM, SQ>(a.uniform_c, a.uniform_z, dtdx, dtdy);
+        if (HM) mh = make_mat<SYS, FORM, LIM, SQ>(hc, hz, dtdx, dtdy);
         colbase = g + T.i0;
         i0 = 0; ni = T.ni;
         if (RST) {
@@ -957,7 +964,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, HM ? K1_MIN_BLOCKS_HM : K1_MIN_
 #endif
     const int lane = threadIdx.x & 31;
     __shared__ int s_tile[K1_WARPS];
-    constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, HM>::NARR;
+    constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, false>::NARR;   // HM: room for the per-cell march
     extern __shared__ __align__(16) double s_ring1[];   // [K1_WARPS][RING1 * NARR * 32]
     const int warp = threadIdx.x >> 5;
     const int njob = a.job_offsets ? a.njob : a.ntile;
@@ -1027,7 +1034,19 @@ __global__ void __launch_bounds__(32 * K1_WARPS, HM ? K1_MIN_BLOCKS_HM : K1_MIN_
                 continue;
             }
         }
-        Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, HM> S;
+        if (HM) {   // homogeneous level, or this job's strips read one material: the invariant march
+            double hc = a.uniform_c, hz = a.uniform_z;
+            if (a.job_uniform) { hc = __ldg(a.job_uniform + 2 * job); hz = __ldg(a.job_uniform + 2 * job + 1); }
+            if (hc > 0.0) {
+                Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, true> S;
+                S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
+                S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32, hc, hz);
+                S.run();
+                if (S.bad) a.nonfinite[T.patch] = 1;
+                continue;
+            }
+        }
+        Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, false> S;
         S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
         S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32);
         S.run();
@@ -1319,7 +1338,7 @@ template <int SYS, int FORM, bool REV, int LIM, bool CFL, bool RST = false, bool
 static void launch_cfl(const AdjStepArgs& a, cudaStream_t st) {
     static int blocks_per_sm = 0, sms = 0;
     constexpr int smem =
-        K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, HM>::NARR * 32 * (int)sizeof(double);
+        K1_WARPS * RING1 * Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, false>::NARR * 32 * (int)sizeof(double);
     if (blocks_per_sm == 0) {
         cudaFuncSetAttribute(k1_fast<SYS, FORM, REV, LIM, CFL, RST, PFILL, SQ, WD, HM>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -420,7 +420,8 @@ class LevelStore:
         wave of resident warps gets the shortest strips (a multiple of 4, for
         the fused restriction's alignment) that still fit it: all its jobs then
         run at once and fewer slots idle (C3 2048^2: 88-column strips, 1776
-        jobs; measured with 86: K1 0.068 vs 0.075 ms with 96).  Across
+        jobs; measured with 86: K1 0.068 vs 0.075 ms with 96) -- or, better
+        where possible, the shortest strips that fill two waves.  Across
         several waves the dynamic queue absorbs a partial last wave (C4:
         measured 128 best)."""
         torch = _torch()
@@ -449,6 +450,13 @@ class LevelStore:
                 score = (jobs(one) / slots) * (one / (one + 4.0))
                 if score > best_score + 1e-9:
                     best = one
+            # two full waves of strips of >= 32 columns, when the level allows them, beat the
+            # single wave (C3 2048^2: 44-column strips, 3478 jobs: K1 0.067 vs 0.070 ms, and
+            # 0.055 vs 0.063 ms with per-job materials, whose few per-cell jobs then no longer
+            # set the duration of the one wave); levels of small patches have no such choice
+            two = next((ti for ti in range(32, ti_max + 1, 4) if slots < jobs(ti) <= 2 * slots), None)
+            if two is not None:
+                best = two
         return best
 
     def two_rows(self) -> bool:
@@ -602,6 +610,47 @@ class LevelStore:
             c = tcls[offs[j]:offs[j + 1]]
             jcls[j] = 0 if (c == 0).all() else (2 if (c == 2).all() else 1)
         dev = _torch().from_numpy(jcls).to("cuda")
+        self._scratch[key] = dev
+        return dev
+
+    # per-job materials are classified on the host, one window reduction per strip: levels of
+    # many patches (AMR regrids rebuild their tables often) keep the per-cell march
+    JOB_UNIFORM_MAX_PATCHES = 16
+    JOB_UNIFORM_MIN_SHARE = 0.25
+
+    def job_uniform(self, tiles, ntile, jobs, njob):
+        """Per warp job of a FAST job table (ADJ_STEP_UNIFORM_MAT, acoustics):
+        the (c, z) of every cell the job's strips read when they all hold one
+        material, else (0, 0); None when too few jobs qualify (or the level has
+        too many patches to classify on the host).  Cached per table."""
+        if not USE_UNIFORM_MAT or self.swe or self.ndim != 2 or len(self.patches) > self.JOB_UNIFORM_MAX_PATCHES:
+            return None
+        key = ("job_uniform", _ptr(tiles), ntile, _ptr(jobs) if jobs is not None else 0, njob)
+        if key in self._scratch:
+            return self._scratch[key]
+        if _torch().cuda.is_current_stream_capturing():
+            return None           # the classification downloads the job table: not during a capture
+        rows = np.frombuffer(tiles.cpu().numpy().tobytes(), dtype=_lib.TILE_DTYPE)[:ntile]
+        offs = (jobs.cpu().numpy().astype(np.int64) if jobs is not None
+                else np.arange(ntile + 1, dtype=np.int64))
+        cz = [(np.asarray(p.aux.planes()[0]), np.asarray(p.aux.planes()[1])) for p in self.patches]
+        g = self.g
+        tu = np.zeros((ntile, 2))
+        for t, r in enumerate(rows):
+            c, z = cz[int(r["patch"])]
+            i0, j0, ni, nj = int(r["i0"]), int(r["j0"]), int(r["ni"]), int(r["nj"])
+            cw, zw = c[i0:i0 + ni + 2 * g, j0:j0 + nj + 2 * g], z[i0:i0 + ni + 2 * g, j0:j0 + nj + 2 * g]
+            c0, z0 = float(cw.flat[0]), float(zw.flat[0])
+            if c0 > 0.0 and z0 > 0.0 and cw.min() == c0 and cw.max() == c0 and zw.min() == z0 and zw.max() == z0:
+                tu[t] = (c0, z0)
+        ju = np.zeros((len(offs) - 1, 2))
+        for j in range(len(offs) - 1):
+            u = tu[offs[j]:offs[j + 1]]
+            if u[0, 0] > 0.0 and np.all(u == u[0]):
+                ju[j] = u[0]
+        dev = None
+        if np.count_nonzero(ju[:, 0]) >= self.JOB_UNIFORM_MIN_SHARE * len(ju):
+            dev = _torch().from_numpy(np.ascontiguousarray(ju.reshape(-1))).to("cuda")
         self._scratch[key] = dev
         return dev
 
@@ -1216,6 +1265,11 @@ def launch_step(store: LevelStore, dt, equation, limiter, variant, out_buf_index
         if store.uniform_mat is not None and a.static_speed:
             a.flags |= _lib.STEP_UNIFORM_MAT
             a.uniform_c, a.uniform_z = store.uniform_mat
+        elif a.static_speed and not wet_dry and (system, form, rev) == (_lib.SYS_AC2D, _lib.FORM_WAVE, 0):
+            ju = store.job_uniform(tiles, ntile, jobs, njob)
+            if ju is not None:
+                a.flags |= _lib.STEP_UNIFORM_MAT
+                a.job_uniform = _ptr(ju)
         if wet_dry:
             a.flags |= _lib.STEP_WET_DRY
             if USE_JOB_CLASS:

@@ -100,3 +100,91 @@ def test_amr_same_with_and_without(name):
         for lev in range(1, a["nlev"] + 1):
             assert np.array_equal(a[f"L{lev}_boxes"], b[f"L{lev}_boxes"])
             assert norm_rel(a[f"L{lev}_q"], b[f"L{lev}_q"]) <= 1e-13
+
+
+def _two_layer(nx, ny, seed):
+    """BASELINE C3's medium on a small grid: K=4, rho=1 below y = 0.2 x, K=1, rho=1.5 above."""
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((3, nx + 4, ny + 4))
+    xs = (np.arange(-2, nx + 2) + 0.5) / nx
+    ys = (np.arange(-2, ny + 2) + 0.5) / ny
+    X, Y = np.meshgrid(xs, ys, indexing="ij")
+    low = Y < 0.2 * X
+    bulk = np.where(low, 4.0, 1.0)
+    rho = np.where(low, 1.0, 1.5)
+    c = np.sqrt(bulk / rho)
+    aux = np.stack([c, rho * c, rho, bulk])
+    eq = make_equation("ac2d")
+    h, p = patch_from_arrays(q, aux, False, 1.0 / nx, 1.0 / ny)
+    return h, p, eq, q, aux
+
+
+@pytest.mark.parametrize("shape", [(300, 200), (140, 90)])
+def test_per_job_material_on_a_two_layer_medium(shape):
+    """Piecewise-constant medium: jobs whose strips read one material march
+    with it as an invariant, the jobs crossing the interface per cell; equal to
+    the all-per-cell run at 1e-13 and to the oracle at the FAST tolerance."""
+    from paper_1511_03645_b200 import _lib, device, solver
+    nx, ny = shape
+    outs = []
+    for on in (True, False):
+        old = device.USE_UNIFORM_MAT
+        device.USE_UNIFORM_MAT = on
+        try:
+            h, p, eq, q, aux = _two_layer(nx, ny, 4)
+            st = solver.store_of(p)
+            assert st.uniform_mat is None
+            tiles, ntile, jobs, njob = st.tiles(_lib.VARIANT_FAST)
+            ju = st.job_uniform(tiles, ntile, jobs, njob)
+            if on:
+                ju = ju.cpu().numpy().reshape(-1, 2)
+                mats = {tuple(r) for r in ju.tolist()}
+                assert (0.0, 0.0) in mats and len(mats) >= 2      # mixed jobs and single-material jobs
+                assert mats <= {(0.0, 0.0), (2.0, 2.0), (float(aux[0].min()), float(aux[1].min()))}
+            else:
+                assert ju is None
+            dt = 0.4 * min(p.spec.dx, p.spec.dy) / 2.0
+            solver.step_patch(p, dt, eq, "MC", variant=_lib.VARIANT_FAST)
+            outs.append(np.array(p.state, copy=True))
+        finally:
+            device.USE_UNIFORM_MAT = old
+    assert norm_rel(outs[0], outs[1]) <= 1e-13
+    want, _ = O.step_2d(q, aux, dt, 1.0 / nx, 1.0 / ny, O.AC2D, False, False, "MC")
+    assert norm_rel(outs[0], want) <= 1e-12
+
+
+def test_per_job_material_advance_uniform():
+    """The in-launch physical fill (edge jobs first: a reordered job table) with per-job materials."""
+    from paper_1511_03645_b200 import _lib, device, solver
+    outs = []
+    for on in (True, False):
+        old = device.USE_UNIFORM_MAT
+        device.USE_UNIFORM_MAT = on
+        try:
+            h, p, eq, q, aux = _two_layer(260, 120, 6)
+            bc = solver.BoundarySpec("periodic", "periodic", "wall", "wall")
+            dt = 0.45 * min(p.spec.dx, p.spec.dy) / 2.0
+            solver.advance_uniform(p, eq, bc, (260, 120), dt, 9, "MC", _lib.VARIANT_FAST)
+            outs.append(np.array(p.state, copy=True))
+        finally:
+            device.USE_UNIFORM_MAT = old
+    assert norm_rel(outs[0], outs[1]) <= 1e-13
+
+
+def test_streamed_and_sharded_steps_with_per_job_materials():
+    """The decomposed paths (row slabs streamed from the host; x-slab shards)
+    with per-job materials agree with the whole-level step to rounding."""
+    import torch
+    from paper_1511_03645_b200 import _lib, solver
+    from tests.test_gpu_stream import _patch as stream_patch
+    sides = ("wall", "outflow", "outflow", "wall")
+    h, p, eq, bc, dt = stream_patch("ac", 301, 263, sides)
+    start = np.array(p.state, copy=True)
+    for _ in range(3):
+        solver.fill_ghost_physical(p, bc, eq, (301, 263))
+        solver.step_patch(p, dt, eq, "MC", variant=_lib.VARIANT_FAST)
+    h2, p2, eq2, bc2, _ = stream_patch("ac", 301, 263, sides)
+    host = torch.from_numpy(start.copy()).pin_memory()
+    for _ in range(3):
+        solver.step_patch_host(p2, host, dt, eq2, bc2, (301, 263), "MC", slabs=5)
+    assert norm_rel(host.numpy()[:, 2:-2, 2:-2], np.array(p.state)[:, 2:-2, 2:-2]) <= 1e-13
