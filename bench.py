@@ -121,7 +121,8 @@ C5_COARSE_STEPS = 50   # BASELINE C5: "across 50 coarse steps"
 C5_STEPS_NOTE = ("C5: 3-level acoustics hierarchy (K=4, rho=1), base 1024^2 in 1024 patches of 32^2, "
                  "ratios 2, 4; 32^2 fine patches from seed 3 covering ~40% / nested; 1 step = one coarse "
                  "step of advance_hierarchy (ghost fill + step + restriction on 11 level-steps); 50 coarse "
-                 "steps timed (CUDA-graph pairs, host bookkeeping by the verified lite shadow)")
+                 "steps timed (CUDA-graph pairs, host bookkeeping by the verified lite shadow); the "
+                 "homogeneous medium runs K1's invariant-material instantiation (ADJ_STEP_UNIFORM_MAT)")
 
 
 def c5_layout(seed=3, cover=0.40):
@@ -368,8 +369,8 @@ def k1_alone_ms(st, dt, eq, variant, launches=10, phys_in=None):
 
 def k1_traffic():
     """DRAM bytes (read + write) per K1 launch on C4 from the committed ncu
-    --set full capture (profiles/r02b_k1_traffic.json), or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02b_k1_traffic.json")
+    --set full capture (profiles/r02c_k1_traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02c_k1_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
@@ -723,6 +724,12 @@ def bench_c3(steps, variant):
     fms = a.elapsed_time(b) / 5
     return {"value": n * n / (ms * 1e-3), "unit": "cell-updates/s", "ms_per_step": ms,
             "k1_ms": k1ms, "k1_achieved_GBps": 64 * n * n / (k1ms * 1e-3) / 1e9, "bytes_per_cell_update": 64,
+            "k1_hbm_frac": 64 * n * n / (k1ms * 1e-3) / 1e9 / peaks()[0],
+            "k1_hbm_frac_48B": 48 * n * n / (k1ms * 1e-3) / 1e9 / peaks()[0],
+            "k1_note": "per-job materials (ADJ_STEP_UNIFORM_MAT): warp jobs whose strips read one layer march "
+                       "with that material as an invariant (no material plane loaded), the jobs crossing "
+                       "y = 0.2 x per cell; k1_hbm_frac keeps SURVEY 8(d)'s 64 B per cell-update (the per-cell "
+                       "form's state + material), k1_hbm_frac_48B counts only the state the invariant march moves",
             "flagging": {"value": n * n / (fms * 1e-3), "unit": "flagged cells/s", "snapshots": len(idx),
                          "cell_snapshots_per_s": n * n * len(idx) / (fms * 1e-3),
                          "achieved_GBps": (24 * n * n * (1 + len(idx)) + n * n / 8) / (fms * 1e-3) / 1e9,

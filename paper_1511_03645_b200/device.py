@@ -170,6 +170,7 @@ class LevelStore:
             cell = (np.arange(NX0)[:, None] * P0 + np.arange(NY0)[None, :]).reshape(-1)
             dst = (np.arange(self.naux)[None, :, None] * self.plane + offs[:, None, None] + cell[None, None, :])
             host_aux[dst.reshape(-1)] = stacked.reshape(-1)
+            planes_all = (stacked[:, 0], stacked[:, 1]) if self.naux >= 2 else None
         if host_aux is not None:
             self.aux.copy_(torch.from_numpy(host_aux))
         else:
@@ -180,6 +181,7 @@ class LevelStore:
             planes = [p.aux.planes() for p in patches]
             for a in range(self.naux):
                 np.concatenate([np.asarray(pl[a], dtype=float).reshape(-1) for pl in planes], out=src[a])
+            planes_all = (src[0], src[1]) if self.naux >= 2 else None
             dev = lambda v: torch.from_numpy(np.ascontiguousarray(v, dtype=np.int64)).to("cuda")
             nx_d, ny_d, off_d, pit_d = dev(NXa), dev(NYa), dev(offs), dev(pitch_a)
             nrow, ncell = int(NXa.sum()), src.shape[1]
@@ -192,7 +194,20 @@ class LevelStore:
             self.aux.view(self.naux, self.plane)[:, dst] = torch.from_numpy(src).to("cuda")
         for k, p in enumerate(patches):
             self._attach(p, k, upload=False)
-        self.uniform_mat = self._uniform_material(patches)
+        # the assembled planes of all patches: one pass each instead of reductions per patch
+        self.uniform_mat = None
+        if USE_UNIFORM_MAT and not self.swe and self.ndim == 2 and planes_all is not None:
+            self.uniform_mat = self._uniform_planes(*planes_all)
+
+    @staticmethod
+    def _uniform_planes(c, z):
+        c0, z0 = float(c.flat[0]), float(z.flat[0])
+        if not (np.isfinite(c0) and np.isfinite(z0) and c0 > 0.0 and z0 > 0.0):
+            return None
+        k = min(c.size, 4096)      # a varying medium usually shows in the first cells
+        if not (np.all(c.flat[:k] == c0) and np.all(z.flat[:k] == z0)):
+            return None
+        return (c0, z0) if np.all(c == c0) and np.all(z == z0) else None
 
     @staticmethod
     def _uniform_material(patches):
@@ -201,17 +216,14 @@ class LevelStore:
         (ADJ_STEP_UNIFORM_MAT) then computes the material terms once per strip."""
         if not USE_UNIFORM_MAT or hasattr(patches[0].aux, "wet") or patches[0].spec.ndim != 2:
             return None
-        c0 = z0 = None
+        first = None
         for p in patches:
             c, z = p.aux.planes()[:2]
-            c, z = np.asarray(c), np.asarray(z)
-            if c0 is None:
-                c0, z0 = float(c.flat[0]), float(z.flat[0])
-                if not (np.isfinite(c0) and np.isfinite(z0) and c0 > 0.0 and z0 > 0.0):
-                    return None
-            if c.min() != c0 or c.max() != c0 or z.min() != z0 or z.max() != z0:
+            u = LevelStore._uniform_planes(np.asarray(c), np.asarray(z))
+            if u is None or (first is not None and u != first):
                 return None
-        return c0, z0
+            first = u
+        return first
 
     # ------------------------------------------------------------------ views
     def _view(self, t, slot, comps):

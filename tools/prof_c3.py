@@ -11,7 +11,10 @@ ts = []
 for _ in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
     out = st._free(st.cur, -1)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(); device.launch_step(st, dt, eq, "MC", _lib.VARIANT_FAST, out); b.record()
+    a.record()
+    device.launch_step(st, dt, eq, "MC", _lib.VARIANT_FAST, out,
+                       phys_in=(bc, eq, (2048, 2048)) if "physin" in sys.argv else None)   # physin: the bench's launch
+    b.record()
     st.ghost_src = st.cur; st.cur = out
     ts.append((a, b))
 torch.cuda.synchronize()
