@@ -812,6 +812,7 @@ struct Strip {
         }
     }
 
+    template <int UNR = MARCH_UNROLL>
     ADJ_D void run() {
         const int s_first = -2;
         s_last = ni + 1;
@@ -833,7 +834,7 @@ struct Strip {
         int base = 0;
         // shallow water: six columns per loop body (fewer loop-carried register moves, 253 -> 244
         // instructions per column; C4 K1 0.2127 -> 0.2110 ms); acoustics measured neutral-to-slower
-#pragma unroll(MARCH_UNROLL)
+#pragma unroll(UNR)
         for (int s = s_first; s <= s_last; s += 3) {
             // one wait per group of three columns, then the columns 3*GROUPS
             // ahead go to the group after the in-flight ones (with K1_LDSNB the
@@ -1025,7 +1026,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, HM ? K1_MIN_BLOCKS_HM : K1_MIN_
                 Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, false> S;
                 S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
                 S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32);
-                S.run();
+                S.template run<1>();   // three columns per loop body here: the kernel also holds the wet/dry march
                 if (S.bad) a.nonfinite[T.patch] = 1;
                 continue;
             }
