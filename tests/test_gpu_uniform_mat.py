@@ -188,3 +188,71 @@ def test_streamed_and_sharded_steps_with_per_job_materials():
     for _ in range(3):
         solver.step_patch_host(p2, host, dt, eq2, bc2, (301, 263), "MC", slabs=5)
     assert norm_rel(host.numpy()[:, 2:-2, 2:-2], np.array(p.state)[:, 2:-2, 2:-2]) <= 1e-13
+
+
+def test_per_job_material_over_several_patches():
+    """A level of 32^2 patches, each with its own constant material and one
+    with a varying one: short strips of different patches share warp jobs, so a
+    packed job is single-material only when all its strips agree.  Every patch
+    equals its own oracle step and the per-cell run."""
+    from paper_1511_03645_b200 import _lib, device, solver
+    rng = np.random.default_rng(11)
+    mats = [(2.0, 2.0), (2.0, 2.0), (1.25, 1.5), (2.0, 2.0), None, (1.25, 1.5), (2.0, 2.0), (2.0, 2.0)]
+    nx = ny = 32
+    dx = dy = 1.0 / 256
+    qs, auxs = [], []
+    for m in mats:
+        qs.append(rng.standard_normal((3, nx + 4, ny + 4)))
+        if m is None:
+            rho = rng.uniform(0.8, 1.5, (nx + 4, ny + 4))
+            bulk = rng.uniform(1.0, 4.0, (nx + 4, ny + 4))
+            c = np.sqrt(bulk / rho)
+            auxs.append(np.stack([c, rho * c, rho, bulk]))
+        else:
+            c, z = m
+            auxs.append(np.stack([np.full((nx + 4, ny + 4), v) for v in (c, z, z / c, z * c)]))
+    eq = make_equation("ac2d")
+    dt = 0.4 * dx / 2.3
+    outs = []
+    for on in (True, False):
+        old = device.USE_UNIFORM_MAT
+        device.USE_UNIFORM_MAT = on
+        try:
+            ps = [patch_from_arrays(q, a, False, dx, dy, lo=(32 * k, 0))[1] for k, (q, a) in enumerate(zip(qs, auxs))]
+            st = device.LevelStore(ps)
+            assert st.uniform_mat is None
+            st.sync_in()
+            tiles, ntile, jobs, njob = st.tiles(_lib.VARIANT_FAST)
+            ju = st.job_uniform(tiles, ntile, jobs, njob)
+            if on:
+                ju = ju.cpu().numpy().reshape(-1, 2)
+                offs = jobs.cpu().numpy()
+                rows = np.frombuffer(tiles.cpu().numpy().tobytes(), dtype=_lib.TILE_DTYPE)[:ntile]
+                for j in range(njob):               # a job is single-material iff all its strips' patches agree
+                    want = {mats[int(r["patch"])] for r in rows[offs[j]:offs[j + 1]]}
+                    assert tuple(ju[j]) == (want.pop() if len(want) == 1 and None not in want else (0.0, 0.0))
+                assert any(offs[j + 1] - offs[j] > 1 and ju[j, 0] == 0.0 for j in range(njob))   # a mixed packed job
+            out = st._free(st.cur)
+            device.launch_step(st, dt, eq, "MC", _lib.VARIANT_FAST, out, accumulate=True)
+            st.cur = out
+            res = [st.view(k).cpu().numpy().copy() for k in range(len(ps))]
+            outs.append(res)
+        finally:
+            device.USE_UNIFORM_MAT = old
+    for k, (q, a) in enumerate(zip(qs, auxs)):
+        want, _ = O.step_2d(q, a, dt, dx, dy, O.AC2D, False, False, "MC")
+        got_on, got_off = outs[0][k][:, 2:-2, 2:-2], outs[1][k][:, 2:-2, 2:-2]
+        assert norm_rel(got_on, got_off) <= 1e-13
+        assert norm_rel(got_on, want[:, 2:-2, 2:-2]) <= 1e-12
+
+
+def test_job_classification_skipped_on_levels_of_many_patches():
+    from paper_1511_03645_b200 import _lib, device
+    rng = np.random.default_rng(2)
+    ps = []
+    for k in range(device.LevelStore.JOB_UNIFORM_MAX_PATCHES + 1):
+        aux = np.stack([np.full((20, 20), v) for v in ((2.0, 2.0, 1.0, 4.0) if k else (1.0, 1.0, 1.0, 1.0))])
+        ps.append(patch_from_arrays(rng.standard_normal((3, 20, 20)), aux, False, 0.1, 0.1, lo=(16 * k, 0))[1])
+    st = device.LevelStore(ps)
+    assert st.uniform_mat is None
+    assert st.job_uniform(*st.tiles(_lib.VARIANT_FAST)) is None
