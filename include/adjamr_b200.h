@@ -539,6 +539,10 @@ int adj_copy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, s
 
 int adj_abi_version(void);
 
+/* sizeof of an argument struct as this library was compiled, by name ("AdjStepArgs", ...); 0 for an
+ * unknown name.  A binding checks its own layout against it before the first call. */
+int adj_struct_size(const char* name);
+
 #ifdef __cplusplus
 }
 #endif

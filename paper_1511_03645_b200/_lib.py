@@ -166,8 +166,12 @@ class AdjFlagMaskArgs(C.Structure):
                 ("max_cells", I32), ("force_regions", C.c_uint32), ("clear_regions", C.c_uint32), ("stream", P)]
 
 
+STRUCTS = [AdjGhostPlan, AdjGhostPlanBuildArgs, AdjGhostPlanFillArgs, AdjStepRestrict, AdjJobFill, AdjStepArgs,
+           AdjPhysArgs, AdjGhostArgs, AdjRestrictArgs, AdjFlagArgs, AdjFunctionalArgs, AdjGaugeArgs, AdjFlagMaskArgs]
+
 EXPORTS = {
     "adj_abi_version": ([], C.c_int),
+    "adj_struct_size": ([C.c_char_p], C.c_int),
     "adj_copy2d_async": ([C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p],
                          C.c_int),
     "adj_last_error": ([], C.c_char_p),
@@ -209,6 +213,10 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         fn.restype = restype
     if lib.adj_abi_version() != ABI_VERSION:
         raise NativeUnavailableError("ABI version mismatch")
+    for cls in STRUCTS:        # the ctypes layouts against the compiled ones
+        if lib.adj_struct_size(cls.__name__.encode()) != C.sizeof(cls):
+            raise NativeUnavailableError(f"{cls.__name__}: ctypes layout ({C.sizeof(cls)} bytes) differs from the "
+                                         f"library's ({lib.adj_struct_size(cls.__name__.encode())})")
     _lib = lib
     return lib
 

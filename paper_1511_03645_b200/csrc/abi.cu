@@ -50,6 +50,17 @@ extern "C" {
 
 int adj_abi_version(void) { return ADJ_ABI_VERSION; }
 
+int adj_struct_size(const char* name) {
+    if (!name) return 0;
+#define ADJ_SZ(T) if (!strcmp(name, #T)) return (int)sizeof(T);
+    ADJ_SZ(AdjPatch) ADJ_SZ(AdjTile) ADJ_SZ(AdjRect) ADJ_SZ(AdjGhostPlan) ADJ_SZ(AdjGhostPlanBuildArgs)
+    ADJ_SZ(AdjGhostPlanFillArgs) ADJ_SZ(AdjStepRestrict) ADJ_SZ(AdjJobFill) ADJ_SZ(AdjStepArgs) ADJ_SZ(AdjPhysArgs)
+    ADJ_SZ(AdjGhostArgs) ADJ_SZ(AdjRestrictArgs) ADJ_SZ(AdjFlagArgs) ADJ_SZ(AdjFunctionalArgs) ADJ_SZ(AdjGauge)
+    ADJ_SZ(AdjGaugeArgs) ADJ_SZ(AdjFlagMaskArgs)
+#undef ADJ_SZ
+    return 0;
+}
+
 const char* adj_last_error(void) { return adj::g_err; }
 
 int adj_step_tile_shape(int variant, int ndim, int32_t* ni, int32_t* nj) {

@@ -104,3 +104,17 @@ def test_integration_stub_matches_header():
     assert re.findall(r'\("(\w+)"', block) == _struct_fields("AdjStepArgs")
     for name in declared_functions():
         assert name in text, name
+
+
+def test_struct_sizes_match_the_compiled_library():
+    """sizeof of every argument struct and table row, ctypes / numpy against the library."""
+    from paper_1511_03645_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("library not built")
+    lib = _lib.load_library()
+    for cls in _lib.STRUCTS:
+        assert lib.adj_struct_size(cls.__name__.encode()) == C.sizeof(cls), cls.__name__
+    assert lib.adj_struct_size(b"AdjPatch") == _lib.PATCH_DTYPE.itemsize
+    assert lib.adj_struct_size(b"AdjTile") == _lib.TILE_DTYPE.itemsize
+    assert lib.adj_struct_size(b"AdjRect") == _lib.RECT_DTYPE.itemsize
+    assert lib.adj_struct_size(b"NoSuchStruct") == 0
