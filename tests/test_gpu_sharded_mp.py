@@ -15,17 +15,6 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True)
-def _per_cell_materials(monkeypatch):
-    """These tests compare differently decomposed FAST runs bitwise.  With per-job
-    materials (ADJ_STEP_UNIFORM_MAT) a cell is stepped by the invariant-material march or by
-    the per-cell one depending on the job it falls in, and the two agree to rounding, not
-    bitwise (tests/test_gpu_uniform_mat.py): the comparison pins the per-cell march, in this
-    process and in spawned ranks."""
-    from paper_1511_03645_b200 import device
-    monkeypatch.setattr(device, "USE_UNIFORM_MAT", False)
-    monkeypatch.setenv("ADJAMR_UNIFORM_MAT", "0")
-
 NY, STEPS = 131, (5, 4, 2)
 
 
