@@ -4,9 +4,11 @@
 // contiguous axis) by ni columns (x).  Lane l owns row j0-2+l for the whole
 // strip, so every global load/store is a coalesced 32-lane row segment; the
 // warp marches along x keeping the last three columns, the last three
-// x-faces and the pipeline values in registers.  y-neighbour data moves
-// between lanes with warp shuffles; no shared memory, no recomputation along
-// x, 4/32 halo lanes along y.
+// x-faces and the pipeline values in registers.  Columns stream in through a
+// per-warp cp.async ring in shared memory (6 columns ahead); y-neighbour data
+// moves between lanes with warp shuffles; nothing is recomputed along x and
+// 4/32 lanes are y halo.  Short strips of several patches share a warp job
+// (job_offsets); persistent CTAs pull jobs from a global queue.
 //
 // Algebra (same scheme as the reference, reorganised; agrees with the EXACT
 // variant / the numpy reference to ~1e-16 norm-relative per step):
@@ -18,11 +20,16 @@
 //    B = sigma_up (1 + m m_up) (identical for minmod / MC / superbee);
 //  * the two transverse splits feeding a cell use the same pair of
 //    materials, so the entering fluctuations are summed before splitting;
-//  * material-only reciprocals use rcp.approx + two Newton steps.
+//  * material-only reciprocals use rcp.approx + one cubic Newton step.
+// Instantiations: CFL (per-face speed maximum) or the static material bound;
+// RST (restriction into the coarser level fused into the step); PFILL
+// (ADJ_STEP_PHYS_IN: the physical ghost fill of the input inside the launch);
+// SQ (dt/dx == dt/dy); WD (ADJ_STEP_WET_DRY: shallow water with dry cells,
+// with per-job classes); HM (ADJ_STEP_UNIFORM_MAT: constant or per-job
+// constant acoustic material, the material terms as loop invariants).
 // Reference: step_patch_2d solver.py:442-512, equations.py:143-349,
-// _limited_waves / _correction_flux solver.py:317-348, TimeReversed
-// equations.py:496-534.  Levels with dry shallow-water cells use the EXACT
-// variant (host dispatch), so no wet/dry logic is needed here.
+// _limited_waves / _correction_flux solver.py:317-348, _swe_effective_states
+// solver.py:357-387, TimeReversed equations.py:496-534.
 #include "adj_common.cuh"
 
 #ifndef K1_MIN_BLOCKS
