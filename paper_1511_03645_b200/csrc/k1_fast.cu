@@ -54,6 +54,10 @@
 #ifndef K1_MARCH_UNROLL_SWE
 #define K1_MARCH_UNROLL_SWE 2   // march loop unroll factor (groups of three columns) on shallow water
 #endif
+#ifndef K1_BULK
+#define K1_BULK 0   // 1 (experiment): single-strip jobs stream their columns with TMA 1D bulk copies
+                    // (cp.async.bulk + mbarrier, one elected lane) instead of per-lane cp.async
+#endif
 #ifndef K1_PREFETCH_CLAMP
 #define K1_PREFETCH_CLAMP 1   // 1: branch-free prefetch (re-read the last column)
 #endif
@@ -554,6 +558,47 @@ struct Strip {
     double dtdx, dtdy, hx, hy;
 
     double* ring;                  // this warp's cp.async ring: [RING1][NARR][32]
+#if K1_BULK
+    bool bulk;                     // this job streams by bulk copies (a single strip on lanes 0..31)
+    unsigned mbar;                 // shared address of this warp's GROUPS mbarriers
+    unsigned* phase;               // per-warp parity bits of the mbarriers (persist across jobs)
+    const double* seg;             // lane 0's row of q_in / aux (segment start), unclamped rows follow
+    const double* segaux;
+
+    // three columns s0.. into slots slot0.. (group g): one expect_tx, 3 * NARR copies of 256 bytes
+    ADJ_D void prefetch_group(int s0, int slot0, int g) const {
+        if (lane == 0) {
+            const unsigned bar = mbar + 8u * g;
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(3 * NARR * 256)
+                         : "memory");
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int sc = s0 + k < s_last ? s0 + k : s_last;
+                const int64_t o = (int64_t)(colbase + sc) * pitch;
+                const double* src[5] = {seg + o, seg + cs + o, seg + 2 * cs + o, segaux + o, segaux + as + o};
+#pragma unroll
+                for (int a_ = 0; a_ < NARR; ++a_) {
+                    const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + ((slot0 + k) * NARR + a_) * 32);
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];\n" ::"r"(dst),
+                        "l"(src[a_]), "r"(bar)
+                        : "memory");
+                }
+            }
+        }
+    }
+    ADJ_D void wait_group_bulk(int g) const {
+        const unsigned bar = mbar + 8u * g, par = (*phase >> g) & 1u;
+        unsigned done = 0;
+        for (int spin = 0; !done; ++spin) {
+            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                         : "=r"(done) : "r"(bar), "r"(par) : "memory");
+            if (spin > (1 << 24)) __trap();      // experiment guard: never hang the device
+        }
+        *phase ^= 1u << g;
+    }
+#endif
     int lane, lup, ldn;            // lane, and the lanes of rows j+1, j-1 (clamped like the shuffles)
     Mat m[3];
     Mat mh;                        // HM: the level's material
@@ -806,6 +851,10 @@ struct Strip {
         if (HM) mh = make_mat<SYS, FORM, LIM, SQ>(hc, hz, dtdx, dtdy);
         colbase = g + T.i0;
         i0 = 0; ni = T.ni;
+#if K1_BULK
+        seg = a.q_in + p.offset + (g + T.j0 - 2);
+        segaux = a.aux + p.offset + (g + T.j0 - 2);
+#endif
         if (RST) {
             const AdjStepRestrict& R = a.fine_restrict;
             ra0 = ra1 = ra2 = 0.0;
@@ -823,8 +872,16 @@ struct Strip {
     ADJ_D void run() {
         const int s_first = -2;
         s_last = ni + 1;
+#if K1_BULK
+        const bool bk = bulk;
+#else
+        constexpr bool bk = false;
+#endif
 #pragma unroll
         for (int gI = 0; gI < GROUPS; ++gI) {
+#if K1_BULK
+            if (bk) { prefetch_group(s_first + 3 * gI, 3 * gI, gI); continue; }
+#endif
             for (int k = 0; k < 3; ++k) prefetch(s_first + 3 * gI + k, 3 * gI + k);
             commit();
         }
@@ -846,14 +903,26 @@ struct Strip {
             // one wait per group of three columns, then the columns 3*GROUPS
             // ahead go to the group after the in-flight ones (with K1_LDSNB the
             // current and previous groups stay resident for neighbour reads)
+#if K1_BULK
+            if (bk) wait_group_bulk(base / 3);
+            else
+#endif
             asm volatile("cp.async.wait_group %0;\n" ::"n"(GROUPS - 1) : "memory");
             const Raw r0 = read(base), r1 = read(base + 1), r2 = read(base + 2);
             int pf = base + 3 * GROUPS;
             if (pf >= RING1) pf -= RING1;
+#if K1_BULK
+            if (bk) {
+                __syncwarp();                      // every lane has read the group before it is overwritten
+                prefetch_group(s + 3 * GROUPS, pf, pf / 3);
+            } else
+#endif
+            {
             prefetch(s + 3 * GROUPS, pf);
             prefetch(s + 3 * GROUPS + 1, pf + 1);
             prefetch(s + 3 * GROUPS + 2, pf + 2);
             commit();
+            }
             constexpr int SL = NARR * 32;          // doubles per column slot
             const double* rb = ring + base * SL;
             const double* rp = (base == 0 ? ring + RING1 * SL : rb) - SL;   // slot before base
@@ -862,6 +931,16 @@ struct Strip {
             column<2>(s + 2, r2, rb + 2 * SL + lup, rb + SL + ldn);
             base = base + 3 == RING1 ? 0 : base + 3;
         }
+#if K1_BULK
+        if (bk) {   // the groups prefetched past the strip's end
+            for (int gI = 0; gI < GROUPS; ++gI) {
+                wait_group_bulk(base / 3);
+                base = base + 3 == RING1 ? 0 : base + 3;
+            }
+            __syncwarp();
+            return;
+        }
+#endif
         asm volatile("cp.async.wait_all;\n" ::: "memory");
     }
 };
@@ -975,6 +1054,16 @@ __global__ void __launch_bounds__(32 * K1_WARPS, HM ? K1_MIN_BLOCKS_HM : K1_MIN_
     constexpr int NARR = Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, false>::NARR;   // HM: room for the per-cell march
     extern __shared__ __align__(16) double s_ring1[];   // [K1_WARPS][RING1 * NARR * 32]
     const int warp = threadIdx.x >> 5;
+#if K1_BULK
+    __shared__ __align__(8) unsigned long long s_mbar[K1_WARPS][NGRP];
+    unsigned bulk_phase = 0;
+    if (lane == 0) {
+        for (int gI = 0; gI < NGRP; ++gI)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&s_mbar[warp][gI])) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
+    __syncwarp();
+#endif
     const int njob = a.job_offsets ? a.njob : a.ntile;
     // Each warp's first job is its warp index (no queue round trip); the job
     // tables are static, so its strip's table entries load before the wait for
@@ -1023,16 +1112,29 @@ __global__ void __launch_bounds__(32 * K1_WARPS, HM ? K1_MIN_BLOCKS_HM : K1_MIN_
                 phys_prefill(a, Tt, a.patches[Tt.patch], lane);
             }
             __threadfence_block();
+#if K1_BULK
+            asm volatile("fence.proxy.async;\n" ::: "memory");   // the bulk copies read these generic stores
+#endif
             __syncwarp();
         }
         const AdjTile T = a.tiles[tix];
         const AdjPatch p = a.patches[T.patch];
+#if K1_BULK
+        // a single strip on lanes 0..31 whose row segments are 16-byte aligned
+        const bool bulk_ok = t1 - t0 == 1 && lane0 == 0 && ((p.offset + T.j0) & 1) == 0 && (p.pitch & 1) == 0 &&
+                             (a.comp_stride & 1) == 0 && (a.aux_stride & 1) == 0;
+        const unsigned bulk_bar = (unsigned)__cvta_generic_to_shared(&s_mbar[warp][0]);
+#define K1_BULK_SET(S) (S).bulk = bulk_ok; (S).mbar = bulk_bar; (S).phase = &bulk_phase;
+#else
+#define K1_BULK_SET(S)
+#endif
         if (WD && a.job_class) {   // wet/dry level: all-wet jobs march without the selects, all-dry ones copy
             const int cls = a.job_class[job];
             if (cls == 0) {
                 Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, false> S;
                 S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
                 S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32);
+                K1_BULK_SET(S)
                 S.template run<1>();   // three columns per loop body here: the kernel also holds the wet/dry march
                 if (S.bad) a.nonfinite[T.patch] = 1;
                 continue;
@@ -1049,6 +1151,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, HM ? K1_MIN_BLOCKS_HM : K1_MIN_
                 Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, true> S;
                 S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
                 S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32, hc, hz);
+                K1_BULK_SET(S)
                 S.run();
                 if (S.bad) a.nonfinite[T.patch] = 1;
                 continue;
@@ -1057,6 +1160,7 @@ __global__ void __launch_bounds__(32 * K1_WARPS, HM ? K1_MIN_BLOCKS_HM : K1_MIN_
         Strip<SYS, FORM, REV, LIM, CFL, RST, SQ, WD, false> S;
         S.smx = 0.0; S.smy = 0.0; S.bad = 0u;
         S.setup(T, p, a, lane, lane0, s_ring1 + warp * RING1 * NARR * 32);
+        K1_BULK_SET(S)
         S.run();
         if (CFL) {   // single-strip jobs only (packed jobs require static_speed)
             const double smx = warp_max(S.smx), smy = warp_max(S.smy);
