@@ -92,6 +92,7 @@ def _ptr(t) -> int:
 # K1's homogeneous-material instantiation on levels whose aux planes are constant (False: always
 # read the planes; same results bitwise)
 USE_UNIFORM_MAT = os.environ.get("ADJAMR_UNIFORM_MAT", "1") == "1"
+USE_MIXED_FIRST = os.environ.get("ADJAMR_MIXED_FIRST", "1") == "1"   # per-cell jobs at the head of the queue
 
 
 class LevelStore:
@@ -552,7 +553,13 @@ class LevelStore:
         ny = self.table_np["ny"][rows["patch"]]
         edge = (rows["i0"] < 2) | (rows["i0"] + rows["ni"] + 2 > nx) | (rows["j0"] < 2) | (rows["j0"] + rows["nj"] + 2 > ny)
         job_edge = np.array([bool(edge[offs[j]:offs[j + 1]].any()) for j in range(len(offs) - 1)])
-        order = np.concatenate([np.flatnonzero(job_edge), np.flatnonzero(~job_edge)])
+        # with per-job materials the few jobs that march per cell are the longest: they start first,
+        # so none of them ends up in the tail of the last wave
+        mixed = np.zeros(len(job_edge), dtype=bool)
+        if USE_MIXED_FIRST and self.job_uniform(tiles, ntile, jobs, njob) is not None:
+            mixed = self._scratch[("job_uniform_np", _ptr(tiles))][:, 0] == 0.0
+        order = np.concatenate([np.flatnonzero(mixed), np.flatnonzero(~mixed & job_edge),
+                                np.flatnonzero(~mixed & ~job_edge)])
         new_rows, new_offs = [], [0]
         for j in order:
             new_rows.extend(rows[offs[j]:offs[j + 1]])
@@ -663,6 +670,7 @@ class LevelStore:
         dev = None
         if np.count_nonzero(ju[:, 0]) >= self.JOB_UNIFORM_MIN_SHARE * len(ju):
             dev = _torch().from_numpy(np.ascontiguousarray(ju.reshape(-1))).to("cuda")
+            self._scratch[("job_uniform_np", _ptr(tiles))] = ju
         self._scratch[key] = dev
         return dev
 

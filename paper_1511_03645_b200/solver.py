@@ -130,7 +130,7 @@ def sample_patch_material(patch: Patch, equation: EquationSet, boundary: Boundar
         patch._store._dry = None
         patch._store._static_speed = None
         patch._store.uniform_mat = device.LevelStore._uniform_material(patch._store.patches)
-        for key in [k for k in patch._store._scratch if isinstance(k, tuple) and k[0] == "job_uniform"]:
+        for key in [k for k in patch._store._scratch if isinstance(k, tuple) and k[0] in ("job_uniform", "job_uniform_np", "tiles_edge_first")]:
             del patch._store._scratch[key]
         av = patch._store.aux_view(patch._slot)
         import torch
