@@ -555,11 +555,12 @@ class LevelStore:
         job_edge = np.array([bool(edge[offs[j]:offs[j + 1]].any()) for j in range(len(offs) - 1)])
         # with per-job materials the few jobs that march per cell are the longest: they start first,
         # so none of them ends up in the tail of the last wave
-        mixed = np.zeros(len(job_edge), dtype=bool)
+        # (the same order by job class on a wet/dry level -- coastal, all-wet, all-dry -- measured
+        # neutral on the C4 coastline, 0.2059 vs 0.2055 ms, and is not applied)
+        prio = np.ones(len(job_edge), dtype=np.int64)
         if USE_MIXED_FIRST and self.job_uniform(tiles, ntile, jobs, njob) is not None:
-            mixed = self._scratch[("job_uniform_np", _ptr(tiles))][:, 0] == 0.0
-        order = np.concatenate([np.flatnonzero(mixed), np.flatnonzero(~mixed & job_edge),
-                                np.flatnonzero(~mixed & ~job_edge)])
+            prio[self._scratch[("job_uniform_np", _ptr(tiles))][:, 0] == 0.0] = 0
+        order = np.argsort(2 * prio + (~job_edge).astype(np.int64), kind="stable")
         new_rows, new_offs = [], [0]
         for j in order:
             new_rows.extend(rows[offs[j]:offs[j + 1]])
